@@ -1,0 +1,62 @@
+"""Jacobian-free Newton with unpreconditioned CG (test infrastructure only).
+
+PAPER.md line 164 / 211 ("matrix-free non-linear solvers"), BASELINE.json
+configs[3], reading A15:
+
+    u = u0
+    repeat newton_steps times:
+        F = F(u);  record ||F||
+        CG on J(u) delta = -F from delta = 0, exactly cg_iters iterations,
+           no preconditioner, no convergence test; p^T J p <= 0 is an error
+        u = u + delta
+    record ||F(u)||
+
+Uses only ``residual`` and ``jvp`` of this oracle. Beyond roundoff growth the
+free-running trajectory is "parity unpinned" (T17): the tests compare it state-
+synchronised (each Newton iterate and CG direction fed to both sides).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .fem import residual, jvp
+
+
+def cg_fixed(apply, b, iters):
+    """Plain CG (Hestenes-Stiefel) from x = 0 for a fixed number of iterations."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    p = r.copy()
+    rr = float(r @ r)
+    dirs = []
+    for _ in range(iters):
+        Ap = apply(p)
+        pAp = float(p @ Ap)
+        if not pAp > 0.0:
+            raise FloatingPointError("CG breakdown: p^T A p <= 0")
+        alpha = rr / pAp
+        dirs.append(p.copy())
+        x += alpha * p
+        r -= alpha * Ap
+        rr_new = float(r @ r)
+        p = r + (rr_new / rr) * p
+        rr = rr_new
+    return x, dirs
+
+
+def newton_cg(pr, u0, newton_steps=5, cg_iters=20, record=False):
+    u = np.array(u0, dtype=np.float64)
+    norms = []
+    iterates = []
+    directions = []
+    for _ in range(newton_steps):
+        F = residual(pr, u)
+        norms.append(float(np.linalg.norm(F)))
+        iterates.append(u.copy())
+        delta, dirs = cg_fixed(lambda x: jvp(pr, u, x), -F, cg_iters)
+        directions.append(dirs)
+        u = u + delta
+    norms.append(float(np.linalg.norm(residual(pr, u))))
+    if record:
+        return u, norms, iterates, directions
+    return u, norms
