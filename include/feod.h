@@ -1,0 +1,152 @@
+/*
+ * feod.h — C-ABI of libfeod: the matrix-free FEOD hot path of
+ * "Scalable Analysis and Design Using Automatic Differentiation"
+ * (Andrej, Kolev, Lazarov; arXiv 2506.00746), built B200-native (sm_100a, fp64).
+ *
+ * Citations: "PAPER.md:nnn" is a line of the paper's LaTeX source
+ * (§2 "Automatic differentiation in finite element analysis"); readings A1..A19
+ * are listed in DESIGN.md §Readings.
+ *
+ * The operator (Eq. 1 at PAPER.md:155):
+ *     F(u) = P^T G^T B^T D(B G P u)
+ *   P    T-vector -> L-vector; on one GPU the identity plus Dirichlet-row
+ *        handling (reading A2): F_i = 0 on Dirichlet rows, u carries its own
+ *        Dirichlet data.
+ *   G    element restriction (gather) L -> E, G^T the atomic-free scatter-add.
+ *   B    sum-factorised interpolation of values and reference gradients at the
+ *        q^3 Gauss points of each hex Q_k element.
+ *   D    pointwise flux, the only differentiated operator.
+ * Its Jacobian action (Eq. 2): J(u) v = d/dt F(u + t v)|_{t=0}
+ *   = P^T G^T B^T J_D(u_q) B G P v, with J_D applied in forward mode by a
+ *   device dual-number type ("native ... dual number type").
+ * Design sensitivity with AD at integration points (reading A14):
+ *   g_e = - sum_{i free} lambda_i dF_i/drho_e.
+ *
+ * Conventions (readings A1-A16):
+ *   - mesh: structured nx x ny x nz hexahedra on the unit cube, trilinear
+ *     geometry from the vertex array (or uniform); Q_k with GLL nodes (A3);
+ *     qorder = Gauss points per axis (A5); reference cube [0,1]^3 (A4).
+ *   - vectors u, v, lambda, r, Jv: length N = (k nx+1)(k ny+1)(k nz+1), fp64,
+ *     x-fastest lexicographic DOF order, Dirichlet entries included (A16).
+ *   - g, rho: length E = nx ny nz, x-fastest lexicographic element order.
+ *   - residual sign: r_i = sum_e int D(grad u).grad phi_i - f phi_i (A1).
+ *
+ * Memory and ownership: every double* argument of the compute calls is a CUDA
+ * DEVICE pointer to caller-owned memory (e.g. a torch.float64 CUDA tensor),
+ * 8-byte aligned, not aliased with any other argument of the same call
+ * (FEOD_EINVAL otherwise). The library owns its tables, geometry and scratch;
+ * feod_destroy frees them. coeffs->rho is borrowed (device, length E) and must
+ * stay valid while calls that read it are in flight.
+ *
+ * Streams: every compute call is asynchronous on the handle's stream (set at
+ * create or with feod_set_stream). One stream per handle at a time: the
+ * handle's scratch (scatter fix-up buffer) is per handle.
+ *
+ * Errors: 0 on success, a negative FEOD_E* code otherwise; feod_last_error()
+ * returns a thread-local message. No C++ exception crosses the ABI. Kernel
+ * execution faults are asynchronous and surface as FEOD_ECUDA at a later call
+ * or synchronisation.
+ */
+#ifndef FEOD_H
+#define FEOD_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FEOD_API __attribute__((visibility("default")))
+#else
+#define FEOD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FEOD_OK 0
+#define FEOD_EINVAL (-1)        /* bad argument (null, aliasing, out of range) */
+#define FEOD_EUNSUPPORTED (-2)  /* valid but not built (order/qorder combination) */
+#define FEOD_ENOMEM (-3)        /* device or host allocation failed */
+#define FEOD_ECUDA (-4)         /* CUDA runtime error */
+
+/* Dirichlet face bits (feod_mesh.dirichlet_faces) */
+#define FEOD_FACE_X0 1u
+#define FEOD_FACE_X1 2u
+#define FEOD_FACE_Y0 4u
+#define FEOD_FACE_Y1 8u
+#define FEOD_FACE_Z0 16u
+#define FEOD_FACE_Z1 32u
+
+typedef struct feod_mesh {
+  int32_t nx, ny, nz;        /* hexahedra per axis, >= 1 */
+  const double* vertices;    /* HOST pointer, (nx+1)(ny+1)(nz+1) x 3 doubles, x-fastest,
+                                copied at create; NULL = uniform grid of the unit cube
+                                (constant-metric fast path, no stored geometry) */
+  uint32_t dirichlet_faces;  /* OR of FEOD_FACE_* */
+} feod_mesh;
+
+typedef enum feod_model {
+  FEOD_PLAPLACE = 0,    /* D = (eps^2 + |grad u|^2)^((p-2)/2) grad u */
+  FEOD_NLDIFF = 1,      /* D = (1 + u^2) grad u                         (BASELINE configs[2]) */
+  FEOD_HEAT_DESIGN = 2  /* D = rho_e^3 (1 + u^2) grad u                 (BASELINE configs[4]) */
+} feod_model;
+
+typedef struct feod_coeffs {
+  feod_model model;
+  double p;             /* PLAPLACE: p >= 2 */
+  double eps;           /* PLAPLACE: eps >= 0 */
+  double f;             /* constant source term */
+  const double* rho;    /* DEVICE pointer, length E; required for HEAT_DESIGN, else ignored */
+} feod_coeffs;
+
+typedef struct feod_op* feod_handle;
+
+/* Create an operator. order k in [1, 6], qorder = k+1 (reading A5; other
+ * combinations return FEOD_EUNSUPPORTED). Builds the 1D tables on the host,
+ * copies the vertices and computes the per-point metric
+ * M_q = w_q detJ_q J_q^{-1} J_q^{-T} (6 doubles per point)
+ * on `cuda_stream` (a cudaStream_t, NULL = legacy default stream). Rejects
+ * meshes with detJ <= 0 at any point (FEOD_EINVAL). Synchronises the stream. */
+FEOD_API int feod_create(const feod_mesh* mesh, int order, int qorder, const feod_coeffs* coeffs,
+                void* cuda_stream, feod_handle* out);
+FEOD_API int feod_destroy(feod_handle h);
+FEOD_API int feod_set_stream(feod_handle h, void* cuda_stream);
+/* Replace rho (HEAT_DESIGN); device pointer, length E. */
+FEOD_API int feod_set_rho(feod_handle h, const double* rho);
+FEOD_API int64_t feod_num_dofs(feod_handle h);
+FEOD_API int64_t feod_num_elems(feod_handle h);
+
+/* r = F(u)                               (Eq. 1)          */
+FEOD_API int feod_residual(feod_handle h, const double* u, double* r);
+/* Jv = J(u) v, one pass with dual<double> (Eq. 2)        */
+FEOD_API int feod_jvp(feod_handle h, const double* u, const double* v, double* Jv);
+/* r = F(u) and Jv = J(u) v from the same dual pass (value and tangent)  */
+FEOD_API int feod_jvp_res(feod_handle h, const double* u, const double* v, double* r, double* Jv);
+/* g_e = -lambda^T dF/drho_e, lambda's Dirichlet entries ignored          *
+ * (A14); HEAT_DESIGN only (others: FEOD_EINVAL)           */
+FEOD_API int feod_design_grad(feod_handle h, const double* u, const double* lambda, double* g);
+
+/* Same operations on HOST buffers: copies host->device, computes, copies
+ * device->host and synchronises the stream before returning (the e2e path).
+ * op: 0 residual(in0=u, out=r), 1 jvp(in0=u, in1=v, out=Jv),
+ *     2 design_grad(in0=u, in1=lambda, out=g). Host memory should be pinned. */
+FEOD_API int feod_apply_host(feod_handle h, int op, const double* in0, const double* in1, double* out);
+
+/* Jacobian-free Newton with unpreconditioned CG (reading A15, BASELINE
+ * configs[3]): u (device, length N) is updated in place; for each of
+ * newton_steps steps: F = F(u), CG on J(u) d = -F from d = 0 for exactly
+ * cg_iters iterations, u += d. norms_host (length newton_steps+1, HOST) gets
+ * ||F|| before each step and after the last. Returns FEOD_EINVAL if
+ * p^T J p <= 0 occurs (CG breakdown). Synchronises the stream. */
+FEOD_API int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg_iters, double* norms_host);
+
+/* BLAS-1 used by the Newton-CG driver (deterministic two-stage reductions).  *
+ * result: DEVICE pointer to one double.                                      */
+FEOD_API int feod_dot(feod_handle h, const double* x, const double* y, int64_t n, double* result);
+
+FEOD_API const char* feod_last_error(void);
+FEOD_API const char* feod_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEOD_H */

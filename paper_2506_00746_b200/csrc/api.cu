@@ -1,0 +1,296 @@
+// C-ABI of libfeod (include/feod.h): validation, handle state, dispatch.
+// Every compute step runs in this library's kernels; there is no CPU path.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/feod.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "tables.h"
+
+using namespace feod;
+
+struct feod_op {
+  int nx, ny, nz, k, q, nd;
+  feod_coeffs coeffs;
+  cudaStream_t st;
+  Tables T;
+  OpParams P;
+  BrickInfo bi;
+  int nbricks;
+  int64_t N, E;
+  double* geom = nullptr;
+  double* shell = nullptr;     // 2 x nbricks x shell
+  double* stage = nullptr;     // host-API staging: 3 x max(N, E)
+  double* red = nullptr;       // kRedBlocks partials + 8 scalars
+  int* flag = nullptr;
+  double* work = nullptr;      // Newton-CG: F, r, p, Ap, d (5 N)
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+static int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FEOD_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call, where)                                   \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where);   \
+  } while (0)
+
+extern "C" const char* feod_last_error(void) { return g_err.c_str(); }
+extern "C" const char* feod_version(void) { return "feod-b200 0.1 (sm_100a, fp64)"; }
+
+static void free_all(feod_op* h) {
+  if (!h) return;
+  cudaFree(h->geom);
+  cudaFree(h->shell);
+  cudaFree(h->stage);
+  cudaFree(h->red);
+  cudaFree(h->flag);
+  cudaFree(h->work);
+}
+
+extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const feod_coeffs* coeffs,
+                           void* cuda_stream, feod_handle* out) {
+  if (!mesh || !coeffs || !out) return fail(FEOD_EINVAL, "feod_create: null argument");
+  *out = nullptr;
+  if (mesh->nx < 1 || mesh->ny < 1 || mesh->nz < 1) return fail(FEOD_EINVAL, "feod_create: nx, ny, nz must be >= 1");
+  if (order < 1 || order > 8) return fail(FEOD_EINVAL, "feod_create: order must be in [1, 8]");
+  if (qorder < 1) return fail(FEOD_EINVAL, "feod_create: qorder must be >= 1");
+  if (order > 6 || qorder != order + 1)
+    return fail(FEOD_EUNSUPPORTED, "feod_create: built for order 1..6 with qorder = order + 1");
+  if (mesh->dirichlet_faces > 63u) return fail(FEOD_EINVAL, "feod_create: dirichlet_faces has unknown bits");
+  if (coeffs->model < FEOD_PLAPLACE || coeffs->model > FEOD_HEAT_DESIGN)
+    return fail(FEOD_EINVAL, "feod_create: unknown model");
+  if (coeffs->model == FEOD_PLAPLACE && !(coeffs->p >= 2.0)) return fail(FEOD_EINVAL, "feod_create: p must be >= 2");
+  if (coeffs->model == FEOD_PLAPLACE && !(coeffs->eps >= 0.0))
+    return fail(FEOD_EINVAL, "feod_create: eps must be >= 0");
+  if (!std::isfinite(coeffs->f)) return fail(FEOD_EINVAL, "feod_create: f must be finite");
+  if (coeffs->model == FEOD_HEAT_DESIGN && !coeffs->rho)
+    return fail(FEOD_EINVAL, "feod_create: HEAT_DESIGN needs rho (device, length E)");
+  const int64_t Mx = (int64_t)order * mesh->nx + 1, My = (int64_t)order * mesh->ny + 1,
+                Mz = (int64_t)order * mesh->nz + 1;
+  if (Mx > (1 << 30) || My > (1 << 30) || Mz > (1 << 30)) return fail(FEOD_EINVAL, "feod_create: mesh too large");
+
+  feod_op* h = new (std::nothrow) feod_op();
+  if (!h) return fail(FEOD_ENOMEM, "feod_create: host allocation");
+  h->nx = mesh->nx; h->ny = mesh->ny; h->nz = mesh->nz;
+  h->k = order; h->q = qorder; h->nd = order + 1;
+  h->coeffs = *coeffs;
+  h->st = (cudaStream_t)cuda_stream;
+  h->N = Mx * My * Mz;
+  h->E = (int64_t)mesh->nx * mesh->ny * mesh->nz;
+  if (!brick_info_nd(h->nd, &h->bi)) { delete h; return fail(FEOD_EUNSUPPORTED, "feod_create: order not built"); }
+
+  // 1D tables (host)
+  std::memset(&h->T, 0, sizeof(Tables));
+  double nodes[kMaxNQ], pts[kMaxNQ], wts[kMaxNQ];
+  gll01(order, nodes);
+  gauss01(qorder, pts, wts);
+  lagrange01(h->nd, nodes, qorder, pts, &h->T.B[0][0], &h->T.G[0][0], kMaxNQ);
+  for (int i = 0; i < qorder; ++i) { h->T.w[i] = wts[i]; h->T.x[i] = pts[i]; }
+
+  OpParams& P = h->P;
+  std::memset(&P, 0, sizeof(P));
+  P.nx = mesh->nx; P.ny = mesh->ny; P.nz = mesh->nz;
+  P.Mx = (int)Mx; P.My = (int)My; P.Mz = (int)Mz;
+  P.nbx = (mesh->nx + h->bi.BX - 1) / h->bi.BX;
+  P.nby = (mesh->ny + h->bi.BY - 1) / h->bi.BY;
+  P.nbz = (mesh->nz + h->bi.BZ - 1) / h->bi.BZ;
+  P.shell_stride = h->bi.shell;
+  P.faces = mesh->dirichlet_faces;
+  P.half_pm2 = 0.5 * (coeffs->p - 2.0);
+  P.eps2 = coeffs->eps * coeffs->eps;
+  P.f = coeffs->f;
+  const double hx = 1.0 / mesh->nx, hy = 1.0 / mesh->ny, hz = 1.0 / mesh->nz;
+  P.cx = hy * hz / hx; P.cy = hx * hz / hy; P.cz = hx * hy / hz; P.vol = hx * hy * hz;
+  P.rho = coeffs->rho;
+  h->nbricks = P.nbx * P.nby * P.nbz;
+
+  auto cleanup_fail = [&](int code) { free_all(h); delete h; return code; };
+  cudaError_t e;
+  if ((e = prepare_nd(h->nd)) != cudaSuccess) return cleanup_fail(cuda_fail(e, "feod_create: kernel attributes"));
+  if ((e = cudaMalloc(&h->shell, sizeof(double) * 2 * (size_t)h->nbricks * P.shell_stride)) != cudaSuccess)
+    return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: shell buffer"));
+  if ((e = cudaMalloc(&h->red, sizeof(double) * (kRedBlocks + 8))) != cudaSuccess)
+    return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: reduction buffer"));
+  if ((e = cudaMalloc(&h->flag, sizeof(int) * 2)) != cudaSuccess)
+    return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: flag"));
+  if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int) * 2, h->st)) != cudaSuccess)
+    return cleanup_fail(cuda_fail(e, "feod_create: memset"));
+
+  if (mesh->vertices) {
+    const size_t nv = (size_t)(mesh->nx + 1) * (mesh->ny + 1) * (mesh->nz + 1) * 3;
+    double* dverts = nullptr;
+    const size_t ng = (size_t)h->E * 6 * qorder * qorder * qorder;
+    if (cudaMalloc(&dverts, sizeof(double) * nv) != cudaSuccess) return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: vertices"));
+    if (cudaMalloc(&h->geom, sizeof(double) * ng) != cudaSuccess) {
+      cudaFree(dverts);
+      return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: geometry (6 doubles per point)"));
+    }
+    e = cudaMemcpyAsync(dverts, mesh->vertices, sizeof(double) * nv, cudaMemcpyHostToDevice, h->st);
+    if (e == cudaSuccess) e = launch_geometry(dverts, mesh->nx, mesh->ny, mesh->nz, qorder, h->T, h->geom, h->flag, h->st);
+    int bad = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
+    cudaFree(dverts);
+    if (e != cudaSuccess) return cleanup_fail(cuda_fail(e, "feod_create: geometry"));
+    if (bad) return cleanup_fail(fail(FEOD_EINVAL, "feod_create: mesh has an element with detJ <= 0"));
+    P.geom = h->geom;
+  } else {
+    if ((e = cudaStreamSynchronize(h->st)) != cudaSuccess) return cleanup_fail(cuda_fail(e, "feod_create: sync"));
+  }
+  *out = h;
+  return FEOD_OK;
+}
+
+extern "C" int feod_destroy(feod_handle h) {
+  if (!h) return fail(FEOD_EINVAL, "feod_destroy: null handle");
+  cudaStreamSynchronize(h->st);
+  free_all(h);
+  delete h;
+  return FEOD_OK;
+}
+
+extern "C" int feod_set_stream(feod_handle h, void* cuda_stream) {
+  if (!h) return fail(FEOD_EINVAL, "feod_set_stream: null handle");
+  h->st = (cudaStream_t)cuda_stream;
+  return FEOD_OK;
+}
+
+extern "C" int feod_set_rho(feod_handle h, const double* rho) {
+  if (!h || !rho) return fail(FEOD_EINVAL, "feod_set_rho: null argument");
+  h->coeffs.rho = rho;
+  h->P.rho = rho;
+  return FEOD_OK;
+}
+
+extern "C" int64_t feod_num_dofs(feod_handle h) { return h ? h->N : -1; }
+extern "C" int64_t feod_num_elems(feod_handle h) { return h ? h->E : -1; }
+
+static int run_op(feod_handle h, int mode, const double* in0, const double* in1, double* out0, double* out1,
+                  double* gout, const char* name) {
+  OpPtrs p{in0, in1, out0, out1, h->shell, h->shell + (size_t)h->nbricks * h->P.shell_stride, gout};
+  cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, h->geom == nullptr, h->nbricks, h->P, h->T, p, h->st);
+  if (e != cudaSuccess) return cuda_fail(e, name);
+  if (mode != MODE_DESIGN) {
+    e = launch_fixup(h->P, h->k, h->bi.BX, h->bi.BY, h->bi.BZ, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
+                     mode == MODE_JVPRES ? out1 : nullptr, h->st);
+    if (e != cudaSuccess) return cuda_fail(e, name);
+  }
+  return FEOD_OK;
+}
+
+extern "C" int feod_residual(feod_handle h, const double* u, double* r) {
+  if (!h || !u || !r) return fail(FEOD_EINVAL, "feod_residual: null argument");
+  if ((const double*)r == u) return fail(FEOD_EINVAL, "feod_residual: r aliases u");
+  return run_op(h, MODE_RES, u, nullptr, r, nullptr, nullptr, "feod_residual");
+}
+
+extern "C" int feod_jvp(feod_handle h, const double* u, const double* v, double* Jv) {
+  if (!h || !u || !v || !Jv) return fail(FEOD_EINVAL, "feod_jvp: null argument");
+  if ((const double*)Jv == u || (const double*)Jv == v) return fail(FEOD_EINVAL, "feod_jvp: Jv aliases an input");
+  return run_op(h, MODE_JVP, u, v, Jv, nullptr, nullptr, "feod_jvp");
+}
+
+extern "C" int feod_jvp_res(feod_handle h, const double* u, const double* v, double* r, double* Jv) {
+  if (!h || !u || !v || !Jv || !r) return fail(FEOD_EINVAL, "feod_jvp_res: null argument");
+  if ((const double*)Jv == u || (const double*)Jv == v || (const double*)r == u || (const double*)r == v || r == Jv)
+    return fail(FEOD_EINVAL, "feod_jvp_res: an output aliases another argument");
+  return run_op(h, MODE_JVPRES, u, v, Jv, r, nullptr, "feod_jvp_res");
+}
+
+extern "C" int feod_design_grad(feod_handle h, const double* u, const double* lambda, double* g) {
+  if (!h || !u || !lambda || !g) return fail(FEOD_EINVAL, "feod_design_grad: null argument");
+  if (h->coeffs.model != FEOD_HEAT_DESIGN) return fail(FEOD_EINVAL, "feod_design_grad: model has no rho");
+  if ((const double*)g == u || (const double*)g == lambda) return fail(FEOD_EINVAL, "feod_design_grad: g aliases an input");
+  return run_op(h, MODE_DESIGN, u, lambda, nullptr, nullptr, g, "feod_design_grad");
+}
+
+extern "C" int feod_apply_host(feod_handle h, int op, const double* in0, const double* in1, double* out) {
+  if (!h || !in0 || !out || (op != 0 && !in1)) return fail(FEOD_EINVAL, "feod_apply_host: null argument");
+  if (op < 0 || op > 2) return fail(FEOD_EINVAL, "feod_apply_host: op must be 0, 1 or 2");
+  const int64_t len = h->N > h->E ? h->N : h->E;
+  if (!h->stage && cudaMalloc(&h->stage, sizeof(double) * 3 * (size_t)len) != cudaSuccess) {
+    h->stage = nullptr;
+    return fail(FEOD_ENOMEM, "feod_apply_host: staging buffers");
+  }
+  double* d0 = h->stage;
+  double* d1 = h->stage + len;
+  double* d2 = h->stage + 2 * len;
+  CK(cudaMemcpyAsync(d0, in0, sizeof(double) * h->N, cudaMemcpyHostToDevice, h->st), "feod_apply_host: H2D");
+  if (op != 0) CK(cudaMemcpyAsync(d1, in1, sizeof(double) * h->N, cudaMemcpyHostToDevice, h->st), "feod_apply_host: H2D");
+  int rc = op == 0 ? feod_residual(h, d0, d2) : op == 1 ? feod_jvp(h, d0, d1, d2) : feod_design_grad(h, d0, d1, d2);
+  if (rc != FEOD_OK) return rc;
+  const int64_t nout = op == 2 ? h->E : h->N;
+  CK(cudaMemcpyAsync(out, d2, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->st), "feod_apply_host: D2H");
+  CK(cudaStreamSynchronize(h->st), "feod_apply_host: sync");
+  return FEOD_OK;
+}
+
+extern "C" int feod_dot(feod_handle h, const double* x, const double* y, int64_t n, double* result) {
+  if (!h || !x || !y || !result || n < 0) return fail(FEOD_EINVAL, "feod_dot: bad argument");
+  CK(dot_partial(x, y, n, h->red, h->st), "feod_dot");
+  CK(reduce_final(h->red, result, h->st), "feod_dot");
+  return FEOD_OK;
+}
+
+extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg_iters, double* norms_host) {
+  if (!h || !u || !norms_host || newton_steps < 0 || cg_iters < 0)
+    return fail(FEOD_EINVAL, "feod_newton_cg: bad argument");
+  const int64_t N = h->N;
+  if (!h->work && cudaMalloc(&h->work, sizeof(double) * 5 * (size_t)N) != cudaSuccess) {
+    h->work = nullptr;
+    return fail(FEOD_ENOMEM, "feod_newton_cg: work vectors");
+  }
+  double* F = h->work;
+  double* r = F + N;
+  double* p = r + N;
+  double* Ap = p + N;
+  double* d = Ap + N;
+  double* part = h->red;
+  double* sc = h->red + kRedBlocks;   // sc[0], sc[2]: rr ping-pong; sc[1]: pAp; sc[3]: ||F||^2
+  int* bad = h->flag + 1;
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), h->st), "feod_newton_cg");
+  for (int step = 0; step <= newton_steps; ++step) {
+    int rc = feod_residual(h, u, F);
+    if (rc) return rc;
+    CK(dot_partial(F, F, N, part, h->st), "feod_newton_cg: norm");
+    CK(reduce_final(part, sc + 3, h->st), "feod_newton_cg: norm");
+    double ff = 0.0;
+    CK(cudaMemcpyAsync(&ff, sc + 3, sizeof(double), cudaMemcpyDeviceToHost, h->st), "feod_newton_cg: D2H");
+    CK(cudaStreamSynchronize(h->st), "feod_newton_cg: sync");
+    norms_host[step] = std::sqrt(ff);
+    if (step == newton_steps) break;
+    CK(cg_init(F, r, p, d, N, h->st), "feod_newton_cg: init");
+    CK(dot_partial(r, r, N, part, h->st), "feod_newton_cg: rr");
+    CK(reduce_final(part, sc + 0, h->st), "feod_newton_cg: rr");
+    for (int it = 0; it < cg_iters; ++it) {
+      double* rr_old = sc + ((it & 1) ? 2 : 0);
+      double* rr_new = sc + ((it & 1) ? 0 : 2);
+      rc = feod_jvp(h, u, p, Ap);
+      if (rc) return rc;
+      CK(dot_partial(p, Ap, N, part, h->st), "feod_newton_cg: pAp");
+      CK(reduce_final(part, sc + 1, h->st), "feod_newton_cg: pAp");
+      CK(cg_update(rr_old, sc + 1, p, Ap, d, r, N, part, bad, h->st), "feod_newton_cg: update");
+      CK(reduce_final(part, rr_new, h->st), "feod_newton_cg: rr");
+      CK(cg_dir(rr_new, rr_old, r, p, N, h->st), "feod_newton_cg: direction");
+    }
+    CK(axpy1(u, d, N, h->st), "feod_newton_cg: u += d");
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st), "feod_newton_cg: D2H");
+    CK(cudaStreamSynchronize(h->st), "feod_newton_cg: sync");
+    if (hbad) return fail(FEOD_EINVAL, "feod_newton_cg: CG breakdown (p^T J p <= 0)");
+  }
+  return FEOD_OK;
+}

@@ -1,0 +1,123 @@
+// K6 — BLAS-1 for the Jacobian-free Newton-CG driver (reading A15): dot
+// products as deterministic two-stage reductions over a FIXED grid (the same
+// partial-sum tree every call), and the fused CG vector updates with the
+// scalars kept on the device (no host round trip inside the CG loop).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace feod {
+
+constexpr int kRedThreads = 256;
+
+FEOD_DEV double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  return sh[0];
+}
+
+__global__ void __launch_bounds__(kRedThreads) dot_partial_kernel(const double* __restrict__ x,
+                                                                  const double* __restrict__ y, int64_t n,
+                                                                  double* __restrict__ partials) {
+  __shared__ double sh[kRedThreads];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)kRedBlocks * kRedThreads)
+    acc = fma(x[i], y[i], acc);
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kRedThreads) reduce_final_kernel(const double* __restrict__ partials,
+                                                                   double* __restrict__ out) {
+  __shared__ double sh[kRedThreads];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += kRedThreads) acc += partials[i];
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+cudaError_t dot_partial(const double* x, const double* y, int64_t n, double* partials, cudaStream_t st) {
+  dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(x, y, n, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_final(const double* partials, double* out, cudaStream_t st) {
+  reduce_final_kernel<<<1, kRedThreads, 0, st>>>(partials, out);
+  return cudaGetLastError();
+}
+
+// r = -F, p = r, d = 0
+__global__ void cg_init_kernel(const double* __restrict__ F, double* __restrict__ r, double* __restrict__ p,
+                               double* __restrict__ d, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = -F[i];
+    r[i] = v;
+    p[i] = v;
+    d[i] = 0.0;
+  }
+}
+
+// alpha = rr / pAp;  d += alpha p;  r -= alpha Ap;  partials of r.r (same fixed grid as dot_partial)
+__global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __restrict__ rr,
+                                                                const double* __restrict__ pAp,
+                                                                const double* __restrict__ p,
+                                                                const double* __restrict__ Ap, double* __restrict__ d,
+                                                                double* __restrict__ r, int64_t n,
+                                                                double* __restrict__ partials, int* __restrict__ bad) {
+  __shared__ double sh[kRedThreads];
+  const double den = *pAp;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !(den > 0.0)) *bad = 1;
+  const double alpha = *rr / den;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)kRedBlocks * kRedThreads) {
+    d[i] = fma(alpha, p[i], d[i]);
+    const double ri = fma(-alpha, Ap[i], r[i]);
+    r[i] = ri;
+    acc = fma(ri, ri, acc);
+  }
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+// p = r + (rr_new / rr_old) p
+__global__ void cg_dir_kernel(const double* __restrict__ rr_new, const double* __restrict__ rr_old,
+                              const double* __restrict__ r, double* __restrict__ p, int64_t n) {
+  const double beta = *rr_new / *rr_old;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], r[i]);
+}
+
+// u += d
+__global__ void axpy1_kernel(double* __restrict__ u, const double* __restrict__ d, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    u[i] += d[i];
+}
+
+static int grid_for(int64_t n) {
+  const int64_t b = (n + 255) / 256;
+  return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+}
+
+cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n, cudaStream_t st) {
+  cg_init_kernel<<<grid_for(n), 256, 0, st>>>(F, r, p, d, n);
+  return cudaGetLastError();
+}
+cudaError_t cg_update(const double* rr, const double* pAp, const double* p, const double* Ap, double* d, double* r,
+                      int64_t n, double* partials, int* bad, cudaStream_t st) {
+  cg_update_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(rr, pAp, p, Ap, d, r, n, partials, bad);
+  return cudaGetLastError();
+}
+cudaError_t cg_dir(const double* rr_new, const double* rr_old, const double* r, double* p, int64_t n,
+                   cudaStream_t st) {
+  cg_dir_kernel<<<grid_for(n), 256, 0, st>>>(rr_new, rr_old, r, p, n);
+  return cudaGetLastError();
+}
+cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st) {
+  axpy1_kernel<<<grid_for(n), 256, 0, st>>>(u, d, n);
+  return cudaGetLastError();
+}
+
+}  // namespace feod

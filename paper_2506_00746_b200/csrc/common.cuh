@@ -1,0 +1,77 @@
+// Shared device-side definitions of libfeod (product path; independent of oracle/).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define FEOD_DEV __device__ __forceinline__
+#define FEOD_HD __host__ __device__ __forceinline__
+
+namespace feod {
+
+enum Mode { MODE_RES = 0, MODE_JVP = 1, MODE_JVPRES = 2, MODE_DESIGN = 3 };
+enum Model { PLAPLACE = 0, NLDIFF = 1, HEAT = 2 };
+constexpr int kMaxNQ = 8;
+
+// 1D tables, passed by value as a kernel parameter: the entries sit in the
+// constant bank and feed DFMA directly (uniform across the warp).
+//   B[i][a] = l_a(x_i), G[i][a] = l_a'(x_i)  (GLL Lagrange basis at Gauss points)
+//   w[i]    = 1D Gauss weight on [0,1]
+//   x[i]    = 1D Gauss point on [0,1] (geometry setup only)
+struct Tables {
+  double B[kMaxNQ][kMaxNQ];
+  double G[kMaxNQ][kMaxNQ];
+  double w[kMaxNQ];
+  double x[kMaxNQ];
+};
+
+// Everything a fused operator kernel needs besides the vectors.
+struct OpParams {
+  int nx, ny, nz;        // elements per axis
+  int Mx, My, Mz;        // DOFs per axis (k n + 1)
+  int nbx, nby, nbz;     // bricks per axis
+  int shell_stride;      // doubles per brick in the shell buffer
+  uint32_t faces;        // Dirichlet face bits
+  // physics
+  double half_pm2;       // (p-2)/2 (PLAPLACE)
+  double eps2;           // eps^2
+  double f;              // source
+  // geometry: uniform grid (geom == nullptr): M = w_q diag(cx, cy, cz), W = w_q * vol
+  double cx, cy, cz, vol;
+  const double* geom;    // [E][6][NQ^3] metric, components xx yy zz xy xz yz
+  const double* rho;     // [E] (HEAT)
+};
+
+FEOD_HD bool is_dirichlet(int X, int Y, int Z, int Mx, int My, int Mz, uint32_t faces) {
+  return ((faces & 1u) && X == 0) || ((faces & 2u) && X == Mx - 1) ||
+         ((faces & 4u) && Y == 0) || ((faces & 8u) && Y == My - 1) ||
+         ((faces & 16u) && Z == 0) || ((faces & 32u) && Z == Mz - 1);
+}
+
+// Rank of a point on the surface of an LX x LY x LZ box (any coordinate at 0
+// or L-1): z=0 plane, then for each middle z a ring, then the z=L-1 plane.
+FEOD_HD int shell_rank(int X, int Y, int Z, int LX, int LY, int LZ) {
+  if (Z == 0) return X + LX * Y;
+  const int base = LX * LY;
+  const int ring = 2 * LX + 2 * (LY - 2);
+  if (Z == LZ - 1) return base + (LZ - 2) * ring + X + LX * Y;
+  const int r = base + (Z - 1) * ring;
+  if (Y == 0) return r + X;
+  if (Y == LY - 1) return r + LX + X;
+  return r + 2 * LX + 2 * (Y - 1) + (X == 0 ? 0 : 1);
+}
+
+FEOD_HD int shell_size(int LX, int LY, int LZ) {
+  return LX * LY * LZ - (LX - 2) * (LY - 2) * (LZ - 2);
+}
+
+// Brick shape (elements per brick along x, y, z) for order k = ND-1: sized so
+// the per-brick element buffer stays well inside shared memory.
+template <int ND> struct BrickShape;
+template <> struct BrickShape<2> { static constexpr int BX = 8, BY = 8, BZ = 4, EB = 32; };
+template <> struct BrickShape<3> { static constexpr int BX = 4, BY = 4, BZ = 4, EB = 16; };
+template <> struct BrickShape<4> { static constexpr int BX = 4, BY = 4, BZ = 4, EB = 8; };
+template <> struct BrickShape<5> { static constexpr int BX = 2, BY = 2, BZ = 4, EB = 8; };
+template <> struct BrickShape<6> { static constexpr int BX = 2, BY = 2, BZ = 2, EB = 4; };
+template <> struct BrickShape<7> { static constexpr int BX = 2, BY = 2, BZ = 2, EB = 4; };
+
+}  // namespace feod

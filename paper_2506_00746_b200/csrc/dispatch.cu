@@ -1,0 +1,43 @@
+// Order dispatch of the fused operator kernels.
+#include "kernels.h"
+
+namespace feod {
+
+bool brick_info_nd(int nd, BrickInfo* bi) {
+  switch (nd) {
+    case 2: return brick_info<2>(bi);
+    case 3: return brick_info<3>(bi);
+    case 4: return brick_info<4>(bi);
+    case 5: return brick_info<5>(bi);
+    case 6: return brick_info<6>(bi);
+    case 7: return brick_info<7>(bi);
+  }
+  return false;
+}
+
+cudaError_t prepare_nd(int nd) {
+  switch (nd) {
+    case 2: return prepare_order<2>();
+    case 3: return prepare_order<3>();
+    case 4: return prepare_order<4>();
+    case 5: return prepare_order<5>();
+    case 6: return prepare_order<6>();
+    case 7: return prepare_order<7>();
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const OpParams& P, const Tables& T,
+                      const OpPtrs& p, cudaStream_t st) {
+  switch (nd) {
+    case 2: return launch_order<2>(mode, model, affine, grid, P, T, p, st);
+    case 3: return launch_order<3>(mode, model, affine, grid, P, T, p, st);
+    case 4: return launch_order<4>(mode, model, affine, grid, P, T, p, st);
+    case 5: return launch_order<5>(mode, model, affine, grid, P, T, p, st);
+    case 6: return launch_order<6>(mode, model, affine, grid, P, T, p, st);
+    case 7: return launch_order<7>(mode, model, affine, grid, P, T, p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace feod

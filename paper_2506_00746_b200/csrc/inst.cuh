@@ -1,0 +1,81 @@
+// Instantiation of the fused operator kernel for one order (ND = k+1 nodes,
+// NQ = k+1 points per axis): 4 modes x 3 models x {affine, stored metric}.
+#pragma once
+#include "kernels.h"
+#include "op_kernel.cuh"
+
+namespace feod {
+
+template <int ND, int NQ, int MODE, int MODEL, bool AFF>
+static cudaError_t launch_one(int grid, const OpParams& P, const Tables& T, const OpPtrs& p, cudaStream_t st) {
+  using S = OpShape<ND, NQ, MODE>;
+  op_kernel<ND, NQ, MODE, MODEL, AFF><<<grid, S::NT, S::SMEM_BYTES, st>>>(P, T, p.in0, p.in1, p.out0, p.out1,
+                                                                          p.shell0, p.shell1, p.gout);
+  return cudaGetLastError();
+}
+
+template <int ND, int NQ, int MODE, int MODEL, bool AFF>
+static cudaError_t prep_one() {
+  using S = OpShape<ND, NQ, MODE>;
+  return cudaFuncSetAttribute(op_kernel<ND, NQ, MODE, MODEL, AFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)S::SMEM_BYTES);
+}
+
+template <int ND, int NQ, int MODE>
+static cudaError_t launch_mode(int model, bool aff, int grid, const OpParams& P, const Tables& T, const OpPtrs& p,
+                               cudaStream_t st) {
+  switch (model) {
+    case PLAPLACE: return aff ? launch_one<ND, NQ, MODE, PLAPLACE, true>(grid, P, T, p, st)
+                              : launch_one<ND, NQ, MODE, PLAPLACE, false>(grid, P, T, p, st);
+    case NLDIFF: return aff ? launch_one<ND, NQ, MODE, NLDIFF, true>(grid, P, T, p, st)
+                            : launch_one<ND, NQ, MODE, NLDIFF, false>(grid, P, T, p, st);
+    case HEAT: return aff ? launch_one<ND, NQ, MODE, HEAT, true>(grid, P, T, p, st)
+                          : launch_one<ND, NQ, MODE, HEAT, false>(grid, P, T, p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int ND, int NQ, int MODE>
+static cudaError_t prep_mode() {
+  cudaError_t e;
+  if ((e = prep_one<ND, NQ, MODE, PLAPLACE, true>()) != cudaSuccess) return e;
+  if ((e = prep_one<ND, NQ, MODE, PLAPLACE, false>()) != cudaSuccess) return e;
+  if ((e = prep_one<ND, NQ, MODE, NLDIFF, true>()) != cudaSuccess) return e;
+  if ((e = prep_one<ND, NQ, MODE, NLDIFF, false>()) != cudaSuccess) return e;
+  if ((e = prep_one<ND, NQ, MODE, HEAT, true>()) != cudaSuccess) return e;
+  return prep_one<ND, NQ, MODE, HEAT, false>();
+}
+
+template <>
+bool brick_info<FEOD_ND>(BrickInfo* bi) {
+  using S = OpShape<FEOD_ND, FEOD_ND, MODE_RES>;
+  bi->BX = S::BX; bi->BY = S::BY; bi->BZ = S::BZ; bi->threads = S::NT; bi->shell = S::SHELL;
+  bi->smem[MODE_RES] = OpShape<FEOD_ND, FEOD_ND, MODE_RES>::SMEM_BYTES;
+  bi->smem[MODE_JVP] = OpShape<FEOD_ND, FEOD_ND, MODE_JVP>::SMEM_BYTES;
+  bi->smem[MODE_JVPRES] = OpShape<FEOD_ND, FEOD_ND, MODE_JVPRES>::SMEM_BYTES;
+  bi->smem[MODE_DESIGN] = OpShape<FEOD_ND, FEOD_ND, MODE_DESIGN>::SMEM_BYTES;
+  return true;
+}
+
+template <>
+cudaError_t prepare_order<FEOD_ND>() {
+  cudaError_t e;
+  if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_RES>()) != cudaSuccess) return e;
+  if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_JVP>()) != cudaSuccess) return e;
+  if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_JVPRES>()) != cudaSuccess) return e;
+  return prep_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>();
+}
+
+template <>
+cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int grid, const OpParams& P, const Tables& T,
+                                  const OpPtrs& p, cudaStream_t st) {
+  switch (mode) {
+    case MODE_RES: return launch_mode<FEOD_ND, FEOD_ND, MODE_RES>(model, aff, grid, P, T, p, st);
+    case MODE_JVP: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVP>(model, aff, grid, P, T, p, st);
+    case MODE_JVPRES: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVPRES>(model, aff, grid, P, T, p, st);
+    case MODE_DESIGN: return launch_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>(model, aff, grid, P, T, p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace feod

@@ -1,0 +1,62 @@
+// Internal launch interface of libfeod (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace feod {
+
+struct OpPtrs {
+  const double* in0;
+  const double* in1;
+  double* out0;
+  double* out1;
+  double* shell0;
+  double* shell1;
+  double* gout;
+};
+
+struct BrickInfo { int BX, BY, BZ, threads, shell; size_t smem[4]; };
+
+cudaError_t launch_geometry(const double* verts, int nx, int ny, int nz, int nq, const Tables& T, double* geom,
+                            int* bad, cudaStream_t st);
+cudaError_t launch_fixup(const OpParams& P, int K, int BX, int BY, int BZ, const double* shell0, double* out0,
+                         const double* shell1, double* out1, cudaStream_t st);
+
+// Per-order entry points (inst_kN.cu), ND = k+1, NQ = k+1.
+template <int ND> bool brick_info(BrickInfo* bi);
+template <int ND> cudaError_t prepare_order();
+template <int ND> cudaError_t launch_order(int mode, int model, bool affine, int grid, const OpParams& P,
+                                           const Tables& T, const OpPtrs& p, cudaStream_t st);
+
+#define FEOD_DECLARE_ORDER(ND)                                                                    \
+  template <> bool brick_info<ND>(BrickInfo * bi);                                                \
+  template <> cudaError_t prepare_order<ND>();                                                    \
+  template <> cudaError_t launch_order<ND>(int mode, int model, bool affine, int grid, const OpParams& P, \
+                                           const Tables& T, const OpPtrs& p, cudaStream_t st);
+FEOD_DECLARE_ORDER(2)
+FEOD_DECLARE_ORDER(3)
+FEOD_DECLARE_ORDER(4)
+FEOD_DECLARE_ORDER(5)
+FEOD_DECLARE_ORDER(6)
+FEOD_DECLARE_ORDER(7)
+
+bool brick_info_nd(int nd, BrickInfo* bi);
+cudaError_t prepare_nd(int nd);
+cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const OpParams& P, const Tables& T,
+                      const OpPtrs& p, cudaStream_t st);
+
+// BLAS-1 (blas1.cu): deterministic fixed-grid two-stage reductions.
+constexpr int kRedBlocks = 296;
+cudaError_t dot_partial(const double* x, const double* y, int64_t n, double* partials, cudaStream_t st);
+cudaError_t reduce_final(const double* partials, double* out, cudaStream_t st);
+
+}  // namespace feod
+
+namespace feod {
+cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n, cudaStream_t st);
+cudaError_t cg_update(const double* rr, const double* pAp, const double* p, const double* Ap, double* d, double* r,
+                      int64_t n, double* partials, int* bad, cudaStream_t st);
+cudaError_t cg_dir(const double* rr_new, const double* rr_old, const double* r, double* p, int64_t n,
+                   cudaStream_t st);
+cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st);
+}  // namespace feod

@@ -1,0 +1,392 @@
+// Fused FEOD operator kernel: G -> B -> D -> B^T -> G^T (-> P^T) for one brick
+// of hexahedra per CTA (PAPER.md:25, Eq. 1 :155, Eq. 2 :160, :199).
+//
+// Structure:
+//  1. the brick's DOF box of each input vector is staged in shared memory
+//     (row-contiguous loads; lambda's Dirichlet entries masked for DESIGN);
+//  2. elements are processed EB at a time, NQ*NQ threads per element, each
+//     thread owning one 1D line of the element; sum factorisation (operator B)
+//     runs as three 1D contractions z -> y -> x in registers, with the line
+//     ownership rotated through a per-element scratch in shared memory;
+//     1D tables B, G come from the kernel-parameter (constant) bank;
+//  3. the pointwise flux D runs on the x-line of points each thread owns, as
+//     double (residual) or dual<double> (JVP / design derivative);
+//  4. B^T runs the same contractions transposed (x -> y -> z) and each element
+//     writes its element vector to a shared-memory E-buffer;
+//  5. G^T: every box point sums its (<= 8) element contributions in a fixed
+//     order; points owned by this brick alone go straight to the output
+//     (P^T: 0 on Dirichlet rows), points on a face shared with a neighbouring
+//     brick go to this brick's slab of the shell buffer, summed later in a
+//     fixed order by fixup_kernel — deterministic, no atomics.
+#pragma once
+#include "common.cuh"
+#include "dual.cuh"
+#include "physics.cuh"
+
+namespace feod {
+
+template <int ND, int NQ, int MODE>
+struct OpShape {
+  using S = BrickShape<ND>;
+  static constexpr int K = ND - 1;
+  static constexpr int BX = S::BX, BY = S::BY, BZ = S::BZ, EB = S::EB;
+  static constexpr int NEL = BX * BY * BZ;
+  static constexpr int LXF = K * BX + 1, LYF = K * BY + 1, LZF = K * BZ + 1;
+  static constexpr int BOX = LXF * LYF * LZF;
+  static constexpr int LINES = NQ * NQ;
+  static constexpr int NT = LINES * EB;
+  static constexpr int ND3 = ND * ND * ND;
+  static constexpr int SCR_A = 2 * ND * ND * NQ, SCR_B = 3 * ND * NQ * NQ;
+  static constexpr int SCR = (SCR_A > SCR_B ? SCR_A : SCR_B) > LINES ? (SCR_A > SCR_B ? SCR_A : SCR_B) : LINES;
+  static constexpr int NIN = (MODE == MODE_RES) ? 1 : 2;
+  static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
+  static constexpr int SMEM_DOUBLES = NIN * BOX + NOUT * NEL * ND3 + EB * SCR;
+  static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
+  static constexpr int SHELL = LXF * LYF * LZF - (LXF - 2) * (LYF - 2) * (LZF - 2);
+};
+
+// Forward interpolation of one field from the smem box: returns, for the
+// x-line (j, l) this thread owns, U[i], dU/dxi1[i], dU/dxi2[i], dU/dxi3[i].
+template <int ND, int NQ, int LXF, int LYF>
+FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, double* scr, int line,
+                            int X0, int Y0, int Z0, double (&out)[4][NQ]) {
+  constexpr int SA = ND * ND * NQ;   // S0 | S1
+  constexpr int SB = ND * NQ * NQ;   // T0 | T1 | T2
+  // ---- z: nodes c -> points l, values (t0) and z-derivative (t1)
+  {
+    const int a = line % NQ, b = line / NQ;
+    if (a < ND && b < ND) {
+      double x[ND];
+#pragma unroll
+      for (int c = 0; c < ND; ++c) x[c] = box[(X0 + a) + LXF * ((Y0 + b) + LYF * (Z0 + c))];
+#pragma unroll
+      for (int l = 0; l < NQ; ++l) {
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < ND; ++c) {
+          t0 = fma(T.B[l][c], x[c], t0);
+          t1 = fma(T.G[l][c], x[c], t1);
+        }
+        scr[a + ND * (b + ND * l)] = t0;
+        scr[SA + a + ND * (b + ND * l)] = t1;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- y: nodes b -> points j
+  {
+    const int a = line % NQ, l = line / NQ;
+    double s0[ND], s1[ND];
+    if (a < ND) {
+#pragma unroll
+      for (int b = 0; b < ND; ++b) {
+        s0[b] = scr[a + ND * (b + ND * l)];
+        s1[b] = scr[SA + a + ND * (b + ND * l)];
+      }
+    }
+    __syncthreads();
+    if (a < ND) {
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+#pragma unroll
+        for (int b = 0; b < ND; ++b) {
+          y0 = fma(T.B[j][b], s0[b], y0);
+          y1 = fma(T.G[j][b], s0[b], y1);
+          y2 = fma(T.B[j][b], s1[b], y2);
+        }
+        scr[a + ND * (j + NQ * l)] = y0;
+        scr[SB + a + ND * (j + NQ * l)] = y1;
+        scr[2 * SB + a + ND * (j + NQ * l)] = y2;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- x: nodes a -> points i
+  {
+    const int j = line % NQ, l = line / NQ;
+    double r0[ND], r1[ND], r2[ND];
+#pragma unroll
+    for (int a = 0; a < ND; ++a) {
+      r0[a] = scr[a + ND * (j + NQ * l)];
+      r1[a] = scr[SB + a + ND * (j + NQ * l)];
+      r2[a] = scr[2 * SB + a + ND * (j + NQ * l)];
+    }
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      double U = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+      for (int a = 0; a < ND; ++a) {
+        U = fma(T.B[i][a], r0[a], U);
+        gx = fma(T.G[i][a], r0[a], gx);
+        gy = fma(T.B[i][a], r1[a], gy);
+        gz = fma(T.B[i][a], r2[a], gz);
+      }
+      out[0][i] = U;
+      out[1][i] = gx;
+      out[2][i] = gy;
+      out[3][i] = gz;
+    }
+  }
+  __syncthreads();
+}
+
+// Transposed interpolation: from the x-line of point values (Fx, Fy, Fz and
+// optionally the value channel V) back to the element's nodal vector; the
+// thread owning node column (a, b) writes re[a + ND (b + ND c)] for all c.
+template <int ND, int NQ, bool HASV>
+FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const double (&F)[4][NQ], double* re,
+                             bool write) {
+  constexpr int SA = ND * ND * NQ;
+  constexpr int SB = ND * NQ * NQ;
+  // ---- x^T: points i -> nodes a
+  {
+    const int j = line % NQ, l = line / NQ;
+#pragma unroll
+    for (int a = 0; a < ND; ++a) {
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        p0 = fma(T.G[i][a], F[0][i], p0);
+        if constexpr (HASV) p0 = fma(T.B[i][a], F[3][i], p0);
+        p1 = fma(T.B[i][a], F[1][i], p1);
+        p2 = fma(T.B[i][a], F[2][i], p2);
+      }
+      scr[a + ND * (j + NQ * l)] = p0;
+      scr[SB + a + ND * (j + NQ * l)] = p1;
+      scr[2 * SB + a + ND * (j + NQ * l)] = p2;
+    }
+  }
+  __syncthreads();
+  // ---- y^T: points j -> nodes b
+  {
+    const int a = line % NQ, l = line / NQ;
+    double p0[NQ], p1[NQ], p2[NQ];
+    if (a < ND) {
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        p0[j] = scr[a + ND * (j + NQ * l)];
+        p1[j] = scr[SB + a + ND * (j + NQ * l)];
+        p2[j] = scr[2 * SB + a + ND * (j + NQ * l)];
+      }
+    }
+    __syncthreads();
+    if (a < ND) {
+#pragma unroll
+      for (int b = 0; b < ND; ++b) {
+        double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          q0 = fma(T.B[j][b], p0[j], q0);
+          q0 = fma(T.G[j][b], p1[j], q0);
+          q1 = fma(T.B[j][b], p2[j], q1);
+        }
+        scr[a + ND * (b + ND * l)] = q0;
+        scr[SA + a + ND * (b + ND * l)] = q1;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- z^T: points l -> nodes c
+  {
+    const int a = line % NQ, b = line / NQ;
+    if (a < ND && b < ND) {
+      double q0[NQ], q1[NQ];
+#pragma unroll
+      for (int l = 0; l < NQ; ++l) {
+        q0[l] = scr[a + ND * (b + ND * l)];
+        q1[l] = scr[SA + a + ND * (b + ND * l)];
+      }
+      if (write) {
+#pragma unroll
+        for (int c = 0; c < ND; ++c) {
+          double r = 0.0;
+#pragma unroll
+          for (int l = 0; l < NQ; ++l) {
+            r = fma(T.B[l][c], q0[l], r);
+            r = fma(T.G[l][c], q1[l], r);
+          }
+          re[a + ND * (b + ND * c)] = r;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int ND, int NQ, int MODE, int MODEL, bool AFFINE>
+__global__ void __launch_bounds__(OpShape<ND, NQ, MODE>::NT)
+op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, const double* __restrict__ in1,
+          double* __restrict__ out0, double* __restrict__ out1, double* __restrict__ shell0,
+          double* __restrict__ shell1, double* __restrict__ gout) {
+  using S = OpShape<ND, NQ, MODE>;
+  constexpr int K = S::K;
+  extern __shared__ double smem[];
+  double* box0 = smem;
+  double* box1 = smem + S::BOX;                     // valid if NIN == 2
+  double* ebuf = smem + S::NIN * S::BOX;            // [NOUT][NEL][ND3]
+  double* scratch = ebuf + S::NOUT * S::NEL * S::ND3;
+
+  const int tid = threadIdx.x;
+  const int brick = blockIdx.x;
+  const int bx = brick % P.nbx, by = (brick / P.nbx) % P.nby, bz = brick / (P.nbx * P.nby);
+  const int ex0 = bx * S::BX, ey0 = by * S::BY, ez0 = bz * S::BZ;
+  const int bxr = min(S::BX, P.nx - ex0), byr = min(S::BY, P.ny - ey0), bzr = min(S::BZ, P.nz - ez0);
+  const int LX = K * bxr + 1, LY = K * byr + 1, LZ = K * bzr + 1;
+  const int gX0 = K * ex0, gY0 = K * ey0, gZ0 = K * ez0;
+
+  // ---- 1. stage the DOF boxes (G, gather)
+  for (int idx = tid; idx < LX * LY * LZ; idx += S::NT) {
+    const int X = idx % LX, Y = (idx / LX) % LY, Z = idx / (LX * LY);
+    const int64_t gidx = (int64_t)(gX0 + X) + (int64_t)P.Mx * ((gY0 + Y) + (int64_t)P.My * (gZ0 + Z));
+    const int sidx = X + S::LXF * (Y + S::LYF * Z);
+    box0[sidx] = __ldg(in0 + gidx);
+    if constexpr (S::NIN == 2) {
+      double val = __ldg(in1 + gidx);
+      if constexpr (MODE == MODE_DESIGN) {
+        if (is_dirichlet(gX0 + X, gY0 + Y, gZ0 + Z, P.Mx, P.My, P.Mz, P.faces)) val = 0.0;
+      }
+      box1[sidx] = val;
+    }
+  }
+  __syncthreads();
+
+  const int line = tid % S::LINES;
+  const int slot = tid / S::LINES;
+  double* scr = scratch + slot * S::SCR;
+  const int jl = line % NQ, ll = line / NQ;   // x-line owned in the point phase
+
+  for (int e0 = 0; e0 < S::NEL; e0 += S::EB) {
+    const int el = e0 + slot;
+    const int exl = el % S::BX, eyl = (el / S::BX) % S::BY, ezl = el / (S::BX * S::BY);
+    const bool valid = (el < S::NEL) && exl < bxr && eyl < byr && ezl < bzr;
+    const int X0 = valid ? K * exl : 0, Y0 = valid ? K * eyl : 0, Z0 = valid ? K * ezl : 0;
+    const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + ezl));
+
+    double fu[4][NQ];
+    forward_field<ND, NQ, S::LXF, S::LYF>(T, box0, scr, line, X0, Y0, Z0, fu);
+    double fv[4][NQ];
+    if constexpr (S::NIN == 2) forward_field<ND, NQ, S::LXF, S::LYF>(T, box1, scr, line, X0, Y0, Z0, fv);
+
+    // ---- 3. pointwise D on the x-line (i, jl, ll)
+    double F0[4][NQ];   // first output channel set (r for RES, Jv for JVP/JVPRES)
+    double F1[4][NQ];   // second (r for JVPRES)
+    double gpart = 0.0;
+    const double wjl = T.w[jl] * T.w[ll];
+    double rho_e = 0.0;
+    if constexpr (MODEL == HEAT) rho_e = valid ? __ldg(P.rho + eg) : 1.0;
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      const double wq = T.w[i] * wjl;
+      Metric M;
+      double W;
+      if constexpr (AFFINE) {
+        M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
+        W = wq * P.vol;
+      } else {
+        constexpr int NQ3 = NQ * NQ * NQ;
+        const double* gm = P.geom + (valid ? eg : 0) * (6 * NQ3) + (i + NQ * line);
+        M = {__ldg(gm), __ldg(gm + NQ3), __ldg(gm + 2 * NQ3), __ldg(gm + 3 * NQ3), __ldg(gm + 4 * NQ3),
+             __ldg(gm + 5 * NQ3)};
+        const double det = M.xx * (M.yy * M.zz - M.yz * M.yz) - M.xy * (M.xy * M.zz - M.yz * M.xz) +
+                           M.xz * (M.xy * M.yz - M.yy * M.xz);
+        W = det / (wq * wq);
+      }
+      if constexpr (MODE == MODE_RES) {
+        const double gh[3] = {fu[1][i], fu[2][i], fu[3][i]};
+        double Fh[3];
+        flux_hat<MODEL>(fu[0][i], gh, M, W, rho_e, P, Fh);
+        F0[0][i] = Fh[0];
+        F0[1][i] = Fh[1];
+        F0[2][i] = Fh[2];
+        F0[3][i] = -P.f * W;
+      } else if constexpr (MODE == MODE_JVP || MODE == MODE_JVPRES) {
+        using D = dual<double>;
+        const D ud(fu[0][i], fv[0][i]);
+        const D gh[3] = {D(fu[1][i], fv[1][i]), D(fu[2][i], fv[2][i]), D(fu[3][i], fv[3][i])};
+        D Fh[3];
+        flux_hat<MODEL>(ud, gh, M, W, rho_e, P, Fh);
+        F0[0][i] = Fh[0].d;
+        F0[1][i] = Fh[1].d;
+        F0[2][i] = Fh[2].d;
+        F0[3][i] = 0.0;
+        if constexpr (MODE == MODE_JVPRES) {
+          F1[0][i] = Fh[0].v;
+          F1[1][i] = Fh[1].v;
+          F1[2][i] = Fh[2].v;
+          F1[3][i] = -P.f * W;
+        }
+      } else {   // MODE_DESIGN: seed d/drho
+        using D = dual<double>;
+        const D ud(fu[0][i]);
+        const D gh[3] = {D(fu[1][i]), D(fu[2][i]), D(fu[3][i])};
+        const D rd(rho_e, 1.0);
+        D Fh[3];
+        flux_hat<MODEL>(ud, gh, M, W, rd, P, Fh);
+        gpart -= fv[1][i] * Fh[0].d + fv[2][i] * Fh[1].d + fv[3][i] * Fh[2].d;
+      }
+    }
+
+    if constexpr (MODE == MODE_DESIGN) {
+      scr[line] = gpart;
+      __syncthreads();
+      if (line == 0 && valid) {
+        double s = 0.0;
+        for (int t = 0; t < S::LINES; ++t) s += scr[t];
+        gout[eg] = s;
+      }
+      __syncthreads();
+    } else {
+      // ---- 4. B^T into the E-buffer
+      const int elc = el < S::NEL ? el : 0;
+      backward_field<ND, NQ, MODE == MODE_RES>(T, scr, line, F0, ebuf + elc * S::ND3, valid);
+      if constexpr (MODE == MODE_JVPRES)
+        backward_field<ND, NQ, true>(T, scr, line, F1, ebuf + (S::NEL + elc) * S::ND3, valid);
+    }
+  }
+
+  if constexpr (S::NOUT > 0) {
+    __syncthreads();
+    // ---- 5. G^T: box points sum their element contributions in a fixed order
+    double* shell_base0 = shell0 + (int64_t)brick * P.shell_stride;
+    double* shell_base1 = (S::NOUT == 2) ? shell1 + (int64_t)brick * P.shell_stride : nullptr;
+    const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx;
+    const bool lowY = ey0 > 0, highY = ey0 + byr < P.ny;
+    const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
+    for (int idx = tid; idx < LX * LY * LZ; idx += S::NT) {
+      const int X = idx % LX, Y = (idx / LX) % LY, Z = idx / (LX * LY);
+      // candidate elements per axis, ascending
+      int exs[2], eys[2], ezs[2], nxc = 0, nyc = 0, nzc = 0;
+      if (X % K == 0 && X > 0) exs[nxc++] = X / K - 1;
+      if (X / K < bxr) exs[nxc++] = X / K;
+      if (Y % K == 0 && Y > 0) eys[nyc++] = Y / K - 1;
+      if (Y / K < byr) eys[nyc++] = Y / K;
+      if (Z % K == 0 && Z > 0) ezs[nzc++] = Z / K - 1;
+      if (Z / K < bzr) ezs[nzc++] = Z / K;
+#pragma unroll
+      for (int o = 0; o < S::NOUT; ++o) {
+        const double* eb = ebuf + o * S::NEL * S::ND3;
+        double s = 0.0;
+        for (int cz = 0; cz < nzc; ++cz)
+          for (int cy = 0; cy < nyc; ++cy)
+            for (int cx = 0; cx < nxc; ++cx) {
+              const int e = exs[cx] + S::BX * (eys[cy] + S::BY * ezs[cz]);
+              const int a = X - K * exs[cx], b = Y - K * eys[cy], c = Z - K * ezs[cz];
+              s += eb[e * S::ND3 + a + ND * (b + ND * c)];
+            }
+        const bool shared = (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) ||
+                            (Y == LY - 1 && highY) || (Z == 0 && lowZ) || (Z == LZ - 1 && highZ);
+        if (shared) {
+          (o == 0 ? shell_base0 : shell_base1)[shell_rank(X, Y, Z, LX, LY, LZ)] = s;
+        } else {
+          const int gx = gX0 + X, gy = gY0 + Y, gz = gZ0 + Z;
+          const int64_t gidx = (int64_t)gx + (int64_t)P.Mx * (gy + (int64_t)P.My * gz);
+          if (is_dirichlet(gx, gy, gz, P.Mx, P.My, P.Mz, P.faces)) s = 0.0;
+          (o == 0 ? out0 : out1)[gidx] = s;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace feod

@@ -1,0 +1,42 @@
+// Pointwise operator D at one quadrature point, written once as a template over
+// the number type T (double for the residual, dual<double> for the JVP and the
+// design derivative) — AD confined to D (Eq. 2 at :160).
+//
+// Metric form: all three fluxes are kappa * grad u, so
+// with the symmetric metric M = w detJ J^{-1} J^{-T} and the reference gradient
+// gh, the test-side quantity is  Fh = W J^{-1} D = kappa * M gh  and
+// |grad u|^2 = gh . M gh / W,  W = w detJ.
+//   PLAPLACE: kappa = (eps^2 + |grad u|^2)^((p-2)/2)
+//   NLDIFF:   kappa = 1 + u^2                                  (BASELINE configs[2])
+//   HEAT:     kappa = rho^3 (1 + u^2)                          (BASELINE configs[4])
+#pragma once
+#include "common.cuh"
+#include "dual.cuh"
+
+namespace feod {
+
+struct Metric { double xx, yy, zz, xy, xz, yz; };
+
+template <int MODEL, class T, class R>
+FEOD_DEV void flux_hat(const T& u, const T gh[3], const Metric& M, double W, const R& rho,
+                       const OpParams& P, T Fh[3]) {
+  T a[3];
+  a[0] = gh[0] * M.xx + gh[1] * M.xy + gh[2] * M.xz;
+  a[1] = gh[0] * M.xy + gh[1] * M.yy + gh[2] * M.yz;
+  a[2] = gh[0] * M.xz + gh[1] * M.yz + gh[2] * M.zz;
+  T kappa;
+  if constexpr (MODEL == PLAPLACE) {
+    T s = (gh[0] * a[0] + gh[1] * a[1] + gh[2] * a[2]) * (1.0 / W) + P.eps2;
+    kappa = pow_special(s, P.half_pm2);
+  } else if constexpr (MODEL == NLDIFF) {
+    kappa = u * u + 1.0;
+  } else {
+    auto r3 = rho * rho * rho;
+    kappa = r3 * (u * u + 1.0);
+  }
+  Fh[0] = kappa * a[0];
+  Fh[1] = kappa * a[1];
+  Fh[2] = kappa * a[2];
+}
+
+}  // namespace feod
