@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the FEOD hot path on B200 (one JSON line on rank 0).
+
+Workload (default C3 = BASELINE.json configs[2], the binding 60 % roofline
+target of SURVEY.md §8(d)): nonlinear diffusion div((1+u^2) grad u) = 1 on a
+64^3 perturbed hex mesh, Q3, 4^3 Gauss points, 7,189,057 DOFs, fp64.
+
+A "step" = one pass of the hot path over the workload: r = F(u) (Eq. 1) and
+Jv = J(u) v (Eq. 2), i.e. feod_residual + feod_jvp. value = DOF applications
+per second over all ranks: 2 N x ranks / step time, in GDOF/s.
+
+Timing: W untimed warm-up steps, then K steps bracketed by a barrier and
+cuda.synchronize, CUDA events on the launching stream, max over ranks. The
+working set (805 MB metric stream + 115 MB of vectors) exceeds the 126 MB L2,
+so no flush is inserted. e2e: the same step through the C-ABI host-buffer
+entry point feod_apply_host (pinned host memory, H2D + D2H inside the region).
+roofline: the fused JVP kernel (dominant launch), algorithmic bytes per launch
+(8 B per DOF per vector read/written + 48 B per quadrature
+point of stored metric) / its event-timed duration, vs the measured HBM copy
+bandwidth in MEASURED_PEAKS.json. cpu_baseline: the CPU oracle (oracle/), as it
+stands, on a bounded element sample of the same workload on this host.
+
+--impl reference: there is no reference implementation to install (the paper
+ships no code); per the task's tier rules the reference arm is the oracle,
+timed on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+HBM_FALLBACK_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+FP64_MEASURED_TFLOPS = 33.0  # profiles/r01_peaks_fp64.json (tools/fp64_peak.cu on a B200)
+
+
+def algorithmic_bytes(w, call):
+    """8 B per DOF per vector touched, 48 B/point metric, 8 B/elem rho and g."""
+    N, E, q3 = w.n_dofs, w.n_elems, w.q ** 3
+    geom = 48 * q3 * E if w.perturbed else 0
+    vec = {"residual": 2, "jvp": 3, "jvp_res": 4, "design": 2}[call]
+    extra = 0
+    if w.model == W.HEAT:
+        extra += 8 * E
+    if call == "design":
+        extra += 8 * E
+    return 8 * N * vec + geom + extra
+
+
+def algorithmic_flops(w, call):
+    """2 x passes x E x (q(k+1)^3 + q^2(k+1)^2 + q^3(k+1) + 3 q^4) + pointwise x E q^3."""
+    k, q, E = w.k, w.q, w.n_elems
+    per_pass = q * (k + 1) ** 3 + q ** 2 * (k + 1) ** 2 + q ** 3 * (k + 1) + 3 * q ** 4
+    passes = {"residual": 2, "jvp": 3, "jvp_res": 3, "design": 2}[call]
+    table = {  # pointwise flops per point (perturbed / affine) from SURVEY.md §8(d)
+        (W.PLAPLACE, True): {"residual": 45, "jvp": 76}, (W.NLDIFF, True): {"residual": 38, "jvp": 43},
+        (W.PLAPLACE, False): {"residual": 16, "jvp": 35}, (W.HEAT, False): {"residual": 12, "jvp": 19, "design": 14},
+        (W.NLDIFF, False): {"residual": 12, "jvp": 19},
+    }
+    pw = table.get((w.model, w.perturbed), {}).get(call, 20)
+    return 2 * passes * E * per_pass + pw * E * q ** 3
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_from_profiles(workload_name):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload_name)
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v == "Active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def _oracle_step(pr, d, el):
+    from oracle import fem as F
+    t0 = time.perf_counter()
+    F._assemble(pr, F._residual_elems(pr, d["u"], el), pr.n_dofs)
+    F._assemble(pr, F._jvp_elems(pr, d["u"], d["v"], el), pr.n_dofs)
+    return time.perf_counter() - t0
+
+
+def oracle_sample_size(pr, d, E, target_s):
+    """Elements per sample so one oracle residual+JVP takes about target_s seconds."""
+    S = 64
+    while True:
+        t = _oracle_step(pr, d, np.arange(min(S, E)))
+        if t > target_s / 4 or S >= E:
+            return min(E, max(1, int(S * target_s / max(t, 1e-3))))
+        S = min(E, S * 4)
+
+
+def cpu_oracle_sample(w, d, target_s=15.0, S=None):
+    """Oracle residual + JVP on a bounded element sample of w; returns GDOF/s, cores, sample, seconds."""
+    import oracle as O
+    pr = O.Problem.from_workload(w, verts=d["verts"], rho=d.get("rho"))
+    cores = len(os.sched_getaffinity(0))
+    E = w.n_elems
+    if S is None:
+        S = oracle_sample_size(pr, d, E, target_s)
+    el = np.arange(S)
+    t = _oracle_step(pr, d, el)
+    frac = S / E
+    value = 2 * w.n_dofs * frac / t / 1e9
+    sample = (f"oracle residual+JVP (dense element matrices, numpy fp64) on the first {S} of {E} elements "
+              f"of {w.name} ({100 * frac:.3f} %), {t:.2f} s, throughput scaled by the element fraction")
+    return value, cores, sample, t
+
+
+def run_reference(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    d = W.draw(w)
+    import oracle as O
+    pr = O.Problem.from_workload(w, verts=d["verts"], rho=d.get("rho"))
+    per_step = min(20.0, 150.0 / max(1, args.steps + args.warmup))
+    S = oracle_sample_size(pr, d, w.n_elems, per_step)
+    vals = []
+    for s in range(args.warmup + args.steps):
+        v, cores, sample, t = cpu_oracle_sample(w, d, S=S)
+        if s >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": "residual+JVP throughput (GDOF/s, fp64)", "value": value,
+            "unit": "GDOF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 2 * w.n_dofs / (value * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_of(w),
+            "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def max_over_ranks(x, world, device=None):
+    """Max of a per-rank float over all ranks (the timing rule: max over ranks)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(units_per_rank, world, seconds):
+    """value = units all ranks processed / the max-over-ranks time (weak scaling replicas)."""
+    return units_per_rank * world / seconds
+
+
+def config_of(w):
+    return {"workload": f"{w.name}: {W.MODEL_NAMES[w.model]}, {w.n}^3 {'perturbed' if w.perturbed else 'affine'} "
+                        f"hexes, Q{w.k}, {w.q}^3 Gauss points (BASELINE.json configs[{int(w.name[1]) - 1}])",
+            "n": w.n, "k": w.k, "q": w.q, "dofs": w.n_dofs, "elems": w.n_elems,
+            "step": "feod_residual + feod_jvp (2 DOF applications per DOF)",
+            "l2": "no flush: working set (stored metric + vectors) exceeds the 126 MB L2" if w.perturbed
+                  else "no flush: vectors (>=115 MB) + scratch exceed L2 only partially"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="feod", choices=["feod", "reference"])
+    ap.add_argument("--workload", default="C3", choices=list(W.CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    w = W.CONFIGS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2506_00746_b200 as fe
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    d = W.draw(w)
+    rho = torch.as_tensor(d["rho"]).cuda() if "rho" in d else None
+    op = fe.from_workload(w, verts=d["verts"], rho=rho)
+    u = torch.as_tensor(d["u"]).cuda()
+    v = torch.as_tensor(d["v"]).cuda()
+    r = torch.empty_like(u)
+    Jv = torch.empty_like(u)
+    N = op.n_dofs
+    stream = torch.cuda.current_stream()
+
+    def step(prof=None):
+        op.residual(u, out=r)
+        if prof is not None:
+            op.profile_next(*prof)
+        op.jvp(u, v, out=Jv)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in ev:   # torch creates the CUDA event lazily: record once so the handle exists
+        a.record(stream)
+        b.record(stream)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for s in range(args.steps):
+        step(prof=ev[s])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    jvp_kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    ms = max_over_ranks(ms, world, device="cuda")
+    ms_per_step = ms / args.steps
+    value = whole_job_rate(2 * N, world, ms_per_step * 1e-3) / 1e9
+
+    # per-call breakdown (rank-local, diagnostics)
+    def time_call(fn, reps=10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+    t_res = time_call(lambda: op.residual(u, out=r))
+    t_jvp = time_call(lambda: op.jvp(u, v, out=Jv))
+
+    # e2e through the C-ABI host-buffer path
+    e2e = None
+    if not args.no_e2e:
+        uh = torch.as_tensor(d["u"]).pin_memory()
+        vh = torch.as_tensor(d["v"]).pin_memory()
+        rh = torch.empty(N, dtype=torch.float64).pin_memory()
+        jh = torch.empty(N, dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            op.apply_host(0, uh, out=rh)
+            op.apply_host(1, uh, vh, out=jh)
+        reps = max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        ts = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            op.apply_host(0, uh, out=rh)
+            op.apply_host(1, uh, vh, out=jh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / reps
+        e_ms = max_over_ranks(e_ms, world, device="cuda")
+        e2e = {"value": whole_job_rate(2 * N, world, e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
+               "h2d_bytes_per_step": 3 * 8 * N, "d2h_bytes_per_step": 2 * 8 * N,
+               "ms_per_step": e_ms, "path": "feod_apply_host (C-ABI, pinned host buffers)"}
+
+    peak, peak_src = read_peaks()
+    jvp_bytes = algorithmic_bytes(w, "jvp")
+    achieved = jvp_bytes / (jvp_kernel_ms * 1e-3) / 1e9
+    traffic = traffic_from_profiles(w.name)
+    roofline = {"bound": "hbm" if w.perturbed else "alu", "kernel": f"op_kernel<JVP> (fused G-B-D-B^T-G^T, {w.name})",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": jvp_bytes, "kernel_ms": jvp_kernel_ms}
+    if not w.perturbed:
+        fl = algorithmic_flops(w, "jvp")
+        ach = fl / (jvp_kernel_ms * 1e-3) / 1e12
+        roofline.update({"achieved": ach, "peak": FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
+                         "frac": ach / FP64_MEASURED_TFLOPS,
+                         "peak_source": "measured DFMA rate, profiles/r01_peaks_fp64.json"})
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        val, cores, sample, _ = cpu_oracle_sample(w, d)
+        cpu = {"value": val, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    fl_res, fl_jvp = algorithmic_flops(w, "residual"), algorithmic_flops(w, "jvp")
+    by_res, by_jvp = algorithmic_bytes(w, "residual"), algorithmic_bytes(w, "jvp")
+    line = {"metric": "residual+JVP throughput (GDOF/s, fp64)", "value": value, "unit": "GDOF/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded workloads/ recipe, SURVEY.md §8(d))", "config": config_of(w),
+            "parallelism": f"replicas x{world} (no data-path collective; DESIGN.md §Multi-GPU)",
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
+            "gpu_launches": args.steps * 4 if (op.n_elems > 1) else args.steps * 2,
+            "calls": {
+                "residual": {"us": t_res * 1e3, "gdof_s": N / (t_res * 1e-3) / 1e9,
+                             "hbm_frac": by_res / (t_res * 1e-3) / 1e9 / peak,
+                             "fp64_frac": fl_res / (t_res * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS},
+                "jvp": {"us": t_jvp * 1e3, "gdof_s": N / (t_jvp * 1e-3) / 1e9,
+                        "hbm_frac": by_jvp / (t_jvp * 1e-3) / 1e9 / peak,
+                        "fp64_frac": fl_jvp / (t_jvp * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS,
+                        "fused_kernel_us": jvp_kernel_ms * 1e3},
+            }}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

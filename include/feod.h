@@ -143,6 +143,12 @@ FEOD_API int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg_i
  * result: DEVICE pointer to one double.                                      */
 FEOD_API int feod_dot(feod_handle h, const double* x, const double* y, int64_t n, double* result);
 
+/* Profiling hook (bench.py roofline): the NEXT operator call on this handle
+ * records cudaEvent_t ev_begin on the handle's stream right before its fused
+ * operator kernel and ev_end right after it (before the scatter fix-up), so
+ * that kernel's duration can be timed live. One-shot; NULLs clear it. */
+FEOD_API int feod_profile_next(feod_handle h, void* ev_begin, void* ev_end);
+
 FEOD_API const char* feod_last_error(void);
 FEOD_API const char* feod_version(void);
 

@@ -29,7 +29,7 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 # every symbol include/feod.h declares (checked by tests/test_abi.py)
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
-           "feod_dot", "feod_last_error", "feod_version")
+           "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
 class FeodError(RuntimeError):
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH):
     lib.feod_apply_host.argtypes = [vp, ctypes.c_int, dp, dp, dp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_dot.argtypes = [vp, dp, dp, i64, dp]
+    lib.feod_profile_next.argtypes = [vp, vp, vp]
     lib.feod_last_error.restype = ctypes.c_char_p
     lib.feod_version.restype = ctypes.c_char_p
     _lib = lib
@@ -200,6 +201,11 @@ class Operator:
         self._sync_stream()
         _check(self.lib.feod_newton_cg(self.h, u.data_ptr(), int(newton_steps), int(cg_iters), norms))
         return u, list(norms)
+
+    def profile_next(self, ev_begin, ev_end):
+        """Time the fused kernel of the next call with two torch.cuda.Event(enable_timing=True)."""
+        _check(self.lib.feod_profile_next(self.h, ctypes.c_void_p(ev_begin.cuda_event),
+                                          ctypes.c_void_p(ev_end.cuda_event)))
 
     def dot(self, x, y):
         x, y = self._dev(x, x.numel(), "x"), self._dev(y, y.numel(), "y")

@@ -28,6 +28,7 @@ struct feod_op {
   double* red = nullptr;       // kRedBlocks partials + 8 scalars
   int* flag = nullptr;
   double* work = nullptr;      // Newton-CG: F, r, p, Ap, d (5 N)
+  cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
 };
 
 static thread_local std::string g_err;
@@ -175,13 +176,24 @@ extern "C" int feod_set_rho(feod_handle h, const double* rho) {
   return FEOD_OK;
 }
 
+extern "C" int feod_profile_next(feod_handle h, void* ev_begin, void* ev_end) {
+  if (!h) return fail(FEOD_EINVAL, "feod_profile_next: null handle");
+  h->prof_begin = (cudaEvent_t)ev_begin;
+  h->prof_end = (cudaEvent_t)ev_end;
+  return FEOD_OK;
+}
+
 extern "C" int64_t feod_num_dofs(feod_handle h) { return h ? h->N : -1; }
 extern "C" int64_t feod_num_elems(feod_handle h) { return h ? h->E : -1; }
 
 static int run_op(feod_handle h, int mode, const double* in0, const double* in1, double* out0, double* out1,
                   double* gout, const char* name) {
   OpPtrs p{in0, in1, out0, out1, h->shell, h->shell + (size_t)h->nbricks * h->P.shell_stride, gout};
+  cudaEvent_t pb = h->prof_begin, pe = h->prof_end;
+  h->prof_begin = h->prof_end = nullptr;
+  if (pb) cudaEventRecord(pb, h->st);
   cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, h->geom == nullptr, h->nbricks, h->P, h->T, p, h->st);
+  if (pe) cudaEventRecord(pe, h->st);
   if (e != cudaSuccess) return cuda_fail(e, name);
   if (mode != MODE_DESIGN) {
     e = launch_fixup(h->P, h->k, h->bi.BX, h->bi.BY, h->bi.BZ, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,

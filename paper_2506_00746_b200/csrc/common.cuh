@@ -69,7 +69,7 @@ FEOD_HD int shell_size(int LX, int LY, int LZ) {
 template <int ND> struct BrickShape;
 template <> struct BrickShape<2> { static constexpr int BX = 8, BY = 8, BZ = 4, EB = 32; };
 template <> struct BrickShape<3> { static constexpr int BX = 4, BY = 4, BZ = 4, EB = 16; };
-template <> struct BrickShape<4> { static constexpr int BX = 4, BY = 4, BZ = 4, EB = 8; };
+template <> struct BrickShape<4> { static constexpr int BX = 4, BY = 4, BZ = 2, EB = 8; };
 template <> struct BrickShape<5> { static constexpr int BX = 2, BY = 2, BZ = 4, EB = 8; };
 template <> struct BrickShape<6> { static constexpr int BX = 2, BY = 2, BZ = 2, EB = 4; };
 template <> struct BrickShape<7> { static constexpr int BX = 2, BY = 2, BZ = 2, EB = 4; };

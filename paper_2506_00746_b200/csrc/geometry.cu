@@ -3,7 +3,8 @@
 // of the trilinear map of each hexahedron (the linear,
 // solution-independent part of B that PAPER.md:25 keeps "excluded from the
 // differentiation loop"). One thread per (element, point); output layout
-// [E][6][q^3] with components xx yy zz xy xz yz and points x-fastest.
+// [E][6][q^3] with components xx yy zz xy xz yz and points ordered (j, l, i),
+// j fastest and i slowest (the operator kernel's x-line ownership).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -55,7 +56,9 @@ __global__ void geometry_kernel(const double* __restrict__ verts, int nx, int ny
     const double det = J[0][0] * A[0][0] + J[0][1] * A[1][0] + J[0][2] * A[2][0];
     if (!(det > 0.0)) atomicExch(bad, 1);
     const double s = T.w[i] * T.w[j] * T.w[l] / det;
-    double* g = geom + e * 6 * nq3 + p;
+    // stored point order: x-line (j, l) fastest, i slowest, so the threads owning
+    // the x-lines of one element read 16 consecutive doubles per (component, i)
+    double* g = geom + e * 6 * nq3 + (j + nq * l) + nq * nq * i;
     auto dot = [&](int r, int c) { return A[r][0] * A[c][0] + A[r][1] * A[c][1] + A[r][2] * A[c][2]; };
     g[0 * nq3] = s * dot(0, 0);
     g[1 * nq3] = s * dot(1, 1);

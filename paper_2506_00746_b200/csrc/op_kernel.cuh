@@ -25,6 +25,36 @@
 
 namespace feod {
 
+// Shared-memory scratch layouts of the line-ownership transposes, padded so
+// that both the producing and the consuming half-warp hit 16 distinct 8-byte
+// bank pairs (for NQ = 4 the outer stride is 20 = 4 mod 16).
+constexpr int pad_stride(int x, int nq) {
+  if (nq == 4) return x + ((4 - x % 16) + 16) % 16;
+  return (x % 2 == 0) ? x + 1 : x;
+}
+
+template <int ND, int NQ>
+struct Lay {
+  // S: Z-step output, written by (a,b) for each l, read by (a,l) for each b
+  static constexpr int SL = pad_stride(ND * ND, NQ);
+  static constexpr int SN = SL * NQ;
+  FEOD_HD static constexpr int S(int a, int b, int l) { return a + ND * b + SL * l; }
+  // T: Y-step output, written by (a,l) for each j, read by (j,l) for each a
+  static constexpr int TJ = pad_stride(NQ * ND, NQ);
+  static constexpr int TN = TJ * NQ;
+  FEOD_HD static constexpr int T(int a, int j, int l) { return l + NQ * a + TJ * j; }
+  // P: X^T output, written by (j,l) for each a, read by (a,l) for each j
+  static constexpr int PA = pad_stride(NQ * NQ, NQ);
+  static constexpr int PN = PA * ND;
+  FEOD_HD static constexpr int Pi(int a, int j, int l) { return l + NQ * j + PA * a; }
+  // Q: Y^T output, written by (a,l) for each b, read by (a,b) for each l
+  static constexpr int QB = pad_stride(ND * NQ, NQ);
+  static constexpr int QN = QB * ND;
+  FEOD_HD static constexpr int Qi(int a, int b, int l) { return a + ND * l + QB * b; }
+  static constexpr int mx(int x, int y) { return x > y ? x : y; }
+  static constexpr int SCR = mx(mx(2 * SN, 3 * TN), mx(mx(3 * PN, 2 * QN), NQ * NQ));
+};
+
 template <int ND, int NQ, int MODE>
 struct OpShape {
   using S = BrickShape<ND>;
@@ -36,8 +66,7 @@ struct OpShape {
   static constexpr int LINES = NQ * NQ;
   static constexpr int NT = LINES * EB;
   static constexpr int ND3 = ND * ND * ND;
-  static constexpr int SCR_A = 2 * ND * ND * NQ, SCR_B = 3 * ND * NQ * NQ;
-  static constexpr int SCR = (SCR_A > SCR_B ? SCR_A : SCR_B) > LINES ? (SCR_A > SCR_B ? SCR_A : SCR_B) : LINES;
+  static constexpr int SCR = Lay<ND, NQ>::SCR;
   static constexpr int NIN = (MODE == MODE_RES) ? 1 : 2;
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
   static constexpr int SMEM_DOUBLES = NIN * BOX + NOUT * NEL * ND3 + EB * SCR;
@@ -45,17 +74,42 @@ struct OpShape {
   static constexpr int SHELL = LXF * LYF * LZF - (LXF - 2) * (LYF - 2) * (LZF - 2);
 };
 
+// Non-coherent global load that the compiler may not sink toward its use: the
+// metric stream is requested before the forward contractions so its HBM
+// latency overlaps them.
+FEOD_DEV double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// Hint the L2 to start fetching a contiguous byte range (TMA prefetch; no
+// completion tracking, no shared memory).
+FEOD_DEV void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Barrier among the threads of one element: the element's scratch is private
+// to its NQ*NQ threads, so when they sit inside one warp a warp barrier is
+// enough and warps run the contraction phases independently of each other.
+template <int LINES>
+FEOD_DEV void elem_sync() {
+  if constexpr (32 % LINES == 0) __syncwarp();
+  else __syncthreads();
+}
+
 // Forward interpolation of one field from the smem box: returns, for the
 // x-line (j, l) this thread owns, U[i], dU/dxi1[i], dU/dxi2[i], dU/dxi3[i].
 template <int ND, int NQ, int LXF, int LYF>
 FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, double* scr, int line,
                             int X0, int Y0, int Z0, double (&out)[4][NQ]) {
-  constexpr int SA = ND * ND * NQ;   // S0 | S1
-  constexpr int SB = ND * NQ * NQ;   // T0 | T1 | T2
+  using L = Lay<ND, NQ>;
+  constexpr int SA = L::SN;   // S0 | S1
+  constexpr int SB = L::TN;   // T0 | T1 | T2
   // ---- z: nodes c -> points l, values (t0) and z-derivative (t1)
   {
     const int a = line % NQ, b = line / NQ;
-    if (a < ND && b < ND) {
+    if ((ND == NQ) || (a < ND && b < ND)) {
       double x[ND];
 #pragma unroll
       for (int c = 0; c < ND; ++c) x[c] = box[(X0 + a) + LXF * ((Y0 + b) + LYF * (Z0 + c))];
@@ -67,25 +121,25 @@ FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, dou
           t0 = fma(T.B[l][c], x[c], t0);
           t1 = fma(T.G[l][c], x[c], t1);
         }
-        scr[a + ND * (b + ND * l)] = t0;
-        scr[SA + a + ND * (b + ND * l)] = t1;
+        scr[L::S(a, b, l)] = t0;
+        scr[SA + L::S(a, b, l)] = t1;
       }
     }
   }
-  __syncthreads();
+  elem_sync<NQ * NQ>();
   // ---- y: nodes b -> points j
   {
     const int a = line % NQ, l = line / NQ;
     double s0[ND], s1[ND];
-    if (a < ND) {
+    if ((ND == NQ) || a < ND) {
 #pragma unroll
       for (int b = 0; b < ND; ++b) {
-        s0[b] = scr[a + ND * (b + ND * l)];
-        s1[b] = scr[SA + a + ND * (b + ND * l)];
+        s0[b] = scr[L::S(a, b, l)];
+        s1[b] = scr[SA + L::S(a, b, l)];
       }
     }
-    __syncthreads();
-    if (a < ND) {
+    elem_sync<NQ * NQ>();
+    if ((ND == NQ) || a < ND) {
 #pragma unroll
       for (int j = 0; j < NQ; ++j) {
         double y0 = 0.0, y1 = 0.0, y2 = 0.0;
@@ -95,22 +149,22 @@ FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, dou
           y1 = fma(T.G[j][b], s0[b], y1);
           y2 = fma(T.B[j][b], s1[b], y2);
         }
-        scr[a + ND * (j + NQ * l)] = y0;
-        scr[SB + a + ND * (j + NQ * l)] = y1;
-        scr[2 * SB + a + ND * (j + NQ * l)] = y2;
+        scr[L::T(a, j, l)] = y0;
+        scr[SB + L::T(a, j, l)] = y1;
+        scr[2 * SB + L::T(a, j, l)] = y2;
       }
     }
   }
-  __syncthreads();
+  elem_sync<NQ * NQ>();
   // ---- x: nodes a -> points i
   {
     const int j = line % NQ, l = line / NQ;
     double r0[ND], r1[ND], r2[ND];
 #pragma unroll
     for (int a = 0; a < ND; ++a) {
-      r0[a] = scr[a + ND * (j + NQ * l)];
-      r1[a] = scr[SB + a + ND * (j + NQ * l)];
-      r2[a] = scr[2 * SB + a + ND * (j + NQ * l)];
+      r0[a] = scr[L::T(a, j, l)];
+      r1[a] = scr[SB + L::T(a, j, l)];
+      r2[a] = scr[2 * SB + L::T(a, j, l)];
     }
 #pragma unroll
     for (int i = 0; i < NQ; ++i) {
@@ -128,7 +182,7 @@ FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, dou
       out[3][i] = gz;
     }
   }
-  __syncthreads();
+  elem_sync<NQ * NQ>();
 }
 
 // Transposed interpolation: from the x-line of point values (Fx, Fy, Fz and
@@ -137,8 +191,9 @@ FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, dou
 template <int ND, int NQ, bool HASV>
 FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const double (&F)[4][NQ], double* re,
                              bool write) {
-  constexpr int SA = ND * ND * NQ;
-  constexpr int SB = ND * NQ * NQ;
+  using L = Lay<ND, NQ>;
+  constexpr int SA = L::QN;   // Q0 | Q1
+  constexpr int SB = L::PN;   // P0 | P1 | P2
   // ---- x^T: points i -> nodes a
   {
     const int j = line % NQ, l = line / NQ;
@@ -152,26 +207,26 @@ FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const doubl
         p1 = fma(T.B[i][a], F[1][i], p1);
         p2 = fma(T.B[i][a], F[2][i], p2);
       }
-      scr[a + ND * (j + NQ * l)] = p0;
-      scr[SB + a + ND * (j + NQ * l)] = p1;
-      scr[2 * SB + a + ND * (j + NQ * l)] = p2;
+      scr[L::Pi(a, j, l)] = p0;
+      scr[SB + L::Pi(a, j, l)] = p1;
+      scr[2 * SB + L::Pi(a, j, l)] = p2;
     }
   }
-  __syncthreads();
+  elem_sync<NQ * NQ>();
   // ---- y^T: points j -> nodes b
   {
     const int a = line % NQ, l = line / NQ;
     double p0[NQ], p1[NQ], p2[NQ];
-    if (a < ND) {
+    if ((ND == NQ) || a < ND) {
 #pragma unroll
       for (int j = 0; j < NQ; ++j) {
-        p0[j] = scr[a + ND * (j + NQ * l)];
-        p1[j] = scr[SB + a + ND * (j + NQ * l)];
-        p2[j] = scr[2 * SB + a + ND * (j + NQ * l)];
+        p0[j] = scr[L::Pi(a, j, l)];
+        p1[j] = scr[SB + L::Pi(a, j, l)];
+        p2[j] = scr[2 * SB + L::Pi(a, j, l)];
       }
     }
-    __syncthreads();
-    if (a < ND) {
+    elem_sync<NQ * NQ>();
+    if ((ND == NQ) || a < ND) {
 #pragma unroll
       for (int b = 0; b < ND; ++b) {
         double q0 = 0.0, q1 = 0.0;
@@ -181,21 +236,21 @@ FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const doubl
           q0 = fma(T.G[j][b], p1[j], q0);
           q1 = fma(T.B[j][b], p2[j], q1);
         }
-        scr[a + ND * (b + ND * l)] = q0;
-        scr[SA + a + ND * (b + ND * l)] = q1;
+        scr[L::Qi(a, b, l)] = q0;
+        scr[SA + L::Qi(a, b, l)] = q1;
       }
     }
   }
-  __syncthreads();
+  elem_sync<NQ * NQ>();
   // ---- z^T: points l -> nodes c
   {
     const int a = line % NQ, b = line / NQ;
-    if (a < ND && b < ND) {
+    if ((ND == NQ) || (a < ND && b < ND)) {
       double q0[NQ], q1[NQ];
 #pragma unroll
       for (int l = 0; l < NQ; ++l) {
-        q0[l] = scr[a + ND * (b + ND * l)];
-        q1[l] = scr[SA + a + ND * (b + ND * l)];
+        q0[l] = scr[L::Qi(a, b, l)];
+        q1[l] = scr[SA + L::Qi(a, b, l)];
       }
       if (write) {
 #pragma unroll
@@ -211,7 +266,7 @@ FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const doubl
       }
     }
   }
-  __syncthreads();
+  elem_sync<NQ * NQ>();
 }
 
 template <int ND, int NQ, int MODE, int MODEL, bool AFFINE>
@@ -236,10 +291,12 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
   const int gX0 = K * ex0, gY0 = K * ey0, gZ0 = K * ez0;
 
   // ---- 1. stage the DOF boxes (G, gather)
-  for (int idx = tid; idx < LX * LY * LZ; idx += S::NT) {
-    const int X = idx % LX, Y = (idx / LX) % LY, Z = idx / (LX * LY);
+  // (the box is walked with its compile-time full-brick shape: cheap index
+  //  arithmetic; points beyond a ragged brick's extent are skipped)
+  for (int sidx = tid; sidx < S::BOX; sidx += S::NT) {
+    const int X = sidx % S::LXF, Y = (sidx / S::LXF) % S::LYF, Z = sidx / (S::LXF * S::LYF);
+    if (X >= LX || Y >= LY || Z >= LZ) continue;
     const int64_t gidx = (int64_t)(gX0 + X) + (int64_t)P.Mx * ((gY0 + Y) + (int64_t)P.My * (gZ0 + Z));
-    const int sidx = X + S::LXF * (Y + S::LYF * Z);
     box0[sidx] = __ldg(in0 + gidx);
     if constexpr (S::NIN == 2) {
       double val = __ldg(in1 + gidx);
@@ -263,6 +320,27 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
     const int X0 = valid ? K * exl : 0, Y0 = valid ? K * eyl : 0, Z0 = valid ? K * ezl : 0;
     const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + ezl));
 
+    // prefetch this element's metric for the owned x-line: the loads are in
+    // flight while the forward contractions run
+    constexpr int NQ3 = NQ * NQ * NQ;
+    double gmr[AFFINE ? 1 : 6][NQ];
+    if constexpr (!AFFINE) {
+      const double* gm = P.geom + (valid ? eg : 0) * (6 * NQ3) + line;
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) gmr[c][i] = ld_stream(gm + c * NQ3 + NQ * NQ * i);
+      // L2 prefetch of the next batch's metric rows (elements are x-rows of the brick)
+      if (tid < S::BY * S::BZ && e0 + S::EB < S::NEL) {
+        const int rowi = (e0 + S::EB) / S::BX + tid;
+        const int ry = rowi % S::BY, rz = rowi / S::BY;
+        if (rowi < (e0 + 2 * S::EB) / S::BX && ry < byr && rz < bzr) {
+          const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + ry) + (int64_t)P.ny * (ez0 + rz));
+          prefetch_l2(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)));
+        }
+      }
+    }
+
     double fu[4][NQ];
     forward_field<ND, NQ, S::LXF, S::LYF>(T, box0, scr, line, X0, Y0, Z0, fu);
     double fv[4][NQ];
@@ -284,10 +362,7 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
         M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
         W = wq * P.vol;
       } else {
-        constexpr int NQ3 = NQ * NQ * NQ;
-        const double* gm = P.geom + (valid ? eg : 0) * (6 * NQ3) + (i + NQ * line);
-        M = {__ldg(gm), __ldg(gm + NQ3), __ldg(gm + 2 * NQ3), __ldg(gm + 3 * NQ3), __ldg(gm + 4 * NQ3),
-             __ldg(gm + 5 * NQ3)};
+        M = {gmr[0][i], gmr[1][i], gmr[2][i], gmr[3][i], gmr[4][i], gmr[5][i]};
         const double det = M.xx * (M.yy * M.zz - M.yz * M.yz) - M.xy * (M.xy * M.zz - M.yz * M.xz) +
                            M.xz * (M.xy * M.yz - M.yy * M.xz);
         W = det / (wq * wq);
@@ -329,13 +404,13 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
 
     if constexpr (MODE == MODE_DESIGN) {
       scr[line] = gpart;
-      __syncthreads();
+      elem_sync<S::LINES>();
       if (line == 0 && valid) {
         double s = 0.0;
         for (int t = 0; t < S::LINES; ++t) s += scr[t];
         gout[eg] = s;
       }
-      __syncthreads();
+      elem_sync<S::LINES>();
     } else {
       // ---- 4. B^T into the E-buffer
       const int elc = el < S::NEL ? el : 0;
@@ -353,26 +428,30 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
     const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx;
     const bool lowY = ey0 > 0, highY = ey0 + byr < P.ny;
     const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
-    for (int idx = tid; idx < LX * LY * LZ; idx += S::NT) {
-      const int X = idx % LX, Y = (idx / LX) % LY, Z = idx / (LX * LY);
-      // candidate elements per axis, ascending
-      int exs[2], eys[2], ezs[2], nxc = 0, nyc = 0, nzc = 0;
-      if (X % K == 0 && X > 0) exs[nxc++] = X / K - 1;
-      if (X / K < bxr) exs[nxc++] = X / K;
-      if (Y % K == 0 && Y > 0) eys[nyc++] = Y / K - 1;
-      if (Y / K < byr) eys[nyc++] = Y / K;
-      if (Z % K == 0 && Z > 0) ezs[nzc++] = Z / K - 1;
-      if (Z / K < bzr) ezs[nzc++] = Z / K;
+    for (int sidx = tid; sidx < S::BOX; sidx += S::NT) {
+      const int X = sidx % S::LXF, Y = (sidx / S::LXF) % S::LYF, Z = sidx / (S::LXF * S::LYF);
+      if (X >= LX || Y >= LY || Z >= LZ) continue;
+      // the (<= 2 per axis) elements containing the point, ascending: lo = X/K - 1
+      // when X sits on an element face, hi = X/K when inside the brick
+      const int qx = X / K, qy = Y / K, qz = Z / K;
+      const bool xl = (X - K * qx == 0) && X > 0, yl = (Y - K * qy == 0) && Y > 0, zl = (Z - K * qz == 0) && Z > 0;
+      const bool xh = qx < bxr, yh = qy < byr, zh = qz < bzr;
 #pragma unroll
       for (int o = 0; o < S::NOUT; ++o) {
         const double* eb = ebuf + o * S::NEL * S::ND3;
         double s = 0.0;
-        for (int cz = 0; cz < nzc; ++cz)
-          for (int cy = 0; cy < nyc; ++cy)
-            for (int cx = 0; cx < nxc; ++cx) {
-              const int e = exs[cx] + S::BX * (eys[cy] + S::BY * ezs[cz]);
-              const int a = X - K * exs[cx], b = Y - K * eys[cy], c = Z - K * ezs[cz];
-              s += eb[e * S::ND3 + a + ND * (b + ND * c)];
+#pragma unroll
+        for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+          for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+              const bool ok = (dz ? zh : zl) && (dy ? yh : yl) && (dx ? xh : xl);
+              const int ex = qx - 1 + dx, ey = qy - 1 + dy, ez = qz - 1 + dz;
+              if (ok) {
+                const int e = ex + S::BX * (ey + S::BY * ez);
+                s += eb[e * S::ND3 + (X - K * ex) + ND * ((Y - K * ey) + ND * (Z - K * ez))];
+              }
             }
         const bool shared = (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) ||
                             (Y == LY - 1 && highY) || (Z == 0 && lowZ) || (Z == LZ - 1 && highZ);

@@ -1,0 +1,111 @@
+"""GPU parity at the full BASELINE.json sizes (C2-C5), in the launch
+configuration bench.py times, on sampled outputs the oracle computes one by
+one (rows from the elements touching them), plus size-independent properties:
+load sums (T6), determinism (T16) and the Euler identity of the design
+gradient (T14 ii)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from gpu_util import rel_l2, problem, operator, cuda, host
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "load_sums.json")))
+
+
+def sample_rows(w, n_random=160, seed=0):
+    """Random rows + rows on brick boundaries, domain faces, edges and corners."""
+    m = w.k * w.n + 1
+    rng = np.random.default_rng(seed)
+    rows = list(rng.choice(m ** 3, n_random, replace=False))
+    brick = {1: 8, 2: 4, 3: 4, 4: 2, 5: 2, 6: 2}[w.k]  # x/y brick edge (DOF planes shared by bricks)
+    planes = sorted({0, 1, m - 2, m - 1} | {w.k * brick * i for i in range(1, w.n // brick + 1) if w.k * brick * i < m})
+    for _ in range(80):
+        I, J, K = rng.choice(planes), rng.choice(planes), rng.integers(0, m)
+        perm = rng.permutation(3)
+        c = np.array([I, J, K])[perm]
+        rows.append(c[0] + m * (c[1] + m * c[2]))
+    rows += [0, m - 1, m * m - 1, m ** 3 - 1, (m ** 3) // 2]
+    return np.unique(np.array(rows, dtype=np.int64))
+
+
+FULL = [W.C2, W.C3, W.C4, W.C5]
+
+
+@pytest.fixture(scope="module", params=FULL, ids=[w.name for w in FULL])
+def full(request):
+    w = request.param
+    d = W.draw(w)
+    return w, d, problem(w, d), operator(w, d)
+
+
+def test_residual_sampled(full):
+    w, d, pr, op = full
+    rows = sample_rows(w)
+    r = host(op.residual(cuda(d["u"])))
+    assert rel_l2(r[rows], O.residual_rows(pr, d["u"], rows)) <= TOL
+
+
+def test_jvp_sampled(full):
+    w, d, pr, op = full
+    rows = sample_rows(w, seed=1)
+    Jv = host(op.jvp(cuda(d["u"]), cuda(d["v"])))
+    assert rel_l2(Jv[rows], O.jvp_rows(pr, d["u"], d["v"], rows)) <= TOL
+    assert np.all(np.isfinite(Jv))
+
+
+def test_design_grad_sampled_and_euler():
+    w = W.C5
+    d = W.draw(w)
+    pr, op = problem(w, d), operator(w, d)
+    u, lam = cuda(d["u"]), cuda(d["lam"])
+    g = host(op.design_grad(u, lam))
+    el = np.unique(np.concatenate([np.random.default_rng(3).choice(w.n_elems, 300, replace=False),
+                                   [0, w.n - 1, w.n_elems - 1, w.n_elems // 2]]))
+    assert rel_l2(g[el], O.design_grad_elems(pr, d["u"], d["lam"], el)) <= TOL
+    # T14 (ii): sum_e rho_e g_e = -3 lambda_free^T (F(u) - F(0)), GPU quantities only
+    F = host(op.residual(u))
+    F0 = host(op.residual(cuda(np.zeros(w.n_dofs))))
+    lm = d["lam"].copy()
+    lm[W.dirichlet_dofs(w.n, w.k, w.faces)] = 0.0
+    lhs, rhs = d["rho"] @ g, -3.0 * (lm @ (F - F0))
+    assert abs(lhs - rhs) <= 1e-11 * np.sum(np.abs(d["rho"] * g))
+
+
+@pytest.mark.parametrize("name,n,k,faces", [("C4", 32, 6, 63), ("C5", 96, 2, 1), ("C1", 4, 2, 63), ("C2", 128, 1, 63)])
+def test_load_sum_fullsize(name, n, k, faces):
+    """T6: r(u=0) = -b and sum_free b = the closed form of App. A.4 (tests/golden/load_sums.json)."""
+    w = W.CONFIGS[name]
+    d = W.draw(w)
+    op = operator(w, d)
+    b = -host(op.residual(cuda(np.zeros(w.n_dofs))))
+    expect = {c["name"]: c["value"] for c in GOLD["cases"]}
+    h = 1.0 / n
+    closed = (1 - 2 * h / (k * (k + 1))) ** 3 if faces == 63 else 1 - h / (k * (k + 1))
+    if name == "C4":
+        assert abs(closed - expect["C4-shape"]) < 1e-15
+    if name == "C5":
+        assert abs(closed - expect["C5-shape"]) < 1e-15
+    # perturbation vanishes on the boundary, so the closed form also holds for C2
+    assert abs(b.sum() - closed) < 1e-12
+
+
+def test_determinism_c2_repeated_jvp():
+    """T16: 100 repeated C2 JVPs are bitwise identical (atomic-free scatter)."""
+    w = W.C2
+    d = W.draw(w)
+    op = operator(w, d)
+    u, v = cuda(d["u"]), cuda(d["v"])
+    import torch
+    ref = op.jvp(u, v)
+    out = torch.empty_like(ref)
+    for _ in range(100):
+        op.jvp(u, v, out=out)
+        assert torch.equal(out, ref)
+    op2 = operator(w, d)
+    assert torch.equal(op2.jvp(u, v), ref)

@@ -1,0 +1,148 @@
+"""GPU-side invariants of the CUDA path itself (no oracle in the loop):
+patch test (T9), p=2 Kronecker stiffness (T7), J(0) (T8), symmetry (T10),
+Taylor order 2 (T12), host-buffer path, error paths."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from gpu_util import rel_l2, cuda, host
+
+pytestmark = pytest.mark.gpu
+
+
+def op_for(n, k, model=0, p=2.0, eps=0.0, f=0.0, faces=63, perturbed=False, rho=None):
+    import paper_2506_00746_b200 as fe
+    verts = W.vertices(n, True) if perturbed else None
+    return fe.Operator(n, n, n, k, k + 1, model, p, eps, f, verts, faces,
+                       None if rho is None else cuda(rho))
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("perturbed", [False, True])
+def test_patch(k, perturbed):
+    n = {1: 9, 2: 5, 3: 5, 4: 3, 5: 3, 6: 3}[k]
+    op = op_for(n, k, model=0, p=3.0, eps=1e-2, f=0.0, perturbed=perturbed)
+    nodes, _ = O.gll_nodes01(k)
+    X = W.node_coords(n, k, perturbed, nodes)
+    u = X @ np.array([0.3, -0.7, 0.45]) + 0.2
+    r = host(op.residual(cuda(u)))
+    free = ~W.dirichlet_dofs(n, k, 63)
+    # un-cancelled scale: same operator on |grad|-sized random data
+    scale = np.linalg.norm(host(op.residual(cuda(np.random.default_rng(0).uniform(-1, 1, u.size)))))
+    assert np.linalg.norm(r[free]) <= 1e-12 * max(scale, 1.0)
+    c = host(op.residual(cuda(np.full(u.size, 0.37))))
+    assert np.max(np.abs(c)) < 1e-13
+
+
+def kron_K(n, k):
+    from test_oracle_fem import kron_stiffness
+    return kron_stiffness(n, n, n, k)
+
+
+@pytest.mark.parametrize("n,k", [(3, 1), (2, 2), (2, 3), (1, 6)])
+def test_p2_kronecker_and_J0(n, k):
+    K, b = kron_K(n, k)
+    N = K.shape[0]
+    mask = W.dirichlet_dofs(n, k, 63)
+    u = np.random.default_rng(1).uniform(-1, 1, N)
+    op = op_for(n, k, model=0, p=2.0, eps=0.0, f=1.0)
+    expect = K @ u - b
+    expect[mask] = 0.0
+    assert rel_l2(host(op.residual(cuda(u))), expect) <= 1e-12
+    v = np.random.default_rng(2).uniform(-1, 1, N)
+    for model, scale in ((0, 1e-2), (1, 1.0), (2, 0.4 ** 3)):
+        opm = op_for(n, k, model=model, p=3.0, eps=1e-2, f=1.0, rho=np.full(n ** 3, 0.4))
+        e = scale * (K @ v)
+        e[mask] = 0.0
+        assert rel_l2(host(opm.jvp(cuda(np.zeros(N)), cuda(v))), e) <= 1e-12
+
+
+@pytest.mark.parametrize("k,p", [(1, 4.0), (2, 3.0), (3, 3.0), (6, 3.0)])
+def test_symmetry_plaplace(k, p):
+    n = {1: 9, 2: 5, 3: 5, 6: 2}[k]
+    op = op_for(n, k, model=0, p=p, eps=1e-2, f=1.0, perturbed=True)
+    mask = W.dirichlet_dofs(n, k, 63)
+    rng = np.random.default_rng(k)
+    u, x, y = (rng.uniform(-1, 1, mask.size) for _ in range(3))
+    x[mask] = 0
+    y[mask] = 0
+    a = x @ host(op.jvp(cuda(u), cuda(y)))
+    b = y @ host(op.jvp(cuda(u), cuda(x)))
+    assert abs(a - b) <= 1e-12 * abs(a)
+
+
+@pytest.mark.parametrize("model,k", [(0, 2), (1, 3), (2, 2)])
+def test_taylor(model, k):
+    n = 4
+    rho = np.random.default_rng(3).uniform(0.1, 1, n ** 3)
+    op = op_for(n, k, model=model, p=3.0, eps=1e-2, f=1.0, perturbed=True, rho=rho, faces=63 if model != 2 else 1)
+    N = (k * n + 1) ** 3
+    rng = np.random.default_rng(4)
+    u, v = rng.uniform(-1, 1, N), rng.uniform(-1, 1, N)
+    F0, Jv = host(op.residual(cuda(u))), host(op.jvp(cuda(u), cuda(v)))
+    errs = [np.linalg.norm(host(op.residual(cuda(u + h * v))) - F0 - h * Jv) for h in (1e-1, 5e-2, 2.5e-2, 1.25e-2)]
+    rates = [np.log2(errs[i] / errs[i + 1]) for i in range(3)]
+    assert all(abs(r - 2) < 0.1 for r in rates), rates
+    r, Jv2 = op.jvp_res(cuda(u), cuda(v))
+    assert np.array_equal(host(Jv2), Jv)
+    assert rel_l2(host(r), F0) <= 1e-14
+
+
+def test_host_buffer_path_matches_device():
+    import torch
+    w = W.C3.resized(6)
+    d = W.draw(w)
+    from gpu_util import operator
+    op = operator(w, d)
+    uh, vh = torch.as_tensor(d["u"]).pin_memory(), torch.as_tensor(d["v"]).pin_memory()
+    assert torch.equal(op.apply_host(0, uh), op.residual(uh.cuda()).cpu())
+    assert torch.equal(op.apply_host(1, uh, vh), op.jvp(uh.cuda(), vh.cuda()).cpu())
+
+
+def test_error_paths():
+    import torch
+    import paper_2506_00746_b200 as fe
+    op = op_for(2, 2, model=0, p=3.0, eps=1e-2, f=1.0)
+    u = cuda(np.zeros(125))
+    with pytest.raises(fe.FeodError) as e:
+        op.design_grad(u, u)
+    assert e.value.code == fe.FEOD_EINVAL
+    with pytest.raises(fe.FeodError):
+        op.residual(u, out=u)            # aliasing
+    with pytest.raises(fe.FeodError):
+        op.residual(cuda(np.zeros(10)))  # wrong length
+    with pytest.raises(fe.FeodError):
+        op.residual(torch.zeros(125, dtype=torch.float32, device="cuda"))
+    bad = W.vertices(2, False).copy()
+    bad[[0, 1]] = bad[[1, 0]]            # swap two vertices: inverted element
+    with pytest.raises(fe.FeodError) as e:
+        fe.Operator(2, 2, 2, 1, 2, 0, 2.0, 0.0, 0.0, bad, 63)
+    assert e.value.code == fe.FEOD_EINVAL
+    with pytest.raises(fe.FeodError) as e:
+        fe.Operator(2, 2, 2, 2, 4)
+    assert e.value.code == fe.FEOD_EUNSUPPORTED
+
+
+def test_nonuniform_box_and_dirichlet_subsets():
+    """nx != ny != nz, odd face subsets, stored metric on a uniform grid: full parity."""
+    import paper_2506_00746_b200 as fe
+    for (nx, ny, nz), k, faces, model in (((5, 3, 9), 2, 1 | 8 | 32, 1), ((10, 3, 2), 1, 2 | 4, 0),
+                                          ((3, 5, 4), 3, 16, 2)):
+        rng = np.random.default_rng(nx)
+        rho = rng.uniform(0.1, 1, nx * ny * nz)
+        x = np.arange(nx + 1) / nx
+        y = np.arange(ny + 1) / ny
+        z = np.arange(nz + 1) / nz
+        Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
+        verts = np.stack([X, Y, Z], -1).reshape(-1, 3) + 0.01 * rng.uniform(-1, 1, ((nx + 1) * (ny + 1) * (nz + 1), 3)) / max(nx, ny, nz)
+        pr = O.Problem(nx, ny, nz, k, k + 1, model, 3.0, 1e-2, 0.5, faces, verts, rho)
+        N = pr.n_dofs
+        u, v, lam = (rng.uniform(-1, 1, N) for _ in range(3))
+        for vv in (None, verts):
+            op = fe.Operator(nx, ny, nz, k, k + 1, model, 3.0, 1e-2, 0.5, vv, faces, cuda(rho))
+            prv = O.Problem(nx, ny, nz, k, k + 1, model, 3.0, 1e-2, 0.5, faces, vv, rho)
+            assert rel_l2(host(op.residual(cuda(u))), O.residual(prv, u)) <= 1e-11
+            assert rel_l2(host(op.jvp(cuda(u), cuda(v))), O.jvp(prv, u, v)) <= 1e-11
+            if model == 2:
+                assert rel_l2(host(op.design_grad(cuda(u), cuda(lam))), O.design_grad(prv, u, lam)) <= 1e-11

@@ -1,0 +1,39 @@
+"""C4 driver (reading A15): Jacobian-free Newton + 20-iteration unpreconditioned
+CG using only feod_jvp (libfeod's feod_newton_cg). State-synchronised strict
+check (T17): at every oracle Newton iterate the GPU residual and the GPU JVP on
+the oracle's CG directions match to 1e-11; loose free-running check of the
+||F|| history and final u at 1e-8 (parity beyond roundoff growth is unpinned)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from gpu_util import rel_l2, problem, operator, cuda, host
+
+pytestmark = pytest.mark.gpu
+
+
+def test_newton_cg_state_synchronised_and_free_running():
+    w = W.C4.resized(2)
+    d = W.draw(w)
+    pr, op = problem(w, d), operator(w, d)
+    u0 = np.zeros(w.n_dofs)
+    u_ref, norms_ref, iterates, dirs = O.newton_cg(pr, u0, 5, 20, record=True)
+    for uk, dk in zip(iterates, dirs):
+        assert rel_l2(host(op.residual(cuda(uk))), O.residual(pr, uk)) <= 1e-11
+        for p in dk[:3] + dk[-2:]:
+            assert rel_l2(host(op.jvp(cuda(uk), cuda(p))), O.jvp(pr, uk, p)) <= 1e-11
+    u, norms = op.newton_cg(cuda(u0), 5, 20)
+    np.testing.assert_allclose(norms, norms_ref, rtol=1e-8)
+    assert rel_l2(host(u), u_ref) <= 1e-8
+
+
+def test_newton_cg_fullsize_runs():
+    w = W.C4
+    d = W.draw(w)
+    op = operator(w, d)
+    u, norms = op.newton_cg(cuda(np.zeros(w.n_dofs)), 5, 20)
+    assert len(norms) == 6 and all(np.isfinite(norms))
+    assert np.all(np.isfinite(host(u)))
+    # A15: at u0 = 0, J = eps^(p-2) K, the first step overshoots (||F|| grows) by design
+    assert norms[1] > norms[0]
