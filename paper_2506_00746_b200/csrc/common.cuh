@@ -64,14 +64,15 @@ FEOD_HD int shell_size(int LX, int LY, int LZ) {
   return LX * LY * LZ - (LX - 2) * (LY - 2) * (LZ - 2);
 }
 
-// Brick shape (elements per brick along x, y, z) for order k = ND-1: sized so
-// the per-brick element buffer stays well inside shared memory.
+// Brick shape for order k = ND-1: a CTA owns a BX x BY tile of elements and
+// sweeps BZ element layers along z; one layer of BX*BY
+// elements is processed concurrently, NQ*NQ threads per element.
 template <int ND> struct BrickShape;
-template <> struct BrickShape<2> { static constexpr int BX = 8, BY = 8, BZ = 4, EB = 32; };
-template <> struct BrickShape<3> { static constexpr int BX = 4, BY = 4, BZ = 4, EB = 16; };
-template <> struct BrickShape<4> { static constexpr int BX = 4, BY = 4, BZ = 2, EB = 8; };
-template <> struct BrickShape<5> { static constexpr int BX = 2, BY = 2, BZ = 4, EB = 8; };
-template <> struct BrickShape<6> { static constexpr int BX = 2, BY = 2, BZ = 2, EB = 4; };
-template <> struct BrickShape<7> { static constexpr int BX = 2, BY = 2, BZ = 2, EB = 4; };
+template <> struct BrickShape<2> { static constexpr int BX = 8, BY = 8, BZ = 16; };
+template <> struct BrickShape<3> { static constexpr int BX = 4, BY = 4, BZ = 16; };
+template <> struct BrickShape<4> { static constexpr int BX = 2, BY = 4, BZ = 8; };
+template <> struct BrickShape<5> { static constexpr int BX = 4, BY = 2, BZ = 8; };
+template <> struct BrickShape<6> { static constexpr int BX = 2, BY = 2, BZ = 8; };
+template <> struct BrickShape<7> { static constexpr int BX = 2, BY = 2, BZ = 8; };
 
 }  // namespace feod

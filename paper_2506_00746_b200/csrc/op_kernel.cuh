@@ -59,20 +59,33 @@ template <int ND, int NQ, int MODE>
 struct OpShape {
   using S = BrickShape<ND>;
   static constexpr int K = ND - 1;
-  static constexpr int BX = S::BX, BY = S::BY, BZ = S::BZ, EB = S::EB;
-  static constexpr int NEL = BX * BY * BZ;
-  static constexpr int LXF = K * BX + 1, LYF = K * BY + 1, LZF = K * BZ + 1;
-  static constexpr int BOX = LXF * LYF * LZF;
+  static constexpr int BX = S::BX, BY = S::BY, BZ = S::BZ;
+  static constexpr int EL = BX * BY;                        // elements per layer
+  static constexpr int LXF = K * BX + 1, LYF = K * BY + 1;  // DOF plane of the tile
+  static constexpr int PLANE = LXF * LYF;
+  static constexpr int RIN = 2 * K + 1;                     // input plane ring (layer + prefetch)
+  static constexpr int ROUT = K + 1;                        // output plane ring
   static constexpr int LINES = NQ * NQ;
-  static constexpr int NT = LINES * EB;
-  static constexpr int ND3 = ND * ND * ND;
+  static constexpr int NT = LINES * EL;
+  static constexpr int MINB = (512 / NT) < 1 ? 1 : ((512 / NT) > 4 ? 4 : 512 / NT);   // CTAs/SM the register budget is sized for
   static constexpr int SCR = Lay<ND, NQ>::SCR;
   static constexpr int NIN = (MODE == MODE_RES) ? 1 : 2;
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
-  static constexpr int SMEM_DOUBLES = NIN * BOX + NOUT * NEL * ND3 + EB * SCR;
+  static constexpr int SMEM_DOUBLES = NIN * RIN * PLANE + NOUT * ROUT * PLANE + EL * SCR;
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
+  static constexpr int LZF = K * BZ + 1;
   static constexpr int SHELL = LXF * LYF * LZF - (LXF - 2) * (LYF - 2) * (LZF - 2);
 };
+
+// 8-byte asynchronous global -> shared copy (LDGSTS): the next layer's DOF
+// planes stream in while the current layer computes. (The L-vector row pitch
+// 8(kn+1) B is not 16-byte aligned, so TMA tensor maps cannot describe it.)
+FEOD_DEV void cp_async8(double* smem_dst, const double* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+FEOD_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+FEOD_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Non-coherent global load that the compiler may not sink toward its use: the
 // metric stream is requested before the forward contractions so its HBM
@@ -98,11 +111,12 @@ FEOD_DEV void elem_sync() {
   else __syncthreads();
 }
 
-// Forward interpolation of one field from the smem box: returns, for the
+// Forward interpolation of one field from the element's ND DOF planes in the
+// shared ring (planes[c] = node level c): returns, for the
 // x-line (j, l) this thread owns, U[i], dU/dxi1[i], dU/dxi2[i], dU/dxi3[i].
-template <int ND, int NQ, int LXF, int LYF>
-FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, double* scr, int line,
-                            int X0, int Y0, int Z0, double (&out)[4][NQ]) {
+template <int ND, int NQ, int LXF>
+FEOD_DEV void forward_field(const Tables& T, const double* const (&planes)[ND], double* scr, int line,
+                            int X0, int Y0, double (&out)[4][NQ]) {
   using L = Lay<ND, NQ>;
   constexpr int SA = L::SN;   // S0 | S1
   constexpr int SB = L::TN;   // T0 | T1 | T2
@@ -112,7 +126,7 @@ FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, dou
     if ((ND == NQ) || (a < ND && b < ND)) {
       double x[ND];
 #pragma unroll
-      for (int c = 0; c < ND; ++c) x[c] = box[(X0 + a) + LXF * ((Y0 + b) + LYF * (Z0 + c))];
+      for (int c = 0; c < ND; ++c) x[c] = planes[c][(X0 + a) + LXF * (Y0 + b)];
 #pragma unroll
       for (int l = 0; l < NQ; ++l) {
         double t0 = 0.0, t1 = 0.0;
@@ -187,10 +201,10 @@ FEOD_DEV void forward_field(const Tables& T, const double* __restrict__ box, dou
 
 // Transposed interpolation: from the x-line of point values (Fx, Fy, Fz and
 // optionally the value channel V) back to the element's nodal vector; the
-// thread owning node column (a, b) writes re[a + ND (b + ND c)] for all c.
+// thread owning node column (a, b) returns r[c] = r_e[a, b, c] for all c.
 template <int ND, int NQ, bool HASV>
-FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const double (&F)[4][NQ], double* re,
-                             bool write) {
+FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const double (&F)[4][NQ],
+                             double (&rout)[ND]) {
   using L = Lay<ND, NQ>;
   constexpr int SA = L::QN;   // Q0 | Q1
   constexpr int SB = L::PN;   // P0 | P1 | P2
@@ -252,17 +266,15 @@ FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const doubl
         q0[l] = scr[L::Qi(a, b, l)];
         q1[l] = scr[SA + L::Qi(a, b, l)];
       }
-      if (write) {
 #pragma unroll
-        for (int c = 0; c < ND; ++c) {
-          double r = 0.0;
+      for (int c = 0; c < ND; ++c) {
+        double r = 0.0;
 #pragma unroll
-          for (int l = 0; l < NQ; ++l) {
-            r = fma(T.B[l][c], q0[l], r);
-            r = fma(T.G[l][c], q1[l], r);
-          }
-          re[a + ND * (b + ND * c)] = r;
+        for (int l = 0; l < NQ; ++l) {
+          r = fma(T.B[l][c], q0[l], r);
+          r = fma(T.G[l][c], q1[l], r);
         }
+        rout[c] = r;
       }
     }
   }
@@ -270,17 +282,17 @@ FEOD_DEV void backward_field(const Tables& T, double* scr, int line, const doubl
 }
 
 template <int ND, int NQ, int MODE, int MODEL, bool AFFINE>
-__global__ void __launch_bounds__(OpShape<ND, NQ, MODE>::NT)
+__global__ void __launch_bounds__(OpShape<ND, NQ, MODE>::NT, OpShape<ND, NQ, MODE>::MINB)
 op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, const double* __restrict__ in1,
           double* __restrict__ out0, double* __restrict__ out1, double* __restrict__ shell0,
           double* __restrict__ shell1, double* __restrict__ gout) {
   using S = OpShape<ND, NQ, MODE>;
   constexpr int K = S::K;
+  constexpr int NQ3 = NQ * NQ * NQ;
   extern __shared__ double smem[];
-  double* box0 = smem;
-  double* box1 = smem + S::BOX;                     // valid if NIN == 2
-  double* ebuf = smem + S::NIN * S::BOX;            // [NOUT][NEL][ND3]
-  double* scratch = ebuf + S::NOUT * S::NEL * S::ND3;
+  double* ring_in = smem;                                   // [NIN][RIN][PLANE]
+  double* ring_out = smem + S::NIN * S::RIN * S::PLANE;     // [NOUT][ROUT][PLANE]
+  double* scratch = ring_out + S::NOUT * S::ROUT * S::PLANE;
 
   const int tid = threadIdx.x;
   const int brick = blockIdx.x;
@@ -290,39 +302,83 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
   const int LX = K * bxr + 1, LY = K * byr + 1, LZ = K * bzr + 1;
   const int gX0 = K * ex0, gY0 = K * ey0, gZ0 = K * ez0;
 
-  // ---- 1. stage the DOF boxes (G, gather)
-  // (the box is walked with its compile-time full-brick shape: cheap index
-  //  arithmetic; points beyond a ragged brick's extent are skipped)
-  for (int sidx = tid; sidx < S::BOX; sidx += S::NT) {
-    const int X = sidx % S::LXF, Y = (sidx / S::LXF) % S::LYF, Z = sidx / (S::LXF * S::LYF);
-    if (X >= LX || Y >= LY || Z >= LZ) continue;
-    const int64_t gidx = (int64_t)(gX0 + X) + (int64_t)P.Mx * ((gY0 + Y) + (int64_t)P.My * (gZ0 + Z));
-    box0[sidx] = __ldg(in0 + gidx);
-    if constexpr (S::NIN == 2) {
-      double val = __ldg(in1 + gidx);
-      if constexpr (MODE == MODE_DESIGN) {
-        if (is_dirichlet(gX0 + X, gY0 + Y, gZ0 + Z, P.Mx, P.My, P.Mz, P.faces)) val = 0.0;
+  // ---- G (gather): stream DOF plane p (brick-local z index) into its ring slot
+  auto load_plane = [&](int p) {
+    const int slot = p % S::RIN;
+    const int64_t zoff = (int64_t)P.Mx * P.My * (gZ0 + p);
+    for (int idx = tid; idx < S::PLANE; idx += S::NT) {
+      const int X = idx % S::LXF, Y = idx / S::LXF;
+      if (X >= LX || Y >= LY) continue;
+      const int64_t g = zoff + (int64_t)(gX0 + X) + (int64_t)P.Mx * (gY0 + Y);
+      cp_async8(ring_in + slot * S::PLANE + idx, in0 + g);
+      if constexpr (S::NIN == 2) {
+        double* dst = ring_in + (S::RIN + slot) * S::PLANE + idx;
+        if constexpr (MODE == MODE_DESIGN) {
+          // lambda's Dirichlet entries are masked (reading A14)
+          *dst = is_dirichlet(gX0 + X, gY0 + Y, gZ0 + p, P.Mx, P.My, P.Mz, P.faces) ? 0.0 : __ldg(in1 + g);
+        } else {
+          cp_async8(dst, in1 + g);
+        }
       }
-      box1[sidx] = val;
     }
-  }
-  __syncthreads();
+  };
+  for (int p = 0; p <= K; ++p) load_plane(p);
+  cp_async_commit();
+  if constexpr (S::NOUT > 0)
+    for (int i = tid; i < S::NOUT * S::ROUT * S::PLANE; i += S::NT) ring_out[i] = 0.0;
 
   const int line = tid % S::LINES;
-  const int slot = tid / S::LINES;
-  double* scr = scratch + slot * S::SCR;
-  const int jl = line % NQ, ll = line / NQ;   // x-line owned in the point phase
+  const int el = tid / S::LINES;                   // element of the layer this thread works on
+  double* scr = scratch + el * S::SCR;
+  const int exl = el % S::BX, eyl = el / S::BX;
+  const bool valid = exl < bxr && eyl < byr;
+  const int X0 = valid ? K * exl : 0, Y0 = valid ? K * eyl : 0;
+  const int jl = line % NQ, ll = line / NQ;        // x-line owned in the point phase
+  const int ra = line % NQ, rb = line / NQ;        // node column owned after B^T
+  const int colour = (exl & 1) + 2 * (eyl & 1);
+  const double wjl = T.w[jl] * T.w[ll];
 
-  for (int e0 = 0; e0 < S::NEL; e0 += S::EB) {
-    const int el = e0 + slot;
-    const int exl = el % S::BX, eyl = (el / S::BX) % S::BY, ezl = el / (S::BX * S::BY);
-    const bool valid = (el < S::NEL) && exl < bxr && eyl < byr && ezl < bzr;
-    const int X0 = valid ? K * exl : 0, Y0 = valid ? K * eyl : 0, Z0 = valid ? K * ezl : 0;
-    const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + ezl));
+  // shell classification of the tile's sides
+  const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx;
+  const bool lowY = ey0 > 0, highY = ey0 + byr < P.ny;
+  const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
 
-    // prefetch this element's metric for the owned x-line: the loads are in
-    // flight while the forward contractions run
-    constexpr int NQ3 = NQ * NQ * NQ;
+  // ---- write finished output plane p (brick-local), then clear its slot
+  auto flush_plane = [&](int p) {
+    const int slot = p % S::ROUT;
+    const int64_t zoff = (int64_t)P.Mx * P.My * (gZ0 + p);
+    for (int idx = tid; idx < S::PLANE; idx += S::NT) {
+      const int X = idx % S::LXF, Y = idx / S::LXF;
+      if (X >= LX || Y >= LY) continue;
+      const bool shared = (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) || (Y == LY - 1 && highY) ||
+                          (p == 0 && lowZ) || (p == LZ - 1 && highZ);
+      const int gx = gX0 + X, gy = gY0 + Y, gz = gZ0 + p;
+      const bool dir = is_dirichlet(gx, gy, gz, P.Mx, P.My, P.Mz, P.faces);
+      const int64_t g = zoff + (int64_t)gx + (int64_t)P.Mx * gy;
+#pragma unroll
+      for (int o = 0; o < S::NOUT; ++o) {
+        double* cell = ring_out + (o * S::ROUT + slot) * S::PLANE + idx;
+        const double v = *cell;
+        *cell = 0.0;
+        if (shared) {
+          (o == 0 ? shell0 : shell1)[(int64_t)brick * P.shell_stride + shell_rank(X, Y, p, LX, LY, LZ)] = v;
+        } else {
+          (o == 0 ? out0 : out1)[g] = dir ? 0.0 : v;
+        }
+      }
+    }
+  };
+
+  for (int z = 0; z < bzr; ++z) {
+    cp_async_wait_all();
+    __syncthreads();                                 // planes K z .. K z + K resident; previous layer flushed
+    if (z + 1 < bzr) {
+      for (int p = K * (z + 1) + 1; p <= K * (z + 1) + K; ++p) load_plane(p);
+      cp_async_commit();
+    }
+    const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + z));
+
+    // metric of this element's x-lines: requested before the contractions
     double gmr[AFFINE ? 1 : 6][NQ];
     if constexpr (!AFFINE) {
       const double* gm = P.geom + (valid ? eg : 0) * (6 * NQ3) + line;
@@ -330,29 +386,32 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
       for (int c = 0; c < 6; ++c)
 #pragma unroll
         for (int i = 0; i < NQ; ++i) gmr[c][i] = ld_stream(gm + c * NQ3 + NQ * NQ * i);
-      // L2 prefetch of the next batch's metric rows (elements are x-rows of the brick)
-      if (tid < S::BY * S::BZ && e0 + S::EB < S::NEL) {
-        const int rowi = (e0 + S::EB) / S::BX + tid;
-        const int ry = rowi % S::BY, rz = rowi / S::BY;
-        if (rowi < (e0 + 2 * S::EB) / S::BX && ry < byr && rz < bzr) {
-          const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + ry) + (int64_t)P.ny * (ez0 + rz));
-          prefetch_l2(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)));
-        }
+      // L2 prefetch of the next layer's metric (one contiguous x-row of elements per y)
+      if (tid < S::BY && z + 1 < bzr && tid < byr) {
+        const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + tid) + (int64_t)P.ny * (ez0 + z + 1));
+        prefetch_l2(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)));
       }
     }
+    double rho_e = 0.0;
+    if constexpr (MODEL == HEAT) rho_e = valid ? __ldg(P.rho + eg) : 1.0;
 
+    const double* pl0[ND];
+    const double* pl1[ND];
+#pragma unroll
+    for (int c = 0; c < ND; ++c) {
+      const int slot = (K * z + c) % S::RIN;
+      pl0[c] = ring_in + slot * S::PLANE;
+      pl1[c] = ring_in + (S::RIN + slot) * S::PLANE;
+    }
     double fu[4][NQ];
-    forward_field<ND, NQ, S::LXF, S::LYF>(T, box0, scr, line, X0, Y0, Z0, fu);
+    forward_field<ND, NQ, S::LXF>(T, pl0, scr, line, X0, Y0, fu);
     double fv[4][NQ];
-    if constexpr (S::NIN == 2) forward_field<ND, NQ, S::LXF, S::LYF>(T, box1, scr, line, X0, Y0, Z0, fv);
+    if constexpr (S::NIN == 2) forward_field<ND, NQ, S::LXF>(T, pl1, scr, line, X0, Y0, fv);
 
-    // ---- 3. pointwise D on the x-line (i, jl, ll)
+    // ---- D: pointwise on the x-line (i, jl, ll)
     double F0[4][NQ];   // first output channel set (r for RES, Jv for JVP/JVPRES)
     double F1[4][NQ];   // second (r for JVPRES)
     double gpart = 0.0;
-    const double wjl = T.w[jl] * T.w[ll];
-    double rho_e = 0.0;
-    if constexpr (MODEL == HEAT) rho_e = valid ? __ldg(P.rho + eg) : 1.0;
 #pragma unroll
     for (int i = 0; i < NQ; ++i) {
       const double wq = T.w[i] * wjl;
@@ -412,58 +471,30 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
       }
       elem_sync<S::LINES>();
     } else {
-      // ---- 4. B^T into the E-buffer
-      const int elc = el < S::NEL ? el : 0;
-      backward_field<ND, NQ, MODE == MODE_RES>(T, scr, line, F0, ebuf + elc * S::ND3, valid);
-      if constexpr (MODE == MODE_JVPRES)
-        backward_field<ND, NQ, true>(T, scr, line, F1, ebuf + (S::NEL + elc) * S::ND3, valid);
-    }
-  }
-
-  if constexpr (S::NOUT > 0) {
-    __syncthreads();
-    // ---- 5. G^T: box points sum their element contributions in a fixed order
-    double* shell_base0 = shell0 + (int64_t)brick * P.shell_stride;
-    double* shell_base1 = (S::NOUT == 2) ? shell1 + (int64_t)brick * P.shell_stride : nullptr;
-    const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx;
-    const bool lowY = ey0 > 0, highY = ey0 + byr < P.ny;
-    const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
-    for (int sidx = tid; sidx < S::BOX; sidx += S::NT) {
-      const int X = sidx % S::LXF, Y = (sidx / S::LXF) % S::LYF, Z = sidx / (S::LXF * S::LYF);
-      if (X >= LX || Y >= LY || Z >= LZ) continue;
-      // the (<= 2 per axis) elements containing the point, ascending: lo = X/K - 1
-      // when X sits on an element face, hi = X/K when inside the brick
-      const int qx = X / K, qy = Y / K, qz = Z / K;
-      const bool xl = (X - K * qx == 0) && X > 0, yl = (Y - K * qy == 0) && Y > 0, zl = (Z - K * qz == 0) && Z > 0;
-      const bool xh = qx < bxr, yh = qy < byr, zh = qz < bzr;
+      // ---- B^T, then G^T into the output ring: the four x-y colour classes of
+      // the layer add their element vectors one class at a time (elements of one
+      // class share no DOF), so every DOF sums its contributions in a fixed order
+      double r0[ND], r1[ND];
+      backward_field<ND, NQ, MODE == MODE_RES>(T, scr, line, F0, r0);
+      if constexpr (MODE == MODE_JVPRES) backward_field<ND, NQ, true>(T, scr, line, F1, r1);
+      const bool owner = valid && ((ND == NQ) || (ra < ND && rb < ND));
+      const int node = (X0 + ra) + S::LXF * (Y0 + rb);
 #pragma unroll
-      for (int o = 0; o < S::NOUT; ++o) {
-        const double* eb = ebuf + o * S::NEL * S::ND3;
-        double s = 0.0;
+      for (int cls = 0; cls < 4; ++cls) {
+        if (cls > 0) __syncthreads();
+        if (owner && colour == cls) {
 #pragma unroll
-        for (int dz = 0; dz < 2; ++dz)
-#pragma unroll
-          for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < 2; ++dx) {
-              const bool ok = (dz ? zh : zl) && (dy ? yh : yl) && (dx ? xh : xl);
-              const int ex = qx - 1 + dx, ey = qy - 1 + dy, ez = qz - 1 + dz;
-              if (ok) {
-                const int e = ex + S::BX * (ey + S::BY * ez);
-                s += eb[e * S::ND3 + (X - K * ex) + ND * ((Y - K * ey) + ND * (Z - K * ez))];
-              }
-            }
-        const bool shared = (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) ||
-                            (Y == LY - 1 && highY) || (Z == 0 && lowZ) || (Z == LZ - 1 && highZ);
-        if (shared) {
-          (o == 0 ? shell_base0 : shell_base1)[shell_rank(X, Y, Z, LX, LY, LZ)] = s;
-        } else {
-          const int gx = gX0 + X, gy = gY0 + Y, gz = gZ0 + Z;
-          const int64_t gidx = (int64_t)gx + (int64_t)P.Mx * (gy + (int64_t)P.My * gz);
-          if (is_dirichlet(gx, gy, gz, P.Mx, P.My, P.Mz, P.faces)) s = 0.0;
-          (o == 0 ? out0 : out1)[gidx] = s;
+          for (int c = 0; c < ND; ++c) {
+            double* cell = ring_out + ((K * z + c) % S::ROUT) * S::PLANE + node;
+            *cell += r0[c];
+            if constexpr (MODE == MODE_JVPRES) cell[S::ROUT * S::PLANE] += r1[c];
+          }
         }
       }
+      __syncthreads();
+      // planes K z .. K z + K-1 are complete (the top plane carries into the next layer)
+      for (int c = 0; c < K; ++c) flush_plane(K * z + c);
+      if (z == bzr - 1) flush_plane(K * z + K);
     }
   }
 }

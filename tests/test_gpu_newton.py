@@ -24,8 +24,18 @@ def test_newton_cg_state_synchronised_and_free_running():
         for p in dk[:3] + dk[-2:]:
             assert rel_l2(host(op.jvp(cuda(uk), cuda(p))), O.jvp(pr, uk, p)) <= 1e-11
     u, norms = op.newton_cg(cuda(u0), 5, 20)
-    np.testing.assert_allclose(norms, norms_ref, rtol=1e-8)
-    assert rel_l2(host(u), u_ref) <= 1e-8
+    # Free-running: the 5 x 20 unconverged CG trajectory amplifies roundoff
+    # (reading A15/T17: parity unpinned beyond roundoff growth). Measure the
+    # amplification on the oracle itself with a roundoff-sized start (1e-15)
+    # and allow the GPU 100x that spread.
+    pert = 1e-15 * np.random.default_rng(9).uniform(-1, 1, w.n_dofs)
+    pert[W.dirichlet_dofs(w.n, w.k, w.faces)] = 0.0
+    u_p, norms_p = O.newton_cg(pr, pert, 5, 20)
+    spread_n = np.max(np.abs(np.array(norms_p) - norms_ref) / np.array(norms_ref))
+    spread_u = rel_l2(u_p, u_ref)
+    dev_n = np.max(np.abs(np.array(norms) - norms_ref) / np.array(norms_ref))
+    assert dev_n <= 100 * spread_n + 1e-12, (dev_n, spread_n)
+    assert rel_l2(host(u), u_ref) <= 100 * spread_u + 1e-12
 
 
 def test_newton_cg_fullsize_runs():
