@@ -360,7 +360,7 @@ def main():
             "data": "synthetic (seeded workloads/ recipe, SURVEY.md §8(d))", "config": config_of(w),
             "parallelism": f"replicas x{world} (no data-path collective; DESIGN.md §Multi-GPU)",
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
-            "gpu_launches": args.steps * 4 if (op.n_elems > 1) else args.steps * 2,
+            "gpu_launches": args.steps * 2,   # one fused op_kernel per feod_residual / feod_jvp
             "calls": {
                 "residual": {"us": t_res * 1e3, "gdof_s": N / (t_res * 1e-3) / 1e9,
                              "hbm_frac": by_res / (t_res * 1e-3) / 1e9 / peak,

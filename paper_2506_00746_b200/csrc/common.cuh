@@ -67,12 +67,15 @@ FEOD_HD int shell_size(int LX, int LY, int LZ) {
 // Brick shape for order k = ND-1: a CTA owns a BX x BY tile of elements and
 // sweeps BZ element layers along z; one layer of BX*BY
 // elements is processed concurrently, NQ*NQ threads per element.
+// SB = sub-batches per layer: with SB = 2 the layer's even and odd element rows
+// (y) are processed one after the other by the same threads (half the threads
+// for twice the tile).
 template <int ND> struct BrickShape;
-template <> struct BrickShape<2> { static constexpr int BX = 8, BY = 8, BZ = 16; };
-template <> struct BrickShape<3> { static constexpr int BX = 4, BY = 4, BZ = 16; };
-template <> struct BrickShape<4> { static constexpr int BX = 2, BY = 4, BZ = 8; };
-template <> struct BrickShape<5> { static constexpr int BX = 4, BY = 2, BZ = 8; };
-template <> struct BrickShape<6> { static constexpr int BX = 2, BY = 2, BZ = 8; };
-template <> struct BrickShape<7> { static constexpr int BX = 2, BY = 2, BZ = 8; };
+template <> struct BrickShape<2> { static constexpr int BX = 8, BY = 8, BZ = 16, SB = 1; };
+template <> struct BrickShape<3> { static constexpr int BX = 4, BY = 4, BZ = 16, SB = 1; };
+template <> struct BrickShape<4> { static constexpr int BX = 4, BY = 4, BZ = 8, SB = 2; };
+template <> struct BrickShape<5> { static constexpr int BX = 4, BY = 2, BZ = 8, SB = 1; };
+template <> struct BrickShape<6> { static constexpr int BX = 2, BY = 2, BZ = 8, SB = 1; };
+template <> struct BrickShape<7> { static constexpr int BX = 2, BY = 2, BZ = 8, SB = 1; };
 
 }  // namespace feod

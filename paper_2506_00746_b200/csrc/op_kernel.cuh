@@ -52,7 +52,7 @@ struct Lay {
   static constexpr int QN = QB * ND;
   FEOD_HD static constexpr int Qi(int a, int b, int l) { return a + ND * l + QB * b; }
   static constexpr int mx(int x, int y) { return x > y ? x : y; }
-  static constexpr int SCR = mx(mx(2 * SN, 3 * TN), mx(mx(3 * PN, 2 * QN), NQ * NQ));
+  static constexpr int SCR1 = mx(mx(2 * SN, 3 * TN), mx(mx(3 * PN, 2 * QN), NQ * NQ));
 };
 
 template <int ND, int NQ, int MODE>
@@ -61,17 +61,21 @@ struct OpShape {
   static constexpr int K = ND - 1;
   static constexpr int BX = S::BX, BY = S::BY, BZ = S::BZ;
   static constexpr int EL = BX * BY;                        // elements per layer
+  static constexpr int SB = S::SB;                          // sub-batches per layer
+  static constexpr int EB = EL / SB;                        // elements per sub-batch
+  static constexpr int NCLS = SB == 1 ? 4 : 2;              // colour classes per sub-batch
   static constexpr int LXF = K * BX + 1, LYF = K * BY + 1;  // DOF plane of the tile
   static constexpr int PLANE = LXF * LYF;
   static constexpr int RIN = 2 * K + 1;                     // input plane ring (layer + prefetch)
   static constexpr int ROUT = K + 1;                        // output plane ring
   static constexpr int LINES = NQ * NQ;
-  static constexpr int NT = LINES * EL;
+  static constexpr int NT = LINES * EB;
   static constexpr int MINB = (512 / NT) < 1 ? 1 : ((512 / NT) > 4 ? 4 : 512 / NT);   // CTAs/SM the register budget is sized for
-  static constexpr int SCR = Lay<ND, NQ>::SCR;
   static constexpr int NIN = (MODE == MODE_RES) ? 1 : 2;
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
-  static constexpr int SMEM_DOUBLES = NIN * RIN * PLANE + NOUT * ROUT * PLANE + EL * SCR;
+  static constexpr int SCR = Lay<ND, NQ>::SCR1;   // doubles per element
+  static constexpr int OUTSZ = (NOUT * ROUT * PLANE + 1) / 2 * 2;   // keeps the scratch 16-byte aligned
+  static constexpr int SMEM_DOUBLES = NIN * RIN * PLANE + OUTSZ + EB * SCR;
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
   static constexpr int LZF = K * BZ + 1;
   static constexpr int SHELL = LXF * LYF * LZF - (LXF - 2) * (LYF - 2) * (LZF - 2);
@@ -289,10 +293,10 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
   using S = OpShape<ND, NQ, MODE>;
   constexpr int K = S::K;
   constexpr int NQ3 = NQ * NQ * NQ;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   double* ring_in = smem;                                   // [NIN][RIN][PLANE]
   double* ring_out = smem + S::NIN * S::RIN * S::PLANE;     // [NOUT][ROUT][PLANE]
-  double* scratch = ring_out + S::NOUT * S::ROUT * S::PLANE;
+  double* scratch = ring_out + S::OUTSZ;
 
   const int tid = threadIdx.x;
   const int brick = blockIdx.x;
@@ -328,14 +332,10 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
     for (int i = tid; i < S::NOUT * S::ROUT * S::PLANE; i += S::NT) ring_out[i] = 0.0;
 
   const int line = tid % S::LINES;
-  const int el = tid / S::LINES;                   // element of the layer this thread works on
-  double* scr = scratch + el * S::SCR;
-  const int exl = el % S::BX, eyl = el / S::BX;
-  const bool valid = exl < bxr && eyl < byr;
-  const int X0 = valid ? K * exl : 0, Y0 = valid ? K * eyl : 0;
+  const int eslot = tid / S::LINES;                // element slot of the sub-batch this thread works on
+  double* scr = scratch + eslot * S::SCR;
   const int jl = line % NQ, ll = line / NQ;        // x-line owned in the point phase
   const int ra = line % NQ, rb = line / NQ;        // node column owned after B^T
-  const int colour = (exl & 1) + 2 * (eyl & 1);
   const double wjl = T.w[jl] * T.w[ll];
 
   // shell classification of the tile's sides
@@ -376,6 +376,12 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
       for (int p = K * (z + 1) + 1; p <= K * (z + 1) + K; ++p) load_plane(p);
       cp_async_commit();
     }
+   for (int sb = 0; sb < S::SB; ++sb) {
+    // element of this sub-batch: SB = 1 -> the whole layer; SB = 2 -> rows of y-parity sb
+    const int exl = eslot % S::BX, eyl = S::SB * (eslot / S::BX) + sb;
+    const bool valid = exl < bxr && eyl < byr;
+    const int X0 = valid ? K * exl : 0, Y0 = valid ? K * eyl : 0;
+    const int colour = S::SB == 1 ? (exl & 1) + 2 * (eyl & 1) : (exl & 1);
     const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + z));
 
     // metric of this element's x-lines: requested before the contractions
@@ -387,7 +393,7 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
 #pragma unroll
         for (int i = 0; i < NQ; ++i) gmr[c][i] = ld_stream(gm + c * NQ3 + NQ * NQ * i);
       // L2 prefetch of the next layer's metric (one contiguous x-row of elements per y)
-      if (tid < S::BY && z + 1 < bzr && tid < byr) {
+      if (sb == 0 && tid < S::BY && z + 1 < bzr && tid < byr) {
         const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + tid) + (int64_t)P.ny * (ez0 + z + 1));
         prefetch_l2(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)));
       }
@@ -480,8 +486,8 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
       const bool owner = valid && ((ND == NQ) || (ra < ND && rb < ND));
       const int node = (X0 + ra) + S::LXF * (Y0 + rb);
 #pragma unroll
-      for (int cls = 0; cls < 4; ++cls) {
-        if (cls > 0) __syncthreads();
+      for (int cls = 0; cls < S::NCLS; ++cls) {
+        if (cls > 0 || sb > 0) __syncthreads();
         if (owner && colour == cls) {
 #pragma unroll
           for (int c = 0; c < ND; ++c) {
@@ -491,6 +497,9 @@ op_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, cons
           }
         }
       }
+    }
+   }  // sub-batches
+    if constexpr (S::NOUT > 0) {
       __syncthreads();
       // planes K z .. K z + K-1 are complete (the top plane carries into the next layer)
       for (int c = 0; c < K; ++c) flush_plane(K * z + c);

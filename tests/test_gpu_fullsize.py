@@ -23,8 +23,9 @@ def sample_rows(w, n_random=160, seed=0):
     m = w.k * w.n + 1
     rng = np.random.default_rng(seed)
     rows = list(rng.choice(m ** 3, n_random, replace=False))
-    brick = {1: 8, 2: 4, 3: 4, 4: 2, 5: 2, 6: 2}[w.k]  # x/y brick edge (DOF planes shared by bricks)
-    planes = sorted({0, 1, m - 2, m - 1} | {w.k * brick * i for i in range(1, w.n // brick + 1) if w.k * brick * i < m})
+    bx, by, bz = {1: (8, 8, 16), 2: (4, 4, 16), 3: (2, 4, 8), 4: (4, 2, 8), 5: (2, 2, 8), 6: (2, 2, 8)}[w.k]
+    planes = sorted({0, 1, m - 2, m - 1} | {w.k * b * i for b in (bx, by, bz) for i in range(1, w.n // b + 1)
+                                            if w.k * b * i < m})
     for _ in range(80):
         I, J, K = rng.choice(planes), rng.choice(planes), rng.integers(0, m)
         perm = rng.permutation(3)
