@@ -99,7 +99,11 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   gll01(order, nodes);
   gauss01(qorder, pts, wts);
   lagrange01(h->nd, nodes, qorder, pts, &h->T.B[0][0], &h->T.G[0][0], kMaxNQ);
-  for (int i = 0; i < qorder; ++i) { h->T.w[i] = wts[i]; h->T.x[i] = pts[i]; }
+  {
+    double id[kMaxNQ * kMaxNQ];   // Lagrange basis of the Gauss points at the Gauss points (identity)
+    lagrange01(qorder, pts, qorder, pts, id, &h->T.D[0][0], kMaxNQ);
+  }
+  for (int i = 0; i < qorder; ++i) { h->T.w[i] = wts[i]; h->T.wi2[i] = 1.0 / (wts[i] * wts[i]); h->T.x[i] = pts[i]; }
 
   OpParams& P = h->P;
   std::memset(&P, 0, sizeof(P));

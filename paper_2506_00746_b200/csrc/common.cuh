@@ -15,12 +15,17 @@ constexpr int kMaxNQ = 8;
 // 1D tables, passed by value as a kernel parameter: the entries sit in the
 // constant bank and feed DFMA directly (uniform across the warp).
 //   B[i][a] = l_a(x_i), G[i][a] = l_a'(x_i)  (GLL Lagrange basis at Gauss points)
-//   w[i]    = 1D Gauss weight on [0,1]
+//   w[i]    = 1D Gauss weight on [0,1]; wi2[i] = 1 / w[i]^2
 //   x[i]    = 1D Gauss point on [0,1] (geometry setup only)
+//   D[i][m] = L_m'(x_i), L_m the Lagrange polynomial of the Gauss points
+//             (collocated derivative: sum_m D[i][m] B[m][a] = G[i][a] exactly,
+//             since l_a has degree k <= q-1)
 struct Tables {
   double B[kMaxNQ][kMaxNQ];
   double G[kMaxNQ][kMaxNQ];
+  double D[kMaxNQ][kMaxNQ];
   double w[kMaxNQ];
+  double wi2[kMaxNQ];   // 1 / w[i]^2
   double x[kMaxNQ];
 };
 

@@ -2,9 +2,10 @@
 //   M_q = w_q detJ_q J_q^{-1} J_q^{-T} = w_q adj(J_q) adj(J_q)^T / detJ_q
 // of the trilinear map of each hexahedron (the linear,
 // solution-independent part of B that PAPER.md:25 keeps "excluded from the
-// differentiation loop"). One thread per (element, point); output layout
-// [E][6][q^3] with components xx yy zz xy xz yz and points ordered (j, l, i),
-// j fastest and i slowest (the operator kernel's x-line ownership).
+// differentiation loop"). One thread per (element, point); components xx yy zz
+// xy xz yz; layout [E][l][6][j][i] (component-major within each z-row l of points, x
+// fastest): the ND*ND threads that own an element's points in plane_kernel read
+// one contiguous 128-byte run per (row, component).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -56,16 +57,15 @@ __global__ void geometry_kernel(const double* __restrict__ verts, int nx, int ny
     const double det = J[0][0] * A[0][0] + J[0][1] * A[1][0] + J[0][2] * A[2][0];
     if (!(det > 0.0)) atomicExch(bad, 1);
     const double s = T.w[i] * T.w[j] * T.w[l] / det;
-    // stored point order: x-line (j, l) fastest, i slowest, so the threads owning
-    // the x-lines of one element read 16 consecutive doubles per (component, i)
-    double* g = geom + e * 6 * nq3 + (j + nq * l) + nq * nq * i;
+    const int nq2 = nq * nq;
+    double* g = geom + e * 6 * nq3 + l * 6 * nq2 + j * nq + i;
     auto dot = [&](int r, int c) { return A[r][0] * A[c][0] + A[r][1] * A[c][1] + A[r][2] * A[c][2]; };
-    g[0 * nq3] = s * dot(0, 0);
-    g[1 * nq3] = s * dot(1, 1);
-    g[2 * nq3] = s * dot(2, 2);
-    g[3 * nq3] = s * dot(0, 1);
-    g[4 * nq3] = s * dot(0, 2);
-    g[5 * nq3] = s * dot(1, 2);
+    g[0 * nq2] = s * dot(0, 0);
+    g[1 * nq2] = s * dot(1, 1);
+    g[2 * nq2] = s * dot(2, 2);
+    g[3 * nq2] = s * dot(0, 1);
+    g[4 * nq2] = s * dot(0, 2);
+    g[5 * nq2] = s * dot(1, 2);
   }
 }
 

@@ -2,22 +2,22 @@
 // NQ = k+1 points per axis): 4 modes x 3 models x {affine, stored metric}.
 #pragma once
 #include "kernels.h"
-#include "op_kernel.cuh"
+#include "plane_kernel.cuh"
 
 namespace feod {
 
 template <int ND, int NQ, int MODE, int MODEL, bool AFF>
 static cudaError_t launch_one(int grid, const OpParams& P, const Tables& T, const OpPtrs& p, cudaStream_t st) {
-  using S = OpShape<ND, NQ, MODE>;
-  op_kernel<ND, NQ, MODE, MODEL, AFF><<<grid, S::NT, S::SMEM_BYTES, st>>>(P, T, p.in0, p.in1, p.out0, p.out1,
+  using S = PShape<ND, MODE>;
+  plane_kernel<ND, MODE, MODEL, AFF><<<grid, S::NT, S::SMEM_BYTES, st>>>(P, T, p.in0, p.in1, p.out0, p.out1,
                                                                           p.shell0, p.shell1, p.gout);
   return cudaGetLastError();
 }
 
 template <int ND, int NQ, int MODE, int MODEL, bool AFF>
 static cudaError_t prep_one() {
-  using S = OpShape<ND, NQ, MODE>;
-  return cudaFuncSetAttribute(op_kernel<ND, NQ, MODE, MODEL, AFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  using S = PShape<ND, MODE>;
+  return cudaFuncSetAttribute(plane_kernel<ND, MODE, MODEL, AFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)S::SMEM_BYTES);
 }
 
@@ -48,12 +48,12 @@ static cudaError_t prep_mode() {
 
 template <>
 bool brick_info<FEOD_ND>(BrickInfo* bi) {
-  using S = OpShape<FEOD_ND, FEOD_ND, MODE_RES>;
+  using S = PShape<FEOD_ND, MODE_RES>;
   bi->BX = S::BX; bi->BY = S::BY; bi->BZ = S::BZ; bi->threads = S::NT; bi->shell = S::SHELL;
-  bi->smem[MODE_RES] = OpShape<FEOD_ND, FEOD_ND, MODE_RES>::SMEM_BYTES;
-  bi->smem[MODE_JVP] = OpShape<FEOD_ND, FEOD_ND, MODE_JVP>::SMEM_BYTES;
-  bi->smem[MODE_JVPRES] = OpShape<FEOD_ND, FEOD_ND, MODE_JVPRES>::SMEM_BYTES;
-  bi->smem[MODE_DESIGN] = OpShape<FEOD_ND, FEOD_ND, MODE_DESIGN>::SMEM_BYTES;
+  bi->smem[MODE_RES] = PShape<FEOD_ND, MODE_RES>::SMEM_BYTES;
+  bi->smem[MODE_JVP] = PShape<FEOD_ND, MODE_JVP>::SMEM_BYTES;
+  bi->smem[MODE_JVPRES] = PShape<FEOD_ND, MODE_JVPRES>::SMEM_BYTES;
+  bi->smem[MODE_DESIGN] = PShape<FEOD_ND, MODE_DESIGN>::SMEM_BYTES;
   return true;
 }
 
