@@ -2,57 +2,62 @@
 // brick of hexahedra per CTA (Eq. 1 at :155, Eq. 2 at :160, the
 // adjoint load of :199). DESIGN.md §6 is the prose version of this file.
 //
-// Work decomposition. A CTA owns a BX x BY tile of elements and sweeps BZ
-// element layers along z. Each element of the current layer is worked on by
-// ND*ND threads arranged as ND lane-groups of ND lanes (a group never straddles
-// a warp). A group's role changes with the phase:
-//   node phase (B, x-y part)   group = DOF plane c of the element, lane = x-point i:
-//       V[b]  = sum_a B[i][a] u[a][b][c]              (x contraction)
-//       W[j]  = sum_b B[j][b] V[b],  Wy[j] = sum_b G[j][b] V[b]   (y contraction)
-//       -> written once to the element's exchange buffer (2 channels)
-//   point phase (B z-part, D, B^T z-part)   group = y-point j, lane = x-point i:
-//       U[l] = sum_c B[l][c] W[c],  Uz[l] = sum_c G[l][c] W[c],  Uy[l] = sum_c B[l][c] Wy[c]
-//       Ux    = sum_m Dh[i][m] U[m]   (collocated x-derivative: the ND lanes of
-//                                      the group hold the x-line; shuffles)
-//       D at the point (double or dual<double>), then the transposed chain:
-//       Ax = V + sum_m Dh[m][i] Fx[m]  (shuffles), PA[c] += B[l][c] Ax + G[l][c] Fz,
-//       PY[c] += B[l][c] Fy           -> written back in place (2 channels)
-//   node phase (B^T, x-y part)  group = DOF plane c, lane = x-point i:
-//       Q[b] = sum_j B[j][b] PA[j] + G[j][b] PY[j];  r[a][b] = sum_i B[i][a] Q[i][b]
-//       (the sum over i is a shuffle reduce-scatter; lane a keeps r[a][.])
-//   G^T: every element adds its ND x ND plane results into a shared output ring
-//       of DOF planes, four x-y colour classes one after the other (elements of
-//       one class share no DOF) -> a fixed summation order, no atomics. Points
-//       on a face shared with a neighbouring brick go to this brick's shell
-//       slab and are summed by fixup_kernel in a fixed order.
-// The DOF planes of u (and v / lambda) stream into a shared ring with cp.async
-// one layer ahead; the per-point metric (perturbed meshes) is read from HBM
-// straight into registers one point-row ahead, with an L2 bulk prefetch of the
-// next layer.
+// Warp-specialised z-sweep. A CTA owns a BX x BY tile of elements and sweeps BZ
+// element layers along z. It runs NWC compute warps and one IO warp that talk
+// only through shared memory and mbarriers (no block-wide barrier in the loop):
+//
+//   IO warp      streams the DOF planes of u (and v / lambda) into a ring with
+//                cp.async, two layers ahead (ring_full / ring_empty); gathers
+//                the element results of the previous layer (e_full / e_empty),
+//                sums every tile DOF's <= 4 x-y contributions in a fixed order,
+//                carries the layer's top DOF plane in registers, applies P^T and
+//                stores (owned DOFs to the output, brick-face DOFs to the shell
+//                slab summed later by fixup_kernel) -> deterministic, no atomics.
+//   compute      each element of the layer is worked on by ND*ND threads, ND
+//   warps        lane-groups of ND lanes (a group never straddles a warp); the
+//                group's role changes with the phase:
+//     node phase (B, x-y)     group = DOF plane c, lane = x-point i:
+//        V[b] = sum_a B[i][a] u[a][b][c],  Vx[b] = sum_a G[i][a] u[a][b][c]
+//        W[j] = sum_b B[j][b] V[b],  Wy[j] = sum_b G[j][b] V[b],  Wx[j] = sum_b B[j][b] Vx[b]
+//        -> the element's exchange slot (3 channels)
+//     point phase (B z, D, B^T z)  group = y-point j, lane = x-point i, loop over l:
+//        U = sum_c B[l][c] W[c], Uz = sum_c G[l][c] W[c], Ux = .. Wx, Uy = .. Wy
+//        D at the point (double or dual<double>), then
+//        PX[c] += B[l][c] Fx,  PY[c] += B[l][c] Fy,  PZ[c] += G[l][c] Fz + B[l][c] V
+//        -> back into the thread's own slot (3 channels)
+//     node phase (B^T, x-y)   group = DOF plane c, lane = x-point i:
+//        QX[b] = sum_j B[j][b] PX[j],  QW[b] = sum_j G[j][b] PY[j] + B[j][b] PZ[j]
+//        r[a][b] = sum_i G[i][a] QX_i[b] + B[i][a] QW_i[b]  (shuffle reduce-scatter
+//        over the group; lane a keeps r[a][.])  -> element buffer for the IO warp
+// The per-point metric (perturbed meshes) is read from HBM straight into
+// registers one point-row ahead, with an L2 bulk prefetch of the next layer.
 #pragma once
 #include "common.cuh"
 #include "dual.cuh"
 #include "physics.cuh"
 
+#ifndef FEOD_MINB_OVERRIDE
+#define FEOD_MINB_OVERRIDE 0
+#endif
 namespace feod {
 
 template <int ND> struct PlaneTile;
-template <> struct PlaneTile<2> { static constexpr int BX = 8, BY = 8, BZ = 16; };
+template <> struct PlaneTile<2> { static constexpr int BX = 8, BY = 4, BZ = 16; };
 template <> struct PlaneTile<3> { static constexpr int BX = 4, BY = 4, BZ = 16; };
-template <> struct PlaneTile<4> { static constexpr int BX = 4, BY = 4, BZ = 16; };
+template <> struct PlaneTile<4> { static constexpr int BX = 4, BY = 2, BZ = 16; };
 template <> struct PlaneTile<5> { static constexpr int BX = 4, BY = 2, BZ = 8; };
 template <> struct PlaneTile<6> { static constexpr int BX = 2, BY = 2, BZ = 8; };
 template <> struct PlaneTile<7> { static constexpr int BX = 2, BY = 2, BZ = 8; };
 
-// ---- compile-time bank-conflict model of the exchange buffer --
+// ---- compile-time bank-conflict model of the exchange slot ----
 // Lane L of warp 0: group g = L / ND, lane-in-group i = L % ND, element e = g / ND,
 // role r = g % ND. Element slot stride SE, x-point stride SI, role stride SJ.
-//  node-phase 8-byte accesses  addr = e SE + i SI + r          (per half-warp)
-//  point-phase 16-byte accesses addr = e SE + i SI + r SJ + 2m (per quarter-warp)
+//  node-phase 8-byte accesses   addr = e SE + i SI + r          (per half-warp)
+//  point-phase 16-byte accesses addr = e SE + i SI + r SJ + 2m  (per quarter-warp)
 constexpr int xb_cost(int nd, int SI, int SJ, int SE) {
   const int gpw = 32 / nd;
   int cost = 0;
-  for (int half = 0; half < 2; ++half) {          // 8-byte: 16 lanes, 16 double-banks
+  for (int half = 0; half < 2; ++half) {
     int cnt[16] = {};
     int seen[16] = {};
     int ns = 0;
@@ -71,7 +76,7 @@ constexpr int xb_cost(int nd, int SI, int SJ, int SE) {
     for (int b = 0; b < 16; ++b) mx = cnt[b] > mx ? cnt[b] : mx;
     cost += mx;
   }
-  for (int q = 0; q < 4; ++q) {                   // 16-byte: 8 lanes, 8 bank quads
+  for (int q = 0; q < 4; ++q) {
     int cnt[8] = {};
     for (int L = 8 * q; L < 8 * q + 8; ++L) {
       const int g = L / nd;
@@ -89,10 +94,11 @@ constexpr int xb_cost(int nd, int SI, int SJ, int SE) {
 
 struct XbPad { int SI, SJ, SE; };
 
-constexpr XbPad xb_pad(int nd, int nin) {
-  XbPad best{2 * nd, 2 * nd * nd, 2 * nd * nd * nd * nin};
+constexpr XbPad xb_pad(int nd, int nin, int nch) {
+  const int s0 = (nch * nd + 1) / 2 * 2;
+  XbPad best{s0, s0 * nd, s0 * nd * nd * nin};
   int bc = 1 << 30;
-  for (int si = 2 * nd; si <= 2 * nd + 14; si += 2)
+  for (int si = s0; si <= s0 + 14; si += 2)
     for (int sj = nd * si; sj <= nd * si + 14; sj += 2)
       for (int pe = 0; pe <= 14; pe += 2) {
         const int se = nin * nd * sj + pe;
@@ -102,8 +108,7 @@ constexpr XbPad xb_pad(int nd, int nin) {
   return best;
 }
 
-// DOF-plane stride of the shared rings: make the ring slots land on different
-// bank pairs (stride = 2 mod 16 doubles).
+// DOF-plane stride of the input ring: ring slots land on different bank pairs.
 constexpr int plane_pad(int n) { return n + ((2 - n % 16) + 16) % 16; }
 
 template <int ND, int MODE>
@@ -113,35 +118,59 @@ struct PShape {
   static constexpr int EL = BX * BY;                         // elements per layer
   static constexpr int GPW = 32 / ND;                        // lane groups per warp
   static constexpr int NG = EL * ND;                         // groups in use
-  static constexpr int NW = (NG + GPW - 1) / GPW;
-  static constexpr int NT = 32 * NW;
+  static constexpr int NWC = (NG + GPW - 1) / GPW;           // compute warps
+  static constexpr int NTC = 32 * NWC;
+  static constexpr int NT = NTC + 32;                        // + the IO warp
   static constexpr bool WARP_ELEM = (32 % (ND * ND)) == 0;   // an element never straddles a warp
-  static constexpr int MINB = (512 / NT) < 1 ? 1 : ((512 / NT) > 4 ? 4 : (512 / NT));
+  static constexpr int MINB = FEOD_MINB_OVERRIDE > 0 ? FEOD_MINB_OVERRIDE : ((65536 / (NT * 128)) < 1 ? 1 : (65536 / (NT * 128)));
   static constexpr int LXF = K * BX + 1, LYF = K * BY + 1;
-  static constexpr int PLANE = plane_pad(LXF * LYF);
-  static constexpr int RIN = 2 * K + 1;                      // current layer (ND planes) + next layer (K planes)
-  static constexpr int ROUT = K + 1;
+  static constexpr int NPOS = LXF * LYF;
+  static constexpr int PLANE = plane_pad(NPOS);
+  static constexpr int RIN = 2 * K + 1;                      // current layer (ND planes) + next (K)
   static constexpr int NIN = (MODE == MODE_RES) ? 1 : 2;
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
-  static constexpr XbPad XP = xb_pad(ND, NIN);
+  static constexpr int NCH = 3;                              // exchange channels
+  static constexpr XbPad XP = xb_pad(ND, NIN, NCH);
   static constexpr int SI = XP.SI, SJ = XP.SJ, SE = XP.SE, SF = ND * SJ;
-  static constexpr int OUTSZ = (NOUT * ROUT * PLANE + 1) / 2 * 2;
+  // element buffer (compute -> IO), per layer parity and output: [EL][c][b][a],
+  // plane stride SC padded so that the lanes writing one b hit distinct banks
+  static constexpr int SC = ND <= 4 ? ND * ND + ((ND - ND * ND) % 16 + 16) % 16 : ND * ND + 1;
+  static constexpr int EBE = ND * SC;                        // per element
+  static constexpr int EBUF = (NOUT > 0 ? NOUT : 0) * EL * EBE;
+  static constexpr int NPIO = (NPOS + 31) / 32;              // tile positions per IO lane
   static constexpr int INSZ = (NIN * RIN * PLANE + 1) / 2 * 2;
-  static constexpr int SMEM_DOUBLES = INSZ + OUTSZ + EL * SE;
+  static constexpr int TAB = (4 * ND * ND + 1) / 2 * 2;      // per-lane 1D tables
+  static constexpr int SMEM_DOUBLES = INSZ + TAB + EL * SE + 2 * EBUF + 8;   // + 8 mbarriers
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
   static constexpr int LZF = K * BZ + 1;
   static constexpr int SHELL = LXF * LYF * LZF - (LXF - 2) * (LYF - 2) * (LZF - 2);
-  static_assert(SE >= NIN * SF, "exchange slot too small");
+  static_assert(EL * EBE < 65536, "packed 16-bit element-buffer offsets");
 };
 
+// ---- async copies and mbarriers (PTX) -----------------------------------------
+FEOD_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 // 8-byte asynchronous global -> shared copy (LDGSTS). The L-vector row pitch
 // 8(kn+1) B is not 16-byte aligned, so TMA tensor maps cannot describe it.
 FEOD_DEV void cp_async8(double* smem_dst, const double* gsrc) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
-FEOD_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-FEOD_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// arrive on the mbarrier when all prior cp.async of this thread have landed
+FEOD_DEV void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+FEOD_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+FEOD_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+FEOD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 // Streaming metric load that the compiler may not sink toward its use.
 FEOD_DEV double ld_stream(const double* p) {
@@ -155,16 +184,15 @@ FEOD_DEV void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <bool WARP_ELEM>
+// Barrier among the compute threads of one element: a warp barrier when an
+// element never straddles a warp, else named barrier 1 over all compute warps.
+template <bool WARP_ELEM, int NTC>
 FEOD_DEV void elem_sync() {
   if constexpr (WARP_ELEM) __syncwarp();
-  else __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"n"(NTC) : "memory");
 }
 
-template <int ND>
-FEOD_DEV double grp_shfl(double v, int src) {
-  return __shfl_sync(0xffffffffu, v, src);
-}
+FEOD_DEV double grp_shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
 template <int ND, int MODE, int MODEL, bool AFFINE>
 __global__ void __launch_bounds__(PShape<ND, MODE>::NT, PShape<ND, MODE>::MINB)
@@ -177,11 +205,183 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   constexpr int NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
   extern __shared__ __align__(16) double smem[];
   double* ring_in = smem;                   // [NIN][RIN][PLANE]
-  double* ring_out = smem + S::INSZ;        // [NOUT][ROUT][PLANE]
-  double* xb = ring_out + S::OUTSZ;         // [EL][SE] exchange slots
+  double* tab = smem + S::INSZ;             // [4][ND lanes][ND]: Brow, Grow, Bt, Gt
+  double* xb = tab + S::TAB;                // [EL][SE] exchange slots (compute warps)
+  double* ebuf = xb + S::EL * S::SE;        // [2 parity][NOUT][EL][EBE] element results
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ebuf + 2 * S::EBUF);
+  uint64_t* ring_full = bars;               // [2] layer z's DOF planes landed      (IO -> compute)
+  uint64_t* ring_empty = bars + 2;          // [2] layer z's node phase done         (compute -> IO)
+  uint64_t* e_full = bars + 4;              // [2] layer z's element results written (compute -> IO)
+  uint64_t* e_empty = bars + 6;             // [2] layer z's element results consumed (IO -> compute)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  const int brick = blockIdx.x;
+  const int bx = brick % P.nbx, by = (brick / P.nbx) % P.nby, bz = brick / (P.nbx * P.nby);
+  const int ex0 = bx * S::BX, ey0 = by * S::BY, ez0 = bz * S::BZ;
+  const int bxr = min(S::BX, P.nx - ex0), byr = min(S::BY, P.ny - ey0), bzr = min(S::BZ, P.nz - ez0);
+  const int LX = K * bxr + 1, LY = K * byr + 1, LZ = K * bzr + 1;
+  const int gX0 = K * ex0, gY0 = K * ey0, gZ0 = K * ez0;
+
+  // per-lane rows of the 1D tables (lane i): Brow[a] = B[i][a], Grow[a] = G[i][a];
+  // rotated for the backward reduce-scatter (lane (i-k)%ND receives the term):
+  // Bt[k] = B[i][(i-k)%ND], Gt[k] = G[i][(i-k)%ND]
+  for (int t = tid; t < ND * ND; t += S::NT) {
+    const int i = t / ND, k = t % ND, dn = (i - k + ND) % ND;
+    tab[t] = T.B[i][k];
+    tab[ND * ND + t] = T.G[i][k];
+    tab[2 * ND * ND + t] = T.B[i][dn];
+    tab[3 * ND * ND + t] = T.G[i][dn];
+  }
+  if (tid == 0) {
+    // ring_full: one cp.async-arrival per IO lane (+ one plain arrival per lane for
+    // the synchronously masked lambda of the design mode)
+    const uint32_t nfull = (MODE == MODE_DESIGN) ? 64u : 32u;
+    mbar_init(&ring_full[0], nfull);
+    mbar_init(&ring_full[1], nfull);
+    mbar_init(&ring_empty[0], S::NWC);
+    mbar_init(&ring_empty[1], S::NWC);
+    mbar_init(&e_full[0], S::NWC);
+    mbar_init(&e_full[1], S::NWC);
+    mbar_init(&e_empty[0], 1);
+    mbar_init(&e_empty[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == S::NWC) {
+    // =========================== IO warp ===================================
+    const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx;
+    const bool lowY = ey0 > 0, highY = ey0 + byr < P.ny;
+    const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
+    // tile-plane positions of this lane: idx = lane + 32 m
+    //   pg     in-plane global offset (gX0 + X) + Mx (gY0 + Y)
+    //   pinfo  bit0 valid, bit1 on a shared x/y brick face, bit2 Dirichlet in x/y,
+    //          bits 3.. index on the shell ring of a middle z-plane
+    //   pxy    X + LX Y (shell index on the bottom / top plane)
+    //   pofs   up to four element-buffer offsets (16-bit packed), fixed order
+    int pg[S::NPIO], pinfo[S::NPIO], pxy[S::NPIO], pcnt[S::NPIO];
+    uint32_t pofs[S::NPIO][2];
+#pragma unroll
+    for (int m = 0; m < S::NPIO; ++m) {
+      const int idx = lane + 32 * m;
+      const int X = idx % S::LXF, Y = idx / S::LXF;
+      const bool v = idx < S::NPOS && X < LX && Y < LY;
+      const int gx = gX0 + X, gy = gY0 + Y;
+      pg[m] = v ? gx + P.Mx * gy : 0;
+      const bool shxy = (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) || (Y == LY - 1 && highY);
+      const bool dxy = ((P.faces & 1u) && gx == 0) || ((P.faces & 2u) && gx == P.Mx - 1) ||
+                       ((P.faces & 4u) && gy == 0) || ((P.faces & 8u) && gy == P.My - 1);
+      const int ringpos = (Y == 0) ? X : (Y == LY - 1) ? LX + X : 2 * LX + 2 * (Y - 1) + (X == 0 ? 0 : 1);
+      pinfo[m] = (v ? 1 : 0) | (shxy ? 2 : 0) | (dxy ? 4 : 0) | (ringpos << 3);
+      pxy[m] = X + LX * Y;
+      int cx[2] = {0, 0}, ax[2] = {0, 0}, cy[2] = {0, 0}, ay[2] = {0, 0}, nxc = 1, nyc = 1;
+      cx[0] = min(X / K, max(bxr - 1, 0));
+      ax[0] = X - K * cx[0];
+      if (ax[0] == 0 && cx[0] > 0) { cx[1] = cx[0]; ax[1] = 0; cx[0] -= 1; ax[0] = K; nxc = 2; }
+      cy[0] = min(Y / K, max(byr - 1, 0));
+      ay[0] = Y - K * cy[0];
+      if (ay[0] == 0 && cy[0] > 0) { cy[1] = cy[0]; ay[1] = 0; cy[0] -= 1; ay[0] = K; nyc = 2; }
+      uint32_t o4[4] = {0, 0, 0, 0};
+      int n = 0;
+      for (int t = 0; t < nyc; ++t)
+        for (int q = 0; q < nxc; ++q)
+          o4[n++] = (uint32_t)((cx[q] + S::BX * cy[t]) * S::EBE + ay[t] * ND + ax[q]);
+      pofs[m][0] = o4[0] | (o4[1] << 16);
+      pofs[m][1] = o4[2] | (o4[3] << 16);
+      pcnt[m] = v ? n : 0;
+    }
+
+    // G: stream DOF plane p (brick-local z index) into its ring slot
+    auto load_plane = [&](int p) {
+      const int slot = p % S::RIN;
+      const int64_t zoff = (int64_t)P.Mx * P.My * (gZ0 + p);
+      const bool dz = ((P.faces & 16u) && gZ0 + p == 0) || ((P.faces & 32u) && gZ0 + p == P.Mz - 1);
+#pragma unroll
+      for (int m = 0; m < S::NPIO; ++m) {
+        if (!(pinfo[m] & 1)) continue;
+        const int idx = lane + 32 * m;
+        const int64_t g = zoff + pg[m];
+        cp_async8(ring_in + slot * S::PLANE + idx, in0 + g);
+        if constexpr (S::NIN == 2) {
+          double* dst = ring_in + (S::RIN + slot) * S::PLANE + idx;
+          if constexpr (MODE == MODE_DESIGN) {
+            // lambda's Dirichlet entries are masked (reading A14)
+            *dst = ((pinfo[m] & 4) || dz) ? 0.0 : __ldg(in1 + g);
+          } else {
+            cp_async8(dst, in1 + g);
+          }
+        }
+      }
+    };
+    auto load_layer = [&](int zz) {   // the DOF planes layer zz needs that are not resident yet
+      const int p0 = (zz == 0) ? 0 : K * zz + 1;
+      for (int p = p0; p <= K * zz + K; ++p) load_plane(p);
+      uint64_t* bar = &ring_full[zz & 1];
+      cp_async_arrive(bar);
+      if constexpr (MODE == MODE_DESIGN) mbar_arrive(bar);
+    };
+
+    // P^T + store of the finished value v of output o at position m, DOF plane p
+    auto store_dof = [&](int o, int m, int p, double v) {
+      const int info = pinfo[m];
+      const bool shared = (info & 2) || (p == 0 && lowZ) || (p == LZ - 1 && highZ);
+      if (shared) {
+        const int base = LX * LY, ring = 2 * LX + 2 * (LY - 2);
+        const int rank = (p == 0) ? pxy[m] : (p == LZ - 1) ? base + (LZ - 2) * ring + pxy[m]
+                                                            : base + (p - 1) * ring + (info >> 3);
+        (o == 0 ? shell0 : shell1)[(int64_t)brick * P.shell_stride + rank] = v;
+      } else {
+        const int gz = gZ0 + p;
+        const bool dir = (info & 4) || ((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1);
+        (o == 0 ? out0 : out1)[(int64_t)P.Mx * P.My * gz + pg[m]] = dir ? 0.0 : v;
+      }
+    };
+
+    double carry[S::NOUT > 0 ? S::NOUT : 1][S::NPIO];
+#pragma unroll
+    for (int o = 0; o < (S::NOUT > 0 ? S::NOUT : 1); ++o)
+#pragma unroll
+      for (int m = 0; m < S::NPIO; ++m) carry[o][m] = 0.0;
+
+    load_layer(0);
+    if (bzr > 1) load_layer(1);
+    for (int z = 0; z < bzr; ++z) {
+      if (z + 2 < bzr) {
+        mbar_wait(&ring_empty[z & 1], (z >> 1) & 1);   // compute is done reading layer z's planes
+        load_layer(z + 2);
+      }
+      if constexpr (S::NOUT > 0) {
+        mbar_wait(&e_full[z & 1], (z >> 1) & 1);
+        const double* eb = ebuf + (z & 1) * S::EBUF;
+        // G^T: every tile DOF sums its (<= 4) x-y contributions in a fixed order;
+        // z-sharing through the carried top plane
+#pragma unroll
+        for (int m = 0; m < S::NPIO; ++m) {
+          if (pcnt[m] == 0) continue;
+          const int off0 = pofs[m][0] & 0xffff, off1 = pofs[m][0] >> 16;
+          const int off2 = pofs[m][1] & 0xffff, off3 = pofs[m][1] >> 16;
+#pragma unroll
+          for (int c = 0; c <= K; ++c) {
+#pragma unroll
+            for (int o = 0; o < S::NOUT; ++o) {
+              const double* e = eb + o * S::EL * S::EBE + c * S::SC;
+              double v = (c == 0) ? carry[o][m] : 0.0;
+              v += e[off0];
+              if (pcnt[m] > 1) v += e[off1];
+              if (pcnt[m] > 2) { v += e[off2]; v += e[off3]; }
+              if (c < K || z == bzr - 1) store_dof(o, m, K * z + c, v);
+              else carry[o][m] = v;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&e_empty[z & 1]);
+      }
+    }
+  } else {
+
+  // ============================== compute warps ==============================
   const int gw = lane / ND;                          // group within the warp
   const int li = lane - gw * ND;                     // lane within the group: x-point i (or node a)
   const int G = warp * S::GPW + gw;
@@ -191,98 +391,23 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   const int gr = Gc - el * ND;                       // group role: plane c / point row j
   const int gbase = lvalid ? lane - li : 0;
   const int lic = lvalid ? li : 0;
-
-  const int brick = blockIdx.x;
-  const int bx = brick % P.nbx, by = (brick / P.nbx) % P.nby, bz = brick / (P.nbx * P.nby);
-  const int ex0 = bx * S::BX, ey0 = by * S::BY, ez0 = bz * S::BZ;
-  const int bxr = min(S::BX, P.nx - ex0), byr = min(S::BY, P.ny - ey0), bzr = min(S::BZ, P.nz - ez0);
-  const int LX = K * bxr + 1, LY = K * byr + 1, LZ = K * bzr + 1;
-  const int gX0 = K * ex0, gY0 = K * ey0, gZ0 = K * ez0;
-
   const int exl = el % S::BX, eyl = el / S::BX;
   const bool evalid = lvalid && exl < bxr && eyl < byr;
   const int X0 = evalid ? K * exl : 0, Y0 = evalid ? K * eyl : 0;
-  const int colour = (exl & 1) + 2 * (eyl & 1);
 
-  // per-lane rows of the 1D tables (lane i; indices rotated for the shuffles)
-  double Brow[ND], Dx[ND], Dt[ND], Bt[ND];
-#pragma unroll
-  for (int a = 0; a < ND; ++a) Brow[a] = T.B[lic][a];
-#pragma unroll
-  for (int k = 0; k < ND; ++k) {
-    const int up = (lic + k) % ND, dn = (lic - k + ND) % ND;
-    Dx[k] = T.D[lic][up];   // all-gather: Ux = sum_k Dx[k] U[(i+k)%ND]
-    Dt[k] = T.D[lic][dn];   // reduce-scatter: lane (i-k) receives D[i][i-k] Fx[i]
-    Bt[k] = T.B[lic][dn];   // reduce-scatter: lane (i-k) receives B[i][i-k] Q[i][.]
-  }
+  const double* Brow = tab + lic * ND;
+  const double* Grow = tab + ND * ND + lic * ND;
+  const double* Bt = tab + 2 * ND * ND + lic * ND;
+  const double* Gt = tab + 3 * ND * ND + lic * ND;
   int src[ND];
 #pragma unroll
   for (int k = 0; k < ND; ++k) src[k] = gbase + (lic + k) % ND;
 
-  // ---- G (gather): stream DOF plane p (brick-local z index) into its ring slot
-  auto load_plane = [&](int p) {
-    const int slot = p % S::RIN;
-    const int64_t zoff = (int64_t)P.Mx * P.My * (gZ0 + p);
-    for (int idx = tid; idx < S::LXF * S::LYF; idx += S::NT) {
-      const int X = idx % S::LXF, Y = idx / S::LXF;
-      if (X >= LX || Y >= LY) continue;
-      const int64_t g = zoff + (int64_t)(gX0 + X) + (int64_t)P.Mx * (gY0 + Y);
-      cp_async8(ring_in + slot * S::PLANE + idx, in0 + g);
-      if constexpr (S::NIN == 2) {
-        double* dst = ring_in + (S::RIN + slot) * S::PLANE + idx;
-        if constexpr (MODE == MODE_DESIGN) {
-          // lambda's Dirichlet entries are masked (reading A14)
-          *dst = is_dirichlet(gX0 + X, gY0 + Y, gZ0 + p, P.Mx, P.My, P.Mz, P.faces) ? 0.0 : __ldg(in1 + g);
-        } else {
-          cp_async8(dst, in1 + g);
-        }
-      }
-    }
-  };
-  for (int p = 0; p <= K; ++p) load_plane(p);
-  cp_async_commit();
-  if constexpr (S::NOUT > 0)
-    for (int i = tid; i < S::NOUT * S::ROUT * S::PLANE; i += S::NT) ring_out[i] = 0.0;
-
-  const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx;
-  const bool lowY = ey0 > 0, highY = ey0 + byr < P.ny;
-  const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
-
-  // ---- P^T + store of a finished output plane p (brick-local), then clear its slot
-  auto flush_plane = [&](int p) {
-    const int slot = p % S::ROUT;
-    const int64_t zoff = (int64_t)P.Mx * P.My * (gZ0 + p);
-    for (int idx = tid; idx < S::LXF * S::LYF; idx += S::NT) {
-      const int X = idx % S::LXF, Y = idx / S::LXF;
-      if (X >= LX || Y >= LY) continue;
-      const bool shared = (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) || (Y == LY - 1 && highY) ||
-                          (p == 0 && lowZ) || (p == LZ - 1 && highZ);
-      const int gx = gX0 + X, gy = gY0 + Y, gz = gZ0 + p;
-      const bool dir = is_dirichlet(gx, gy, gz, P.Mx, P.My, P.Mz, P.faces);
-      const int64_t g = zoff + (int64_t)gx + (int64_t)P.Mx * gy;
-#pragma unroll
-      for (int o = 0; o < S::NOUT; ++o) {
-        double* cell = ring_out + (o * S::ROUT + slot) * S::PLANE + idx;
-        const double v = *cell;
-        *cell = 0.0;
-        if (shared) {
-          (o == 0 ? shell0 : shell1)[(int64_t)brick * P.shell_stride + shell_rank(X, Y, p, LX, LY, LZ)] = v;
-        } else {
-          (o == 0 ? out0 : out1)[g] = dir ? 0.0 : v;
-        }
-      }
-    }
-  };
-
   double* const xe = xb + el * S::SE;   // this element's exchange slot
+  const double wij = T.w[lic] * T.w[gr];
+  const double iwij2 = T.wi2[lic] * T.wi2[gr];
 
   for (int z = 0; z < bzr; ++z) {
-    cp_async_wait_all();
-    __syncthreads();                                 // planes K z .. K z + K resident; previous layer done
-    if (z + 1 < bzr) {
-      for (int p = K * (z + 1) + 1; p <= K * (z + 1) + K; ++p) load_plane(p);
-      cp_async_commit();
-    }
     const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + z));
     // metric of this thread's points (i = li, j = gr, l): layout [E][l][6][j][i]
     const double* gm = nullptr;
@@ -299,76 +424,67 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     double rho_e = 0.0;
     if constexpr (MODEL == HEAT) rho_e = evalid ? __ldg(P.rho + eg) : 1.0;
 
+    mbar_wait(&ring_full[z & 1], (z >> 1) & 1);
+
     // ---- node phase (B, x and y): group = plane c = gr, lane = x-point i
 #pragma unroll
     for (int f = 0; f < S::NIN; ++f) {
       const double* pl = ring_in + (f * S::RIN + (K * z + gr) % S::RIN) * S::PLANE + X0 + S::LXF * Y0;
-      double V[ND];
+      double V[ND], Vx[ND];
 #pragma unroll
       for (int b = 0; b < ND; ++b) {
-        double acc = 0.0;
+        double acc = 0.0, accx = 0.0;
 #pragma unroll
-        for (int a = 0; a < ND; ++a) acc = fma(Brow[a], pl[a + S::LXF * b], acc);
+        for (int a = 0; a < ND; ++a) {
+          const double ua = pl[a + S::LXF * b];
+          acc = fma(Brow[a], ua, acc);
+          accx = fma(Grow[a], ua, accx);
+        }
         V[b] = acc;
+        Vx[b] = accx;
       }
       double* xo = xe + f * S::SF + lic * S::SI + gr;
 #pragma unroll
       for (int j = 0; j < ND; ++j) {
-        double w = 0.0, wy = 0.0;
+        double w = 0.0, wy = 0.0, wx = 0.0;
 #pragma unroll
         for (int b = 0; b < ND; ++b) {
           w = fma(T.B[j][b], V[b], w);
           wy = fma(T.G[j][b], V[b], wy);
+          wx = fma(T.B[j][b], Vx[b], wx);
         }
         if (lvalid) {
           xo[j * S::SJ] = w;
-          xo[j * S::SJ + ND] = wy;
+          xo[j * S::SJ + ND] = wx;
+          xo[j * S::SJ + 2 * ND] = wy;
         }
       }
     }
-    elem_sync<S::WARP_ELEM>();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring_empty[z & 1]);   // this warp no longer reads layer z's planes
+    elem_sync<S::WARP_ELEM, S::NTC>();
 
-    // ---- point phase: group = y-point j = gr, lane = x-point i
-    double U[S::NIN][NQ], Uz[S::NIN][NQ], Uy[S::NIN][NQ];
+    // ---- point phase: group = y-point j = gr, lane = x-point i; inputs stay in registers
+    double w[S::NIN][3 * ND];   // [W | Wx | Wy] over c
 #pragma unroll
     for (int f = 0; f < S::NIN; ++f) {
       const double* xi = xe + f * S::SF + gr * S::SJ + lic * S::SI;
-      double w[ND], wy[ND];
 #pragma unroll
-      for (int c = 0; c < ND; c += 2) {
-        if (c + 1 < ND) {
-          const double2 t0 = *reinterpret_cast<const double2*>(xi + c);
-          w[c] = t0.x;
-          w[c + 1] = t0.y;
-        } else {
-          w[c] = xi[c];
-        }
+      for (int c = 0; c + 1 < 3 * ND; c += 2) {
+        const double2 t0 = *reinterpret_cast<const double2*>(xi + c);
+        w[f][c] = t0.x;
+        w[f][c + 1] = t0.y;
       }
-#pragma unroll
-      for (int c = 0; c < ND; ++c) wy[c] = xi[ND + c];
-#pragma unroll
-      for (int l = 0; l < NQ; ++l) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll
-        for (int c = 0; c < ND; ++c) {
-          a0 = fma(T.B[l][c], w[c], a0);
-          a1 = fma(T.G[l][c], w[c], a1);
-          a2 = fma(T.B[l][c], wy[c], a2);
-        }
-        U[f][l] = a0;
-        Uz[f][l] = a1;
-        Uy[f][l] = a2;
-      }
+      if constexpr ((3 * ND) % 2) w[f][3 * ND - 1] = xi[3 * ND - 1];
     }
 
-    double PA[S::NOUT > 0 ? S::NOUT : 1][ND], PY[S::NOUT > 0 ? S::NOUT : 1][ND];
+    constexpr int NO1 = S::NOUT > 0 ? S::NOUT : 1;
+    double PX[NO1][ND], PY[NO1][ND], PZ[NO1][ND];
 #pragma unroll
-    for (int o = 0; o < (S::NOUT > 0 ? S::NOUT : 1); ++o)
+    for (int o = 0; o < NO1; ++o)
 #pragma unroll
-      for (int c = 0; c < ND; ++c) PA[o][c] = PY[o][c] = 0.0;
+      for (int c = 0; c < ND; ++c) PX[o][c] = PY[o][c] = PZ[o][c] = 0.0;
     double gpart = 0.0;
-    const double wij = T.w[lic] * T.w[gr];
-    const double iwij2 = T.wi2[lic] * T.wi2[gr];
 
 #pragma unroll
     for (int l = 0; l < NQ; ++l) {
@@ -389,26 +505,34 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
                            M.xz * (M.xy * M.yz - M.yy * M.xz);
         W = det * (iwij2 * T.wi2[l]);   // W = w detJ = det(M) / w^2
       }
-      // collocated x-derivative over the group's x-line
-      double Ux[S::NIN];
+      // z-contraction of row l
+      double Ul[S::NIN], Uzl[S::NIN], Uyl[S::NIN], Ux[S::NIN];
 #pragma unroll
       for (int f = 0; f < S::NIN; ++f) {
-        double ux = Dx[0] * U[f][l];
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-        for (int k = 1; k < ND; ++k) ux = fma(Dx[k], grp_shfl<ND>(U[f][l], src[k]), ux);
-        Ux[f] = ux;
+        for (int c = 0; c < ND; ++c) {
+          a0 = fma(T.B[l][c], w[f][c], a0);
+          a1 = fma(T.G[l][c], w[f][c], a1);
+          a2 = fma(T.B[l][c], w[f][ND + c], a2);
+          a3 = fma(T.B[l][c], w[f][2 * ND + c], a3);
+        }
+        Ul[f] = a0;
+        Uzl[f] = a1;
+        Ux[f] = a2;
+        Uyl[f] = a3;
       }
       double F0[4], F1[4];   // Fx, Fy, Fz, V of output 0 (and 1)
       if constexpr (MODE == MODE_RES) {
-        const double gh[3] = {Ux[0], Uy[0][l], Uz[0][l]};
+        const double gh[3] = {Ux[0], Uyl[0], Uzl[0]};
         double Fh[3];
-        flux_hat<MODEL>(U[0][l], gh, M, W, rho_e, P, Fh);
+        flux_hat<MODEL>(Ul[0], gh, M, W, rho_e, P, Fh);
         F0[0] = Fh[0]; F0[1] = Fh[1]; F0[2] = Fh[2];
         F0[3] = -P.f * W;
       } else if constexpr (MODE == MODE_JVP || MODE == MODE_JVPRES) {
         using D = dual<double>;
-        const D ud(U[0][l], U[1][l]);
-        const D gh[3] = {D(Ux[0], Ux[1]), D(Uy[0][l], Uy[1][l]), D(Uz[0][l], Uz[1][l])};
+        const D ud(Ul[0], Ul[1]);
+        const D gh[3] = {D(Ux[0], Ux[1]), D(Uyl[0], Uyl[1]), D(Uzl[0], Uzl[1])};
         D Fh[3];
         flux_hat<MODEL>(ud, gh, M, W, rho_e, P, Fh);
         F0[0] = Fh[0].d; F0[1] = Fh[1].d; F0[2] = Fh[2].d;
@@ -419,97 +543,94 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         }
       } else {   // MODE_DESIGN: seed d/drho; field 1 is lambda
         using D = dual<double>;
-        const D ud(U[0][l]);
-        const D gh[3] = {D(Ux[0]), D(Uy[0][l]), D(Uz[0][l])};
+        const D ud(Ul[0]);
+        const D gh[3] = {D(Ux[0]), D(Uyl[0]), D(Uzl[0])};
         const D rd(rho_e, 1.0);
         D Fh[3];
         flux_hat<MODEL>(ud, gh, M, W, rd, P, Fh);
-        gpart -= Ux[1] * Fh[0].d + Uy[1][l] * Fh[1].d + Uz[1][l] * Fh[2].d;
+        gpart -= Ux[1] * Fh[0].d + Uyl[1] * Fh[1].d + Uzl[1] * Fh[2].d;
       }
-      // transposed chain at the point: x (collocated, shuffles) then z
+      // transposed z-contraction at the point
 #pragma unroll
       for (int o = 0; o < S::NOUT; ++o) {
         const double* Fo = (o == 0) ? F0 : F1;
-        double ax = fma(Dt[0], Fo[0], Fo[3]);
-#pragma unroll
-        for (int k = 1; k < ND; ++k) ax += grp_shfl<ND>(Dt[k] * Fo[0], src[k]);
 #pragma unroll
         for (int c = 0; c < ND; ++c) {
-          PA[o][c] = fma(T.B[l][c], ax, fma(T.G[l][c], Fo[2], PA[o][c]));
+          PX[o][c] = fma(T.B[l][c], Fo[0], PX[o][c]);
           PY[o][c] = fma(T.B[l][c], Fo[1], PY[o][c]);
+          PZ[o][c] = fma(T.G[l][c], Fo[2], fma(T.B[l][c], Fo[3], PZ[o][c]));
         }
       }
     }
 
     if constexpr (MODE == MODE_DESIGN) {
-      elem_sync<S::WARP_ELEM>();                     // all forward inputs of the element consumed
+      elem_sync<S::WARP_ELEM, S::NTC>();             // all forward inputs of the element consumed
       if (lvalid) xe[gr * ND + lic] = gpart;
-      elem_sync<S::WARP_ELEM>();
+      elem_sync<S::WARP_ELEM, S::NTC>();
       if (evalid && gr == 0 && lic == 0) {
         double s = 0.0;
         for (int t = 0; t < ND * ND; ++t) s += xe[t];
         gout[eg] = s;
       }
+      elem_sync<S::WARP_ELEM, S::NTC>();             // sums read before the next layer's writes
     } else {
-      // write PA, PY in place of this thread's (consumed) forward inputs
+      // write PX, PY, PZ in place of this thread's (consumed) forward inputs
 #pragma unroll
       for (int o = 0; o < S::NOUT; ++o) {
         double* xo = xe + o * S::SF + gr * S::SJ + lic * S::SI;
+        double pv[3 * ND];
+#pragma unroll
+        for (int c = 0; c < ND; ++c) { pv[c] = PX[o][c]; pv[ND + c] = PY[o][c]; pv[2 * ND + c] = PZ[o][c]; }
         if (lvalid) {
 #pragma unroll
-          for (int c = 0; c < ND; c += 2) {
-            if (c + 1 < ND) *reinterpret_cast<double2*>(xo + c) = make_double2(PA[o][c], PA[o][c + 1]);
-            else xo[c] = PA[o][c];
-          }
-#pragma unroll
-          for (int c = 0; c < ND; ++c) xo[ND + c] = PY[o][c];
+          for (int c = 0; c + 1 < 3 * ND; c += 2) *reinterpret_cast<double2*>(xo + c) = make_double2(pv[c], pv[c + 1]);
+          if constexpr ((3 * ND) % 2) xo[3 * ND - 1] = pv[3 * ND - 1];
         }
       }
-      elem_sync<S::WARP_ELEM>();
+      elem_sync<S::WARP_ELEM, S::NTC>();
 
       // ---- node phase (B^T, y and x): group = plane c = gr, lane = x-point i
       double R[S::NOUT][ND];
 #pragma unroll
       for (int o = 0; o < S::NOUT; ++o) {
         const double* xi = xe + o * S::SF + lic * S::SI + gr;
-        double Q[ND];
+        double QX[ND], QW[ND];
 #pragma unroll
-        for (int b = 0; b < ND; ++b) Q[b] = 0.0;
+        for (int b = 0; b < ND; ++b) QX[b] = QW[b] = 0.0;
 #pragma unroll
         for (int j = 0; j < ND; ++j) {
-          const double pa = xi[j * S::SJ], py = xi[j * S::SJ + ND];
+          const double px = xi[j * S::SJ], py = xi[j * S::SJ + ND], pz = xi[j * S::SJ + 2 * ND];
 #pragma unroll
-          for (int b = 0; b < ND; ++b) Q[b] = fma(T.B[j][b], pa, fma(T.G[j][b], py, Q[b]));
+          for (int b = 0; b < ND; ++b) {
+            QX[b] = fma(T.B[j][b], px, QX[b]);
+            QW[b] = fma(T.G[j][b], py, fma(T.B[j][b], pz, QW[b]));
+          }
         }
-        // r[a][b] = sum_i B[i][a] Q_i[b]: lane a keeps its row
+        // r[a][b] = sum_i G[i][a] QX_i[b] + B[i][a] QW_i[b]: lane a keeps its row
 #pragma unroll
         for (int b = 0; b < ND; ++b) {
-          double r = Bt[0] * Q[b];
+          double r = fma(Gt[0], QX[b], Bt[0] * QW[b]);
 #pragma unroll
-          for (int k = 1; k < ND; ++k) r += grp_shfl<ND>(Bt[k] * Q[b], src[k]);
+          for (int k = 1; k < ND; ++k) r += grp_shfl(fma(Gt[k], QX[b], Bt[k] * QW[b]), src[k]);
           R[o][b] = r;
         }
       }
-      // ---- G^T into the output ring: four x-y colour classes in turn
-      const int slot = (K * z + gr) % S::ROUT;
+      // element results -> the IO warp (double-buffered by layer parity)
+      if (z >= 2) mbar_wait(&e_empty[z & 1], ((z >> 1) - 1) & 1);
+      double* eb = ebuf + (z & 1) * S::EBUF + el * S::EBE + gr * S::SC + lic;
+      if (lvalid) {
 #pragma unroll
-      for (int cls = 0; cls < 4; ++cls) {
-        if (cls > 0) __syncthreads();
-        if (evalid && colour == cls) {
+        for (int o = 0; o < S::NOUT; ++o)
 #pragma unroll
-          for (int o = 0; o < S::NOUT; ++o) {
-            double* cell = ring_out + (o * S::ROUT + slot) * S::PLANE + (X0 + lic) + S::LXF * Y0;
-#pragma unroll
-            for (int b = 0; b < ND; ++b) cell[S::LXF * b] += R[o][b];
-          }
-        }
+          for (int b = 0; b < ND; ++b) eb[o * S::EL * S::EBE + b * ND] = R[o][b];
       }
-      __syncthreads();
-      // planes K z .. K z + K-1 are complete (the top plane carries into the next layer)
-      for (int c = 0; c < K; ++c) flush_plane(K * z + c);
-      if (z == bzr - 1) flush_plane(K * z + K);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&e_full[z & 1]);
+      elem_sync<S::WARP_ELEM, S::NTC>();             // P reads done before the next layer's writes
     }
   }
+  }   // compute warps
+
 }
 
 }  // namespace feod
