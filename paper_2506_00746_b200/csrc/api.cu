@@ -200,8 +200,8 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   if (pe) cudaEventRecord(pe, h->st);
   if (e != cudaSuccess) return cuda_fail(e, name);
   if (mode != MODE_DESIGN) {
-    e = launch_fixup(h->P, h->k, h->bi.BX, h->bi.BY, h->bi.BZ, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
-                     mode == MODE_JVPRES ? out1 : nullptr, h->st);
+    e = fixup_nd(h->nd, h->P, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
+                 mode == MODE_JVPRES ? out1 : nullptr, h->st);
     if (e != cudaSuccess) return cuda_fail(e, name);
   }
   return FEOD_OK;

@@ -40,4 +40,17 @@ cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const 
   return cudaErrorInvalidValue;
 }
 
+cudaError_t fixup_nd(int nd, const OpParams& P, const double* shell0, double* out0, const double* shell1, double* out1,
+                     cudaStream_t st) {
+  switch (nd) {
+    case 2: return fixup_order<2>(P, shell0, out0, shell1, out1, st);
+    case 3: return fixup_order<3>(P, shell0, out0, shell1, out1, st);
+    case 4: return fixup_order<4>(P, shell0, out0, shell1, out1, st);
+    case 5: return fixup_order<5>(P, shell0, out0, shell1, out1, st);
+    case 6: return fixup_order<6>(P, shell0, out0, shell1, out1, st);
+    case 7: return fixup_order<7>(P, shell0, out0, shell1, out1, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace feod

@@ -2,6 +2,7 @@
 // NQ = k+1 points per axis): 4 modes x 3 models x {affine, stored metric}.
 #pragma once
 #include "kernels.h"
+#include "fixup.cuh"
 #include "plane_kernel.cuh"
 
 namespace feod {
@@ -76,6 +77,13 @@ cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int grid, const
     case MODE_DESIGN: return launch_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>(model, aff, grid, P, T, p, st);
   }
   return cudaErrorInvalidValue;
+}
+
+template <>
+cudaError_t fixup_order<FEOD_ND>(const OpParams& P, const double* shell0, double* out0, const double* shell1,
+                                 double* out1, cudaStream_t st) {
+  using S = PShape<FEOD_ND, MODE_RES>;
+  return launch_fixup_t<S::K, S::BX, S::BY, S::BZ>(P, shell0, out0, shell1, out1, st);
 }
 
 }  // namespace feod

@@ -19,20 +19,22 @@ struct BrickInfo { int BX, BY, BZ, threads, shell; size_t smem[4]; };
 
 cudaError_t launch_geometry(const double* verts, int nx, int ny, int nz, int nq, const Tables& T, double* geom,
                             int* bad, cudaStream_t st);
-cudaError_t launch_fixup(const OpParams& P, int K, int BX, int BY, int BZ, const double* shell0, double* out0,
-                         const double* shell1, double* out1, cudaStream_t st);
 
 // Per-order entry points (inst_kN.cu), ND = k+1, NQ = k+1.
 template <int ND> bool brick_info(BrickInfo* bi);
 template <int ND> cudaError_t prepare_order();
 template <int ND> cudaError_t launch_order(int mode, int model, bool affine, int grid, const OpParams& P,
                                            const Tables& T, const OpPtrs& p, cudaStream_t st);
+template <int ND> cudaError_t fixup_order(const OpParams& P, const double* shell0, double* out0, const double* shell1,
+                                          double* out1, cudaStream_t st);
 
 #define FEOD_DECLARE_ORDER(ND)                                                                    \
   template <> bool brick_info<ND>(BrickInfo * bi);                                                \
   template <> cudaError_t prepare_order<ND>();                                                    \
   template <> cudaError_t launch_order<ND>(int mode, int model, bool affine, int grid, const OpParams& P, \
-                                           const Tables& T, const OpPtrs& p, cudaStream_t st);
+                                           const Tables& T, const OpPtrs& p, cudaStream_t st);            \
+  template <> cudaError_t fixup_order<ND>(const OpParams& P, const double* shell0, double* out0,          \
+                                          const double* shell1, double* out1, cudaStream_t st);
 FEOD_DECLARE_ORDER(2)
 FEOD_DECLARE_ORDER(3)
 FEOD_DECLARE_ORDER(4)
@@ -44,6 +46,8 @@ bool brick_info_nd(int nd, BrickInfo* bi);
 cudaError_t prepare_nd(int nd);
 cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const OpParams& P, const Tables& T,
                       const OpPtrs& p, cudaStream_t st);
+cudaError_t fixup_nd(int nd, const OpParams& P, const double* shell0, double* out0, const double* shell1, double* out1,
+                     cudaStream_t st);
 
 // BLAS-1 (blas1.cu): deterministic fixed-grid two-stage reductions.
 constexpr int kRedBlocks = 296;
