@@ -122,7 +122,12 @@ struct PShape {
   static constexpr int NTC = 32 * NWC;
   static constexpr int NT = NTC + 32;                        // + the IO warp
   static constexpr bool WARP_ELEM = (32 % (ND * ND)) == 0;   // an element never straddles a warp
-  static constexpr int MINB = FEOD_MINB_OVERRIDE > 0 ? FEOD_MINB_OVERRIDE : ((65536 / (NT * 128)) < 1 ? 1 : (65536 / (NT * 128)));
+  // register budget: 128 per thread (occupancy first), except the two-field
+  // (tangent) modes of Q5/Q6, whose per-thread state stays in registers (one CTA per SM)
+  static constexpr int MINB = FEOD_MINB_OVERRIDE > 0 ? FEOD_MINB_OVERRIDE
+                              : (ND >= 6 && (MODE == MODE_JVP || MODE == MODE_JVPRES))
+                                    ? 1
+                                    : ((65536 / (NT * 128)) < 1 ? 1 : (65536 / (NT * 128)));
   static constexpr int LXF = K * BX + 1, LYF = K * BY + 1;
   static constexpr int NPOS = LXF * LYF;
   static constexpr int PLANE = plane_pad(NPOS);

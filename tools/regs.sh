@@ -13,7 +13,8 @@ for line in sys.stdin:
     if m: sp = m.groups(); continue
     m = re.search(r'Used (\d+) registers', line)
     if m and name:
-        t = re.search(r'ILi(\d)ELi(\d)ELi(\d)ELb(\d)', name)
+        t = re.search(r'plane_kernelILi(\d)ELi(\d)ELi(\d)ELb(\d)', name)
+        if not t: name = None; continue
         print('ND=%s mode=%s model=%s affine=%s  regs=%s spill_st=%s spill_ld=%s' % (t.groups() + (m.group(1),) + sp))
         name = None
 "
