@@ -336,7 +336,7 @@ def main():
     jvp_bytes = algorithmic_bytes(w, "jvp")
     achieved = jvp_bytes / (jvp_kernel_ms * 1e-3) / 1e9
     traffic = traffic_from_profiles(w.name)
-    roofline = {"bound": "hbm" if w.perturbed else "alu", "kernel": f"op_kernel<JVP> (fused G-B-D-B^T-G^T, {w.name})",
+    roofline = {"bound": "hbm" if w.perturbed else "alu", "kernel": f"plane_kernel<JVP> (fused G-B-D-B^T-G^T, {w.name})",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": jvp_bytes, "kernel_ms": jvp_kernel_ms}
@@ -360,7 +360,7 @@ def main():
             "data": "synthetic (seeded workloads/ recipe, SURVEY.md §8(d))", "config": config_of(w),
             "parallelism": f"replicas x{world} (no data-path collective; DESIGN.md §Multi-GPU)",
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
-            "gpu_launches": args.steps * 2,   # one fused op_kernel per feod_residual / feod_jvp
+            "gpu_launches": args.steps * 4,   # per call: the fused plane_kernel + the brick-face fixup_kernel
             "calls": {
                 "residual": {"us": t_res * 1e3, "gdof_s": N / (t_res * 1e-3) / 1e9,
                              "hbm_frac": by_res / (t_res * 1e-3) / 1e9 / peak,

@@ -14,6 +14,6 @@ if [ "${NCU:-1}" = "1" ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1
   echo "ncu launches rc=$?"
   $CMD > gpurun_out/plain2_$TAG.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:op_kernel -s 6 -c 2 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"plane_kernel|fixup" -s 12 -c 4 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
   echo "ncu full rc=$?"
 fi
