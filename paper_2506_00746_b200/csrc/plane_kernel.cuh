@@ -35,6 +35,9 @@
 #include "common.cuh"
 #include "dual.cuh"
 #include "physics.cuh"
+#ifdef FEOD_PROFILE_IO
+#include <cstdio>
+#endif
 
 #ifndef FEOD_MINB_OVERRIDE
 #define FEOD_MINB_OVERRIDE 0
@@ -137,10 +140,11 @@ struct PShape {
   static constexpr int NCH = 3;                              // exchange channels
   static constexpr XbPad XP = xb_pad(ND, NIN, NCH);
   static constexpr int SI = XP.SI, SJ = XP.SJ, SE = XP.SE, SF = ND * SJ;
-  // element buffer (compute -> IO), per layer parity and output: [EL][c][b][a],
-  // plane stride SC padded so that the lanes writing one b hit distinct banks
-  static constexpr int SC = ND <= 4 ? ND * ND + ((ND - ND * ND) % 16 + 16) % 16 : ND * ND + 1;
-  static constexpr int EBE = ND * SC;                        // per element
+  // element buffer (compute -> IO), per layer parity and output: [EL][b][a][c]
+  // with the DOF planes c fastest (the IO warp reads a node's ND planes with
+  // 16-byte loads); NDP = ND rounded up to even keeps them 16-byte aligned
+  static constexpr int NDP = (ND + 1) / 2 * 2;
+  static constexpr int EBE = ND * ND * NDP;                  // per element
   static constexpr int EBUF = (NOUT > 0 ? NOUT : 0) * EL * EBE;
   static constexpr int NPIO = (NPOS + 31) / 32;              // tile positions per IO lane
   static constexpr int INSZ = (NIN * RIN * PLANE + 1) / 2 * 2;
@@ -291,7 +295,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       int n = 0;
       for (int t = 0; t < nyc; ++t)
         for (int q = 0; q < nxc; ++q)
-          o4[n++] = (uint32_t)((cx[q] + S::BX * cy[t]) * S::EBE + ay[t] * ND + ax[q]);
+          o4[n++] = (uint32_t)((cx[q] + S::BX * cy[t]) * S::EBE + (ay[t] * ND + ax[q]) * S::NDP);
       pofs[m][0] = o4[0] | (o4[1] << 16);
       pofs[m][1] = o4[2] | (o4[3] << 16);
       pcnt[m] = v ? n : 0;
@@ -329,6 +333,9 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
 
     // P^T + store of the finished value v of output o at position m, DOF plane p
     auto store_dof = [&](int o, int m, int p, double v) {
+#ifdef FEOD_KO_STORE
+      if (v != 1.2345e300) return;
+#endif
       const int info = pinfo[m];
       const bool shared = (info & 2) || (p == 0 && lowZ) || (p == LZ - 1 && highZ);
       if (shared) {
@@ -343,47 +350,109 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       }
     };
 
+    // middle layers (brick planes 1 .. LZ-2: no bottom/top face, no z-Dirichlet
+    // plane) have an affine destination in the plane index p:
+    //   shell: brick*stride + base + (p-1)*ring + ringpos      out: Mx*My*(gZ0 + p) + pg
+    // fptr[m] points at p = 0 (an offset, possibly before the array start, never
+    // dereferenced there), fstr[m] is the per-plane stride; zero-valued on Dirichlet x/y rows
+    int64_t fptr[S::NOUT > 0 ? S::NOUT : 1][S::NPIO];
+    int fstr[S::NPIO];
+#pragma unroll
+    for (int m = 0; m < S::NPIO; ++m) {
+      const int info = pinfo[m];
+      const int base = LX * LY, ring = 2 * LX + 2 * (LY - 2);
+      const bool sh = info & 2;
+      fstr[m] = sh ? ring : P.Mx * P.My;
+#pragma unroll
+      for (int o = 0; o < (S::NOUT > 0 ? S::NOUT : 1); ++o) {
+        const double* b0 = sh ? (o == 0 ? shell0 : shell1) : (o == 0 ? out0 : out1);
+        const int64_t off = sh ? (int64_t)brick * P.shell_stride + base - ring + (info >> 3)
+                               : (int64_t)P.Mx * P.My * gZ0 + pg[m];
+        fptr[o][m] = reinterpret_cast<int64_t>(b0) + off * (int64_t)sizeof(double);
+      }
+    }
+
     double carry[S::NOUT > 0 ? S::NOUT : 1][S::NPIO];
 #pragma unroll
     for (int o = 0; o < (S::NOUT > 0 ? S::NOUT : 1); ++o)
 #pragma unroll
       for (int m = 0; m < S::NPIO; ++m) carry[o][m] = 0.0;
 
+#ifdef FEOD_PROFILE_IO
+    long long t_wre = 0, t_load = 0, t_wef = 0, t_gt = 0, t0 = clock64(), t1;
+#define FEOD_TICK(acc) do { t1 = clock64(); acc += t1 - t0; t0 = t1; } while (0)
+#else
+#define FEOD_TICK(acc) do { } while (0)
+#endif
     load_layer(0);
     if (bzr > 1) load_layer(1);
+    FEOD_TICK(t_load);
     for (int z = 0; z < bzr; ++z) {
       if (z + 2 < bzr) {
         mbar_wait(&ring_empty[z & 1], (z >> 1) & 1);   // compute is done reading layer z's planes
+        FEOD_TICK(t_wre);
         load_layer(z + 2);
+        FEOD_TICK(t_load);
       }
       if constexpr (S::NOUT > 0) {
         mbar_wait(&e_full[z & 1], (z >> 1) & 1);
+        FEOD_TICK(t_wef);
         const double* eb = ebuf + (z & 1) * S::EBUF;
         // G^T: every tile DOF sums its (<= 4) x-y contributions in a fixed order;
         // z-sharing through the carried top plane
+        // all ND planes of a contributing node come in 16-byte loads
 #pragma unroll
         for (int m = 0; m < S::NPIO; ++m) {
-          if (pcnt[m] == 0) continue;
-          const int off0 = pofs[m][0] & 0xffff, off1 = pofs[m][0] >> 16;
-          const int off2 = pofs[m][1] & 0xffff, off3 = pofs[m][1] >> 16;
+          const int n = pcnt[m];
+          if (n == 0) continue;
+          const int off[4] = {(int)(pofs[m][0] & 0xffff), (int)(pofs[m][0] >> 16), (int)(pofs[m][1] & 0xffff),
+                              (int)(pofs[m][1] >> 16)};
 #pragma unroll
-          for (int c = 0; c <= K; ++c) {
+          for (int o = 0; o < S::NOUT; ++o) {
+            const double* e = eb + o * S::EL * S::EBE;
+            double v[S::NDP];
 #pragma unroll
-            for (int o = 0; o < S::NOUT; ++o) {
-              const double* e = eb + o * S::EL * S::EBE + c * S::SC;
-              double v = (c == 0) ? carry[o][m] : 0.0;
-              v += e[off0];
-              if (pcnt[m] > 1) v += e[off1];
-              if (pcnt[m] > 2) { v += e[off2]; v += e[off3]; }
-              if (c < K || z == bzr - 1) store_dof(o, m, K * z + c, v);
-              else carry[o][m] = v;
+            for (int c = 0; c < S::NDP; c += 2) {
+              const double2 t0 = *reinterpret_cast<const double2*>(e + off[0] + c);
+              v[c] = t0.x;
+              v[c + 1] = t0.y;
+            }
+#pragma unroll
+            for (int t = 1; t < 4; ++t) {
+              if (t < n) {
+#pragma unroll
+                for (int c = 0; c < S::NDP; c += 2) {
+                  const double2 t1 = *reinterpret_cast<const double2*>(e + off[t] + c);
+                  v[c] += t1.x;
+                  v[c + 1] += t1.y;
+                }
+              }
+            }
+            v[0] = carry[o][m] + v[0];
+            if (z > 0 && z < bzr - 1) {   // middle layer: affine destination, one add per store
+              const bool zero = (pinfo[m] & 6) == 4;
+              double* d = reinterpret_cast<double*>(fptr[o][m]) + (int64_t)(K * z) * fstr[m];
+#pragma unroll
+              for (int c = 0; c < K; ++c) d[(int64_t)c * fstr[m]] = zero ? 0.0 : v[c];
+              carry[o][m] = v[K];
+            } else {
+#pragma unroll
+              for (int c = 0; c < K; ++c) store_dof(o, m, K * z + c, v[c]);
+              if (z == bzr - 1) store_dof(o, m, K * z + K, v[K]);
+              else carry[o][m] = v[K];
             }
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&e_empty[z & 1]);
+        FEOD_TICK(t_gt);
       }
     }
+#ifdef FEOD_PROFILE_IO
+    if (lane == 0 && blockIdx.x % 97 == 0)
+      printf("IO blk %d layers %d: wait_ring_empty %lld load %lld wait_e_full %lld gather_store %lld cycles/layer\n", blockIdx.x,
+             bzr, t_wre / bzr, t_load / bzr, t_wef / bzr, t_gt / bzr);
+#endif
   } else {
 
   // ============================== compute warps ==============================
@@ -412,6 +481,9 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   const double wij = T.w[lic] * T.w[gr];
   const double iwij2 = T.wi2[lic] * T.wi2[gr];
 
+#ifdef FEOD_PROFILE_IO
+  long long c_wrf = 0, c_wee = 0, c_start = clock64();
+#endif
   for (int z = 0; z < bzr; ++z) {
     const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + z));
     // metric of this thread's points (i = li, j = gr, l): layout [E][l][6][j][i]
@@ -429,7 +501,13 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     double rho_e = 0.0;
     if constexpr (MODEL == HEAT) rho_e = evalid ? __ldg(P.rho + eg) : 1.0;
 
+#ifdef FEOD_PROFILE_IO
+    long long c0 = clock64();
+#endif
     mbar_wait(&ring_full[z & 1], (z >> 1) & 1);
+#ifdef FEOD_PROFILE_IO
+    c_wrf += clock64() - c0;
+#endif
 
     // ---- node phase (B, x and y): group = plane c = gr, lane = x-point i
 #pragma unroll
@@ -621,19 +699,30 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         }
       }
       // element results -> the IO warp (double-buffered by layer parity)
+#ifdef FEOD_PROFILE_IO
+      long long c1 = clock64();
+#endif
       if (z >= 2) mbar_wait(&e_empty[z & 1], ((z >> 1) - 1) & 1);
-      double* eb = ebuf + (z & 1) * S::EBUF + el * S::EBE + gr * S::SC + lic;
+#ifdef FEOD_PROFILE_IO
+      c_wee += clock64() - c1;
+#endif
+      double* eb = ebuf + (z & 1) * S::EBUF + el * S::EBE + lic * S::NDP + gr;
       if (lvalid) {
 #pragma unroll
         for (int o = 0; o < S::NOUT; ++o)
 #pragma unroll
-          for (int b = 0; b < ND; ++b) eb[o * S::EL * S::EBE + b * ND] = R[o][b];
+          for (int b = 0; b < ND; ++b) eb[o * S::EL * S::EBE + b * ND * S::NDP] = R[o][b];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&e_full[z & 1]);
       elem_sync<S::WARP_ELEM, S::NTC>();             // P reads done before the next layer's writes
     }
   }
+#ifdef FEOD_PROFILE_IO
+  if (tid == 0 && blockIdx.x % 97 == 0)
+    printf("CW blk %d: total %lld wait_ring_full %lld wait_e_empty %lld cycles/layer\n", blockIdx.x,
+           (clock64() - c_start) / bzr, c_wrf / bzr, c_wee / bzr);
+#endif
   }   // compute warps
 
 }

@@ -2,7 +2,7 @@
 # Registers / spills of the fused kernels of one order (ptxas -v), e.g. tools/regs.sh 3
 k=${1:-3}
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -Iinclude \
-  -Xptxas -v -c paper_2506_00746_b200/csrc/inst_k$k.cu -o /tmp/regs_k$k.o 2>&1 | \
+  ${EXTRA} -Xptxas -v -c paper_2506_00746_b200/csrc/inst_k$k.cu -o /tmp/regs_k$k.o 2>&1 | \
   python3 -c "
 import sys, re
 name = None; sp = None
