@@ -27,6 +27,7 @@ struct feod_op {
   double* stage = nullptr;     // host-API staging: 3 x max(N, E)
   double* red = nullptr;       // kRedBlocks partials + 8 scalars
   int* flag = nullptr;
+  unsigned long long* sched = nullptr;   // dynamic brick scheduling ticket counter
   double* work = nullptr;      // Newton-CG: F, r, p, Ap, d (5 N)
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
 };
@@ -58,6 +59,7 @@ static void free_all(feod_op* h) {
   cudaFree(h->stage);
   cudaFree(h->red);
   cudaFree(h->flag);
+  cudaFree(h->sched);
   cudaFree(h->work);
 }
 
@@ -131,6 +133,12 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
     return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: reduction buffer"));
   if ((e = cudaMalloc(&h->flag, sizeof(int) * 2)) != cudaSuccess)
     return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: flag"));
+  if ((e = cudaMalloc(&h->sched, sizeof(unsigned long long))) != cudaSuccess)
+    return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: scheduler counter"));
+  if ((e = cudaMemsetAsync(h->sched, 0, sizeof(unsigned long long), h->st)) != cudaSuccess)
+    return cleanup_fail(cuda_fail(e, "feod_create: memset"));
+  P.sched = h->sched;
+  P.sched_base = 0;
   if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int) * 2, h->st)) != cudaSuccess)
     return cleanup_fail(cuda_fail(e, "feod_create: memset"));
 
@@ -196,7 +204,10 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   cudaEvent_t pb = h->prof_begin, pe = h->prof_end;
   h->prof_begin = h->prof_end = nullptr;
   if (pb) cudaEventRecord(pb, h->st);
-  cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, h->geom == nullptr, h->nbricks, h->P, h->T, p, h->st);
+  int grid = 0;
+  cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, h->geom == nullptr, h->nbricks, h->P, h->T, p, h->st, &grid);
+  // every CTA claims one ticket per brick it processes plus one that ends it
+  h->P.sched_base += (unsigned long long)h->nbricks + (unsigned long long)grid;
   if (pe) cudaEventRecord(pe, h->st);
   if (e != cudaSuccess) return cuda_fail(e, name);
   if (mode != MODE_DESIGN) {

@@ -44,6 +44,10 @@ struct OpParams {
   double cx, cy, cz, vol;
   const double* geom;    // [E][6][NQ^3] metric, components xx yy zz xy xz yz
   const double* rho;     // [E] (HEAT)
+  // dynamic brick scheduling: tickets atomicAdd(sched, 1) - sched_base < #bricks
+  // are bricks, the rest end a CTA; the host advances sched_base by #bricks + grid
+  unsigned long long* sched;
+  unsigned long long sched_base;
 };
 
 FEOD_HD bool is_dirichlet(int X, int Y, int Z, int Mx, int My, int Mz, uint32_t faces) {

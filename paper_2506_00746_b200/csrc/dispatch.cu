@@ -28,14 +28,14 @@ cudaError_t prepare_nd(int nd) {
 }
 
 cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const OpParams& P, const Tables& T,
-                      const OpPtrs& p, cudaStream_t st) {
+                      const OpPtrs& p, cudaStream_t st, int* grid_out) {
   switch (nd) {
-    case 2: return launch_order<2>(mode, model, affine, grid, P, T, p, st);
-    case 3: return launch_order<3>(mode, model, affine, grid, P, T, p, st);
-    case 4: return launch_order<4>(mode, model, affine, grid, P, T, p, st);
-    case 5: return launch_order<5>(mode, model, affine, grid, P, T, p, st);
-    case 6: return launch_order<6>(mode, model, affine, grid, P, T, p, st);
-    case 7: return launch_order<7>(mode, model, affine, grid, P, T, p, st);
+    case 2: return launch_order<2>(mode, model, affine, grid, P, T, p, st, grid_out);
+    case 3: return launch_order<3>(mode, model, affine, grid, P, T, p, st, grid_out);
+    case 4: return launch_order<4>(mode, model, affine, grid, P, T, p, st, grid_out);
+    case 5: return launch_order<5>(mode, model, affine, grid, P, T, p, st, grid_out);
+    case 6: return launch_order<6>(mode, model, affine, grid, P, T, p, st, grid_out);
+    case 7: return launch_order<7>(mode, model, affine, grid, P, T, p, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }

@@ -7,11 +7,27 @@
 
 namespace feod {
 
+// Persistent grid: as many CTAs as fit on the device at once (occupancy x SMs),
+// never more than there are bricks; each CTA walks bricks blockIdx.x + k gridDim.x.
 template <int ND, int NQ, int MODE, int MODEL, bool AFF>
-static cudaError_t launch_one(int grid, const OpParams& P, const Tables& T, const OpPtrs& p, cudaStream_t st) {
+static cudaError_t launch_one(int nbricks, const OpParams& P, const Tables& T, const OpPtrs& p, cudaStream_t st,
+                              int* grid_out) {
   using S = PShape<ND, MODE>;
-  plane_kernel<ND, MODE, MODEL, AFF><<<grid, S::NT, S::SMEM_BYTES, st>>>(P, T, p.in0, p.in1, p.out0, p.out1,
-                                                                          p.shell0, p.shell1, p.gout);
+  const size_t smem = S::SMEM_BYTES;
+  static int slots = 0;   // per instantiation; one device per process (replicas)
+  if (slots == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plane_kernel<ND, MODE, MODEL, AFF>, S::NT, smem);
+    if (e != cudaSuccess) return e;
+    slots = sms * (occ > 0 ? occ : 1);
+  }
+  const int grid = nbricks < slots ? nbricks : slots;
+  *grid_out = grid;
+  plane_kernel<ND, MODE, MODEL, AFF><<<grid, S::NT, smem, st>>>(P, T, p.in0, p.in1, p.out0, p.out1, p.shell0,
+                                                                p.shell1, p.gout);
   return cudaGetLastError();
 }
 
@@ -24,14 +40,14 @@ static cudaError_t prep_one() {
 
 template <int ND, int NQ, int MODE>
 static cudaError_t launch_mode(int model, bool aff, int grid, const OpParams& P, const Tables& T, const OpPtrs& p,
-                               cudaStream_t st) {
+                               cudaStream_t st, int* grid_out) {
   switch (model) {
-    case PLAPLACE: return aff ? launch_one<ND, NQ, MODE, PLAPLACE, true>(grid, P, T, p, st)
-                              : launch_one<ND, NQ, MODE, PLAPLACE, false>(grid, P, T, p, st);
-    case NLDIFF: return aff ? launch_one<ND, NQ, MODE, NLDIFF, true>(grid, P, T, p, st)
-                            : launch_one<ND, NQ, MODE, NLDIFF, false>(grid, P, T, p, st);
-    case HEAT: return aff ? launch_one<ND, NQ, MODE, HEAT, true>(grid, P, T, p, st)
-                          : launch_one<ND, NQ, MODE, HEAT, false>(grid, P, T, p, st);
+    case PLAPLACE: return aff ? launch_one<ND, NQ, MODE, PLAPLACE, true>(grid, P, T, p, st, grid_out)
+                              : launch_one<ND, NQ, MODE, PLAPLACE, false>(grid, P, T, p, st, grid_out);
+    case NLDIFF: return aff ? launch_one<ND, NQ, MODE, NLDIFF, true>(grid, P, T, p, st, grid_out)
+                            : launch_one<ND, NQ, MODE, NLDIFF, false>(grid, P, T, p, st, grid_out);
+    case HEAT: return aff ? launch_one<ND, NQ, MODE, HEAT, true>(grid, P, T, p, st, grid_out)
+                          : launch_one<ND, NQ, MODE, HEAT, false>(grid, P, T, p, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }
@@ -69,12 +85,12 @@ cudaError_t prepare_order<FEOD_ND>() {
 
 template <>
 cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int grid, const OpParams& P, const Tables& T,
-                                  const OpPtrs& p, cudaStream_t st) {
+                                  const OpPtrs& p, cudaStream_t st, int* grid_out) {
   switch (mode) {
-    case MODE_RES: return launch_mode<FEOD_ND, FEOD_ND, MODE_RES>(model, aff, grid, P, T, p, st);
-    case MODE_JVP: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVP>(model, aff, grid, P, T, p, st);
-    case MODE_JVPRES: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVPRES>(model, aff, grid, P, T, p, st);
-    case MODE_DESIGN: return launch_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>(model, aff, grid, P, T, p, st);
+    case MODE_RES: return launch_mode<FEOD_ND, FEOD_ND, MODE_RES>(model, aff, grid, P, T, p, st, grid_out);
+    case MODE_JVP: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVP>(model, aff, grid, P, T, p, st, grid_out);
+    case MODE_JVPRES: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVPRES>(model, aff, grid, P, T, p, st, grid_out);
+    case MODE_DESIGN: return launch_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>(model, aff, grid, P, T, p, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }

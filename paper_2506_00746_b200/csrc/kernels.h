@@ -24,7 +24,7 @@ cudaError_t launch_geometry(const double* verts, int nx, int ny, int nz, int nq,
 template <int ND> bool brick_info(BrickInfo* bi);
 template <int ND> cudaError_t prepare_order();
 template <int ND> cudaError_t launch_order(int mode, int model, bool affine, int grid, const OpParams& P,
-                                           const Tables& T, const OpPtrs& p, cudaStream_t st);
+                                           const Tables& T, const OpPtrs& p, cudaStream_t st, int* grid_out);
 template <int ND> cudaError_t fixup_order(const OpParams& P, const double* shell0, double* out0, const double* shell1,
                                           double* out1, cudaStream_t st);
 
@@ -32,7 +32,7 @@ template <int ND> cudaError_t fixup_order(const OpParams& P, const double* shell
   template <> bool brick_info<ND>(BrickInfo * bi);                                                \
   template <> cudaError_t prepare_order<ND>();                                                    \
   template <> cudaError_t launch_order<ND>(int mode, int model, bool affine, int grid, const OpParams& P, \
-                                           const Tables& T, const OpPtrs& p, cudaStream_t st);            \
+                                           const Tables& T, const OpPtrs& p, cudaStream_t st, int* grid_out); \
   template <> cudaError_t fixup_order<ND>(const OpParams& P, const double* shell0, double* out0,          \
                                           const double* shell1, double* out1, cudaStream_t st);
 FEOD_DECLARE_ORDER(2)
@@ -45,7 +45,7 @@ FEOD_DECLARE_ORDER(7)
 bool brick_info_nd(int nd, BrickInfo* bi);
 cudaError_t prepare_nd(int nd);
 cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const OpParams& P, const Tables& T,
-                      const OpPtrs& p, cudaStream_t st);
+                      const OpPtrs& p, cudaStream_t st, int* grid_out);
 cudaError_t fixup_nd(int nd, const OpParams& P, const double* shell0, double* out0, const double* shell1, double* out1,
                      cudaStream_t st);
 

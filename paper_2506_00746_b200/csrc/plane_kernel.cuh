@@ -134,7 +134,7 @@ struct PShape {
   static constexpr int LXF = K * BX + 1, LYF = K * BY + 1;
   static constexpr int NPOS = LXF * LYF;
   static constexpr int PLANE = plane_pad(NPOS);
-  static constexpr int RIN = 2 * K + 1;                      // current layer (ND planes) + next (K)
+  static constexpr int RIN = 2 * ND;                         // current layer + next layer (a brick's first layer: ND planes)
   static constexpr int NIN = (MODE == MODE_RES) ? 1 : 2;
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
   static constexpr int NCH = 3;                              // exchange channels
@@ -149,7 +149,7 @@ struct PShape {
   static constexpr int NPIO = (NPOS + 31) / 32;              // tile positions per IO lane
   static constexpr int INSZ = (NIN * RIN * PLANE + 1) / 2 * 2;
   static constexpr int TAB = (4 * ND * ND + 1) / 2 * 2;      // per-lane 1D tables
-  static constexpr int SMEM_DOUBLES = INSZ + TAB + EL * SE + 2 * EBUF + 8;   // + 8 mbarriers
+  static constexpr int SMEM_DOUBLES = INSZ + TAB + EL * SE + 2 * EBUF + 8 + 4;   // + 8 mbarriers + brick queue
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
   static constexpr int LZF = K * BZ + 1;
   static constexpr int SHELL = LXF * LYF * LZF - (LXF - 2) * (LYF - 2) * (LZF - 2);
@@ -203,6 +203,32 @@ FEOD_DEV void elem_sync() {
 
 FEOD_DEV double grp_shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
+// Geometry of brick b: tile origin, ragged extents, DOF box, neighbour flags.
+struct Brick {
+  int b, ex0, ey0, ez0, bxr, byr, bzr, LX, LY, LZ, gX0, gY0, gZ0;
+  bool lowX, highX, lowY, highY, lowZ, highZ;
+};
+template <int K, int BX, int BY, int BZ>
+FEOD_DEV Brick brick_geo(const OpParams& P, int b) {
+  Brick g;
+  g.b = b;
+  const int bx = b % P.nbx, by = (b / P.nbx) % P.nby, bz = b / (P.nbx * P.nby);
+  g.ex0 = bx * BX; g.ey0 = by * BY; g.ez0 = bz * BZ;
+  g.bxr = min(BX, P.nx - g.ex0); g.byr = min(BY, P.ny - g.ey0); g.bzr = min(BZ, P.nz - g.ez0);
+  g.LX = K * g.bxr + 1; g.LY = K * g.byr + 1; g.LZ = K * g.bzr + 1;
+  g.gX0 = K * g.ex0; g.gY0 = K * g.ey0; g.gZ0 = K * g.ez0;
+  g.lowX = g.ex0 > 0; g.highX = g.ex0 + g.bxr < P.nx;
+  g.lowY = g.ey0 > 0; g.highY = g.ey0 + g.byr < P.ny;
+  g.lowZ = g.ez0 > 0; g.highZ = g.ez0 + g.bzr < P.nz;
+  return g;
+}
+
+// Persistent CTAs with dynamic brick scheduling: the IO warp claims bricks from
+// a global ticket counter (P.sched) and publishes them in a small shared queue;
+// a CTA-global layer counter L drives the mbarrier phases and a CTA-global plane
+// counter the input-ring slots, so the IO warp streams the next brick's first
+// layers while the compute warps finish the current one. CTAs that run faster
+// (the schedulers favour older warps) simply take more bricks.
 template <int ND, int MODE, int MODEL, bool AFFINE>
 __global__ void __launch_bounds__(PShape<ND, MODE>::NT, PShape<ND, MODE>::MINB)
 plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, const double* __restrict__ in1,
@@ -222,15 +248,12 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   uint64_t* ring_empty = bars + 2;          // [2] layer z's node phase done         (compute -> IO)
   uint64_t* e_full = bars + 4;              // [2] layer z's element results written (compute -> IO)
   uint64_t* e_empty = bars + 6;             // [2] layer z's element results consumed (IO -> compute)
+  int* bq = reinterpret_cast<int*>(bars + 8);   // [8] claimed brick of the CTA's n-th brick (-1: done)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int brick = blockIdx.x;
-  const int bx = brick % P.nbx, by = (brick / P.nbx) % P.nby, bz = brick / (P.nbx * P.nby);
-  const int ex0 = bx * S::BX, ey0 = by * S::BY, ez0 = bz * S::BZ;
-  const int bxr = min(S::BX, P.nx - ex0), byr = min(S::BY, P.ny - ey0), bzr = min(S::BZ, P.nz - ez0);
-  const int LX = K * bxr + 1, LY = K * byr + 1, LZ = K * bzr + 1;
-  const int gX0 = K * ex0, gY0 = K * ey0, gZ0 = K * ez0;
+  const int nbricks = P.nbx * P.nby * P.nbz;
+  const int G = gridDim.x;
 
   // per-lane rows of the 1D tables (lane i): Brow[a] = B[i][a], Grow[a] = G[i][a];
   // rotated for the backward reduce-scatter (lane (i-k)%ND receives the term):
@@ -244,8 +267,9 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   }
   if (tid == 0) {
     // ring_full: one cp.async-arrival per IO lane (+ one plain arrival per lane for
-    // the synchronously masked lambda of the design mode)
-    const uint32_t nfull = (MODE == MODE_DESIGN) ? 64u : 32u;
+    // the synchronously masked lambda of the design mode) + one plain arrival of
+    // IO lane 0 that publishes the brick queue
+    const uint32_t nfull = (MODE == MODE_DESIGN) ? 65u : 33u;
     mbar_init(&ring_full[0], nfull);
     mbar_init(&ring_full[1], nfull);
     mbar_init(&ring_empty[0], S::NWC);
@@ -260,147 +284,185 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
 
   if (warp == S::NWC) {
     // =========================== IO warp ===================================
-    const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx;
-    const bool lowY = ey0 > 0, highY = ey0 + byr < P.ny;
-    const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
-    // tile-plane positions of this lane: idx = lane + 32 m
-    //   pg     in-plane global offset (gX0 + X) + Mx (gY0 + Y)
-    //   pinfo  bit0 valid, bit1 on a shared x/y brick face, bit2 Dirichlet in x/y,
-    //          bits 3.. index on the shell ring of a middle z-plane
-    //   pxy    X + LX Y (shell index on the bottom / top plane)
-    //   pofs   up to four element-buffer offsets (16-bit packed), fixed order
-    int pg[S::NPIO], pinfo[S::NPIO], pxy[S::NPIO], pcnt[S::NPIO];
-    uint32_t pofs[S::NPIO][2];
-#pragma unroll
-    for (int m = 0; m < S::NPIO; ++m) {
-      const int idx = lane + 32 * m;
-      const int X = idx % S::LXF, Y = idx / S::LXF;
-      const bool v = idx < S::NPOS && X < LX && Y < LY;
-      const int gx = gX0 + X, gy = gY0 + Y;
-      pg[m] = v ? gx + P.Mx * gy : 0;
-      const bool shxy = (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) || (Y == LY - 1 && highY);
-      const bool dxy = ((P.faces & 1u) && gx == 0) || ((P.faces & 2u) && gx == P.Mx - 1) ||
-                       ((P.faces & 4u) && gy == 0) || ((P.faces & 8u) && gy == P.My - 1);
-      const int ringpos = (Y == 0) ? X : (Y == LY - 1) ? LX + X : 2 * LX + 2 * (Y - 1) + (X == 0 ? 0 : 1);
-      pinfo[m] = (v ? 1 : 0) | (shxy ? 2 : 0) | (dxy ? 4 : 0) | (ringpos << 3);
-      pxy[m] = X + LX * Y;
-      int cx[2] = {0, 0}, ax[2] = {0, 0}, cy[2] = {0, 0}, ay[2] = {0, 0}, nxc = 1, nyc = 1;
-      cx[0] = min(X / K, max(bxr - 1, 0));
-      ax[0] = X - K * cx[0];
-      if (ax[0] == 0 && cx[0] > 0) { cx[1] = cx[0]; ax[1] = 0; cx[0] -= 1; ax[0] = K; nxc = 2; }
-      cy[0] = min(Y / K, max(byr - 1, 0));
-      ay[0] = Y - K * cy[0];
-      if (ay[0] == 0 && cy[0] > 0) { cy[1] = cy[0]; ay[1] = 0; cy[0] -= 1; ay[0] = K; nyc = 2; }
-      uint32_t o4[4] = {0, 0, 0, 0};
-      int n = 0;
-      for (int t = 0; t < nyc; ++t)
-        for (int q = 0; q < nxc; ++q)
-          o4[n++] = (uint32_t)((cx[q] + S::BX * cy[t]) * S::EBE + (ay[t] * ND + ax[q]) * S::NDP);
-      pofs[m][0] = o4[0] | (o4[1] << 16);
-      pofs[m][1] = o4[2] | (o4[3] << 16);
-      pcnt[m] = v ? n : 0;
-    }
-
-    // G: stream DOF plane p (brick-local z index) into its ring slot
-    auto load_plane = [&](int p) {
-      const int slot = p % S::RIN;
-      const int64_t zoff = (int64_t)P.Mx * P.My * (gZ0 + p);
-      const bool dz = ((P.faces & 16u) && gZ0 + p == 0) || ((P.faces & 32u) && gZ0 + p == P.Mz - 1);
+    // loader cursor (brick lb, layer lz, ring base of the brick) and storer cursor
+    // (brick sb, layer sz); tile-plane positions of this lane: idx = lane + 32 m
+    Brick gl, gs;
+    int lz = 0, sz = 0, lbase = 0, ln = 0, sn = 0;   // loader / storer brick ordinals
+    bool ldone = false;
+    //   loader:  lpg   in-plane global offset (gX0 + X) + Mx (gY0 + Y); lpinfo bit0 valid, bit2 Dirichlet in x/y
+    int lpg[S::NPIO], lpinfo[S::NPIO];
+    auto loader_positions = [&]() {
 #pragma unroll
       for (int m = 0; m < S::NPIO; ++m) {
-        if (!(pinfo[m] & 1)) continue;
         const int idx = lane + 32 * m;
-        const int64_t g = zoff + pg[m];
+        const int X = idx % S::LXF, Y = idx / S::LXF;
+        const bool v = idx < S::NPOS && X < gl.LX && Y < gl.LY;
+        const int gx = gl.gX0 + X, gy = gl.gY0 + Y;
+        lpg[m] = v ? gx + P.Mx * gy : 0;
+        const bool dxy = ((P.faces & 1u) && gx == 0) || ((P.faces & 2u) && gx == P.Mx - 1) ||
+                         ((P.faces & 4u) && gy == 0) || ((P.faces & 8u) && gy == P.My - 1);
+        lpinfo[m] = (v ? 1 : 0) | (dxy ? 4 : 0);
+      }
+    };
+    //   storer:  pg, pinfo (bit1 on a shared x/y brick face, bits 3.. ring index),
+    //            pxy = X + LX Y, pcnt / pofs = element-buffer contributions in a
+    //            fixed order, fptr / fstr = affine destination of middle layers
+    int pg[S::NPIO], pinfo[S::NPIO], pxy[S::NPIO], pcnt[S::NPIO];
+    uint32_t pofs[S::NPIO][2];
+    int64_t fptr[S::NOUT > 0 ? S::NOUT : 1][S::NPIO];
+    int fstr[S::NPIO];
+    double carry[S::NOUT > 0 ? S::NOUT : 1][S::NPIO];
+    auto storer_positions = [&]() {
+#pragma unroll
+      for (int m = 0; m < S::NPIO; ++m) {
+        const int idx = lane + 32 * m;
+        const int X = idx % S::LXF, Y = idx / S::LXF;
+        const bool v = idx < S::NPOS && X < gs.LX && Y < gs.LY;
+        const int gx = gs.gX0 + X, gy = gs.gY0 + Y;
+        pg[m] = v ? gx + P.Mx * gy : 0;
+        const bool shxy = (X == 0 && gs.lowX) || (X == gs.LX - 1 && gs.highX) || (Y == 0 && gs.lowY) ||
+                          (Y == gs.LY - 1 && gs.highY);
+        const bool dxy = ((P.faces & 1u) && gx == 0) || ((P.faces & 2u) && gx == P.Mx - 1) ||
+                         ((P.faces & 4u) && gy == 0) || ((P.faces & 8u) && gy == P.My - 1);
+        const int ringpos = (Y == 0) ? X : (Y == gs.LY - 1) ? gs.LX + X : 2 * gs.LX + 2 * (Y - 1) + (X == 0 ? 0 : 1);
+        pinfo[m] = (v ? 1 : 0) | (shxy ? 2 : 0) | (dxy ? 4 : 0) | (ringpos << 3);
+        pxy[m] = X + gs.LX * Y;
+        int cx[2] = {0, 0}, ax[2] = {0, 0}, cy[2] = {0, 0}, ay[2] = {0, 0}, nxc = 1, nyc = 1;
+        cx[0] = min(X / K, max(gs.bxr - 1, 0));
+        ax[0] = X - K * cx[0];
+        if (ax[0] == 0 && cx[0] > 0) { cx[1] = cx[0]; ax[1] = 0; cx[0] -= 1; ax[0] = K; nxc = 2; }
+        cy[0] = min(Y / K, max(gs.byr - 1, 0));
+        ay[0] = Y - K * cy[0];
+        if (ay[0] == 0 && cy[0] > 0) { cy[1] = cy[0]; ay[1] = 0; cy[0] -= 1; ay[0] = K; nyc = 2; }
+        uint32_t o4[4] = {0, 0, 0, 0};
+        int n = 0;
+        for (int t = 0; t < nyc; ++t)
+          for (int q = 0; q < nxc; ++q)
+            o4[n++] = (uint32_t)((cx[q] + S::BX * cy[t]) * S::EBE + (ay[t] * ND + ax[q]) * S::NDP);
+        pofs[m][0] = o4[0] | (o4[1] << 16);
+        pofs[m][1] = o4[2] | (o4[3] << 16);
+        pcnt[m] = v ? n : 0;
+        // middle layers (brick planes 1 .. LZ-2: no bottom/top face, no z-Dirichlet
+        // plane) have an affine destination in the plane index p:
+        //   shell: brick*stride + base + (p-1)*ring + ringpos      out: Mx*My*(gZ0 + p) + pg
+        const int base = gs.LX * gs.LY, ring = 2 * gs.LX + 2 * (gs.LY - 2);
+        fstr[m] = shxy ? ring : P.Mx * P.My;
+#pragma unroll
+        for (int o = 0; o < (S::NOUT > 0 ? S::NOUT : 1); ++o) {
+          const double* b0 = shxy ? (o == 0 ? shell0 : shell1) : (o == 0 ? out0 : out1);
+          const int64_t off = shxy ? (int64_t)gs.b * P.shell_stride + base - ring + ringpos
+                                   : (int64_t)P.Mx * P.My * gs.gZ0 + pg[m];
+          fptr[o][m] = reinterpret_cast<int64_t>(b0) + off * (int64_t)sizeof(double);
+          carry[o][m] = 0.0;
+        }
+      }
+    };
+
+    // G: stream DOF plane p of the loader brick into its ring slot
+    auto load_plane = [&](int p) {
+      const int slot = (lbase + p) % S::RIN;
+      const int64_t zoff = (int64_t)P.Mx * P.My * (gl.gZ0 + p);
+      const bool dz = ((P.faces & 16u) && gl.gZ0 + p == 0) || ((P.faces & 32u) && gl.gZ0 + p == P.Mz - 1);
+#pragma unroll
+      for (int m = 0; m < S::NPIO; ++m) {
+        if (!(lpinfo[m] & 1)) continue;
+        const int idx = lane + 32 * m;
+        const int64_t g = zoff + lpg[m];
         cp_async8(ring_in + slot * S::PLANE + idx, in0 + g);
         if constexpr (S::NIN == 2) {
           double* dst = ring_in + (S::RIN + slot) * S::PLANE + idx;
           if constexpr (MODE == MODE_DESIGN) {
             // lambda's Dirichlet entries are masked (reading A14)
-            *dst = ((pinfo[m] & 4) || dz) ? 0.0 : __ldg(in1 + g);
+            *dst = ((lpinfo[m] & 4) || dz) ? 0.0 : __ldg(in1 + g);
           } else {
             cp_async8(dst, in1 + g);
           }
         }
       }
     };
-    auto load_layer = [&](int zz) {   // the DOF planes layer zz needs that are not resident yet
-      const int p0 = (zz == 0) ? 0 : K * zz + 1;
-      for (int p = p0; p <= K * zz + K; ++p) load_plane(p);
-      uint64_t* bar = &ring_full[zz & 1];
+    // load global layer LL (the loader cursor's next layer) and advance the cursor
+    auto load_layer = [&](int LL) {
+      uint64_t* bar = &ring_full[LL & 1];
+      if (lz == 0) {   // claim the next brick and publish it
+        int id = -1;
+        if (lane == 0) {
+          const unsigned long long t = atomicAdd(P.sched, 1ull) - P.sched_base;
+          id = t < (unsigned long long)nbricks ? (int)t : -1;
+          bq[ln & 7] = id;
+        }
+        id = __shfl_sync(0xffffffffu, id, 0);
+        ++ln;
+        if (id < 0) {   // phantom layer: lets the compute warps read the end marker
+          ldone = true;
+          mbar_arrive(bar);
+          if constexpr (MODE == MODE_DESIGN) mbar_arrive(bar);
+          if (lane == 0) mbar_arrive(bar);
+          return;
+        }
+        gl = brick_geo<K, S::BX, S::BY, S::BZ>(P, id);
+        loader_positions();
+      }
+      const int p0 = (lz == 0) ? 0 : K * lz + 1;
+      for (int p = p0; p <= K * lz + K; ++p) load_plane(p);
       cp_async_arrive(bar);
       if constexpr (MODE == MODE_DESIGN) mbar_arrive(bar);
+      if (lane == 0) mbar_arrive(bar);
+      if (++lz == gl.bzr) {
+        lbase += gl.LZ;
+        lz = 0;
+      }
     };
 
-    // P^T + store of the finished value v of output o at position m, DOF plane p
+    // P^T + store of the finished value v of output o at position m, DOF plane p (general path)
     auto store_dof = [&](int o, int m, int p, double v) {
-#ifdef FEOD_KO_STORE
-      if (v != 1.2345e300) return;
-#endif
       const int info = pinfo[m];
-      const bool shared = (info & 2) || (p == 0 && lowZ) || (p == LZ - 1 && highZ);
+      const bool shared = (info & 2) || (p == 0 && gs.lowZ) || (p == gs.LZ - 1 && gs.highZ);
       if (shared) {
-        const int base = LX * LY, ring = 2 * LX + 2 * (LY - 2);
-        const int rank = (p == 0) ? pxy[m] : (p == LZ - 1) ? base + (LZ - 2) * ring + pxy[m]
-                                                            : base + (p - 1) * ring + (info >> 3);
-        (o == 0 ? shell0 : shell1)[(int64_t)brick * P.shell_stride + rank] = v;
+        const int base = gs.LX * gs.LY, ring = 2 * gs.LX + 2 * (gs.LY - 2);
+        const int rank = (p == 0) ? pxy[m] : (p == gs.LZ - 1) ? base + (gs.LZ - 2) * ring + pxy[m]
+                                                               : base + (p - 1) * ring + (info >> 3);
+        (o == 0 ? shell0 : shell1)[(int64_t)gs.b * P.shell_stride + rank] = v;
       } else {
-        const int gz = gZ0 + p;
+        const int gz = gs.gZ0 + p;
         const bool dir = (info & 4) || ((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1);
         (o == 0 ? out0 : out1)[(int64_t)P.Mx * P.My * gz + pg[m]] = dir ? 0.0 : v;
       }
     };
 
-    // middle layers (brick planes 1 .. LZ-2: no bottom/top face, no z-Dirichlet
-    // plane) have an affine destination in the plane index p:
-    //   shell: brick*stride + base + (p-1)*ring + ringpos      out: Mx*My*(gZ0 + p) + pg
-    // fptr[m] points at p = 0 (an offset, possibly before the array start, never
-    // dereferenced there), fstr[m] is the per-plane stride; zero-valued on Dirichlet x/y rows
-    int64_t fptr[S::NOUT > 0 ? S::NOUT : 1][S::NPIO];
-    int fstr[S::NPIO];
-#pragma unroll
-    for (int m = 0; m < S::NPIO; ++m) {
-      const int info = pinfo[m];
-      const int base = LX * LY, ring = 2 * LX + 2 * (LY - 2);
-      const bool sh = info & 2;
-      fstr[m] = sh ? ring : P.Mx * P.My;
-#pragma unroll
-      for (int o = 0; o < (S::NOUT > 0 ? S::NOUT : 1); ++o) {
-        const double* b0 = sh ? (o == 0 ? shell0 : shell1) : (o == 0 ? out0 : out1);
-        const int64_t off = sh ? (int64_t)brick * P.shell_stride + base - ring + (info >> 3)
-                               : (int64_t)P.Mx * P.My * gZ0 + pg[m];
-        fptr[o][m] = reinterpret_cast<int64_t>(b0) + off * (int64_t)sizeof(double);
-      }
-    }
-
-    double carry[S::NOUT > 0 ? S::NOUT : 1][S::NPIO];
-#pragma unroll
-    for (int o = 0; o < (S::NOUT > 0 ? S::NOUT : 1); ++o)
-#pragma unroll
-      for (int m = 0; m < S::NPIO; ++m) carry[o][m] = 0.0;
-
 #ifdef FEOD_PROFILE_IO
     long long t_wre = 0, t_load = 0, t_wef = 0, t_gt = 0, t0 = clock64(), t1;
+    int nl = 0;
 #define FEOD_TICK(acc) do { t1 = clock64(); acc += t1 - t0; t0 = t1; } while (0)
 #else
 #define FEOD_TICK(acc) do { } while (0)
 #endif
     load_layer(0);
-    if (bzr > 1) load_layer(1);
+    if (!ldone) load_layer(1);
     FEOD_TICK(t_load);
-    for (int z = 0; z < bzr; ++z) {
-      if (z + 2 < bzr) {
-        mbar_wait(&ring_empty[z & 1], (z >> 1) & 1);   // compute is done reading layer z's planes
+    for (int L = 0;; ++L) {
+      if (sz == 0) {   // storer moves to its next brick (claimed by the loader already)
+        __syncwarp();
+        const int id = bq[sn & 7];
+        ++sn;
+        if (id < 0) break;
+        gs = brick_geo<K, S::BX, S::BY, S::BZ>(P, id);
+        storer_positions();
+      }
+      if (!ldone) {
+        mbar_wait(&ring_empty[L & 1], (L >> 1) & 1);   // compute is done reading layer L's planes
         FEOD_TICK(t_wre);
-        load_layer(z + 2);
+        load_layer(L + 2);
         FEOD_TICK(t_load);
       }
       if constexpr (S::NOUT > 0) {
-        mbar_wait(&e_full[z & 1], (z >> 1) & 1);
+        const int z = sz;
+        const int bzr = gs.bzr;
+        mbar_wait(&e_full[L & 1], (L >> 1) & 1);
         FEOD_TICK(t_wef);
-        const double* eb = ebuf + (z & 1) * S::EBUF;
-        // G^T: every tile DOF sums its (<= 4) x-y contributions in a fixed order;
+        const double* eb = ebuf + (L & 1) * S::EBUF;
+        // G^T: every tile DOF sums its (<= 4) x-y contributions in a fixed order
+        // (all ND planes of a contributing node come in 16-byte loads);
         // z-sharing through the carried top plane
-        // all ND planes of a contributing node come in 16-byte loads
 #pragma unroll
         for (int m = 0; m < S::NPIO; ++m) {
           const int n = pcnt[m];
@@ -444,30 +506,32 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&e_empty[z & 1]);
+        if (lane == 0) mbar_arrive(&e_empty[L & 1]);
         FEOD_TICK(t_gt);
       }
+#ifdef FEOD_PROFILE_IO
+      ++nl;
+#endif
+      if (++sz == gs.bzr) sz = 0;
     }
 #ifdef FEOD_PROFILE_IO
-    if (lane == 0 && blockIdx.x % 97 == 0)
+    if (lane == 0 && blockIdx.x % 97 == 0 && nl > 0)
       printf("IO blk %d layers %d: wait_ring_empty %lld load %lld wait_e_full %lld gather_store %lld cycles/layer\n", blockIdx.x,
-             bzr, t_wre / bzr, t_load / bzr, t_wef / bzr, t_gt / bzr);
+             nl, t_wre / nl, t_load / nl, t_wef / nl, t_gt / nl);
 #endif
   } else {
 
   // ============================== compute warps ==============================
   const int gw = lane / ND;                          // group within the warp
   const int li = lane - gw * ND;                     // lane within the group: x-point i (or node a)
-  const int G = warp * S::GPW + gw;
-  const bool lvalid = gw < S::GPW && G < S::NG;      // lane carries real work
-  const int Gc = lvalid ? G : 0;
+  const int grp = warp * S::GPW + gw;
+  const bool lvalid = gw < S::GPW && grp < S::NG;    // lane carries real work
+  const int Gc = lvalid ? grp : 0;
   const int el = Gc / ND;                            // element slot in the layer
   const int gr = Gc - el * ND;                       // group role: plane c / point row j
   const int gbase = lvalid ? lane - li : 0;
   const int lic = lvalid ? li : 0;
   const int exl = el % S::BX, eyl = el / S::BX;
-  const bool evalid = lvalid && exl < bxr && eyl < byr;
-  const int X0 = evalid ? K * exl : 0, Y0 = evalid ? K * eyl : 0;
 
   const double* Brow = tab + lic * ND;
   const double* Grow = tab + ND * ND + lic * ND;
@@ -483,8 +547,21 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
 
 #ifdef FEOD_PROFILE_IO
   long long c_wrf = 0, c_wee = 0, c_start = clock64();
+  unsigned long long ns_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_start));
 #endif
-  for (int z = 0; z < bzr; ++z) {
+  int L = 0;       // CTA-global layer counter (mbarrier phases, element-buffer parity)
+  int rbase = 0;   // CTA-global index of the brick's first DOF plane (input-ring slots)
+  for (int n = 0;; ++n) {
+  // the first layer of the CTA's n-th brick: its planes (or the end marker) are published
+  mbar_wait(&ring_full[L & 1], (L >> 1) & 1);
+  const int bid = bq[n & 7];
+  if (bid < 0) break;
+  const Brick gb = brick_geo<K, S::BX, S::BY, S::BZ>(P, bid);
+  const int ex0 = gb.ex0, ey0 = gb.ey0, ez0 = gb.ez0, bxr = gb.bxr, byr = gb.byr, bzr = gb.bzr;
+  const bool evalid = lvalid && exl < bxr && eyl < byr;
+  const int X0 = evalid ? K * exl : 0, Y0 = evalid ? K * eyl : 0;
+  for (int z = 0; z < bzr; ++z, ++L) {
     const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + z));
     // metric of this thread's points (i = li, j = gr, l): layout [E][l][6][j][i]
     const double* gm = nullptr;
@@ -504,7 +581,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
 #ifdef FEOD_PROFILE_IO
     long long c0 = clock64();
 #endif
-    mbar_wait(&ring_full[z & 1], (z >> 1) & 1);
+    if (z > 0) mbar_wait(&ring_full[L & 1], (L >> 1) & 1);
 #ifdef FEOD_PROFILE_IO
     c_wrf += clock64() - c0;
 #endif
@@ -512,7 +589,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     // ---- node phase (B, x and y): group = plane c = gr, lane = x-point i
 #pragma unroll
     for (int f = 0; f < S::NIN; ++f) {
-      const double* pl = ring_in + (f * S::RIN + (K * z + gr) % S::RIN) * S::PLANE + X0 + S::LXF * Y0;
+      const double* pl = ring_in + (f * S::RIN + (rbase + K * z + gr) % S::RIN) * S::PLANE + X0 + S::LXF * Y0;
       double V[ND], Vx[ND];
 #pragma unroll
       for (int b = 0; b < ND; ++b) {
@@ -544,7 +621,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&ring_empty[z & 1]);   // this warp no longer reads layer z's planes
+    if (lane == 0) mbar_arrive(&ring_empty[L & 1]);   // this warp no longer reads layer L's planes
     elem_sync<S::WARP_ELEM, S::NTC>();
 
     // ---- point phase: group = y-point j = gr, lane = x-point i; inputs stay in registers
@@ -702,11 +779,11 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
 #ifdef FEOD_PROFILE_IO
       long long c1 = clock64();
 #endif
-      if (z >= 2) mbar_wait(&e_empty[z & 1], ((z >> 1) - 1) & 1);
+      if (L >= 2) mbar_wait(&e_empty[L & 1], ((L >> 1) - 1) & 1);
 #ifdef FEOD_PROFILE_IO
       c_wee += clock64() - c1;
 #endif
-      double* eb = ebuf + (z & 1) * S::EBUF + el * S::EBE + lic * S::NDP + gr;
+      double* eb = ebuf + (L & 1) * S::EBUF + el * S::EBE + lic * S::NDP + gr;
       if (lvalid) {
 #pragma unroll
         for (int o = 0; o < S::NOUT; ++o)
@@ -714,14 +791,19 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
           for (int b = 0; b < ND; ++b) eb[o * S::EL * S::EBE + b * ND * S::NDP] = R[o][b];
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&e_full[z & 1]);
+      if (lane == 0) mbar_arrive(&e_full[L & 1]);
       elem_sync<S::WARP_ELEM, S::NTC>();             // P reads done before the next layer's writes
     }
   }
+  rbase += gb.LZ;
+  }   // bricks
 #ifdef FEOD_PROFILE_IO
-  if (tid == 0 && blockIdx.x % 97 == 0)
-    printf("CW blk %d: total %lld wait_ring_full %lld wait_e_empty %lld cycles/layer\n", blockIdx.x,
-           (clock64() - c_start) / bzr, c_wrf / bzr, c_wee / bzr);
+  unsigned long long ns_end;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_end));
+  if (tid == 0 && (blockIdx.x % 97 == 0 || blockIdx.x == gridDim.x - 1) && L > 0)
+    printf("CW mode %d blk %d: total %lld wait_ring_full %lld wait_e_empty %lld cycles/layer (%d layers), start %llu end %llu ns, %.1f us, %.0f MHz\n", MODE, blockIdx.x,
+           (clock64() - c_start) / L, c_wrf / L, c_wee / L, L, ns_start % 100000000ull, ns_end % 100000000ull, (ns_end - ns_start) * 1e-3,
+           (double)(clock64() - c_start) / (double)(ns_end - ns_start) * 1e3);
 #endif
   }   // compute warps
 
