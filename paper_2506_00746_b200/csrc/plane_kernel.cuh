@@ -251,7 +251,8 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   int* bq = reinterpret_cast<int*>(bars + 8);   // [8] claimed brick of the CTA's n-th brick (-1: done)
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
+  const int lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform: lets the compiler keep table constants in uniform registers
   const int nbricks = P.nbx * P.nby * P.nbz;
   const int G = gridDim.x;
 
