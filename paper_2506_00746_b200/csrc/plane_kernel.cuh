@@ -443,7 +443,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     for (int L = 0;; ++L) {
       if (sz == 0) {   // storer moves to its next brick (claimed by the loader already)
         __syncwarp();
-        const int id = bq[sn & 7];
+        const int id = __shfl_sync(0xffffffffu, bq[sn & 7], 0);
         ++sn;
         if (id < 0) break;
         gs = brick_geo<K, S::BX, S::BY, S::BZ>(P, id);
@@ -556,7 +556,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   for (int n = 0;; ++n) {
   // the first layer of the CTA's n-th brick: its planes (or the end marker) are published
   mbar_wait(&ring_full[L & 1], (L >> 1) & 1);
-  const int bid = bq[n & 7];
+  const int bid = __shfl_sync(0xffffffffu, bq[n & 7], 0);   // warp-uniform brick id
   if (bid < 0) break;
   const Brick gb = brick_geo<K, S::BX, S::BY, S::BZ>(P, bid);
   const int ex0 = gb.ex0, ey0 = gb.ey0, ez0 = gb.ez0, bxr = gb.bxr, byr = gb.byr, bzr = gb.bzr;
