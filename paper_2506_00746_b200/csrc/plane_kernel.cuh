@@ -137,7 +137,9 @@ struct PShape {
   static constexpr int RIN = 2 * ND;                         // current layer + next layer (a brick's first layer: ND planes)
   static constexpr int NIN = (MODE == MODE_RES) ? 1 : 2;
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
-  static constexpr int NCH = 3;                              // exchange channels
+  // exchange channels: 2 ([W | Wy], x-derivative collocated over the lane group,
+  // fewer FLOPs) up to Q4; 3 ([W | Wx | Wy], no cross-lane traffic) for Q5/Q6
+  static constexpr int NCH = ND >= 6 ? 3 : 2;
   static constexpr XbPad XP = xb_pad(ND, NIN, NCH);
   static constexpr int SI = XP.SI, SJ = XP.SJ, SE = XP.SE, SF = ND * SJ;
   // element buffer (compute -> IO), per layer parity and output: [EL][b][a][c]
@@ -256,15 +258,23 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   const int nbricks = P.nbx * P.nby * P.nbz;
   const int G = gridDim.x;
 
-  // per-lane rows of the 1D tables (lane i): Brow[a] = B[i][a], Grow[a] = G[i][a];
-  // rotated for the backward reduce-scatter (lane (i-k)%ND receives the term):
-  // Bt[k] = B[i][(i-k)%ND], Gt[k] = G[i][(i-k)%ND]
+  // per-lane rows of the 1D tables (lane i), rotated for the group shuffles:
+  //   2 channels: Brow[a] = B[i][a]; Dx[k] = Dh[i][(i+k)%ND] (Ux = sum_k Dx[k] U_{(i+k)%ND});
+  //               DxT[k] = Dh[(i+k)%ND][i] (Ax = sum_k DxT[k] Fx_{(i+k)%ND});
+  //               Bt[k] = B[i][(i-k)%ND] (reduce-scatter: lane (i-k)%ND receives B[i][i-k] Q_i)
+  //   3 channels: Brow[a] = B[i][a]; Grow[a] = G[i][a]; Bt[k] = B[i][(i-k)%ND]; Gt[k] = G[i][(i-k)%ND]
   for (int t = tid; t < ND * ND; t += S::NT) {
-    const int i = t / ND, k = t % ND, dn = (i - k + ND) % ND;
+    const int i = t / ND, k = t % ND, up = (i + k) % ND, dn = (i - k + ND) % ND;
     tab[t] = T.B[i][k];
-    tab[ND * ND + t] = T.G[i][k];
-    tab[2 * ND * ND + t] = T.B[i][dn];
-    tab[3 * ND * ND + t] = T.G[i][dn];
+    if constexpr (S::NCH == 2) {
+      tab[ND * ND + t] = T.D[i][up];
+      tab[2 * ND * ND + t] = T.D[up][i];
+      tab[3 * ND * ND + t] = T.B[i][dn];
+    } else {
+      tab[ND * ND + t] = T.G[i][k];
+      tab[2 * ND * ND + t] = T.B[i][dn];
+      tab[3 * ND * ND + t] = T.G[i][dn];
+    }
   }
   if (tid == 0) {
     // ring_full: one cp.async-arrival per IO lane (+ one plain arrival per lane for
@@ -535,9 +545,11 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   const int exl = el % S::BX, eyl = el / S::BX;
 
   const double* Brow = tab + lic * ND;
-  const double* Grow = tab + ND * ND + lic * ND;
-  const double* Bt = tab + 2 * ND * ND + lic * ND;
-  const double* Gt = tab + 3 * ND * ND + lic * ND;
+  const double* Dx = tab + ND * ND + lic * ND;                                      // 2 channels
+  const double* DxT = tab + 2 * ND * ND + lic * ND;                                // 2 channels
+  const double* Grow = tab + ND * ND + lic * ND;                                    // 3 channels
+  const double* Gt = tab + 3 * ND * ND + lic * ND;                                  // 3 channels
+  const double* Bt = tab + (S::NCH == 2 ? 3 : 2) * ND * ND + lic * ND;
   int src[ND];
 #pragma unroll
   for (int k = 0; k < ND; ++k) src[k] = gbase + (lic + k) % ND;
@@ -599,7 +611,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         for (int a = 0; a < ND; ++a) {
           const double ua = pl[a + S::LXF * b];
           acc = fma(Brow[a], ua, acc);
-          accx = fma(Grow[a], ua, accx);
+          if constexpr (S::NCH == 3) accx = fma(Grow[a], ua, accx);
         }
         V[b] = acc;
         Vx[b] = accx;
@@ -612,12 +624,12 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         for (int b = 0; b < ND; ++b) {
           w = fma(T.B[j][b], V[b], w);
           wy = fma(T.G[j][b], V[b], wy);
-          wx = fma(T.B[j][b], Vx[b], wx);
+          if constexpr (S::NCH == 3) wx = fma(T.B[j][b], Vx[b], wx);
         }
-        if (lvalid) {
+        if (lvalid) {   // [W | Wy] or [W | Wy | Wx]
           xo[j * S::SJ] = w;
-          xo[j * S::SJ + ND] = wx;
-          xo[j * S::SJ + 2 * ND] = wy;
+          xo[j * S::SJ + ND] = wy;
+          if constexpr (S::NCH == 3) xo[j * S::SJ + 2 * ND] = wx;
         }
       }
     }
@@ -626,25 +638,52 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     elem_sync<S::WARP_ELEM, S::NTC>();
 
     // ---- point phase: group = y-point j = gr, lane = x-point i; inputs stay in registers
-    double w[S::NIN][3 * ND];   // [W | Wx | Wy] over c
+    double w[S::NIN][S::NCH * ND];   // [W | Wy (| Wx)] over c
 #pragma unroll
     for (int f = 0; f < S::NIN; ++f) {
       const double* xi = xe + f * S::SF + gr * S::SJ + lic * S::SI;
 #pragma unroll
-      for (int c = 0; c + 1 < 3 * ND; c += 2) {
+      for (int c = 0; c + 1 < S::NCH * ND; c += 2) {
         const double2 t0 = *reinterpret_cast<const double2*>(xi + c);
         w[f][c] = t0.x;
         w[f][c + 1] = t0.y;
       }
-      if constexpr ((3 * ND) % 2) w[f][3 * ND - 1] = xi[3 * ND - 1];
+      if constexpr ((S::NCH * ND) % 2) w[f][S::NCH * ND - 1] = xi[S::NCH * ND - 1];
+    }
+    // values at all z-points of the column, then the collocated x-derivative
+    // with one batched all-gather over the group's x-line
+    constexpr int NB = S::NCH == 2 ? NQ : 1;   // batched column arrays (2 channels only)
+    double U[S::NIN][NB], Ux[S::NIN][NB];
+    if constexpr (S::NCH == 2) {
+#pragma unroll
+      for (int f = 0; f < S::NIN; ++f)
+#pragma unroll
+        for (int l = 0; l < NQ; ++l) {
+          double a0 = 0.0;
+#pragma unroll
+          for (int c = 0; c < ND; ++c) a0 = fma(T.B[l][c], w[f][c], a0);
+          U[f][l] = a0;
+        }
+#pragma unroll
+      for (int f = 0; f < S::NIN; ++f)
+#pragma unroll
+        for (int l = 0; l < NQ; ++l) {
+          double ux = Dx[0] * U[f][l];
+#pragma unroll
+          for (int k = 1; k < ND; ++k) ux = fma(Dx[k], grp_shfl(U[f][l], src[k]), ux);
+          Ux[f][l] = ux;
+        }
     }
 
     constexpr int NO1 = S::NOUT > 0 ? S::NOUT : 1;
-    double PX[NO1][ND], PY[NO1][ND], PZ[NO1][ND];
+    double PZ[NO1][ND], PY[NO1][ND], FX[NO1][NB], PX[NO1][S::NCH == 3 ? ND : 1];
 #pragma unroll
     for (int o = 0; o < NO1; ++o)
 #pragma unroll
-      for (int c = 0; c < ND; ++c) PX[o][c] = PY[o][c] = PZ[o][c] = 0.0;
+      for (int c = 0; c < ND; ++c) {
+        PZ[o][c] = PY[o][c] = 0.0;
+        if constexpr (S::NCH == 3) PX[o][c] = 0.0;
+      }
     double gpart = 0.0;
 
 #pragma unroll
@@ -666,26 +705,33 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
                            M.xz * (M.xy * M.yz - M.yy * M.xz);
         W = det * (iwij2 * T.wi2[l]);   // W = w detJ = det(M) / w^2
       }
-      // z-contraction of row l
-      double Ul[S::NIN], Uzl[S::NIN], Uyl[S::NIN], Ux[S::NIN];
+      // z- and y-derivative of row l (3 channels: value and x-derivative too)
+      double Ul[S::NIN], Uxl[S::NIN], Uzl[S::NIN], Uyl[S::NIN];
 #pragma unroll
       for (int f = 0; f < S::NIN; ++f) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
         for (int c = 0; c < ND; ++c) {
-          a0 = fma(T.B[l][c], w[f][c], a0);
           a1 = fma(T.G[l][c], w[f][c], a1);
           a2 = fma(T.B[l][c], w[f][ND + c], a2);
-          a3 = fma(T.B[l][c], w[f][2 * ND + c], a3);
+          if constexpr (S::NCH == 3) {
+            a0 = fma(T.B[l][c], w[f][c], a0);
+            a3 = fma(T.B[l][c], w[f][2 * ND + c], a3);
+          }
         }
-        Ul[f] = a0;
         Uzl[f] = a1;
-        Ux[f] = a2;
-        Uyl[f] = a3;
+        Uyl[f] = a2;
+        if constexpr (S::NCH == 3) {
+          Ul[f] = a0;
+          Uxl[f] = a3;
+        } else {
+          Ul[f] = U[f][l];
+          Uxl[f] = Ux[f][l];
+        }
       }
       double F0[4], F1[4];   // Fx, Fy, Fz, V of output 0 (and 1)
       if constexpr (MODE == MODE_RES) {
-        const double gh[3] = {Ux[0], Uyl[0], Uzl[0]};
+        const double gh[3] = {Uxl[0], Uyl[0], Uzl[0]};
         double Fh[3];
         flux_hat<MODEL>(Ul[0], gh, M, W, rho_e, P, Fh);
         F0[0] = Fh[0]; F0[1] = Fh[1]; F0[2] = Fh[2];
@@ -693,7 +739,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       } else if constexpr (MODE == MODE_JVP || MODE == MODE_JVPRES) {
         using D = dual<double>;
         const D ud(Ul[0], Ul[1]);
-        const D gh[3] = {D(Ux[0], Ux[1]), D(Uyl[0], Uyl[1]), D(Uzl[0], Uzl[1])};
+        const D gh[3] = {D(Uxl[0], Uxl[1]), D(Uyl[0], Uyl[1]), D(Uzl[0], Uzl[1])};
         D Fh[3];
         flux_hat<MODEL>(ud, gh, M, W, rho_e, P, Fh);
         F0[0] = Fh[0].d; F0[1] = Fh[1].d; F0[2] = Fh[2].d;
@@ -705,23 +751,38 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       } else {   // MODE_DESIGN: seed d/drho; field 1 is lambda
         using D = dual<double>;
         const D ud(Ul[0]);
-        const D gh[3] = {D(Ux[0]), D(Uyl[0]), D(Uzl[0])};
+        const D gh[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
         const D rd(rho_e, 1.0);
         D Fh[3];
         flux_hat<MODEL>(ud, gh, M, W, rd, P, Fh);
-        gpart -= Ux[1] * Fh[0].d + Uyl[1] * Fh[1].d + Uzl[1] * Fh[2].d;
+        gpart -= Uxl[1] * Fh[0].d + Uyl[1] * Fh[1].d + Uzl[1] * Fh[2].d;
       }
-      // transposed z-contraction at the point
+      // transposed z-contraction of the y, z and value channels at the point;
+      // the x channel is kept for the batched transposed x-derivative below
 #pragma unroll
       for (int o = 0; o < S::NOUT; ++o) {
         const double* Fo = (o == 0) ? F0 : F1;
+        if constexpr (S::NCH == 2) FX[o][l] = Fo[0];
 #pragma unroll
         for (int c = 0; c < ND; ++c) {
-          PX[o][c] = fma(T.B[l][c], Fo[0], PX[o][c]);
+          if constexpr (S::NCH == 3) PX[o][c] = fma(T.B[l][c], Fo[0], PX[o][c]);
           PY[o][c] = fma(T.B[l][c], Fo[1], PY[o][c]);
           PZ[o][c] = fma(T.G[l][c], Fo[2], fma(T.B[l][c], Fo[3], PZ[o][c]));
         }
       }
+    }
+    // 2 channels: transposed collocated x-derivative (one batched all-gather), then its z-contraction
+    if constexpr (S::NCH == 2) {
+#pragma unroll
+      for (int o = 0; o < S::NOUT; ++o)
+#pragma unroll
+        for (int l = 0; l < NQ; ++l) {
+          double ax = DxT[0] * FX[o][l];
+#pragma unroll
+          for (int k = 1; k < ND; ++k) ax = fma(DxT[k], grp_shfl(FX[o][l], src[k]), ax);
+#pragma unroll
+          for (int c = 0; c < ND; ++c) PZ[o][c] = fma(T.B[l][c], ax, PZ[o][c]);
+        }
     }
 
     if constexpr (MODE == MODE_DESIGN) {
@@ -735,17 +796,23 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       }
       elem_sync<S::WARP_ELEM, S::NTC>();             // sums read before the next layer's writes
     } else {
-      // write PX, PY, PZ in place of this thread's (consumed) forward inputs
+      // write PZ, PY in place of this thread's (consumed) forward inputs
 #pragma unroll
       for (int o = 0; o < S::NOUT; ++o) {
         double* xo = xe + o * S::SF + gr * S::SJ + lic * S::SI;
-        double pv[3 * ND];
+        if (lvalid) {   // [PZ | PY (| PX)]
 #pragma unroll
-        for (int c = 0; c < ND; ++c) { pv[c] = PX[o][c]; pv[ND + c] = PY[o][c]; pv[2 * ND + c] = PZ[o][c]; }
-        if (lvalid) {
-#pragma unroll
-          for (int c = 0; c + 1 < 3 * ND; c += 2) *reinterpret_cast<double2*>(xo + c) = make_double2(pv[c], pv[c + 1]);
-          if constexpr ((3 * ND) % 2) xo[3 * ND - 1] = pv[3 * ND - 1];
+          for (int c = 0; c + 1 < ND; c += 2) {
+            *reinterpret_cast<double2*>(xo + c) = make_double2(PZ[o][c], PZ[o][c + 1]);
+            *reinterpret_cast<double2*>(xo + ND + c) = make_double2(PY[o][c], PY[o][c + 1]);
+            if constexpr (S::NCH == 3)
+              *reinterpret_cast<double2*>(xo + 2 * ND + c) = make_double2(PX[o][c], PX[o][c + 1]);
+          }
+          if constexpr (ND % 2) {
+            xo[ND - 1] = PZ[o][ND - 1];
+            xo[2 * ND - 1] = PY[o][ND - 1];
+            if constexpr (S::NCH == 3) xo[3 * ND - 1] = PX[o][ND - 1];
+          }
         }
       }
       elem_sync<S::WARP_ELEM, S::NTC>();
@@ -755,25 +822,35 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
 #pragma unroll
       for (int o = 0; o < S::NOUT; ++o) {
         const double* xi = xe + o * S::SF + lic * S::SI + gr;
-        double QX[ND], QW[ND];
+        // Q[b] = sum_j B[j][b] PZ[j] + G[j][b] PY[j]  (3 channels: QX[b] = sum_j B[j][b] PX[j] apart)
+        double Q[ND], QX[ND];
 #pragma unroll
-        for (int b = 0; b < ND; ++b) QX[b] = QW[b] = 0.0;
+        for (int b = 0; b < ND; ++b) Q[b] = QX[b] = 0.0;
 #pragma unroll
         for (int j = 0; j < ND; ++j) {
-          const double px = xi[j * S::SJ], py = xi[j * S::SJ + ND], pz = xi[j * S::SJ + 2 * ND];
+          const double pz = xi[j * S::SJ], py = xi[j * S::SJ + ND];
 #pragma unroll
-          for (int b = 0; b < ND; ++b) {
-            QX[b] = fma(T.B[j][b], px, QX[b]);
-            QW[b] = fma(T.G[j][b], py, fma(T.B[j][b], pz, QW[b]));
+          for (int b = 0; b < ND; ++b) Q[b] = fma(T.B[j][b], pz, fma(T.G[j][b], py, Q[b]));
+          if constexpr (S::NCH == 3) {
+            const double px = xi[j * S::SJ + 2 * ND];
+#pragma unroll
+            for (int b = 0; b < ND; ++b) QX[b] = fma(T.B[j][b], px, QX[b]);
           }
         }
-        // r[a][b] = sum_i G[i][a] QX_i[b] + B[i][a] QW_i[b]: lane a keeps its row
+        // r[a][b] = sum_i B[i][a] Q_i[b] (+ G[i][a] QX_i[b]): lane a keeps its row
 #pragma unroll
         for (int b = 0; b < ND; ++b) {
-          double r = fma(Gt[0], QX[b], Bt[0] * QW[b]);
+          if constexpr (S::NCH == 2) {
+            double r = Bt[0] * Q[b];
 #pragma unroll
-          for (int k = 1; k < ND; ++k) r += grp_shfl(fma(Gt[k], QX[b], Bt[k] * QW[b]), src[k]);
-          R[o][b] = r;
+            for (int k = 1; k < ND; ++k) r += grp_shfl(Bt[k] * Q[b], src[k]);
+            R[o][b] = r;
+          } else {
+            double r = fma(Gt[0], QX[b], Bt[0] * Q[b]);
+#pragma unroll
+            for (int k = 1; k < ND; ++k) r += grp_shfl(fma(Gt[k], QX[b], Bt[k] * Q[b]), src[k]);
+            R[o][b] = r;
+          }
         }
       }
       // element results -> the IO warp (double-buffered by layer parity)
