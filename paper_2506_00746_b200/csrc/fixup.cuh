@@ -19,22 +19,6 @@ namespace feod {
 
 constexpr int kFixThreads = 128;
 
-// brick index along one axis of global DOF coordinate g, and whether g sits on
-// an interior brick face (then the lower brick, local index P, contributes too)
-struct Axis { int b, loc, n; };
-
-template <int PS>
-FEOD_DEV Axis axis_of(int g, int nb) {
-  int b = g / PS;
-  if (b >= nb) b = nb - 1;
-  const int loc = g - b * PS;
-  Axis a;
-  a.b = b;
-  a.loc = loc;
-  a.n = (loc == 0 && b > 0) ? 2 : 1;
-  return a;
-}
-
 // box extent of brick b along an axis (the last brick may be ragged)
 template <int K, int B>
 FEOD_DEV int box_len(int b, int ne) { return K * min(B, ne - b * B) + 1; }
@@ -50,6 +34,13 @@ FEOD_DEV int srank(int lx, int ly, int lz, int LX, int LY, int LZ) {
   return r + 2 * LX + 2 * (ly - 1) + (lx == 0 ? 0 : 1);
 }
 
+// offset of brick-local (lx, ly, lz) in the shell buffer
+template <int K, int BX, int BY, int BZ>
+FEOD_DEV int64_t shell_off(const OpParams& P, int bx, int by, int bz, int lx, int ly, int lz) {
+  const int LX = box_len<K, BX>(bx, P.nx), LY = box_len<K, BY>(by, P.ny), LZ = box_len<K, BZ>(bz, P.nz);
+  return (bx + (int64_t)P.nbx * (by + (int64_t)P.nby * bz)) * P.shell_stride + srank(lx, ly, lz, LX, LY, LZ);
+}
+
 template <int K, int BX, int BY, int BZ, bool TWO>
 __global__ void __launch_bounds__(kFixThreads) fixup_kernel(const OpParams P, int bxX, int bxY, int nX, int nY,
                                                             const double* __restrict__ shell0, double* __restrict__ out0,
@@ -57,42 +48,56 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(const OpParams P, in
   constexpr int PX = K * BX, PY = K * BY, PZ = K * BZ;
   int blk = blockIdx.x;
   int X, Y, Z;
-  if (blk < nY) {                            // set Y: row along X
+  // contributors along the three axes: brick index and local index of each (up to 2);
+  // the shared axis of the set and the row's fixed coordinate are CTA-uniform
+  int bxa[2], lxa[2], bya[2], lya[2], bza[2], lza[2], nx, ny, nz;
+  auto single = [](int g, int PS, int nb, int* b, int* l, int& n) {
+    int bb = g / PS;
+    if (bb >= nb) bb = nb - 1;
+    b[0] = bb; l[0] = g - bb * PS; n = 1;
+    if (l[0] == 0 && bb > 0) { b[1] = bb; l[1] = 0; b[0] = bb - 1; l[0] = PS; n = 2; }
+  };
+  if (blk < nY) {                            // set Y: row along X (X on an x-plane skipped)
     const int xb = blk % bxY, rest = blk / bxY;
-    Y = (rest % (P.nby - 1) + 1) * PY;
+    const int m = rest % (P.nby - 1) + 1;
     Z = rest / (P.nby - 1);
+    Y = m * PY;
     X = xb * kFixThreads + threadIdx.x;
     if (X >= P.Mx || (X % PX == 0 && X > 0 && X < P.Mx - 1)) return;
-  } else if (blk < nY + nX) {                // set X: row along Y
+    bya[0] = m - 1; lya[0] = PY; bya[1] = m; lya[1] = 0; ny = 2;
+    single(Z, PZ, P.nbz, bza, lza, nz);
+    bxa[0] = min(X / PX, P.nbx - 1); lxa[0] = X - bxa[0] * PX; nx = 1;
+  } else if (blk < nY + nX) {                // set X: row along Y (edges and corners too)
     blk -= nY;
     const int xb = blk % bxX, rest = blk / bxX;
-    X = (rest % (P.nbx - 1) + 1) * PX;
+    const int m = rest % (P.nbx - 1) + 1;
     Z = rest / (P.nbx - 1);
+    X = m * PX;
     Y = xb * kFixThreads + threadIdx.x;
     if (Y >= P.My) return;
-  } else {                                   // set Z: row along X
+    bxa[0] = m - 1; lxa[0] = PX; bxa[1] = m; lxa[1] = 0; nx = 2;
+    single(Z, PZ, P.nbz, bza, lza, nz);
+    single(Y, PY, P.nby, bya, lya, ny);
+  } else {                                   // set Z: row along X (X / Y on a plane skipped)
     blk -= nY + nX;
     const int xb = blk % bxY, rest = blk / bxY;
-    Z = (rest % (P.nbz - 1) + 1) * PZ;
+    const int m = rest % (P.nbz - 1) + 1;
     Y = rest / (P.nbz - 1);
     if (Y % PY == 0 && Y > 0 && Y < P.My - 1) return;
     X = xb * kFixThreads + threadIdx.x;
     if (X >= P.Mx || (X % PX == 0 && X > 0 && X < P.Mx - 1)) return;
+    Z = m * PZ;
+    bza[0] = m - 1; lza[0] = PZ; bza[1] = m; lza[1] = 0; nz = 2;
+    bya[0] = min(Y / PY, P.nby - 1); lya[0] = Y - bya[0] * PY; ny = 1;
+    bxa[0] = min(X / PX, P.nbx - 1); lxa[0] = X - bxa[0] * PX; nx = 1;
   }
-  const Axis ax = axis_of<PX>(X, P.nbx), ay = axis_of<PY>(Y, P.nby), az = axis_of<PZ>(Z, P.nbz);
-  // gather all contributions first (independent loads), then sum in fixed order
+  // gather the (2, 4 or 8) contributions first, then sum in fixed order (z, y, x ascending)
   double v0[8], v1[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int cx = q & 1, cy = (q >> 1) & 1, cz = q >> 2;
-    v0[q] = 0.0;
-    v1[q] = 0.0;
-    if (cx < ax.n && cy < ay.n && cz < az.n) {
-      // c = 0 is the lower brick when the axis is shared
-      const int bxx = ax.b - (ax.n - 1 - cx), byy = ay.b - (ay.n - 1 - cy), bzz = az.b - (az.n - 1 - cz);
-      const int LX = box_len<K, BX>(bxx, P.nx), LY = box_len<K, BY>(byy, P.ny), LZ = box_len<K, BZ>(bzz, P.nz);
-      const int lx = (bxx < ax.b) ? LX - 1 : ax.loc, ly = (byy < ay.b) ? LY - 1 : ay.loc, lz = (bzz < az.b) ? LZ - 1 : az.loc;
-      const int64_t o = (bxx + (int64_t)P.nbx * (byy + (int64_t)P.nby * bzz)) * P.shell_stride + srank(lx, ly, lz, LX, LY, LZ);
+    if (cx < nx && cy < ny && cz < nz) {
+      const int64_t o = shell_off<K, BX, BY, BZ>(P, bxa[cx], bya[cy], bza[cz], lxa[cx], lya[cy], lza[cz]);
       v0[q] = __ldcs(shell0 + o);
       if constexpr (TWO) v1[q] = __ldcs(shell1 + o);
     }
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(const OpParams P, in
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int cx = q & 1, cy = (q >> 1) & 1, cz = q >> 2;
-    if (cx < ax.n && cy < ay.n && cz < az.n) {
+    if (cx < nx && cy < ny && cz < nz) {
       s0 += v0[q];
       if constexpr (TWO) s1 += v1[q];
     }
