@@ -46,7 +46,7 @@ namespace feod {
 
 template <int ND> struct PlaneTile;
 template <> struct PlaneTile<2> { static constexpr int BX = 8, BY = 4, BZ = 16; };
-template <> struct PlaneTile<3> { static constexpr int BX = 4, BY = 4, BZ = 16; };
+template <> struct PlaneTile<3> { static constexpr int BX = 4, BY = 3, BZ = 16; };
 template <> struct PlaneTile<4> { static constexpr int BX = 4, BY = 2, BZ = 16; };
 template <> struct PlaneTile<5> { static constexpr int BX = 4, BY = 2, BZ = 8; };
 template <> struct PlaneTile<6> { static constexpr int BX = 2, BY = 2, BZ = 8; };
@@ -58,7 +58,7 @@ template <> struct PlaneTile<7> { static constexpr int BX = 2, BY = 2, BZ = 8; }
 //  node-phase 8-byte accesses   addr = e SE + i SI + r          (per half-warp)
 //  point-phase 16-byte accesses addr = e SE + i SI + r SJ + 2m  (per quarter-warp)
 constexpr int xb_cost(int nd, int SI, int SJ, int SE) {
-  const int gpw = 32 / nd;
+  const int gpw = (nd * nd <= 32) ? (32 / (nd * nd)) * nd : 32 / nd;   // as PShape::GPW
   int cost = 0;
   for (int half = 0; half < 2; ++half) {
     int cnt[16] = {};
@@ -119,12 +119,14 @@ struct PShape {
   static constexpr int K = ND - 1;
   static constexpr int BX = PlaneTile<ND>::BX, BY = PlaneTile<ND>::BY, BZ = PlaneTile<ND>::BZ;
   static constexpr int EL = BX * BY;                         // elements per layer
-  static constexpr int GPW = 32 / ND;                        // lane groups per warp
+  // lane groups per warp: whole elements per warp when an element fits (ND^2 <= 32),
+  // so that element-level syncs are warp barriers (Q2: 3 elements on 27 lanes)
+  static constexpr int GPW = (ND * ND <= 32) ? (32 / (ND * ND)) * ND : 32 / ND;
   static constexpr int NG = EL * ND;                         // groups in use
   static constexpr int NWC = (NG + GPW - 1) / GPW;           // compute warps
   static constexpr int NTC = 32 * NWC;
   static constexpr int NT = NTC + 32;                        // + the IO warp
-  static constexpr bool WARP_ELEM = (32 % (ND * ND)) == 0;   // an element never straddles a warp
+  static constexpr bool WARP_ELEM = (GPW % ND) == 0;         // an element never straddles a warp
   // register budget: 128 per thread (occupancy first), except the two-field
   // (tangent) modes of Q5/Q6, whose per-thread state stays in registers (one CTA per SM)
   static constexpr int MINB = FEOD_MINB_OVERRIDE > 0 ? FEOD_MINB_OVERRIDE
