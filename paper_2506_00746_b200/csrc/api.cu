@@ -2,6 +2,7 @@
 // Every compute step runs in this library's kernels; there is no CPU path.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -28,6 +29,8 @@ struct feod_op {
   double* red = nullptr;       // kRedBlocks partials + 8 scalars
   int* flag = nullptr;
   unsigned long long* sched = nullptr;   // dynamic brick scheduling ticket counter
+  unsigned long long* bdone = nullptr;   // per-brick completion epochs (fix-up dependencies)
+  int2* fixrows = nullptr;               // fix-up rows in launch order
   double* work = nullptr;      // Newton-CG: F, r, p, Ap, d (5 N)
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
 };
@@ -60,6 +63,8 @@ static void free_all(feod_op* h) {
   cudaFree(h->red);
   cudaFree(h->flag);
   cudaFree(h->sched);
+  cudaFree(h->bdone);
+  cudaFree(h->fixrows);
   cudaFree(h->work);
 }
 
@@ -139,6 +144,31 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
     return cleanup_fail(cuda_fail(e, "feod_create: memset"));
   P.sched = h->sched;
   P.sched_base = 0;
+  if ((e = cudaMalloc(&h->bdone, sizeof(unsigned long long) * (size_t)h->nbricks)) != cudaSuccess)
+    return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: brick epochs"));
+  if ((e = cudaMemsetAsync(h->bdone, 0, sizeof(unsigned long long) * (size_t)h->nbricks, h->st)) != cudaSuccess)
+    return cleanup_fail(cuda_fail(e, "feod_create: memset"));
+  P.bdone = h->bdone;
+  {
+    // fix-up rows, stably sorted by the last brick ticket they read
+    const int nrows = fixup_rows_nd(h->nd, P, nullptr, nullptr);
+    if (nrows < 0) return cleanup_fail(fail(FEOD_EUNSUPPORTED, "feod_create: fix-up rows"));
+    std::vector<int2> rows(nrows), sorted(nrows);
+    std::vector<unsigned long long> keys(nrows);
+    std::vector<int> idx(nrows);
+    fixup_rows_nd(h->nd, P, rows.data(), keys.data());
+    for (int i = 0; i < nrows; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return keys[a] < keys[b]; });
+    for (int i = 0; i < nrows; ++i) sorted[i] = rows[idx[i]];
+    P.nfixrows = nrows;
+    if (nrows > 0) {
+      if ((e = cudaMalloc(&h->fixrows, sizeof(int2) * (size_t)nrows)) != cudaSuccess)
+        return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: fix-up rows"));
+      if ((e = cudaMemcpy(h->fixrows, sorted.data(), sizeof(int2) * (size_t)nrows, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return cleanup_fail(cuda_fail(e, "feod_create: fix-up rows copy"));
+    }
+    P.fixrows = h->fixrows;
+  }
   if ((e = cudaMemsetAsync(h->flag, 0, sizeof(int) * 2, h->st)) != cudaSuccess)
     return cleanup_fail(cuda_fail(e, "feod_create: memset"));
 
@@ -205,13 +235,14 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   h->prof_begin = h->prof_end = nullptr;
   if (pb) cudaEventRecord(pb, h->st);
   int grid = 0;
+  const unsigned long long epoch = h->P.sched_base + 1;   // what the IO warps publish per finished brick
   cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, h->geom == nullptr, h->nbricks, h->P, h->T, p, h->st, &grid);
   // every CTA claims one ticket per brick it processes plus one that ends it
   h->P.sched_base += (unsigned long long)h->nbricks + (unsigned long long)grid;
   if (pe) cudaEventRecord(pe, h->st);
   if (e != cudaSuccess) return cuda_fail(e, name);
   if (mode != MODE_DESIGN) {
-    e = fixup_nd(h->nd, h->P, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
+    e = fixup_nd(h->nd, h->P, epoch, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
                  mode == MODE_JVPRES ? out1 : nullptr, h->st);
     if (e != cudaSuccess) return cuda_fail(e, name);
   }

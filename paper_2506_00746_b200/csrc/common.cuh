@@ -48,6 +48,11 @@ struct OpParams {
   // are bricks, the rest end a CTA; the host advances sched_base by #bricks + grid
   unsigned long long* sched;
   unsigned long long sched_base;
+  // fix-up dependencies: bdone[b] = sched_base + 1 of the last call whose IO warp
+  // finished brick b's stores (release); fixrows = the fix-up rows in launch order
+  unsigned long long* bdone;
+  const int2* fixrows;
+  int nfixrows;
 };
 
 FEOD_HD bool is_dirichlet(int X, int Y, int Z, int Mx, int My, int Mz, uint32_t faces) {

@@ -40,17 +40,29 @@ cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const 
   return cudaErrorInvalidValue;
 }
 
-cudaError_t fixup_nd(int nd, const OpParams& P, const double* shell0, double* out0, const double* shell1, double* out1,
-                     cudaStream_t st) {
+cudaError_t fixup_nd(int nd, const OpParams& P, unsigned long long epoch, const double* shell0, double* out0,
+                     const double* shell1, double* out1, cudaStream_t st) {
   switch (nd) {
-    case 2: return fixup_order<2>(P, shell0, out0, shell1, out1, st);
-    case 3: return fixup_order<3>(P, shell0, out0, shell1, out1, st);
-    case 4: return fixup_order<4>(P, shell0, out0, shell1, out1, st);
-    case 5: return fixup_order<5>(P, shell0, out0, shell1, out1, st);
-    case 6: return fixup_order<6>(P, shell0, out0, shell1, out1, st);
-    case 7: return fixup_order<7>(P, shell0, out0, shell1, out1, st);
+    case 2: return fixup_order<2>(P, epoch, shell0, out0, shell1, out1, st);
+    case 3: return fixup_order<3>(P, epoch, shell0, out0, shell1, out1, st);
+    case 4: return fixup_order<4>(P, epoch, shell0, out0, shell1, out1, st);
+    case 5: return fixup_order<5>(P, epoch, shell0, out0, shell1, out1, st);
+    case 6: return fixup_order<6>(P, epoch, shell0, out0, shell1, out1, st);
+    case 7: return fixup_order<7>(P, epoch, shell0, out0, shell1, out1, st);
   }
   return cudaErrorInvalidValue;
+}
+
+int fixup_rows_nd(int nd, const OpParams& P, int2* rows, unsigned long long* keys) {
+  switch (nd) {
+    case 2: return fixup_rows_order<2>(P, rows, keys);
+    case 3: return fixup_rows_order<3>(P, rows, keys);
+    case 4: return fixup_rows_order<4>(P, rows, keys);
+    case 5: return fixup_rows_order<5>(P, rows, keys);
+    case 6: return fixup_rows_order<6>(P, rows, keys);
+    case 7: return fixup_rows_order<7>(P, rows, keys);
+  }
+  return -1;
 }
 
 }  // namespace feod

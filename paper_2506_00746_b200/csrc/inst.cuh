@@ -96,10 +96,16 @@ cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int grid, const
 }
 
 template <>
-cudaError_t fixup_order<FEOD_ND>(const OpParams& P, const double* shell0, double* out0, const double* shell1,
-                                 double* out1, cudaStream_t st) {
+cudaError_t fixup_order<FEOD_ND>(const OpParams& P, unsigned long long epoch, const double* shell0, double* out0,
+                                 const double* shell1, double* out1, cudaStream_t st) {
   using S = PShape<FEOD_ND, MODE_RES>;
-  return launch_fixup_t<S::K, S::BX, S::BY, S::BZ>(P, shell0, out0, shell1, out1, st);
+  return launch_fixup_t<S::K, S::BX, S::BY, S::BZ>(P, epoch, shell0, out0, shell1, out1, st);
+}
+
+template <>
+int fixup_rows_order<FEOD_ND>(const OpParams& P, int2* rows, unsigned long long* keys) {
+  using S = PShape<FEOD_ND, MODE_RES>;
+  return fixup_rows<S::K, S::BX, S::BY, S::BZ>(P, rows, keys);
 }
 
 }  // namespace feod

@@ -25,16 +25,18 @@ template <int ND> bool brick_info(BrickInfo* bi);
 template <int ND> cudaError_t prepare_order();
 template <int ND> cudaError_t launch_order(int mode, int model, bool affine, int grid, const OpParams& P,
                                            const Tables& T, const OpPtrs& p, cudaStream_t st, int* grid_out);
-template <int ND> cudaError_t fixup_order(const OpParams& P, const double* shell0, double* out0, const double* shell1,
-                                          double* out1, cudaStream_t st);
+template <int ND> cudaError_t fixup_order(const OpParams& P, unsigned long long epoch, const double* shell0,
+                                          double* out0, const double* shell1, double* out1, cudaStream_t st);
+template <int ND> int fixup_rows_order(const OpParams& P, int2* rows, unsigned long long* keys);
 
 #define FEOD_DECLARE_ORDER(ND)                                                                    \
   template <> bool brick_info<ND>(BrickInfo * bi);                                                \
   template <> cudaError_t prepare_order<ND>();                                                    \
   template <> cudaError_t launch_order<ND>(int mode, int model, bool affine, int grid, const OpParams& P, \
                                            const Tables& T, const OpPtrs& p, cudaStream_t st, int* grid_out); \
-  template <> cudaError_t fixup_order<ND>(const OpParams& P, const double* shell0, double* out0,          \
-                                          const double* shell1, double* out1, cudaStream_t st);
+  template <> cudaError_t fixup_order<ND>(const OpParams& P, unsigned long long epoch, const double* shell0, \
+                                          double* out0, const double* shell1, double* out1, cudaStream_t st); \
+  template <> int fixup_rows_order<ND>(const OpParams& P, int2* rows, unsigned long long* keys);
 FEOD_DECLARE_ORDER(2)
 FEOD_DECLARE_ORDER(3)
 FEOD_DECLARE_ORDER(4)
@@ -46,8 +48,9 @@ bool brick_info_nd(int nd, BrickInfo* bi);
 cudaError_t prepare_nd(int nd);
 cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const OpParams& P, const Tables& T,
                       const OpPtrs& p, cudaStream_t st, int* grid_out);
-cudaError_t fixup_nd(int nd, const OpParams& P, const double* shell0, double* out0, const double* shell1, double* out1,
-                     cudaStream_t st);
+cudaError_t fixup_nd(int nd, const OpParams& P, unsigned long long epoch, const double* shell0, double* out0,
+                     const double* shell1, double* out1, cudaStream_t st);
+int fixup_rows_nd(int nd, const OpParams& P, int2* rows, unsigned long long* keys);
 
 // BLAS-1 (blas1.cu): deterministic fixed-grid two-stage reductions.
 constexpr int kRedBlocks = 296;

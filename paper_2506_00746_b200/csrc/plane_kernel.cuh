@@ -35,7 +35,7 @@
 #include "common.cuh"
 #include "dual.cuh"
 #include "physics.cuh"
-#ifdef FEOD_PROFILE_IO
+#if defined(FEOD_PROFILE_IO) || defined(FEOD_PROFILE_TAIL)
 #include <cstdio>
 #endif
 
@@ -192,6 +192,36 @@ FEOD_DEV double ld_stream(const double* p) {
   return v;
 }
 
+// L2 eviction-priority policies (createpolicy) for the streamed metric and the
+// shell slab the fix-up reads right after the kernel.
+#ifndef FEOD_L2_METRIC_FIRST
+#define FEOD_L2_METRIC_FIRST 0
+#endif
+#ifndef FEOD_L2_SHELL_LAST
+#define FEOD_L2_SHELL_LAST 0
+#endif
+FEOD_DEV uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+FEOD_DEV uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+FEOD_DEV double ld_stream_pol(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+FEOD_DEV void st_pol(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+FEOD_DEV void prefetch_l2_pol(const void* p, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol) : "memory");
+}
+
 // L2 prefetch of a contiguous byte range (bulk-copy engine; no completion tracking).
 FEOD_DEV void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -254,6 +284,8 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   uint64_t* e_empty = bars + 6;             // [2] layer z's element results consumed (IO -> compute)
   int* bq = reinterpret_cast<int*>(bars + 8);   // [8] claimed brick of the CTA's n-th brick (-1: done)
 
+  // the fix-up kernel may launch now: it waits per brick on P.bdone, not on this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform: lets the compiler keep table constants in uniform registers
@@ -426,6 +458,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       }
     };
 
+    const uint64_t pol_shell = FEOD_L2_SHELL_LAST ? l2_policy_last() : 0;
     // P^T + store of the finished value v of output o at position m, DOF plane p (general path)
     auto store_dof = [&](int o, int m, int p, double v) {
       const int info = pinfo[m];
@@ -434,7 +467,9 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         const int base = gs.LX * gs.LY, ring = 2 * gs.LX + 2 * (gs.LY - 2);
         const int rank = (p == 0) ? pxy[m] : (p == gs.LZ - 1) ? base + (gs.LZ - 2) * ring + pxy[m]
                                                                : base + (p - 1) * ring + (info >> 3);
-        (o == 0 ? shell0 : shell1)[(int64_t)gs.b * P.shell_stride + rank] = v;
+        double* d = (o == 0 ? shell0 : shell1) + (int64_t)gs.b * P.shell_stride + rank;
+        if constexpr (FEOD_L2_SHELL_LAST) st_pol(d, v, pol_shell);
+        else *d = v;
       } else {
         const int gz = gs.gZ0 + p;
         const bool dir = (info & 4) || ((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1);
@@ -508,7 +543,13 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
               const bool zero = (pinfo[m] & 6) == 4;
               double* d = reinterpret_cast<double*>(fptr[o][m]) + (int64_t)(K * z) * fstr[m];
 #pragma unroll
-              for (int c = 0; c < K; ++c) d[(int64_t)c * fstr[m]] = zero ? 0.0 : v[c];
+              if (FEOD_L2_SHELL_LAST && (pinfo[m] & 2)) {
+#pragma unroll
+                for (int c = 0; c < K; ++c) st_pol(d + (int64_t)c * fstr[m], v[c], pol_shell);
+              } else {
+#pragma unroll
+                for (int c = 0; c < K; ++c) d[(int64_t)c * fstr[m]] = zero ? 0.0 : v[c];
+              }
               carry[o][m] = v[K];
             } else {
 #pragma unroll
@@ -525,7 +566,17 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
 #ifdef FEOD_PROFILE_IO
       ++nl;
 #endif
-      if (++sz == gs.bzr) sz = 0;
+      if (++sz == gs.bzr) {
+        sz = 0;
+        if constexpr (S::NOUT > 0) {   // brick done: publish its epoch to the fix-up rows that read it
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(P.bdone + gs.b), "l"(P.sched_base + 1)
+                         : "memory");
+          }
+        }
+      }
     }
 #ifdef FEOD_PROFILE_IO
     if (lane == 0 && blockIdx.x % 97 == 0 && nl > 0)
@@ -559,11 +610,16 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   double* const xe = xb + el * S::SE;   // this element's exchange slot
   const double wij = T.w[lic] * T.w[gr];
   const double iwij2 = T.wi2[lic] * T.wi2[gr];
+  const uint64_t pol_metric = FEOD_L2_METRIC_FIRST ? l2_policy_first() : 0;
 
 #ifdef FEOD_PROFILE_IO
   long long c_wrf = 0, c_wee = 0, c_start = clock64();
   unsigned long long ns_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_start));
+#endif
+#ifdef FEOD_PROFILE_TAIL
+  unsigned long long tail_t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tail_t0));
 #endif
   int L = 0;       // CTA-global layer counter (mbarrier phases, element-buffer parity)
   int rbase = 0;   // CTA-global index of the brick's first DOF plane (input-ring slots)
@@ -584,10 +640,13 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     if constexpr (!AFFINE) {
       gm = P.geom + (evalid ? eg : 0) * (6 * NQ3) + gr * NQ + lic;
 #pragma unroll
-      for (int c = 0; c < 6; ++c) mnext[c] = ld_stream(gm + c * NQ2);
+      for (int c = 0; c < 6; ++c) mnext[c] = FEOD_L2_METRIC_FIRST ? ld_stream_pol(gm + c * NQ2, pol_metric) : ld_stream(gm + c * NQ2);
       if (tid < byr && z + 1 < bzr) {   // L2 prefetch of the next layer's metric, one x-row of elements per y
         const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + tid) + (int64_t)P.ny * (ez0 + z + 1));
-        prefetch_l2(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)));
+        if constexpr (FEOD_L2_METRIC_FIRST)
+          prefetch_l2_pol(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)), pol_metric);
+        else
+          prefetch_l2(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)));
       }
     }
     double rho_e = 0.0;
@@ -701,7 +760,9 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         M = {mnext[0], mnext[1], mnext[2], mnext[3], mnext[4], mnext[5]};
         if (l + 1 < NQ) {
 #pragma unroll
-          for (int c = 0; c < 6; ++c) mnext[c] = ld_stream(gm + (l + 1) * 6 * NQ2 + c * NQ2);
+          for (int c = 0; c < 6; ++c)
+            mnext[c] = FEOD_L2_METRIC_FIRST ? ld_stream_pol(gm + (l + 1) * 6 * NQ2 + c * NQ2, pol_metric)
+                                            : ld_stream(gm + (l + 1) * 6 * NQ2 + c * NQ2);
         }
         const double det = M.xx * (M.yy * M.zz - M.yz * M.yz) - M.xy * (M.xy * M.zz - M.yz * M.xz) +
                            M.xz * (M.xy * M.yz - M.yy * M.xz);
@@ -877,6 +938,13 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   }
   rbase += gb.LZ;
   }   // bricks
+#ifdef FEOD_PROFILE_TAIL
+  {
+    unsigned long long tail_t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tail_t1));
+    if (tid == 0) printf("TAIL %d %llu %d %d %llu %llu\n", MODE, P.sched_base, blockIdx.x, L, tail_t0, tail_t1);
+  }
+#endif
 #ifdef FEOD_PROFILE_IO
   unsigned long long ns_end;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_end));

@@ -15,8 +15,11 @@ from gpu_util import rel_l2, problem, operator, cuda, host
 pytestmark = pytest.mark.gpu
 TOL = 1e-11
 
-# (recipe, reduced n): n chosen so the mesh spans several bricks with a ragged last brick
-CASES = [(W.C1, 4), (W.C1, 7), (W.C2, 11), (W.C3, 6), (W.C3, 5), (W.C4, 3), (W.C5, 6), (W.C5, 9)]
+# (recipe, reduced n): n chosen so the mesh spans several bricks with a ragged last brick;
+# the last four cases also span two brick slabs in z (BZ = 16, Q6: 8), so every fix-up set
+# (x-, y- and z-faces, edges, corners) is exercised on full vectors
+CASES = [(W.C1, 4), (W.C1, 7), (W.C2, 11), (W.C3, 6), (W.C3, 5), (W.C4, 3), (W.C5, 6), (W.C5, 9),
+         (W.C3, 18), (W.C5, 17), (W.C2, 19), (W.C4, 9)]
 
 
 def _case(w, n):
