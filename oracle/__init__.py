@@ -12,6 +12,7 @@ What it computes (§2, Eq. 1 line 155 and Eq. 2; reference
 
 * ``residual``   r = P^T G^T B^T D(B G P u)                         (Eq. 1)
 * ``jvp``        J(u) v = P^T G^T B^T J_D(u_q) B G P v              (Eq. 2)
+* ``vjp``        J(u)^T w, the transpose of Eq. 2
 * ``design_grad`` g_e = -lambda^T dF/drho_e with the derivative taken at the
   integration points ("adjoint loads", line 199)
 * ``element_tangent`` K_e = B^T J_D B                              (Eq. 3)
@@ -28,13 +29,13 @@ paper or to mathematics, see DESIGN.md §Oracle. The Newton-CG trajectory
 beyond roundoff growth is "parity unpinned" (T17).
 """
 from .rules import gauss_legendre01, gll_nodes01, lagrange_eval
-from .fem import Problem, residual, jvp, design_grad, element_tangent, dense_jacobian
+from .fem import Problem, residual, jvp, vjp, design_grad, element_tangent, dense_jacobian
 from .fem import residual_rows, jvp_rows, design_grad_elems, dirichlet_mask, dof_map
 from .flux import flux, flux_dg, flux_du, flux_drho
 from .newton import newton_cg
 
 __all__ = [
-    "gauss_legendre01", "gll_nodes01", "lagrange_eval", "Problem", "residual", "jvp",
+    "gauss_legendre01", "gll_nodes01", "lagrange_eval", "Problem", "residual", "jvp", "vjp",
     "design_grad", "element_tangent", "dense_jacobian", "residual_rows", "jvp_rows",
     "design_grad_elems", "dirichlet_mask", "dof_map", "flux", "flux_dg", "flux_du",
     "flux_drho", "newton_cg",

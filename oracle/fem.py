@@ -238,6 +238,32 @@ def jvp(pr: Problem, u, v):
     return _assemble(pr, _jvp_elems(pr, np.asarray(u, float), np.asarray(v, float)), pr.n_dofs)
 
 
+def _vjp_elems(pr, u, w, elems=None):
+    w = np.array(w, dtype=np.float64)
+    w[dirichlet_mask(pr)] = 0.0           # J has zero Dirichlet rows, so J^T drops w there (A2)
+    parts = []
+    for ch in _chunks(pr, elems):
+        U, g = ch.interp(u)
+        _, gw = ch.interp(w)
+        kw = _params(pr, ch)
+        # column j of J (Eq. 2): sum_q W grad phi_i . (Dg grad phi_j + Du phi_j); transposed:
+        #   (J^T w)_j = sum_q W [(Dg^T grad w) . grad phi_j + (Du . grad w) phi_j]
+        Gbar = np.einsum("eqcd,eqc->eqd", fx.flux_dg(pr.model, U, g, **kw), gw)
+        Sbar = np.einsum("eqc,eqc->eq", fx.flux_du(pr.model, U, g, **kw), gw)
+        parts.append((ch.dofs, ch.test_grad(Gbar) + ch.test_val(Sbar)))
+    return parts
+
+
+def vjp(pr: Problem, u, w):
+    """Transpose of Eq. 2 (the adjoint of line 199):
+    J(u)^T w = P^T G^T B^T J_D(u_q)^T B G (Z w), Z zeroing w's Dirichlet entries
+    (the rows J drops, reading A2); every output row is kept (no P^T row mask)."""
+    idx_val = _vjp_elems(pr, np.asarray(u, float), w)
+    idx = np.concatenate([d.ravel() for d, _ in idx_val]) if idx_val else np.zeros(0, int)
+    val = np.concatenate([v.ravel() for _, v in idx_val]) if idx_val else np.zeros(0)
+    return np.bincount(idx, weights=val, minlength=pr.n_dofs)
+
+
 def _design_elems(pr, u, lam, elems=None):
     lam = np.array(lam, dtype=np.float64)
     lam[dirichlet_mask(pr)] = 0.0         # only free rows count (reading A14)

@@ -387,3 +387,27 @@ def test_newton_cg_linear_case():
     exact[free] = np.linalg.solve(K[np.ix_(free, free)], b[free])
     np.testing.assert_allclose(u, exact, rtol=1e-10, atol=1e-14)
     assert norms[-1] < 1e-12 * norms[0]
+
+
+# ------------------------------------------------------------------ T15 transposed Jacobian (NEXT-1)
+@pytest.mark.parametrize("c", CASES13, ids=lambda c: f"n{c['n']}k{c['k']}m{c['model']}")
+def test_t15_vjp_is_transposed_dense_jacobian(c):
+    """J^T w against the transpose of the dense Jacobian that T13 pins to central
+    finite differences of the residual, and the adjoint identity <w, J v> = <J^T w, v>
+    against the (separately pinned) JVP."""
+    n = c["n"]
+    rho = np.random.default_rng(4).uniform(0.1, 1, n ** 3)
+    pr = prob(n, c["k"], model=c["model"], perturbed=c["perturbed"], faces=c["faces"],
+              p=c["p"], eps=c["eps"], rho=rho)
+    u = rand_free(pr, 11)
+    rng = np.random.default_rng(12)
+    w, v = rng.uniform(-1, 1, pr.n_dofs), rng.uniform(-1, 1, pr.n_dofs)
+    A = O.dense_jacobian(pr, u)
+    JTw = O.vjp(pr, u, w)
+    np.testing.assert_allclose(JTw, A.T @ w, rtol=0, atol=1e-12 * np.max(np.abs(A)) * np.abs(w).sum())
+    lhs, rhs = w @ O.jvp(pr, u, v), JTw @ v
+    assert abs(lhs - rhs) <= 1e-12 * (np.abs(w) @ np.abs(A) @ np.abs(v))
+    # w's Dirichlet entries do not matter
+    w2 = w.copy()
+    w2[O.dirichlet_mask(pr)] = 7.0
+    np.testing.assert_array_equal(O.vjp(pr, u, w2), JTw)
