@@ -22,7 +22,7 @@
  * Design sensitivity with AD at integration points (reading A14):
  *   g_e = - sum_{i free} lambda_i dF_i/drho_e.
  *
- * Conventions (readings A1-A16):
+ * Conventions (readings A1-A17):
  *   - mesh: structured nx x ny x nz hexahedra on the unit cube, trilinear
  *     geometry from the vertex array (or uniform); Q_k with GLL nodes (A3);
  *     qorder = Gauss points per axis (A5); reference cube [0,1]^3 (A4).
@@ -121,6 +121,12 @@ FEOD_API int feod_residual(feod_handle h, const double* u, double* r);
 FEOD_API int feod_jvp(feod_handle h, const double* u, const double* v, double* Jv);
 /* r = F(u) and Jv = J(u) v from the same dual pass (value and tangent)  */
 FEOD_API int feod_jvp_res(feod_handle h, const double* u, const double* v, double* r, double* Jv);
+/* JTw = J(u)^T w, the transpose of Eq. 2 — the adjoint   *
+ * action behind PAPER.md:199's adjoint analysis.   *
+ * J has zero Dirichlet rows (A2), so w's Dirichlet entries are ignored   *
+ * and every row of JTw is kept (reading A17). One pass: J_D^T at each    *
+ * point from two dual evaluations (DESIGN.md §2 A17).                    */
+FEOD_API int feod_vjp(feod_handle h, const double* u, const double* w, double* JTw);
 /* g_e = -lambda^T dF/drho_e, lambda's Dirichlet entries ignored          *
  * (A14); HEAT_DESIGN only (others: FEOD_EINVAL)           */
 FEOD_API int feod_design_grad(feod_handle h, const double* u, const double* lambda, double* g);
@@ -128,7 +134,8 @@ FEOD_API int feod_design_grad(feod_handle h, const double* u, const double* lamb
 /* Same operations on HOST buffers: copies host->device, computes, copies
  * device->host and synchronises the stream before returning (the e2e path).
  * op: 0 residual(in0=u, out=r), 1 jvp(in0=u, in1=v, out=Jv),
- *     2 design_grad(in0=u, in1=lambda, out=g). Host memory should be pinned. */
+ *     2 design_grad(in0=u, in1=lambda, out=g), 3 vjp(in0=u, in1=w, out=JTw).
+ * Host memory should be pinned. */
 FEOD_API int feod_apply_host(feod_handle h, int op, const double* in0, const double* in1, double* out);
 
 /* Jacobian-free Newton with unpreconditioned CG (reading A15, BASELINE

@@ -28,7 +28,7 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 
 # every symbol include/feod.h declares (checked by tests/test_abi.py)
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
-           "feod_residual", "feod_jvp", "feod_jvp_res", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
+           "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
@@ -73,6 +73,7 @@ def load_library(path: str = LIB_PATH):
     lib.feod_jvp.argtypes = [vp, dp, dp, dp]
     lib.feod_jvp_res.argtypes = [vp, dp, dp, dp, dp]
     lib.feod_design_grad.argtypes = [vp, dp, dp, dp]
+    lib.feod_vjp.argtypes = [vp, dp, dp, dp]
     lib.feod_apply_host.argtypes = [vp, ctypes.c_int, dp, dp, dp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_dot.argtypes = [vp, dp, dp, i64, dp]
@@ -167,6 +168,14 @@ class Operator:
         self._sync_stream()
         _check(self.lib.feod_jvp_res(self.h, u.data_ptr(), v.data_ptr(), r.data_ptr(), Jv.data_ptr()))
         return r, Jv
+
+    def vjp(self, u, w, out=None):
+        """J(u)^T w (feod_vjp): w's Dirichlet entries ignored, every row kept."""
+        u, w = self._dev(u, self.n_dofs, "u"), self._dev(w, self.n_dofs, "w")
+        JTw = out if out is not None else self._torch.empty_like(u)
+        self._sync_stream()
+        _check(self.lib.feod_vjp(self.h, u.data_ptr(), w.data_ptr(), JTw.data_ptr()))
+        return JTw
 
     def design_grad(self, u, lam, out=None):
         u, lam = self._dev(u, self.n_dofs, "u"), self._dev(lam, self.n_dofs, "lam")

@@ -242,7 +242,9 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   if (pe) cudaEventRecord(pe, h->st);
   if (e != cudaSuccess) return cuda_fail(e, name);
   if (mode != MODE_DESIGN) {
-    e = fixup_nd(h->nd, h->P, epoch, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
+    OpParams Pf = h->P;
+    if (mode == MODE_VJP) Pf.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
+    e = fixup_nd(h->nd, Pf, epoch, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
                  mode == MODE_JVPRES ? out1 : nullptr, h->st);
     if (e != cudaSuccess) return cuda_fail(e, name);
   }
@@ -268,6 +270,12 @@ extern "C" int feod_jvp_res(feod_handle h, const double* u, const double* v, dou
   return run_op(h, MODE_JVPRES, u, v, Jv, r, nullptr, "feod_jvp_res");
 }
 
+extern "C" int feod_vjp(feod_handle h, const double* u, const double* w, double* JTw) {
+  if (!h || !u || !w || !JTw) return fail(FEOD_EINVAL, "feod_vjp: null argument");
+  if ((const double*)JTw == u || (const double*)JTw == w) return fail(FEOD_EINVAL, "feod_vjp: JTw aliases an input");
+  return run_op(h, MODE_VJP, u, w, JTw, nullptr, nullptr, "feod_vjp");
+}
+
 extern "C" int feod_design_grad(feod_handle h, const double* u, const double* lambda, double* g) {
   if (!h || !u || !lambda || !g) return fail(FEOD_EINVAL, "feod_design_grad: null argument");
   if (h->coeffs.model != FEOD_HEAT_DESIGN) return fail(FEOD_EINVAL, "feod_design_grad: model has no rho");
@@ -277,7 +285,7 @@ extern "C" int feod_design_grad(feod_handle h, const double* u, const double* la
 
 extern "C" int feod_apply_host(feod_handle h, int op, const double* in0, const double* in1, double* out) {
   if (!h || !in0 || !out || (op != 0 && !in1)) return fail(FEOD_EINVAL, "feod_apply_host: null argument");
-  if (op < 0 || op > 2) return fail(FEOD_EINVAL, "feod_apply_host: op must be 0, 1 or 2");
+  if (op < 0 || op > 3) return fail(FEOD_EINVAL, "feod_apply_host: op must be 0, 1, 2 or 3");
   const int64_t len = h->N > h->E ? h->N : h->E;
   if (!h->stage && cudaMalloc(&h->stage, sizeof(double) * 3 * (size_t)len) != cudaSuccess) {
     h->stage = nullptr;
@@ -288,7 +296,10 @@ extern "C" int feod_apply_host(feod_handle h, int op, const double* in0, const d
   double* d2 = h->stage + 2 * len;
   CK(cudaMemcpyAsync(d0, in0, sizeof(double) * h->N, cudaMemcpyHostToDevice, h->st), "feod_apply_host: H2D");
   if (op != 0) CK(cudaMemcpyAsync(d1, in1, sizeof(double) * h->N, cudaMemcpyHostToDevice, h->st), "feod_apply_host: H2D");
-  int rc = op == 0 ? feod_residual(h, d0, d2) : op == 1 ? feod_jvp(h, d0, d1, d2) : feod_design_grad(h, d0, d1, d2);
+  int rc = op == 0 ? feod_residual(h, d0, d2)
+           : op == 1 ? feod_jvp(h, d0, d1, d2)
+           : op == 2 ? feod_design_grad(h, d0, d1, d2)
+                     : feod_vjp(h, d0, d1, d2);
   if (rc != FEOD_OK) return rc;
   const int64_t nout = op == 2 ? h->E : h->N;
   CK(cudaMemcpyAsync(out, d2, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->st), "feod_apply_host: D2H");

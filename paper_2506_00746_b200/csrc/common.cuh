@@ -8,7 +8,8 @@
 
 namespace feod {
 
-enum Mode { MODE_RES = 0, MODE_JVP = 1, MODE_JVPRES = 2, MODE_DESIGN = 3 };
+enum Mode { MODE_RES = 0, MODE_JVP = 1, MODE_JVPRES = 2, MODE_DESIGN = 3, MODE_VJP = 4 };
+constexpr int kModes = 5;
 enum Model { PLAPLACE = 0, NLDIFF = 1, HEAT = 2 };
 constexpr int kMaxNQ = 8;
 

@@ -1,5 +1,5 @@
 // Instantiation of the fused operator kernel for one order (ND = k+1 nodes,
-// NQ = k+1 points per axis): 4 modes x 3 models x {affine, stored metric}.
+// NQ = k+1 points per axis): 5 modes x 3 models x {affine, stored metric}.
 #pragma once
 #include "kernels.h"
 #include "fixup.cuh"
@@ -71,6 +71,7 @@ bool brick_info<FEOD_ND>(BrickInfo* bi) {
   bi->smem[MODE_JVP] = PShape<FEOD_ND, MODE_JVP>::SMEM_BYTES;
   bi->smem[MODE_JVPRES] = PShape<FEOD_ND, MODE_JVPRES>::SMEM_BYTES;
   bi->smem[MODE_DESIGN] = PShape<FEOD_ND, MODE_DESIGN>::SMEM_BYTES;
+  bi->smem[MODE_VJP] = PShape<FEOD_ND, MODE_VJP>::SMEM_BYTES;
   return true;
 }
 
@@ -80,7 +81,8 @@ cudaError_t prepare_order<FEOD_ND>() {
   if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_RES>()) != cudaSuccess) return e;
   if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_JVP>()) != cudaSuccess) return e;
   if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_JVPRES>()) != cudaSuccess) return e;
-  return prep_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>();
+  if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>()) != cudaSuccess) return e;
+  return prep_mode<FEOD_ND, FEOD_ND, MODE_VJP>();
 }
 
 template <>
@@ -91,6 +93,7 @@ cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int grid, const
     case MODE_JVP: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVP>(model, aff, grid, P, T, p, st, grid_out);
     case MODE_JVPRES: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVPRES>(model, aff, grid, P, T, p, st, grid_out);
     case MODE_DESIGN: return launch_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>(model, aff, grid, P, T, p, st, grid_out);
+    case MODE_VJP: return launch_mode<FEOD_ND, FEOD_ND, MODE_VJP>(model, aff, grid, P, T, p, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }

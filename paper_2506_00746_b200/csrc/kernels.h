@@ -15,7 +15,7 @@ struct OpPtrs {
   double* gout;
 };
 
-struct BrickInfo { int BX, BY, BZ, threads, shell; size_t smem[4]; };
+struct BrickInfo { int BX, BY, BZ, threads, shell; size_t smem[kModes]; };
 
 cudaError_t launch_geometry(const double* verts, int nx, int ny, int nz, int nq, const Tables& T, double* geom,
                             int* bad, cudaStream_t st);

@@ -130,7 +130,7 @@ struct PShape {
   // register budget: 128 per thread (occupancy first), except the two-field
   // (tangent) modes of Q5/Q6, whose per-thread state stays in registers (one CTA per SM)
   static constexpr int MINB = FEOD_MINB_OVERRIDE > 0 ? FEOD_MINB_OVERRIDE
-                              : (ND >= 6 && (MODE == MODE_JVP || MODE == MODE_JVPRES))
+                              : (ND >= 6 && (MODE == MODE_JVP || MODE == MODE_JVPRES || MODE == MODE_VJP))
                                     ? 1
                                     : ((65536 / (NT * 128)) < 1 ? 1 : (65536 / (NT * 128)));
   static constexpr int LXF = K * BX + 1, LYF = K * BY + 1;
@@ -314,7 +314,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     // ring_full: one cp.async-arrival per IO lane (+ one plain arrival per lane for
     // the synchronously masked lambda of the design mode) + one plain arrival of
     // IO lane 0 that publishes the brick queue
-    const uint32_t nfull = (MODE == MODE_DESIGN) ? 65u : 33u;
+    const uint32_t nfull = (MODE == MODE_DESIGN || MODE == MODE_VJP) ? 65u : 33u;
     mbar_init(&ring_full[0], nfull);
     mbar_init(&ring_full[1], nfull);
     mbar_init(&ring_empty[0], S::NWC);
@@ -416,8 +416,8 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         cp_async8(ring_in + slot * S::PLANE + idx, in0 + g);
         if constexpr (S::NIN == 2) {
           double* dst = ring_in + (S::RIN + slot) * S::PLANE + idx;
-          if constexpr (MODE == MODE_DESIGN) {
-            // lambda's Dirichlet entries are masked (reading A14)
+          if constexpr (MODE == MODE_DESIGN || MODE == MODE_VJP) {
+            // lambda's / w's Dirichlet entries are masked (readings A14, A17)
             *dst = ((lpinfo[m] & 4) || dz) ? 0.0 : __ldg(in1 + g);
           } else {
             cp_async8(dst, in1 + g);
@@ -440,7 +440,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         if (id < 0) {   // phantom layer: lets the compute warps read the end marker
           ldone = true;
           mbar_arrive(bar);
-          if constexpr (MODE == MODE_DESIGN) mbar_arrive(bar);
+          if constexpr (MODE == MODE_DESIGN || MODE == MODE_VJP) mbar_arrive(bar);
           if (lane == 0) mbar_arrive(bar);
           return;
         }
@@ -450,7 +450,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       const int p0 = (lz == 0) ? 0 : K * lz + 1;
       for (int p = p0; p <= K * lz + K; ++p) load_plane(p);
       cp_async_arrive(bar);
-      if constexpr (MODE == MODE_DESIGN) mbar_arrive(bar);
+      if constexpr (MODE == MODE_DESIGN || MODE == MODE_VJP) mbar_arrive(bar);
       if (lane == 0) mbar_arrive(bar);
       if (++lz == gl.bzr) {
         lbase += gl.LZ;
@@ -472,7 +472,9 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         else *d = v;
       } else {
         const int gz = gs.gZ0 + p;
-        const bool dir = (info & 4) || ((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1);
+        // P^T: Dirichlet rows are zero, except for J^T w, which keeps every row (reading A17)
+        const bool dir = MODE != MODE_VJP &&
+                         ((info & 4) || ((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1));
         (o == 0 ? out0 : out1)[(int64_t)P.Mx * P.My * gz + pg[m]] = dir ? 0.0 : v;
       }
     };
@@ -540,7 +542,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
             }
             v[0] = carry[o][m] + v[0];
             if (z > 0 && z < bzr - 1) {   // middle layer: affine destination, one add per store
-              const bool zero = (pinfo[m] & 6) == 4;
+              const bool zero = MODE != MODE_VJP && (pinfo[m] & 6) == 4;
               double* d = reinterpret_cast<double*>(fptr[o][m]) + (int64_t)(K * z) * fstr[m];
 #pragma unroll
               if (FEOD_L2_SHELL_LAST && (pinfo[m] & 2)) {
@@ -811,6 +813,22 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
           F1[0] = Fh[0].v; F1[1] = Fh[1].v; F1[2] = Fh[2].v;
           F1[3] = -P.f * W;
         }
+      } else if constexpr (MODE == MODE_VJP) {
+        // J^T w at the point (field 1 is w): value channel gw . dFh/du, flux channel
+        // (dFh/dgh)^T gw. For the three models dFh/dgh = kappa M + c (M gh)(M gh)^T is
+        // symmetric (kappa depends on gh only through gh . M gh), so the transpose is the
+        // forward derivative along (0, gw); dFh/du is the one along (1, 0) (DESIGN.md §2 A17)
+        using D = dual<double>;
+        const D uw(Ul[0]);
+        const D gw[3] = {D(Uxl[0], Uxl[1]), D(Uyl[0], Uyl[1]), D(Uzl[0], Uzl[1])};
+        D Fg[3];
+        flux_hat<MODEL>(uw, gw, M, W, rho_e, P, Fg);
+        const D uu(Ul[0], 1.0);
+        const D gu[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
+        D Fu[3];
+        flux_hat<MODEL>(uu, gu, M, W, rho_e, P, Fu);
+        F0[0] = Fg[0].d; F0[1] = Fg[1].d; F0[2] = Fg[2].d;
+        F0[3] = Uxl[1] * Fu[0].d + Uyl[1] * Fu[1].d + Uzl[1] * Fu[2].d;
       } else {   // MODE_DESIGN: seed d/drho; field 1 is lambda
         using D = dual<double>;
         const D ud(Ul[0]);

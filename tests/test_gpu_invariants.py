@@ -146,3 +146,24 @@ def test_nonuniform_box_and_dirichlet_subsets():
             assert rel_l2(host(op.jvp(cuda(u), cuda(v))), O.jvp(prv, u, v)) <= 1e-11
             if model == 2:
                 assert rel_l2(host(op.design_grad(cuda(u), cuda(lam))), O.design_grad(prv, u, lam)) <= 1e-11
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_vjp_adjoint_identity_fullsize(name):
+    """<w, J v> = <J^T w, v> through the CUDA path alone at BASELINE size, and J^T w
+    ignores w's Dirichlet entries (holds at any size; no oracle in the loop)."""
+    import paper_2506_00746_b200 as fe
+    import torch
+    w = W.CONFIGS[name]
+    d = W.draw(w)
+    rho = torch.as_tensor(d["rho"]).cuda() if "rho" in d else None
+    op = fe.from_workload(w, verts=d["verts"], rho=rho)
+    rng = np.random.default_rng(77)
+    u, v, a = cuda(d["u"]), cuda(d["v"]), cuda(rng.uniform(-1, 1, op.n_dofs))
+    Jv, JTa = op.jvp(u, v), op.vjp(u, a)
+    lhs, rhs = float(torch.dot(a, Jv)), float(torch.dot(JTa, v))
+    scale = float(torch.dot(a.abs(), Jv.abs()) + torch.dot(JTa.abs(), v.abs()))
+    assert abs(lhs - rhs) <= 1e-11 * scale
+    mask = cuda(W.dirichlet_dofs(w.n, w.k, w.faces).astype(np.float64))
+    a2 = a + 5.0 * mask
+    assert torch.equal(op.vjp(u, a2), JTa)

@@ -55,3 +55,13 @@ def test_design_grad_parity(n):
     g_ref = O.design_grad(pr, d["u"], d["lam"])
     g = host(op.design_grad(cuda(d["u"]), cuda(d["lam"])))
     assert rel_l2(g, g_ref) <= TOL
+
+
+@pytest.mark.parametrize("w,n", CASES, ids=[f"{w.name}n{n}" for w, n in CASES])
+def test_vjp_parity(w, n):
+    """J(u)^T w (NEXT-1) against the oracle's transposed Eq. 2; w = the recipe's v draw."""
+    ww, d = _case(w, n)
+    pr, op = problem(ww, d), operator(ww, d)
+    ref = O.vjp(pr, d["u"], d["v"])
+    got = host(op.vjp(cuda(d["u"]), cuda(d["v"])))
+    assert rel_l2(got, ref) <= TOL
