@@ -49,7 +49,7 @@ def algorithmic_bytes(w, call):
     """8 B per DOF per vector touched, 48 B/point metric, 8 B/elem rho and g."""
     N, E, q3 = w.n_dofs, w.n_elems, w.q ** 3
     geom = 48 * q3 * E if w.perturbed else 0
-    vec = {"residual": 2, "jvp": 3, "jvp_res": 4, "design": 2}[call]
+    vec = {"residual": 2, "jvp": 3, "vjp": 3, "jvp_res": 4, "design": 2}[call]
     extra = 0
     if w.model == W.HEAT:
         extra += 8 * E
@@ -62,13 +62,13 @@ def algorithmic_flops(w, call):
     """2 x passes x E x (q(k+1)^3 + q^2(k+1)^2 + q^3(k+1) + 3 q^4) + pointwise x E q^3."""
     k, q, E = w.k, w.q, w.n_elems
     per_pass = q * (k + 1) ** 3 + q ** 2 * (k + 1) ** 2 + q ** 3 * (k + 1) + 3 * q ** 4
-    passes = {"residual": 2, "jvp": 3, "jvp_res": 3, "design": 2}[call]
+    passes = {"residual": 2, "jvp": 3, "vjp": 3, "jvp_res": 3, "design": 2}[call]
     table = {  # pointwise flops per point (perturbed / affine) from SURVEY.md §8(d)
         (W.PLAPLACE, True): {"residual": 45, "jvp": 76}, (W.NLDIFF, True): {"residual": 38, "jvp": 43},
         (W.PLAPLACE, False): {"residual": 16, "jvp": 35}, (W.HEAT, False): {"residual": 12, "jvp": 19, "design": 14},
         (W.NLDIFF, False): {"residual": 12, "jvp": 19},
     }
-    pw = table.get((w.model, w.perturbed), {}).get(call, 20)
+    pw = table.get((w.model, w.perturbed), {}).get("jvp" if call == "vjp" else call, 20)
     return 2 * passes * E * per_pass + pw * E * q ** 3
 
 
@@ -304,6 +304,12 @@ def main():
         return a.elapsed_time(b) / reps
     t_res = time_call(lambda: op.residual(u, out=r))
     t_jvp = time_call(lambda: op.jvp(u, v, out=Jv))
+    JTw = torch.empty_like(u)
+    t_vjp = time_call(lambda: op.vjp(u, v, out=JTw))   # NEXT-1 (diagnostic, not in the step)
+    t_des = None
+    if w.model == W.HEAT:
+        g = torch.empty(op.n_elems, dtype=torch.float64, device=u.device)
+        t_des = time_call(lambda: op.design_grad(u, v, out=g))
 
     # e2e through the C-ABI host-buffer path
     e2e = None
@@ -369,7 +375,15 @@ def main():
                         "hbm_frac": by_jvp / (t_jvp * 1e-3) / 1e9 / peak,
                         "fp64_frac": fl_jvp / (t_jvp * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS,
                         "fused_kernel_us": jvp_kernel_ms * 1e3},
+                "vjp": {"us": t_vjp * 1e3, "gdof_s": N / (t_vjp * 1e-3) / 1e9,
+                        "hbm_frac": algorithmic_bytes(w, "vjp") / (t_vjp * 1e-3) / 1e9 / peak,
+                        "fp64_frac": algorithmic_flops(w, "vjp") / (t_vjp * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS},
             }}
+    if t_des is not None:
+        line["calls"]["design_grad"] = {"us": t_des * 1e3, "gdof_s": N / (t_des * 1e-3) / 1e9,
+                                        "hbm_frac": algorithmic_bytes(w, "design") / (t_des * 1e-3) / 1e9 / peak,
+                                        "fp64_frac": algorithmic_flops(w, "design") / (t_des * 1e-3) / 1e12
+                                        / FP64_MEASURED_TFLOPS}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

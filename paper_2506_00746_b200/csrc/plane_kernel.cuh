@@ -417,8 +417,11 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         if constexpr (S::NIN == 2) {
           double* dst = ring_in + (S::RIN + slot) * S::PLANE + idx;
           if constexpr (MODE == MODE_DESIGN || MODE == MODE_VJP) {
-            // lambda's / w's Dirichlet entries are masked (readings A14, A17)
-            *dst = ((lpinfo[m] & 4) || dz) ? 0.0 : __ldg(in1 + g);
+            // lambda's / w's Dirichlet entries are masked (readings A14, A17): those
+            // slots get a plain zero store (published by the lane's plain arrival),
+            // the rest stream in with cp.async like every other field
+            if ((lpinfo[m] & 4) || dz) *dst = 0.0;
+            else cp_async8(dst, in1 + g);
           } else {
             cp_async8(dst, in1 + g);
           }
