@@ -227,6 +227,8 @@ def main():
     ap.add_argument("--workload", default="C3", choices=list(W.CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--newton", action="store_true",
+                    help="also time the Newton-CG driver (A15: 5 steps x 20 CG from u0 = 0; default on for C4)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     w = W.CONFIGS[args.workload]
@@ -306,6 +308,9 @@ def main():
     t_jvp = time_call(lambda: op.jvp(u, v, out=Jv))
     JTw = torch.empty_like(u)
     t_vjp = time_call(lambda: op.vjp(u, v, out=JTw))   # NEXT-1 (diagnostic, not in the step)
+    # NEXT-2 stored linearisation: one linearize (F(u) + D's linearisation) then J v from it
+    t_lin = time_call(lambda: op.linearize(u, out=r))
+    t_jlin = time_call(lambda: op.jvp_lin(v, out=JTw))
     t_des = None
     if w.model == W.HEAT:
         g = torch.empty(op.n_elems, dtype=torch.float64, device=u.device)
@@ -375,10 +380,45 @@ def main():
                         "hbm_frac": by_jvp / (t_jvp * 1e-3) / 1e9 / peak,
                         "fp64_frac": fl_jvp / (t_jvp * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS,
                         "fused_kernel_us": jvp_kernel_ms * 1e3},
+                "linearize": {"us": t_lin * 1e3, "gdof_s": N / (t_lin * 1e-3) / 1e9},
+                "jvp_lin": {"us": t_jlin * 1e3, "gdof_s": N / (t_jlin * 1e-3) / 1e9},
                 "vjp": {"us": t_vjp * 1e3, "gdof_s": N / (t_vjp * 1e-3) / 1e9,
                         "hbm_frac": algorithmic_bytes(w, "vjp") / (t_vjp * 1e-3) / 1e9 / peak,
                         "fp64_frac": algorithmic_flops(w, "vjp") / (t_vjp * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS},
             }}
+    if (args.newton or w.name == "C4") and world == 1:
+        # a10 / SURVEY §8(d) C4 row: total device time of the whole driver, 2 warm-up runs, 3 timed
+        u0 = torch.zeros_like(u)
+        for _ in range(2):
+            op.newton_cg(u0, 5, 20)
+        torch.cuda.synchronize()
+        tn = []
+        for _ in range(3):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            _, norms = op.newton_cg(u0, 5, 20)
+            b_.record(stream)
+            torch.cuda.synchronize()
+            tn.append(a_.elapsed_time(b_))
+        n_jvp, n_res = 5 * 20, 6
+        op.set_newton_linearization(True)
+        op.newton_cg(u0, 5, 20)
+        torch.cuda.synchronize()
+        tl = []
+        for _ in range(3):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            _, norms_l = op.newton_cg(u0, 5, 20)
+            b_.record(stream)
+            torch.cuda.synchronize()
+            tl.append(a_.elapsed_time(b_))
+        op.set_newton_linearization(False)
+        line["newton_cg_stored_linearization"] = {"ms": statistics.median(tl), "ms_min": min(tl), "norms": norms_l,
+                                                  "note": "feod_set_newton_linearization(1): feod_linearize per step, "
+                                                          "feod_jvp_lin per CG iteration (NEXT-2)"}
+        line["newton_cg"] = {"ms": statistics.median(tn), "ms_min": min(tn), "jvp_calls": n_jvp, "residual_calls": n_res,
+                             "norms": norms, "op_share_ms": (n_jvp * t_jvp + n_res * t_res),
+                             "note": "feod_newton_cg, device time incl. host syncs once per Newton step"}
     if t_des is not None:
         line["calls"]["design_grad"] = {"us": t_des * 1e3, "gdof_s": N / (t_des * 1e-3) / 1e9,
                                         "hbm_frac": algorithmic_bytes(w, "design") / (t_des * 1e-3) / 1e9 / peak,

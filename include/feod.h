@@ -127,6 +127,17 @@ FEOD_API int feod_jvp_res(feod_handle h, const double* u, const double* v, doubl
  * and every row of JTw is kept (reading A17). One pass: J_D^T at each    *
  * point from two dual evaluations (DESIGN.md §2 A17).                    */
 FEOD_API int feod_vjp(feod_handle h, const double* u, const double* w, double* JTw);
+/* Stored linearisation (Fig. 1 caption:  *
+ * "store only the innermost, pointwise operator component"):               *
+ * feod_linearize computes r = F(u) and, in the same pass, stores per        *
+ * quadrature point dFh/dgh (symmetric 3x3, 6 values, reading A17) and,      *
+ * for NLDIFF / HEAT_DESIGN, dFh/du (3 values) in a handle-owned buffer      *
+ * (allocated at the first call: 8 x {6|9} x E x qorder^3 bytes).            *
+ * feod_jvp_lin then applies J(u) v from that buffer alone (one field        *
+ * forward, no metric, no u): same conventions as feod_jvp. FEOD_EINVAL if   *
+ * no linearisation is stored. A later feod_linearize replaces it.          */
+FEOD_API int feod_linearize(feod_handle h, const double* u, double* r);
+FEOD_API int feod_jvp_lin(feod_handle h, const double* v, double* Jv);
 /* g_e = -lambda^T dF/drho_e, lambda's Dirichlet entries ignored          *
  * (A14); HEAT_DESIGN only (others: FEOD_EINVAL)           */
 FEOD_API int feod_design_grad(feod_handle h, const double* u, const double* lambda, double* g);
@@ -145,6 +156,10 @@ FEOD_API int feod_apply_host(feod_handle h, int op, const double* in0, const dou
  * ||F|| before each step and after the last. Returns FEOD_EINVAL if
  * p^T J p <= 0 occurs (CG breakdown). Synchronises the stream. */
 FEOD_API int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg_iters, double* norms_host);
+/* Newton-CG Jacobian: 0 (default) matrix-free feod_jvp at the current u;   *
+ * 1 feod_linearize once per Newton step (it also yields F) and            *
+ * feod_jvp_lin in every CG iteration.                                      */
+FEOD_API int feod_set_newton_linearization(feod_handle h, int stored);
 
 /* BLAS-1 used by the Newton-CG driver (deterministic two-stage reductions).  *
  * result: DEVICE pointer to one double.                                      */

@@ -28,7 +28,8 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 
 # every symbol include/feod.h declares (checked by tests/test_abi.py)
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
-           "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
+           "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
+           "feod_set_newton_linearization", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
@@ -74,6 +75,9 @@ def load_library(path: str = LIB_PATH):
     lib.feod_jvp_res.argtypes = [vp, dp, dp, dp, dp]
     lib.feod_design_grad.argtypes = [vp, dp, dp, dp]
     lib.feod_vjp.argtypes = [vp, dp, dp, dp]
+    lib.feod_linearize.argtypes = [vp, dp, dp]
+    lib.feod_jvp_lin.argtypes = [vp, dp, dp]
+    lib.feod_set_newton_linearization.argtypes = [vp, ctypes.c_int]
     lib.feod_apply_host.argtypes = [vp, ctypes.c_int, dp, dp, dp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_dot.argtypes = [vp, dp, dp, i64, dp]
@@ -176,6 +180,25 @@ class Operator:
         self._sync_stream()
         _check(self.lib.feod_vjp(self.h, u.data_ptr(), w.data_ptr(), JTw.data_ptr()))
         return JTw
+
+    def linearize(self, u, out=None):
+        """r = F(u), and store the pointwise linearisation at u (feod_linearize)."""
+        u = self._dev(u, self.n_dofs, "u")
+        r = out if out is not None else self._torch.empty_like(u)
+        self._sync_stream()
+        _check(self.lib.feod_linearize(self.h, u.data_ptr(), r.data_ptr()))
+        return r
+
+    def jvp_lin(self, v, out=None):
+        """J(u) v at the u of the last linearize() (feod_jvp_lin)."""
+        v = self._dev(v, self.n_dofs, "v")
+        Jv = out if out is not None else self._torch.empty_like(v)
+        self._sync_stream()
+        _check(self.lib.feod_jvp_lin(self.h, v.data_ptr(), Jv.data_ptr()))
+        return Jv
+
+    def set_newton_linearization(self, stored: bool):
+        _check(self.lib.feod_set_newton_linearization(self.h, 1 if stored else 0))
 
     def design_grad(self, u, lam, out=None):
         u, lam = self._dev(u, self.n_dofs, "u"), self._dev(lam, self.n_dofs, "lam")

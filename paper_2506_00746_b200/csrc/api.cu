@@ -32,6 +32,9 @@ struct feod_op {
   unsigned long long* bdone = nullptr;   // per-brick completion epochs (fix-up dependencies)
   int2* fixrows = nullptr;               // fix-up rows in launch order
   double* work = nullptr;      // Newton-CG: F, r, p, Ap, d (5 N)
+  double* lin = nullptr;       // stored linearisation (feod_linearize), lin_values x E x q^3
+  bool lin_valid = false;
+  int newton_lin = 0;          // Newton-CG: 0 matrix-free JVP, 1 stored linearisation
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
 };
 
@@ -66,6 +69,7 @@ static void free_all(feod_op* h) {
   cudaFree(h->bdone);
   cudaFree(h->fixrows);
   cudaFree(h->work);
+  cudaFree(h->lin);
 }
 
 extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const feod_coeffs* coeffs,
@@ -236,7 +240,9 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   if (pb) cudaEventRecord(pb, h->st);
   int grid = 0;
   const unsigned long long epoch = h->P.sched_base + 1;   // what the IO warps publish per finished brick
-  cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, h->geom == nullptr, h->nbricks, h->P, h->T, p, h->st, &grid);
+  // MODE_PAJVP reads the stored linearisation only, whatever the geometry
+  const bool aff = mode == MODE_PAJVP ? true : h->geom == nullptr;
+  cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, aff, h->nbricks, h->P, h->T, p, h->st, &grid);
   // every CTA claims one ticket per brick it processes plus one that ends it
   h->P.sched_base += (unsigned long long)h->nbricks + (unsigned long long)grid;
   if (pe) cudaEventRecord(pe, h->st);
@@ -274,6 +280,35 @@ extern "C" int feod_vjp(feod_handle h, const double* u, const double* w, double*
   if (!h || !u || !w || !JTw) return fail(FEOD_EINVAL, "feod_vjp: null argument");
   if ((const double*)JTw == u || (const double*)JTw == w) return fail(FEOD_EINVAL, "feod_vjp: JTw aliases an input");
   return run_op(h, MODE_VJP, u, w, JTw, nullptr, nullptr, "feod_vjp");
+}
+
+extern "C" int feod_linearize(feod_handle h, const double* u, double* r) {
+  if (!h || !u || !r) return fail(FEOD_EINVAL, "feod_linearize: null argument");
+  if ((const double*)r == u) return fail(FEOD_EINVAL, "feod_linearize: r aliases u");
+  if (!h->lin) {
+    const size_t n = (size_t)lin_values(h->coeffs.model) * (size_t)h->E * h->q * h->q * h->q;
+    if (cudaMalloc(&h->lin, sizeof(double) * n) != cudaSuccess) {
+      h->lin = nullptr;
+      return fail(FEOD_ENOMEM, "feod_linearize: linearisation buffer");
+    }
+    h->P.lin = h->lin;
+  }
+  const int rc = run_op(h, MODE_LIN, u, nullptr, r, nullptr, nullptr, "feod_linearize");
+  h->lin_valid = rc == FEOD_OK;
+  return rc;
+}
+
+extern "C" int feod_jvp_lin(feod_handle h, const double* v, double* Jv) {
+  if (!h || !v || !Jv) return fail(FEOD_EINVAL, "feod_jvp_lin: null argument");
+  if ((const double*)Jv == v) return fail(FEOD_EINVAL, "feod_jvp_lin: Jv aliases v");
+  if (!h->lin_valid) return fail(FEOD_EINVAL, "feod_jvp_lin: no linearisation stored (call feod_linearize)");
+  return run_op(h, MODE_PAJVP, v, nullptr, Jv, nullptr, nullptr, "feod_jvp_lin");
+}
+
+extern "C" int feod_set_newton_linearization(feod_handle h, int stored) {
+  if (!h || (stored != 0 && stored != 1)) return fail(FEOD_EINVAL, "feod_set_newton_linearization: bad argument");
+  h->newton_lin = stored;
+  return FEOD_OK;
 }
 
 extern "C" int feod_design_grad(feod_handle h, const double* u, const double* lambda, double* g) {
@@ -332,7 +367,7 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
   int* bad = h->flag + 1;
   CK(cudaMemsetAsync(bad, 0, sizeof(int), h->st), "feod_newton_cg");
   for (int step = 0; step <= newton_steps; ++step) {
-    int rc = feod_residual(h, u, F);
+    int rc = h->newton_lin ? feod_linearize(h, u, F) : feod_residual(h, u, F);
     if (rc) return rc;
     CK(dot_partial(F, F, N, part, h->st), "feod_newton_cg: norm");
     CK(reduce_final(part, sc + 3, h->st), "feod_newton_cg: norm");
@@ -347,7 +382,7 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
     for (int it = 0; it < cg_iters; ++it) {
       double* rr_old = sc + ((it & 1) ? 2 : 0);
       double* rr_new = sc + ((it & 1) ? 0 : 2);
-      rc = feod_jvp(h, u, p, Ap);
+      rc = h->newton_lin ? feod_jvp_lin(h, p, Ap) : feod_jvp(h, u, p, Ap);
       if (rc) return rc;
       CK(dot_partial(p, Ap, N, part, h->st), "feod_newton_cg: pAp");
       CK(reduce_final(part, sc + 1, h->st), "feod_newton_cg: pAp");

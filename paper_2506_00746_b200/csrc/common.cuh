@@ -8,8 +8,8 @@
 
 namespace feod {
 
-enum Mode { MODE_RES = 0, MODE_JVP = 1, MODE_JVPRES = 2, MODE_DESIGN = 3, MODE_VJP = 4 };
-constexpr int kModes = 5;
+enum Mode { MODE_RES = 0, MODE_JVP = 1, MODE_JVPRES = 2, MODE_DESIGN = 3, MODE_VJP = 4, MODE_LIN = 5, MODE_PAJVP = 6 };
+constexpr int kModes = 7;
 enum Model { PLAPLACE = 0, NLDIFF = 1, HEAT = 2 };
 constexpr int kMaxNQ = 8;
 
@@ -21,6 +21,10 @@ constexpr int kMaxNQ = 8;
 //   D[i][m] = L_m'(x_i), L_m the Lagrange polynomial of the Gauss points
 //             (collocated derivative: sum_m D[i][m] B[m][a] = G[i][a] exactly,
 //             since l_a has degree k <= q-1)
+// Values per quadrature point of the stored linearisation (MODE_LIN -> MODE_PAJVP,
+// SURVEY §8(f) NEXT-2): dFh/dgh (symmetric, 6) and, when kappa depends on u, dFh/du (3).
+FEOD_HD constexpr int lin_values(int model) { return model == 0 ? 6 : 9; }
+
 struct Tables {
   double B[kMaxNQ][kMaxNQ];
   double G[kMaxNQ][kMaxNQ];
@@ -43,7 +47,8 @@ struct OpParams {
   double f;              // source
   // geometry: uniform grid (geom == nullptr): M = w_q diag(cx, cy, cz), W = w_q * vol
   double cx, cy, cz, vol;
-  const double* geom;    // [E][6][NQ^3] metric, components xx yy zz xy xz yz
+  const double* geom;    // [E][NQ][6][NQ][NQ] metric, components xx yy zz xy xz yz
+  double* lin;           // [E][NQ][lin_values][NQ][NQ] stored linearisation (MODE_LIN writes, MODE_PAJVP reads)
   const double* rho;     // [E] (HEAT)
   // dynamic brick scheduling: tickets atomicAdd(sched, 1) - sched_base < #bricks
   // are bricks, the rest end a CTA; the host advances sched_base by #bricks + grid

@@ -1,5 +1,5 @@
 // Instantiation of the fused operator kernel for one order (ND = k+1 nodes,
-// NQ = k+1 points per axis): 5 modes x 3 models x {affine, stored metric}.
+// NQ = k+1 points per axis): 7 modes x 3 models x {affine, stored metric}.
 #pragma once
 #include "kernels.h"
 #include "fixup.cuh"
@@ -72,6 +72,8 @@ bool brick_info<FEOD_ND>(BrickInfo* bi) {
   bi->smem[MODE_JVPRES] = PShape<FEOD_ND, MODE_JVPRES>::SMEM_BYTES;
   bi->smem[MODE_DESIGN] = PShape<FEOD_ND, MODE_DESIGN>::SMEM_BYTES;
   bi->smem[MODE_VJP] = PShape<FEOD_ND, MODE_VJP>::SMEM_BYTES;
+  bi->smem[MODE_LIN] = PShape<FEOD_ND, MODE_LIN>::SMEM_BYTES;
+  bi->smem[MODE_PAJVP] = PShape<FEOD_ND, MODE_PAJVP>::SMEM_BYTES;
   return true;
 }
 
@@ -82,7 +84,9 @@ cudaError_t prepare_order<FEOD_ND>() {
   if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_JVP>()) != cudaSuccess) return e;
   if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_JVPRES>()) != cudaSuccess) return e;
   if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>()) != cudaSuccess) return e;
-  return prep_mode<FEOD_ND, FEOD_ND, MODE_VJP>();
+  if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_VJP>()) != cudaSuccess) return e;
+  if ((e = prep_mode<FEOD_ND, FEOD_ND, MODE_LIN>()) != cudaSuccess) return e;
+  return prep_mode<FEOD_ND, FEOD_ND, MODE_PAJVP>();
 }
 
 template <>
@@ -94,6 +98,8 @@ cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int grid, const
     case MODE_JVPRES: return launch_mode<FEOD_ND, FEOD_ND, MODE_JVPRES>(model, aff, grid, P, T, p, st, grid_out);
     case MODE_DESIGN: return launch_mode<FEOD_ND, FEOD_ND, MODE_DESIGN>(model, aff, grid, P, T, p, st, grid_out);
     case MODE_VJP: return launch_mode<FEOD_ND, FEOD_ND, MODE_VJP>(model, aff, grid, P, T, p, st, grid_out);
+    case MODE_LIN: return launch_mode<FEOD_ND, FEOD_ND, MODE_LIN>(model, aff, grid, P, T, p, st, grid_out);
+    case MODE_PAJVP: return launch_mode<FEOD_ND, FEOD_ND, MODE_PAJVP>(model, aff, grid, P, T, p, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }

@@ -137,7 +137,7 @@ struct PShape {
   static constexpr int NPOS = LXF * LYF;
   static constexpr int PLANE = plane_pad(NPOS);
   static constexpr int RIN = 2 * ND;                         // current layer + next layer (a brick's first layer: ND planes)
-  static constexpr int NIN = (MODE == MODE_RES) ? 1 : 2;
+  static constexpr int NIN = (MODE == MODE_RES || MODE == MODE_LIN || MODE == MODE_PAJVP) ? 1 : 2;
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
   // exchange channels: 2 ([W | Wy], x-derivative collocated over the lane group,
   // fewer FLOPs) up to Q4; 3 ([W | Wx | Wy], no cross-lane traffic) for Q5/Q6
@@ -192,39 +192,13 @@ FEOD_DEV double ld_stream(const double* p) {
   return v;
 }
 
-// L2 eviction-priority policies (createpolicy) for the streamed metric and the
-// shell slab the fix-up reads right after the kernel.
-#ifndef FEOD_L2_METRIC_FIRST
-#define FEOD_L2_METRIC_FIRST 0
-#endif
-#ifndef FEOD_L2_SHELL_LAST
-#define FEOD_L2_SHELL_LAST 0
-#endif
-FEOD_DEV uint64_t l2_policy_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-FEOD_DEV uint64_t l2_policy_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-FEOD_DEV double ld_stream_pol(const double* p, uint64_t pol) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-FEOD_DEV void st_pol(double* p, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-FEOD_DEV void prefetch_l2_pol(const void* p, uint32_t bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol) : "memory");
-}
-
 // L2 prefetch of a contiguous byte range (bulk-copy engine; no completion tracking).
+// The bulk engine needs a 16-byte aligned start and a multiple of 16 bytes: the
+// range is widened to that (odd per-element strides, e.g. 9 x 27 doubles, exist).
 FEOD_DEV void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+  const uint64_t a = reinterpret_cast<uint64_t>(p);
+  const uint64_t a0 = a & ~uint64_t(15), a1 = (a + bytes + 15) & ~uint64_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
 }
 
 // Barrier among the compute threads of one element: a warp barrier when an
@@ -461,7 +435,6 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       }
     };
 
-    const uint64_t pol_shell = FEOD_L2_SHELL_LAST ? l2_policy_last() : 0;
     // P^T + store of the finished value v of output o at position m, DOF plane p (general path)
     auto store_dof = [&](int o, int m, int p, double v) {
       const int info = pinfo[m];
@@ -470,9 +443,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         const int base = gs.LX * gs.LY, ring = 2 * gs.LX + 2 * (gs.LY - 2);
         const int rank = (p == 0) ? pxy[m] : (p == gs.LZ - 1) ? base + (gs.LZ - 2) * ring + pxy[m]
                                                                : base + (p - 1) * ring + (info >> 3);
-        double* d = (o == 0 ? shell0 : shell1) + (int64_t)gs.b * P.shell_stride + rank;
-        if constexpr (FEOD_L2_SHELL_LAST) st_pol(d, v, pol_shell);
-        else *d = v;
+        (o == 0 ? shell0 : shell1)[(int64_t)gs.b * P.shell_stride + rank] = v;
       } else {
         const int gz = gs.gZ0 + p;
         // P^T: Dirichlet rows are zero, except for J^T w, which keeps every row (reading A17)
@@ -548,13 +519,8 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
               const bool zero = MODE != MODE_VJP && (pinfo[m] & 6) == 4;
               double* d = reinterpret_cast<double*>(fptr[o][m]) + (int64_t)(K * z) * fstr[m];
 #pragma unroll
-              if (FEOD_L2_SHELL_LAST && (pinfo[m] & 2)) {
 #pragma unroll
-                for (int c = 0; c < K; ++c) st_pol(d + (int64_t)c * fstr[m], v[c], pol_shell);
-              } else {
-#pragma unroll
-                for (int c = 0; c < K; ++c) d[(int64_t)c * fstr[m]] = zero ? 0.0 : v[c];
-              }
+              for (int c = 0; c < K; ++c) d[(int64_t)c * fstr[m]] = zero ? 0.0 : v[c];
               carry[o][m] = v[K];
             } else {
 #pragma unroll
@@ -612,10 +578,12 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
 #pragma unroll
   for (int k = 0; k < ND; ++k) src[k] = gbase + (lic + k) % ND;
 
+  // per-point global stream: the metric (stored-metric meshes) or the stored linearisation (MODE_PAJVP)
+  constexpr int NSV = (MODE == MODE_PAJVP) ? lin_values(MODEL) : 6;
+  constexpr bool STREAM = (MODE == MODE_PAJVP) || !AFFINE;
   double* const xe = xb + el * S::SE;   // this element's exchange slot
   const double wij = T.w[lic] * T.w[gr];
   const double iwij2 = T.wi2[lic] * T.wi2[gr];
-  const uint64_t pol_metric = FEOD_L2_METRIC_FIRST ? l2_policy_first() : 0;
 
 #ifdef FEOD_PROFILE_IO
   long long c_wrf = 0, c_wee = 0, c_start = clock64();
@@ -639,23 +607,22 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   const int X0 = evalid ? K * exl : 0, Y0 = evalid ? K * eyl : 0;
   for (int z = 0; z < bzr; ++z, ++L) {
     const int64_t eg = (int64_t)(ex0 + exl) + (int64_t)P.nx * ((ey0 + eyl) + (int64_t)P.ny * (ez0 + z));
-    // metric of this thread's points (i = li, j = gr, l): layout [E][l][6][j][i]
+    // per-point stream of this thread's points (i = li, j = gr, l), layout [E][l][NSV][j][i]:
+    // the metric (NSV = 6) on stored-metric meshes, or the stored linearisation (MODE_PAJVP)
     const double* gm = nullptr;
-    double mnext[AFFINE ? 1 : 6];
-    if constexpr (!AFFINE) {
-      gm = P.geom + (evalid ? eg : 0) * (6 * NQ3) + gr * NQ + lic;
+    double mnext[STREAM ? NSV : 1];
+    if constexpr (STREAM) {
+      const double* sb = (MODE == MODE_PAJVP) ? P.lin : P.geom;
+      gm = sb + (evalid ? eg : 0) * (NSV * NQ3) + gr * NQ + lic;
 #pragma unroll
-      for (int c = 0; c < 6; ++c) mnext[c] = FEOD_L2_METRIC_FIRST ? ld_stream_pol(gm + c * NQ2, pol_metric) : ld_stream(gm + c * NQ2);
-      if (tid < byr && z + 1 < bzr) {   // L2 prefetch of the next layer's metric, one x-row of elements per y
+      for (int c = 0; c < NSV; ++c) mnext[c] = ld_stream(gm + c * NQ2);
+      if (tid < byr && z + 1 < bzr) {   // L2 prefetch of the next layer's stream, one x-row of elements per y
         const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + tid) + (int64_t)P.ny * (ez0 + z + 1));
-        if constexpr (FEOD_L2_METRIC_FIRST)
-          prefetch_l2_pol(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)), pol_metric);
-        else
-          prefetch_l2(P.geom + e1 * (6 * NQ3), (uint32_t)(bxr * 6 * NQ3 * sizeof(double)));
+        prefetch_l2(sb + e1 * (NSV * NQ3), (uint32_t)(bxr * NSV * NQ3 * sizeof(double)));
       }
     }
     double rho_e = 0.0;
-    if constexpr (MODEL == HEAT) rho_e = evalid ? __ldg(P.rho + eg) : 1.0;
+    if constexpr (MODEL == HEAT && MODE != MODE_PAJVP) rho_e = evalid ? __ldg(P.rho + eg) : 1.0;
 
 #ifdef FEOD_PROFILE_IO
     long long c0 = clock64();
@@ -758,17 +725,20 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       Metric M;
       double W;
       const double wq = wij * T.w[l];
-      if constexpr (AFFINE) {
+      double sv[STREAM ? NSV : 1];   // this point's stream values
+      if constexpr (STREAM) {
+#pragma unroll
+        for (int c = 0; c < NSV; ++c) sv[c] = mnext[c];
+        if (l + 1 < NQ) {
+#pragma unroll
+          for (int c = 0; c < NSV; ++c) mnext[c] = ld_stream(gm + (l + 1) * NSV * NQ2 + c * NQ2);
+        }
+      }
+      if constexpr (AFFINE || MODE == MODE_PAJVP) {
         M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
         W = wq * P.vol;
       } else {
-        M = {mnext[0], mnext[1], mnext[2], mnext[3], mnext[4], mnext[5]};
-        if (l + 1 < NQ) {
-#pragma unroll
-          for (int c = 0; c < 6; ++c)
-            mnext[c] = FEOD_L2_METRIC_FIRST ? ld_stream_pol(gm + (l + 1) * 6 * NQ2 + c * NQ2, pol_metric)
-                                            : ld_stream(gm + (l + 1) * 6 * NQ2 + c * NQ2);
-        }
+        M = {sv[0], sv[1], sv[2], sv[3], sv[4], sv[5]};
         const double det = M.xx * (M.yy * M.zz - M.yz * M.yz) - M.xy * (M.xy * M.zz - M.yz * M.xz) +
                            M.xz * (M.xy * M.yz - M.yy * M.xz);
         W = det * (iwij2 * T.wi2[l]);   // W = w detJ = det(M) / w^2
@@ -832,6 +802,50 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         flux_hat<MODEL>(uu, gu, M, W, rho_e, P, Fu);
         F0[0] = Fg[0].d; F0[1] = Fg[1].d; F0[2] = Fg[2].d;
         F0[3] = Uxl[1] * Fu[0].d + Uyl[1] * Fu[1].d + Uzl[1] * Fu[2].d;
+      } else if constexpr (MODE == MODE_LIN) {
+        // r = F(u) as MODE_RES, and the linearisation of D at the point for MODE_PAJVP:
+        // A = dFh/dgh from three dual evaluations along e_x, e_y, e_z (symmetric,
+        // reading A17; the upper triangle is stored), b = dFh/du along (1, 0)
+        using D = dual<double>;
+        const D ud(Ul[0]);
+        double A[3][3];
+        D Fh[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const D gh[3] = {D(Uxl[0], k == 0 ? 1.0 : 0.0), D(Uyl[0], k == 1 ? 1.0 : 0.0), D(Uzl[0], k == 2 ? 1.0 : 0.0)};
+          flux_hat<MODEL>(ud, gh, M, W, rho_e, P, Fh);
+#pragma unroll
+          for (int m = 0; m < 3; ++m) A[m][k] = Fh[m].d;
+        }
+        F0[0] = Fh[0].v; F0[1] = Fh[1].v; F0[2] = Fh[2].v;
+        F0[3] = -P.f * W;
+        constexpr int NL = lin_values(MODEL);
+        double lv[NL];
+        lv[0] = A[0][0]; lv[1] = A[1][1]; lv[2] = A[2][2]; lv[3] = A[0][1]; lv[4] = A[0][2]; lv[5] = A[1][2];
+        if constexpr (NL == 9) {
+          const D uu(Ul[0], 1.0);
+          const D gu[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
+          D Fu[3];
+          flux_hat<MODEL>(uu, gu, M, W, rho_e, P, Fu);
+          lv[6] = Fu[0].d; lv[7] = Fu[1].d; lv[8] = Fu[2].d;
+        }
+        if (evalid) {
+          double* lp = P.lin + eg * (NL * NQ3) + l * NL * NQ2 + gr * NQ + lic;
+#pragma unroll
+          for (int c = 0; c < NL; ++c) lp[c * NQ2] = lv[c];
+        }
+      } else if constexpr (MODE == MODE_PAJVP) {
+        // J(u0) v from the stored linearisation: F' = A gh_v + b v (field 0 is v)
+        const double g0 = Uxl[0], g1 = Uyl[0], g2 = Uzl[0];
+        F0[0] = sv[0] * g0 + sv[3] * g1 + sv[4] * g2;
+        F0[1] = sv[3] * g0 + sv[1] * g1 + sv[5] * g2;
+        F0[2] = sv[4] * g0 + sv[5] * g1 + sv[2] * g2;
+        if constexpr (NSV == 9) {
+          F0[0] = fma(sv[6], Ul[0], F0[0]);
+          F0[1] = fma(sv[7], Ul[0], F0[1]);
+          F0[2] = fma(sv[8], Ul[0], F0[2]);
+        }
+        F0[3] = 0.0;
       } else {   // MODE_DESIGN: seed d/drho; field 1 is lambda
         using D = dual<double>;
         const D ud(Ul[0]);

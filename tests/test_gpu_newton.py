@@ -47,3 +47,23 @@ def test_newton_cg_fullsize_runs():
     assert np.all(np.isfinite(host(u)))
     # A15: at u0 = 0, J = eps^(p-2) K, the first step overshoots (||F|| grows) by design
     assert norms[1] > norms[0]
+
+
+def test_newton_cg_stored_linearization():
+    """Same driver with feod_linearize once per Newton step and feod_jvp_lin in CG
+    (NEXT-2): free-running against the oracle with the same roundoff-growth bound."""
+    w = W.C4.resized(2)
+    d = W.draw(w)
+    pr, op = problem(w, d), operator(w, d)
+    u0 = np.zeros(w.n_dofs)
+    u_ref, norms_ref = O.newton_cg(pr, u0, 5, 20)
+    pert = 1e-15 * np.random.default_rng(9).uniform(-1, 1, w.n_dofs)
+    pert[W.dirichlet_dofs(w.n, w.k, w.faces)] = 0.0
+    u_p, norms_p = O.newton_cg(pr, pert, 5, 20)
+    spread_n = np.max(np.abs(np.array(norms_p) - norms_ref) / np.array(norms_ref))
+    spread_u = rel_l2(u_p, u_ref)
+    op.set_newton_linearization(True)
+    u, norms = op.newton_cg(cuda(u0), 5, 20)
+    dev_n = np.max(np.abs(np.array(norms) - norms_ref) / np.array(norms_ref))
+    assert dev_n <= 100 * spread_n + 1e-12, (dev_n, spread_n)
+    assert rel_l2(host(u), u_ref) <= 100 * spread_u + 1e-12

@@ -65,3 +65,15 @@ def test_vjp_parity(w, n):
     ref = O.vjp(pr, d["u"], d["v"])
     got = host(op.vjp(cuda(d["u"]), cuda(d["v"])))
     assert rel_l2(got, ref) <= TOL
+
+
+@pytest.mark.parametrize("w,n", CASES, ids=[f"{w.name}n{n}" for w, n in CASES])
+def test_linearize_and_jvp_lin_parity(w, n):
+    """NEXT-2: feod_linearize returns F(u) and stores D's linearisation; feod_jvp_lin
+    applies J(u) from it alone. Both against the oracle's Eq. 1 / Eq. 2."""
+    ww, d = _case(w, n)
+    pr, op = problem(ww, d), operator(ww, d)
+    r = host(op.linearize(cuda(d["u"])))
+    assert rel_l2(r, O.residual(pr, d["u"])) <= TOL
+    Jv = host(op.jvp_lin(cuda(d["v"])))
+    assert rel_l2(Jv, O.jvp(pr, d["u"], d["v"])) <= TOL
