@@ -2,12 +2,16 @@
 // products as deterministic two-stage reductions over a FIXED grid (the same
 // partial-sum tree every call), and the fused CG vector updates with the
 // scalars kept on the device (no host round trip inside the CG loop).
+// HBM-bound: a full-occupancy fixed grid (8 CTAs x 256 threads per SM) and
+// kUnroll independent element streams per thread keep enough loads in flight.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace feod {
 
 constexpr int kRedThreads = 256;
+constexpr int kUnroll = 4;
+constexpr int64_t kRedStride = (int64_t)kRedBlocks * kRedThreads;
 
 FEOD_DEV double block_sum(double v, double* sh) {
   sh[threadIdx.x] = v;
@@ -23,10 +27,19 @@ __global__ void __launch_bounds__(kRedThreads) dot_partial_kernel(const double* 
                                                                   const double* __restrict__ y, int64_t n,
                                                                   double* __restrict__ partials) {
   __shared__ double sh[kRedThreads];
-  double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)kRedBlocks * kRedThreads)
-    acc = fma(x[i], y[i], acc);
-  const double s = block_sum(acc, sh);
+  double acc[kUnroll] = {};
+  int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+  for (; i + (kUnroll - 1) * kRedStride < n; i += kUnroll * kRedStride) {
+    double xv[kUnroll], yv[kUnroll];
+#pragma unroll
+    for (int t = 0; t < kUnroll; ++t) { xv[t] = __ldcs(x + i + t * kRedStride); yv[t] = __ldcs(y + i + t * kRedStride); }
+#pragma unroll
+    for (int t = 0; t < kUnroll; ++t) acc[t] = fma(xv[t], yv[t], acc[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < kUnroll - 1; ++t)
+    if (i < n) { acc[t] = fma(x[i], y[i], acc[t]); i += kRedStride; }
+  const double s = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
@@ -71,14 +84,34 @@ __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __
   const double den = *pAp;
   if (blockIdx.x == 0 && threadIdx.x == 0 && !(den > 0.0)) *bad = 1;
   const double alpha = *rr / den;
-  double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x; i < n; i += (int64_t)kRedBlocks * kRedThreads) {
-    d[i] = fma(alpha, p[i], d[i]);
-    const double ri = fma(-alpha, Ap[i], r[i]);
-    r[i] = ri;
-    acc = fma(ri, ri, acc);
+  double acc[kUnroll] = {};
+  int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+  for (; i + (kUnroll - 1) * kRedStride < n; i += kUnroll * kRedStride) {
+    double pv[kUnroll], av[kUnroll], dv[kUnroll], rv[kUnroll];
+#pragma unroll
+    for (int t = 0; t < kUnroll; ++t) {
+      const int64_t j = i + t * kRedStride;
+      pv[t] = __ldcs(p + j); av[t] = __ldcs(Ap + j); dv[t] = d[j]; rv[t] = r[j];
+    }
+#pragma unroll
+    for (int t = 0; t < kUnroll; ++t) {
+      const int64_t j = i + t * kRedStride;
+      d[j] = fma(alpha, pv[t], dv[t]);
+      const double ri = fma(-alpha, av[t], rv[t]);
+      r[j] = ri;
+      acc[t] = fma(ri, ri, acc[t]);
+    }
   }
-  const double s = block_sum(acc, sh);
+#pragma unroll
+  for (int t = 0; t < kUnroll - 1; ++t)
+    if (i < n) {
+      d[i] = fma(alpha, p[i], d[i]);
+      const double ri = fma(-alpha, Ap[i], r[i]);
+      r[i] = ri;
+      acc[t] = fma(ri, ri, acc[t]);
+      i += kRedStride;
+    }
+  const double s = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
@@ -86,8 +119,16 @@ __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __
 __global__ void cg_dir_kernel(const double* __restrict__ rr_new, const double* __restrict__ rr_old,
                               const double* __restrict__ r, double* __restrict__ p, int64_t n) {
   const double beta = *rr_new / *rr_old;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], r[i]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+    double pv[kUnroll], rv[kUnroll];
+#pragma unroll
+    for (int t = 0; t < kUnroll; ++t) { pv[t] = p[i + t * stride]; rv[t] = __ldcs(r + i + t * stride); }
+#pragma unroll
+    for (int t = 0; t < kUnroll; ++t) p[i + t * stride] = fma(beta, pv[t], rv[t]);
+  }
+  for (; i < n; i += stride) p[i] = fma(beta, p[i], r[i]);
 }
 
 // u += d
@@ -98,7 +139,7 @@ __global__ void axpy1_kernel(double* __restrict__ u, const double* __restrict__ 
 
 static int grid_for(int64_t n) {
   const int64_t b = (n + 255) / 256;
-  return (int)(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
+  return (int)(b < kRedBlocks ? (b > 0 ? b : 1) : kRedBlocks);
 }
 
 cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n, cudaStream_t st) {

@@ -53,7 +53,7 @@ cudaError_t fixup_nd(int nd, const OpParams& P, unsigned long long epoch, const 
 int fixup_rows_nd(int nd, const OpParams& P, int2* rows, unsigned long long* keys);
 
 // BLAS-1 (blas1.cu): deterministic fixed-grid two-stage reductions.
-constexpr int kRedBlocks = 296;
+constexpr int kRedBlocks = 148 * 8;   // fixed reduction grid: full occupancy on 148 SMs
 cudaError_t dot_partial(const double* x, const double* y, int64_t n, double* partials, cudaStream_t st);
 cudaError_t reduce_final(const double* partials, double* out, cudaStream_t st);
 
