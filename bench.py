@@ -419,6 +419,19 @@ def main():
         line["newton_cg"] = {"ms": statistics.median(tn), "ms_min": min(tn), "jvp_calls": n_jvp, "residual_calls": n_res,
                              "norms": norms, "op_share_ms": (n_jvp * t_jvp + n_res * t_res),
                              "note": "feod_newton_cg, device time incl. host syncs once per Newton step"}
+    if w.model == W.HEAT and world == 1:
+        # NEXT-1: adjoint solve, 50 BiCGStab iterations (2 J^T applications each), rhs = the recipe's lambda draw
+        lam_rhs = torch.as_tensor(d["lam"]).cuda()
+        op.adjoint_solve(u, lam_rhs, iters=5)
+        torch.cuda.synchronize()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        _, hist = op.adjoint_solve(u, lam_rhs, iters=50)
+        b_.record(stream)
+        torch.cuda.synchronize()
+        line["adjoint_solve"] = {"ms": a_.elapsed_time(b_), "iters": 50, "vjp_calls": 100,
+                                 "res_first": hist[0], "res_last": hist[-1],
+                                 "note": "feod_adjoint_solve, unpreconditioned BiCGStab on P^T J^T (device time)"}
     if t_des is not None:
         line["calls"]["design_grad"] = {"us": t_des * 1e3, "gdof_s": N / (t_des * 1e-3) / 1e9,
                                         "hbm_frac": algorithmic_bytes(w, "design") / (t_des * 1e-3) / 1e9 / peak,

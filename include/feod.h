@@ -127,6 +127,17 @@ FEOD_API int feod_jvp_res(feod_handle h, const double* u, const double* v, doubl
  * and every row of JTw is kept (reading A17). One pass: J_D^T at each    *
  * point from two dual evaluations (DESIGN.md §2 A17).                    */
 FEOD_API int feod_vjp(feod_handle h, const double* u, const double* w, double* JTw);
+/* Adjoint solve (the adjoint analysis of PAPER.md:199): *
+ * lambda (device, length N) <- `iters` BiCGStab iterations from lambda = 0 on  *
+ *   P^T J(u)^T lambda = P^T rhs   over the free DOFs (lambda_Dir = 0),         *
+ * the operator applied by the fused J^T kernel (feod_vjp with P^T). Fixed      *
+ * iteration count, device-resident scalars, deterministic reductions.          *
+ * res_norms_host (HOST, length iters+1, or NULL) gets ||P^T(rhs - J^T lambda)||*
+ * as BiCGStab's recursive residual before the first and after each iteration.  *
+ * A converged solve (r = 0) stays frozen; FEOD_EINVAL on a true breakdown     *
+ * ((rhat, v) = 0 while (rhat, r) != 0). Synchronises.                          */
+FEOD_API int feod_adjoint_solve(feod_handle h, const double* u, const double* rhs, double* lambda, int iters,
+                                double* res_norms_host);
 /* Stored linearisation (Fig. 1 caption:  *
  * "store only the innermost, pointwise operator component"):               *
  * feod_linearize computes r = F(u) and, in the same pass, stores per        *

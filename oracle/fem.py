@@ -264,6 +264,17 @@ def vjp(pr: Problem, u, w):
     return np.bincount(idx, weights=val, minlength=pr.n_dofs)
 
 
+def adjoint_solve(pr: Problem, u, rhs):
+    """Dense reference for feod_adjoint_solve: lambda with lambda_Dir = 0 and
+    (J(u)^T lambda)_f = rhs_f on the free rows f, i.e. the transpose of the
+    free-free block of the Eq. 3 Jacobian, solved by numpy.linalg.solve."""
+    A = dense_jacobian(pr, u)
+    f = np.flatnonzero(~dirichlet_mask(pr))
+    lam = np.zeros(pr.n_dofs)
+    lam[f] = np.linalg.solve(A[np.ix_(f, f)].T, np.asarray(rhs, float)[f])
+    return lam
+
+
 def _design_elems(pr, u, lam, elems=None):
     lam = np.array(lam, dtype=np.float64)
     lam[dirichlet_mask(pr)] = 0.0         # only free rows count (reading A14)

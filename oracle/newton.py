@@ -60,3 +60,36 @@ def newton_cg(pr, u0, newton_steps=5, cg_iters=20, record=False):
     if record:
         return u, norms, iterates, directions
     return u, norms
+
+
+def bicgstab_fixed(apply, b, iters):
+    """Unpreconditioned BiCGStab (van der Vorst 1992) from x = 0, shadow residual
+    rhat = b, for a fixed number of iterations; a converged state (r = 0) freezes.
+    Returns x and the recursive residual norms (before the first and after each
+    iteration). Reference for feod_adjoint_solve's iteration."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    rhat = b.copy()
+    p = np.zeros_like(b)
+    v = np.zeros_like(b)
+    rho_old = alpha = omega = 0.0
+    hist = [float(np.linalg.norm(r))]
+    for it in range(iters):
+        rho = float(rhat @ r)
+        if it == 0:
+            p = r.copy()
+        else:
+            beta = 0.0 if (rho_old == 0.0 or omega == 0.0) else (rho / rho_old) * (alpha / omega)
+            p = r + beta * (p - omega * v)
+        v = apply(p)
+        rv = float(rhat @ v)
+        alpha = rho / rv if rv != 0.0 else 0.0
+        s = r - alpha * v
+        t = apply(s)
+        tt = float(t @ t)
+        omega = float(t @ s) / tt if tt > 0.0 else 0.0
+        x = x + alpha * p + omega * s
+        r = s - omega * t
+        rho_old = rho
+        hist.append(float(np.linalg.norm(r)))
+    return x, hist

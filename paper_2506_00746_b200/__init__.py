@@ -29,7 +29,7 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 # every symbol include/feod.h declares (checked by tests/test_abi.py)
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
-           "feod_set_newton_linearization", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
+           "feod_set_newton_linearization", "feod_adjoint_solve", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
@@ -78,6 +78,7 @@ def load_library(path: str = LIB_PATH):
     lib.feod_linearize.argtypes = [vp, dp, dp]
     lib.feod_jvp_lin.argtypes = [vp, dp, dp]
     lib.feod_set_newton_linearization.argtypes = [vp, ctypes.c_int]
+    lib.feod_adjoint_solve.argtypes = [vp, dp, dp, dp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_apply_host.argtypes = [vp, ctypes.c_int, dp, dp, dp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_dot.argtypes = [vp, dp, dp, i64, dp]
@@ -196,6 +197,16 @@ class Operator:
         self._sync_stream()
         _check(self.lib.feod_jvp_lin(self.h, v.data_ptr(), Jv.data_ptr()))
         return Jv
+
+    def adjoint_solve(self, u, rhs, iters=50):
+        """lambda from `iters` BiCGStab iterations on P^T J(u)^T lambda = P^T rhs
+        (feod_adjoint_solve); returns (lambda, residual-norm history)."""
+        u, rhs = self._dev(u, self.n_dofs, "u"), self._dev(rhs, self.n_dofs, "rhs")
+        lam = self._torch.empty_like(u)
+        norms = (ctypes.c_double * (iters + 1))()
+        self._sync_stream()
+        _check(self.lib.feod_adjoint_solve(self.h, u.data_ptr(), rhs.data_ptr(), lam.data_ptr(), int(iters), norms))
+        return lam, list(norms)
 
     def set_newton_linearization(self, stored: bool):
         _check(self.lib.feod_set_newton_linearization(self.h, 1 if stored else 0))

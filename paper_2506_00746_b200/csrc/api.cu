@@ -26,13 +26,14 @@ struct feod_op {
   double* geom = nullptr;
   double* shell = nullptr;     // 2 x nbricks x shell
   double* stage = nullptr;     // host-API staging: 3 x max(N, E)
-  double* red = nullptr;       // kRedBlocks partials + 8 scalars
+  double* red = nullptr;       // kRedBlocks partials, 24 scalars, kRedBlocks partials
   int* flag = nullptr;
   unsigned long long* sched = nullptr;   // dynamic brick scheduling ticket counter
   unsigned long long* bdone = nullptr;   // per-brick completion epochs (fix-up dependencies)
   int2* fixrows = nullptr;               // fix-up rows in launch order
   double* work = nullptr;      // Newton-CG: F, r, p, Ap, d (5 N)
   double* lin = nullptr;       // stored linearisation (feod_linearize), lin_values x E x q^3
+  double* kwork = nullptr;     // adjoint BiCGStab: b, r, rhat, p, v, s, t (7 padded N)
   bool lin_valid = false;
   int newton_lin = 0;          // Newton-CG: 0 matrix-free JVP, 1 stored linearisation
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
@@ -70,6 +71,7 @@ static void free_all(feod_op* h) {
   cudaFree(h->fixrows);
   cudaFree(h->work);
   cudaFree(h->lin);
+  cudaFree(h->kwork);
 }
 
 extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const feod_coeffs* coeffs,
@@ -138,7 +140,7 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   if ((e = prepare_nd(h->nd)) != cudaSuccess) return cleanup_fail(cuda_fail(e, "feod_create: kernel attributes"));
   if ((e = cudaMalloc(&h->shell, sizeof(double) * 2 * (size_t)h->nbricks * P.shell_stride)) != cudaSuccess)
     return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: shell buffer"));
-  if ((e = cudaMalloc(&h->red, sizeof(double) * (kRedBlocks + 8))) != cudaSuccess)
+  if ((e = cudaMalloc(&h->red, sizeof(double) * (2 * kRedBlocks + 32))) != cudaSuccess)
     return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: reduction buffer"));
   if ((e = cudaMalloc(&h->flag, sizeof(int) * 2)) != cudaSuccess)
     return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: flag"));
@@ -249,7 +251,7 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   if (e != cudaSuccess) return cuda_fail(e, name);
   if (mode != MODE_DESIGN) {
     OpParams Pf = h->P;
-    if (mode == MODE_VJP) Pf.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
+    if (mode == MODE_VJP && h->P.vjp_keep_rows) Pf.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
     e = fixup_nd(h->nd, Pf, epoch, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
                  mode == MODE_JVPRES ? out1 : nullptr, h->st);
     if (e != cudaSuccess) return cuda_fail(e, name);
@@ -279,7 +281,79 @@ extern "C" int feod_jvp_res(feod_handle h, const double* u, const double* v, dou
 extern "C" int feod_vjp(feod_handle h, const double* u, const double* w, double* JTw) {
   if (!h || !u || !w || !JTw) return fail(FEOD_EINVAL, "feod_vjp: null argument");
   if ((const double*)JTw == u || (const double*)JTw == w) return fail(FEOD_EINVAL, "feod_vjp: JTw aliases an input");
+  h->P.vjp_keep_rows = 1;
   return run_op(h, MODE_VJP, u, w, JTw, nullptr, nullptr, "feod_vjp");
+}
+
+extern "C" int feod_adjoint_solve(feod_handle h, const double* u, const double* rhs, double* lambda, int iters,
+                                  double* res_norms_host) {
+  if (!h || !u || !rhs || !lambda || iters < 0) return fail(FEOD_EINVAL, "feod_adjoint_solve: bad argument");
+  if (lambda == u || lambda == rhs) return fail(FEOD_EINVAL, "feod_adjoint_solve: lambda aliases an input");
+  const int64_t N = h->N;
+  const size_t NP = ((size_t)N + 31) / 32 * 32;
+  if (!h->kwork && cudaMalloc(&h->kwork, sizeof(double) * 7 * NP) != cudaSuccess) {
+    h->kwork = nullptr;
+    return fail(FEOD_ENOMEM, "feod_adjoint_solve: work vectors");
+  }
+  double* b = h->kwork;          // rhs with P^T applied
+  double* r = b + NP;
+  double* rhat = r + NP;
+  double* p = rhat + NP;
+  double* v = p + NP;
+  double* s = v + NP;
+  double* t = s + NP;
+  double* part = h->red;
+  double* part2 = h->red + kRedBlocks + 32;
+  double* sc = h->red + kRedBlocks + 8;
+  int* bad = h->flag + 1;
+  // A y = P^T J(u)^T y on the free rows (y's Dirichlet entries are ignored by J^T)
+  auto apply = [&](const double* y, double* out) {
+    h->P.vjp_keep_rows = 0;
+    const int rc = run_op(h, MODE_VJP, u, y, out, nullptr, nullptr, "feod_adjoint_solve");
+    h->P.vjp_keep_rows = 1;
+    return rc;
+  };
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), h->st), "feod_adjoint_solve");
+  CK(cudaMemcpyAsync(b, rhs, sizeof(double) * N, cudaMemcpyDeviceToDevice, h->st), "feod_adjoint_solve");
+  CK(mask_dirichlet(b, h->P, h->st), "feod_adjoint_solve: mask");
+  CK(bicg_init(b, lambda, r, rhat, p, v, N, h->st), "feod_adjoint_solve: init");
+  std::vector<double> r2s;
+  auto record = [&]() -> int {
+    if (!res_norms_host) return FEOD_OK;
+    double r2 = 0.0;
+    CK(cudaMemcpyAsync(&r2, sc + 7, sizeof(double), cudaMemcpyDeviceToHost, h->st), "feod_adjoint_solve: D2H");
+    CK(cudaStreamSynchronize(h->st), "feod_adjoint_solve: sync");
+    r2s.push_back(std::sqrt(r2));
+    return FEOD_OK;
+  };
+  CK(dot_partial(r, r, N, part, h->st), "feod_adjoint_solve: rr");
+  CK(reduce_final(part, sc + 7, h->st), "feod_adjoint_solve: rr");
+  CK(cudaMemcpyAsync(sc + 0, sc + 7, sizeof(double), cudaMemcpyDeviceToDevice, h->st), "feod_adjoint_solve");
+  if (int rc = record()) return rc;
+  for (int it = 0; it < iters; ++it) {
+    // sc[it & 1] holds rho_new = (rhat, r)
+    CK(bicg_p(sc, it, r, v, p, N, h->st), "feod_adjoint_solve: p");
+    if (int rc = apply(p, v)) return rc;
+    CK(dot_partial(rhat, v, N, part, h->st), "feod_adjoint_solve: rv");
+    CK(reduce_final(part, sc + 4, h->st), "feod_adjoint_solve: rv");
+    CK(bicg_s(sc, it, r, v, s, N, bad, h->st), "feod_adjoint_solve: s");
+    if (int rc = apply(s, t)) return rc;
+    CK(dot_partial(t, s, N, part, h->st), "feod_adjoint_solve: ts");
+    CK(reduce_final(part, sc + 5, h->st), "feod_adjoint_solve: ts");
+    CK(dot_partial(t, t, N, part, h->st), "feod_adjoint_solve: tt");
+    CK(reduce_final(part, sc + 6, h->st), "feod_adjoint_solve: tt");
+    CK(bicg_x(sc, p, s, t, rhat, lambda, r, N, part, part2, bad, h->st), "feod_adjoint_solve: x");
+    CK(reduce_final(part, sc + ((it + 1) & 1), h->st), "feod_adjoint_solve: rho");
+    CK(reduce_final(part2, sc + 7, h->st), "feod_adjoint_solve: rr");
+    if (int rc = record()) return rc;
+  }
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st), "feod_adjoint_solve: D2H");
+  CK(cudaStreamSynchronize(h->st), "feod_adjoint_solve: sync");
+  if (res_norms_host)
+    for (size_t i = 0; i < r2s.size(); ++i) res_norms_host[i] = r2s[i];
+  if (hbad) return fail(FEOD_EINVAL, "feod_adjoint_solve: BiCGStab breakdown");
+  return FEOD_OK;
 }
 
 extern "C" int feod_linearize(feod_handle h, const double* u, double* r) {

@@ -49,6 +49,7 @@ struct OpParams {
   double cx, cy, cz, vol;
   const double* geom;    // [E][NQ][6][NQ][NQ] metric, components xx yy zz xy xz yz
   double* lin;           // [E][NQ][lin_values][NQ][NQ] stored linearisation (MODE_LIN writes, MODE_PAJVP reads)
+  int vjp_keep_rows;     // MODE_VJP: 1 keeps every row of J^T w (feod_vjp), 0 applies P^T (adjoint solve)
   const double* rho;     // [E] (HEAT)
   // dynamic brick scheduling: tickets atomicAdd(sched, 1) - sched_base < #bricks
   // are bricks, the rest end a CTA; the host advances sched_base by #bricks + grid

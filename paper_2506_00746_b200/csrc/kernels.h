@@ -66,4 +66,13 @@ cudaError_t cg_update(const double* rr, const double* pAp, const double* p, cons
 cudaError_t cg_dir(const double* rr_new, const double* rr_old, const double* r, double* p, int64_t n,
                    cudaStream_t st);
 cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st);
+// BiCGStab for the adjoint solve (krylov.cu)
+cudaError_t mask_dirichlet(double* x, const OpParams& P, cudaStream_t st);
+cudaError_t bicg_init(const double* b, double* x, double* r, double* rhat, double* p, double* v, int64_t n,
+                      cudaStream_t st);
+cudaError_t bicg_p(const double* sc, int it, const double* r, const double* v, double* p, int64_t n, cudaStream_t st);
+cudaError_t bicg_s(double* sc, int it, const double* r, const double* v, double* s, int64_t n, int* bad,
+                   cudaStream_t st);
+cudaError_t bicg_x(double* sc, const double* p, const double* s, const double* t, const double* rhat, double* x,
+                   double* r, int64_t n, double* part_rr, double* part_r2, int* bad, cudaStream_t st);
 }  // namespace feod

@@ -447,7 +447,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       } else {
         const int gz = gs.gZ0 + p;
         // P^T: Dirichlet rows are zero, except for J^T w, which keeps every row (reading A17)
-        const bool dir = MODE != MODE_VJP &&
+        const bool dir = !(MODE == MODE_VJP && P.vjp_keep_rows) &&
                          ((info & 4) || ((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1));
         (o == 0 ? out0 : out1)[(int64_t)P.Mx * P.My * gz + pg[m]] = dir ? 0.0 : v;
       }
@@ -516,7 +516,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
             }
             v[0] = carry[o][m] + v[0];
             if (z > 0 && z < bzr - 1) {   // middle layer: affine destination, one add per store
-              const bool zero = MODE != MODE_VJP && (pinfo[m] & 6) == 4;
+              const bool zero = !(MODE == MODE_VJP && P.vjp_keep_rows) && (pinfo[m] & 6) == 4;
               double* d = reinterpret_cast<double*>(fptr[o][m]) + (int64_t)(K * z) * fstr[m];
 #pragma unroll
 #pragma unroll

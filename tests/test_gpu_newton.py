@@ -67,3 +67,49 @@ def test_newton_cg_stored_linearization():
     dev_n = np.max(np.abs(np.array(norms) - norms_ref) / np.array(norms_ref))
     assert dev_n <= 100 * spread_n + 1e-12, (dev_n, spread_n)
     assert rel_l2(host(u), u_ref) <= 100 * spread_u + 1e-12
+
+
+@pytest.mark.parametrize("n", [3, 4])
+def test_adjoint_solve_converges_to_dense(n):
+    """feod_adjoint_solve (BiCGStab on P^T J^T, NEXT-1) on small C5 heat cases (J
+    nonsymmetric). rho = 1 keeps the unpreconditioned iteration well conditioned, so
+    120 iterations converge: lambda against the oracle's dense solve. With the
+    recipe's rho (cond ~1e4) the first 25 residual norms follow the oracle's
+    BiCGStab on the same operator within 100x the oracle's own roundoff spread."""
+    w = W.C5.resized(n)
+    d = W.draw(w)
+    rhs = np.random.default_rng(5).uniform(-1, 1, w.n_dofs)
+    mask = W.dirichlet_dofs(w.n, w.k, w.faces)
+    d1 = dict(d, rho=np.ones(w.n_elems))
+    pr1, op1 = problem(w, d1), operator(w, d1)
+    lam_ref = O.adjoint_solve(pr1, d["u"], rhs)
+    lam, norms = op1.adjoint_solve(cuda(d["u"]), cuda(rhs), iters=120)
+    lam = host(lam)
+    assert np.all(lam[mask] == 0.0)
+    assert norms[-1] <= 1e-11 * norms[0]
+    assert rel_l2(lam, lam_ref) <= 1e-9
+    lam2, _ = op1.adjoint_solve(cuda(d["u"]), cuda(rhs), iters=120)   # deterministic
+    assert np.array_equal(host(lam2), lam)
+    pr, op = problem(w, d), operator(w, d)
+    b = rhs.copy()
+    b[mask] = 0.0
+    def apply(y):
+        out = O.vjp(pr, d["u"], y)
+        out[mask] = 0.0
+        return out
+    _, h_ref = O.bicgstab_fixed(apply, b, 25)
+    # the oracle's own spread under a roundoff-sized change of the right-hand side
+    bp = b * (1.0 + 1e-15 * np.random.default_rng(8).uniform(-1, 1, b.size))
+    _, h_p = O.bicgstab_fixed(apply, bp, 25)
+    spread = np.abs(np.array(h_p) - h_ref) / np.array(h_ref)
+    _, h = op.adjoint_solve(cuda(d["u"]), cuda(rhs), iters=25)
+    dev = np.abs(np.array(h) - h_ref) / np.array(h_ref)
+    assert np.all(dev <= 100 * np.maximum.accumulate(spread) + 1e-12), (dev, spread)
+
+
+def test_adjoint_solve_fullsize_runs():
+    w = W.C5
+    d = W.draw(w)
+    op = operator(w, d)
+    lam, norms = op.adjoint_solve(cuda(d["u"]), cuda(d["lam"]), iters=30)
+    assert np.all(np.isfinite(host(lam))) and norms[-1] < 0.5 * norms[0]

@@ -411,3 +411,36 @@ def test_t15_vjp_is_transposed_dense_jacobian(c):
     w2 = w.copy()
     w2[O.dirichlet_mask(pr)] = 7.0
     np.testing.assert_array_equal(O.vjp(pr, u, w2), JTw)
+
+
+def test_t16_adjoint_solve_dense():
+    """The dense adjoint solution satisfies (J^T lambda)_free = rhs_free through the
+    separately pinned J^T w (T15), with lambda_Dir = 0 (heat model: nonsymmetric J)."""
+    n, k = 3, 2
+    rng = np.random.default_rng(31)
+    rho = rng.uniform(0.1, 1, n ** 3)
+    pr = prob(n, k, model=HT, perturbed=True, faces=1, f=1.0, rho=rho)
+    u = rand_free(pr, 32)
+    rhs = rng.uniform(-1, 1, pr.n_dofs)
+    lam = O.adjoint_solve(pr, u, rhs)
+    mask = O.dirichlet_mask(pr)
+    assert np.all(lam[mask] == 0.0)
+    res = O.vjp(pr, u, lam) - rhs
+    assert np.linalg.norm(res[~mask]) <= 1e-10 * np.linalg.norm(rhs)
+    A = O.dense_jacobian(pr, u)[np.ix_(~mask, ~mask)]
+    assert np.max(np.abs(A - A.T)) > 1e-3 * np.max(np.abs(A))   # the free block is genuinely nonsymmetric
+
+
+def test_bicgstab_fixed_solves_nonsymmetric():
+    """Pin for the reference BiCGStab: on a nonsymmetric, diagonally dominant matrix
+    it reaches numpy.linalg.solve's answer, and its recursive residual matches the
+    true residual."""
+    rng = np.random.default_rng(3)
+    n = 60
+    A = rng.uniform(-1, 1, (n, n)) + n * np.eye(n)
+    b = rng.uniform(-1, 1, n)
+    x, hist = O.bicgstab_fixed(lambda y: A @ y, b, 40)
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=0, atol=1e-12)
+    assert hist[-1] <= 1e-12 * hist[0]
+    x5, h5 = O.bicgstab_fixed(lambda y: A @ y, b, 5)
+    assert abs(np.linalg.norm(b - A @ x5) - h5[-1]) <= 1e-10 * h5[0]
