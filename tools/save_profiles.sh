@@ -16,12 +16,17 @@ json.dump({"C3": int(num(jvp["dram__bytes_read.sum"]) + num(jvp["dram__bytes_wri
                       "plane_kernel<4,1,1,0> (C3 JVP), one ncu --set full launch"},
           open("profiles/traffic.json", "w"), indent=1)
 rows = [r for r in csv.reader(open("profiles/r01_launches_C3_plane.csv")) if len(r) > 14 and r[12] == "gpu__time_duration.sum"]
+seq = [(r[4].split("(")[0], float(r[14]) / 1000) for r in rows]
+# the bench's steps come first after the setup kernel: (warmup 3 + steps 2) x 4 launches
+# (residual, its fix-up, JVP, its fix-up); the per-call diagnostics that follow are not in the step
+step = [x for x in seq if "geometry" not in x[0]][:20]
 agg = collections.defaultdict(list)
-for r in rows:
-    agg[r[4].split("(")[0]].append(float(r[14]) / 1000)
-tot = sum(sum(v) for k, v in agg.items() if "geometry" not in k)
-out = {k: {"n": len(v), "mean_us": sum(v) / len(v), "share_of_step": (sum(v) / tot if "geometry" not in k else None)}
-       for k, v in agg.items()}
+for k, t in step:
+    agg[k].append(t)
+tot = sum(t for _, t in step)
+out = {k: {"n": len(v), "mean_us": sum(v) / len(v), "share_of_step": sum(v) / tot} for k, v in agg.items()}
+out["_note"] = ("ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialised); the 20 launches of "
+                "bench.py --steps 2 --warmup 3 (5 steps x [plane_kernel<RES>, fixup, plane_kernel<JVP>, fixup])")
 json.dump(out, open("profiles/r01_launches_C3_plane_summary.json", "w"), indent=1)
 print(json.dumps(out, indent=1))
 PY
