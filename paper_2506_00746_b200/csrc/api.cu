@@ -31,7 +31,6 @@ struct feod_op {
   unsigned long long* sched = nullptr;   // dynamic brick scheduling ticket counter
   unsigned long long* bdone = nullptr;   // per-brick completion epochs (fix-up dependencies)
   int2* fixrows = nullptr;               // fix-up rows in launch order
-  unsigned* ycnt = nullptr;              // y-face arrival counters (bricks x BZ)
   double* work = nullptr;      // Newton-CG: F, r, p, Ap, d (5 N)
   double* lin = nullptr;       // stored linearisation (feod_linearize), lin_values x E x q^3
   double* kwork = nullptr;     // adjoint BiCGStab: b, r, rhat, p, v, s, t (7 padded N)
@@ -70,7 +69,6 @@ static void free_all(feod_op* h) {
   cudaFree(h->sched);
   cudaFree(h->bdone);
   cudaFree(h->fixrows);
-  cudaFree(h->ycnt);
   cudaFree(h->work);
   cudaFree(h->lin);
   cudaFree(h->kwork);
@@ -157,11 +155,6 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   if ((e = cudaMemsetAsync(h->bdone, 0, sizeof(unsigned long long) * (size_t)h->nbricks, h->st)) != cudaSuccess)
     return cleanup_fail(cuda_fail(e, "feod_create: memset"));
   P.bdone = h->bdone;
-  if ((e = cudaMalloc(&h->ycnt, sizeof(unsigned) * (size_t)h->nbricks * h->bi.BZ)) != cudaSuccess)
-    return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: y-face counters"));
-  if ((e = cudaMemsetAsync(h->ycnt, 0, sizeof(unsigned) * (size_t)h->nbricks * h->bi.BZ, h->st)) != cudaSuccess)
-    return cleanup_fail(cuda_fail(e, "feod_create: memset"));
-  P.ycnt = h->ycnt;
   {
     // fix-up rows, stably sorted by the last brick ticket they read
     const int nrows = fixup_rows_nd(h->nd, P, nullptr, nullptr);

@@ -50,7 +50,6 @@ struct OpParams {
   const double* geom;    // [E][NQ][6][NQ][NQ] metric, components xx yy zz xy xz yz
   double* lin;           // [E][NQ][lin_values][NQ][NQ] stored linearisation (MODE_LIN writes, MODE_PAJVP reads)
   int vjp_keep_rows;     // MODE_VJP: 1 keeps every row of J^T w (feod_vjp), 0 applies P^T (adjoint solve)
-  unsigned* ycnt;        // [bricks][BZ] arrivals at the low y-face of brick b, layer z (two per call)
   const double* rho;     // [E] (HEAT)
   // dynamic brick scheduling: tickets atomicAdd(sched, 1) - sched_base < #bricks
   // are bricks, the rest end a CTA; the host advances sched_base by #bricks + grid

@@ -6,10 +6,8 @@
 //
 // One CTA per DOF row; threads stride along the row (consecutive threads touch
 // consecutive X, or Y on set X):
-//   set 0 (Y): DOF planes Y = m PY (m = 1..nby-1), rows along X at Z (X on an interior x-plane
-//              skipped) — no longer launched: plane_kernel sums the y-face interiors itself
-//              (last-arriving brick per face and layer); the y-face DOFs on z-planes are in set 1
-//   set 1 (Z): planes Z = m PZ, rows along X at Y (X on an x-plane skipped)
+//   set 0 (Y): DOF planes Y = m PY (m = 1..nby-1), rows along X at Z (X on an interior x-plane skipped)
+//   set 1 (Z): planes Z = m PZ, rows along X at Y (X on an x-plane or Y on a y-plane skipped)
 //   set 2 (X): planes X = m PX, rows along Y at Z (x-y / x-z edges and corners too)
 // Shell slab of a brick with box LX x LY x LZ (common.cuh shell_rank): the z = 0
 // plane, one ring per middle z, the z = LZ-1 plane.
@@ -192,9 +190,17 @@ int fixup_rows(const OpParams& P, int2* rows, unsigned long long* keys) {
   constexpr int PY = K * BY, PZ = K * BZ;
   int c = 0;
   auto bmax = [](int g, int PS, int nb) { int b[2], l[2], k; axis_contrib(g, PS, nb, b, l, k); return b[k - 1]; };
-  // set Y (y-face interiors) is summed inside plane_kernel; its y-z edges join set Z
+  for (int m = 1; m < P.nby; ++m)
+    for (int Z = 0; Z < P.Mz; ++Z) {
+      if (rows) {
+        rows[c] = make_int2(0 << 24 | m, Z);
+        keys[c] = (unsigned long long)((P.nbx - 1) + (int64_t)P.nbx * (m + (int64_t)P.nby * bmax(Z, PZ, P.nbz)));
+      }
+      ++c;
+    }
   for (int m = 1; m < P.nbz; ++m)
     for (int Y = 0; Y < P.My; ++Y) {
+      if (Y % PY == 0 && Y > 0 && Y < P.My - 1) continue;
       if (rows) {
         rows[c] = make_int2(1 << 24 | m, Y);
         keys[c] = (unsigned long long)((P.nbx - 1) + (int64_t)P.nbx * (bmax(Y, PY, P.nby) + (int64_t)P.nby * m));

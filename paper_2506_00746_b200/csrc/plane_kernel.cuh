@@ -453,46 +453,6 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       }
     };
 
-    // y-face interiors (2 contributors, no x- or z-face): after both bricks sharing the
-    // face have stored layer z to their shell slabs, the second one to finish (per-face,
-    // per-layer counter ycnt, incremented twice per call) sums the two values in the
-    // fixed order (lower brick first), applies P^T and writes the output — those DOFs
-    // never go through the fix-up kernel. last: bit0 the low face, bit1 the high face.
-    auto yface_sums = [&](int last, int z, int bzr) {
-      const int x0 = gs.lowX ? 1 : 0, x1 = gs.highX ? gs.LX - 2 : gs.LX - 1;
-      const int nxp = x1 - x0 + 1;
-      int p0 = K * z, p1 = K * z + K - 1 + (z == bzr - 1 ? 1 : 0);
-      if (p0 == 0 && gs.lowZ) p0 = 1;
-      if (p1 == gs.LZ - 1 && gs.highZ) p1 = gs.LZ - 2;
-      const int cnt = nxp * (p1 - p0 + 1);
-      const bool keep = MODE == MODE_VJP && P.vjp_keep_rows;
-#pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        if (!(last & (1 << f))) continue;
-        const int blo = f == 0 ? gs.b - P.nbx : gs.b, bhi = f == 0 ? gs.b : gs.b + P.nbx;
-        const int LYlo = f == 0 ? K * S::BY + 1 : gs.LY;
-        const int LYhi = f == 0 ? gs.LY : K * min(S::BY, P.ny - (gs.ey0 + gs.byr)) + 1;
-        const int gy = f == 0 ? gs.gY0 : gs.gY0 + gs.LY - 1;
-        for (int t = lane; t < cnt; t += 32) {
-          const int p = p0 + t / nxp, X = x0 + t % nxp;
-          const int64_t olo = (int64_t)blo * P.shell_stride + shell_rank(X, LYlo - 1, p, gs.LX, LYlo, gs.LZ);
-          const int64_t ohi = (int64_t)bhi * P.shell_stride + shell_rank(X, 0, p, gs.LX, LYhi, gs.LZ);
-          const int gx = gs.gX0 + X, gz = gs.gZ0 + p;
-          const bool dir = !keep && (((P.faces & 1u) && gx == 0) || ((P.faces & 2u) && gx == P.Mx - 1) ||
-                                     ((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1));
-          const int64_t g = (int64_t)gx + (int64_t)P.Mx * (gy + (int64_t)P.My * gz);
-          double s[S::NOUT > 0 ? S::NOUT : 1];
-#pragma unroll
-          for (int o = 0; o < S::NOUT; ++o) {
-            const double* sh = o == 0 ? shell0 : shell1;
-            s[o] = __ldcg(sh + olo) + __ldcg(sh + ohi);   // L2: written by another SM in this kernel
-          }
-#pragma unroll
-          for (int o = 0; o < S::NOUT; ++o) (o == 0 ? out0 : out1)[g] = dir ? 0.0 : s[o];
-        }
-      }
-    };
-
 #ifdef FEOD_PROFILE_IO
     long long t_wre = 0, t_load = 0, t_wef = 0, t_gt = 0, t0 = clock64(), t1;
     int nl = 0;
@@ -559,6 +519,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
               const bool zero = !(MODE == MODE_VJP && P.vjp_keep_rows) && (pinfo[m] & 6) == 4;
               double* d = reinterpret_cast<double*>(fptr[o][m]) + (int64_t)(K * z) * fstr[m];
 #pragma unroll
+#pragma unroll
               for (int c = 0; c < K; ++c) d[(int64_t)c * fstr[m]] = zero ? 0.0 : v[c];
               carry[o][m] = v[K];
             } else {
@@ -571,18 +532,6 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&e_empty[L & 1]);
-        if (gs.lowY || gs.highY) {
-          __threadfence();   // this lane's shell stores of layer z are visible GPU-wide
-          __syncwarp();
-          int last = 0;
-          if (lane == 0) {
-            if (gs.lowY && (atomicAdd(P.ycnt + (int64_t)gs.b * S::BZ + z, 1u) & 1u)) last |= 1;
-            if (gs.highY && (atomicAdd(P.ycnt + (int64_t)(gs.b + P.nbx) * S::BZ + z, 1u) & 1u)) last |= 2;
-            if (last) __threadfence();
-          }
-          last = __shfl_sync(0xffffffffu, last, 0);
-          if (last) yface_sums(last, z, bzr);
-        }
         FEOD_TICK(t_gt);
       }
 #ifdef FEOD_PROFILE_IO
