@@ -311,6 +311,7 @@ def main():
     # NEXT-2 stored linearisation: one linearize (F(u) + D's linearisation) then J v from it
     t_lin = time_call(lambda: op.linearize(u, out=r))
     t_jlin = time_call(lambda: op.jvp_lin(v, out=JTw))
+    t_diag = time_call(lambda: op.jacobi_diag(out=JTw))
     t_des = None
     if w.model == W.HEAT:
         g = torch.empty(op.n_elems, dtype=torch.float64, device=u.device)
@@ -382,6 +383,7 @@ def main():
                         "fused_kernel_us": jvp_kernel_ms * 1e3},
                 "linearize": {"us": t_lin * 1e3, "gdof_s": N / (t_lin * 1e-3) / 1e9},
                 "jvp_lin": {"us": t_jlin * 1e3, "gdof_s": N / (t_jlin * 1e-3) / 1e9},
+                "jacobi_diag": {"us": t_diag * 1e3},
                 "vjp": {"us": t_vjp * 1e3, "gdof_s": N / (t_vjp * 1e-3) / 1e9,
                         "hbm_frac": algorithmic_bytes(w, "vjp") / (t_vjp * 1e-3) / 1e9 / peak,
                         "fp64_frac": algorithmic_flops(w, "vjp") / (t_vjp * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS},
@@ -412,10 +414,24 @@ def main():
             b_.record(stream)
             torch.cuda.synchronize()
             tl.append(a_.elapsed_time(b_))
-        op.set_newton_linearization(False)
         line["newton_cg_stored_linearization"] = {"ms": statistics.median(tl), "ms_min": min(tl), "norms": norms_l,
                                                   "note": "feod_set_newton_linearization(1): feod_linearize per step, "
                                                           "feod_jvp_lin per CG iteration (NEXT-2)"}
+        op.set_newton_linearization(2)
+        op.newton_cg(u0, 5, 20)
+        torch.cuda.synchronize()
+        tj = []
+        for _ in range(3):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            _, norms_j = op.newton_cg(u0, 5, 20)
+            b_.record(stream)
+            torch.cuda.synchronize()
+            tj.append(a_.elapsed_time(b_))
+        op.set_newton_linearization(0)
+        line["newton_pcg_jacobi"] = {"ms": statistics.median(tj), "ms_min": min(tj), "norms": norms_j,
+                                     "note": "feod_set_newton_linearization(2): + feod_jacobi_diag per step, "
+                                             "Jacobi-preconditioned CG (NEXT-3)"}
         line["newton_cg"] = {"ms": statistics.median(tn), "ms_min": min(tn), "jvp_calls": n_jvp, "residual_calls": n_res,
                              "norms": norms, "op_share_ms": (n_jvp * t_jvp + n_res * t_res),
                              "note": "feod_newton_cg, device time incl. host syncs once per Newton step"}

@@ -148,6 +148,11 @@ FEOD_API int feod_adjoint_solve(feod_handle h, const double* u, const double* rh
  * forward, no metric, no u): same conventions as feod_jvp. FEOD_EINVAL if   *
  * no linearisation is stored. A later feod_linearize replaces it.          */
 FEOD_API int feod_linearize(feod_handle h, const double* u, double* r);
+/* diag (device, length N) <- the diagonal of J at the stored linearisation  *
+ * on free rows, 1 on Dirichlet rows (J's rows there are zero). Sum-         *
+ * factorised per element with squared 1D tables, assembled by 8 element     *
+ * colours (no atomics, deterministic). FEOD_EINVAL without feod_linearize.  */
+FEOD_API int feod_jacobi_diag(feod_handle h, double* diag);
 FEOD_API int feod_jvp_lin(feod_handle h, const double* v, double* Jv);
 /* g_e = -lambda^T dF/drho_e, lambda's Dirichlet entries ignored          *
  * (A14); HEAT_DESIGN only (others: FEOD_EINVAL)           */
@@ -169,7 +174,8 @@ FEOD_API int feod_apply_host(feod_handle h, int op, const double* in0, const dou
 FEOD_API int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg_iters, double* norms_host);
 /* Newton-CG Jacobian: 0 (default) matrix-free feod_jvp at the current u;   *
  * 1 feod_linearize once per Newton step (it also yields F) and            *
- * feod_jvp_lin in every CG iteration.                                      */
+ * feod_jvp_lin in every CG iteration; 2 as 1 plus Jacobi preconditioning   *
+ * (feod_jacobi_diag once per Newton step, CG becomes PCG).  */
 FEOD_API int feod_set_newton_linearization(feod_handle h, int stored);
 
 /* BLAS-1 used by the Newton-CG driver (deterministic two-stage reductions).  *

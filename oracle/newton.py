@@ -19,32 +19,46 @@ from __future__ import annotations
 
 import numpy as np
 
-from .fem import residual, jvp
+from .fem import residual, jvp, element_tangent, dof_map, dirichlet_mask
 
 
-def cg_fixed(apply, b, iters):
-    """Plain CG (Hestenes-Stiefel) from x = 0 for a fixed number of iterations."""
+def cg_fixed(apply, b, iters, diag=None):
+    """Plain CG (Hestenes-Stiefel) from x = 0 for a fixed number of iterations;
+    with ``diag`` the Jacobi-preconditioned CG (z = r / diag)."""
     x = np.zeros_like(b)
     r = b.copy()
-    p = r.copy()
-    rr = float(r @ r)
+    z = r / diag if diag is not None else r.copy()
+    p = z.copy()
+    rz = float(r @ z)
     dirs = []
     for _ in range(iters):
         Ap = apply(p)
         pAp = float(p @ Ap)
         if not pAp > 0.0:
             raise FloatingPointError("CG breakdown: p^T A p <= 0")
-        alpha = rr / pAp
+        alpha = rz / pAp
         dirs.append(p.copy())
         x += alpha * p
         r -= alpha * Ap
-        rr_new = float(r @ r)
-        p = r + (rr_new / rr) * p
-        rr = rr_new
+        z = r / diag if diag is not None else r
+        rz_new = float(r @ z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
     return x, dirs
 
 
-def newton_cg(pr, u0, newton_steps=5, cg_iters=20, record=False):
+def jacobi_diag(pr, u):
+    """Diagonal of J(u) (Eq. 3 element tangents, diagonal entries scattered with
+    numpy.bincount) on free rows, 1 on Dirichlet rows (J's rows there are zero)."""
+    el = np.arange(pr.n_elems)
+    Ke = element_tangent(pr, u, el)
+    dofs = dof_map(pr, el)
+    d = np.bincount(dofs.ravel(), weights=np.einsum("eii->ei", Ke).ravel(), minlength=pr.n_dofs)
+    d[dirichlet_mask(pr)] = 1.0
+    return d
+
+
+def newton_cg(pr, u0, newton_steps=5, cg_iters=20, record=False, jacobi=False):
     u = np.array(u0, dtype=np.float64)
     norms = []
     iterates = []
@@ -53,7 +67,7 @@ def newton_cg(pr, u0, newton_steps=5, cg_iters=20, record=False):
         F = residual(pr, u)
         norms.append(float(np.linalg.norm(F)))
         iterates.append(u.copy())
-        delta, dirs = cg_fixed(lambda x: jvp(pr, u, x), -F, cg_iters)
+        delta, dirs = cg_fixed(lambda x: jvp(pr, u, x), -F, cg_iters, jacobi_diag(pr, u) if jacobi else None)
         directions.append(dirs)
         u = u + delta
     norms.append(float(np.linalg.norm(residual(pr, u))))

@@ -29,7 +29,7 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 # every symbol include/feod.h declares (checked by tests/test_abi.py)
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
-           "feod_set_newton_linearization", "feod_adjoint_solve", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
+           "feod_set_newton_linearization", "feod_jacobi_diag", "feod_adjoint_solve", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
@@ -78,6 +78,7 @@ def load_library(path: str = LIB_PATH):
     lib.feod_linearize.argtypes = [vp, dp, dp]
     lib.feod_jvp_lin.argtypes = [vp, dp, dp]
     lib.feod_set_newton_linearization.argtypes = [vp, ctypes.c_int]
+    lib.feod_jacobi_diag.argtypes = [vp, dp]
     lib.feod_adjoint_solve.argtypes = [vp, dp, dp, dp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_apply_host.argtypes = [vp, ctypes.c_int, dp, dp, dp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
@@ -208,8 +209,16 @@ class Operator:
         _check(self.lib.feod_adjoint_solve(self.h, u.data_ptr(), rhs.data_ptr(), lam.data_ptr(), int(iters), norms))
         return lam, list(norms)
 
-    def set_newton_linearization(self, stored: bool):
-        _check(self.lib.feod_set_newton_linearization(self.h, 1 if stored else 0))
+    def set_newton_linearization(self, stored):
+        """0/False matrix-free, 1/True stored linearisation, 2 stored + Jacobi PCG."""
+        _check(self.lib.feod_set_newton_linearization(self.h, int(stored)))
+
+    def jacobi_diag(self, out=None):
+        """Diagonal of J at the last linearize() (feod_jacobi_diag)."""
+        d = out if out is not None else self._torch.empty(self.n_dofs, dtype=self._torch.float64, device=self.device)
+        self._sync_stream()
+        _check(self.lib.feod_jacobi_diag(self.h, d.data_ptr()))
+        return d
 
     def design_grad(self, u, lam, out=None):
         u, lam = self._dev(u, self.n_dofs, "u"), self._dev(lam, self.n_dofs, "lam")

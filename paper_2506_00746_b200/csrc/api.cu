@@ -35,7 +35,8 @@ struct feod_op {
   double* lin = nullptr;       // stored linearisation (feod_linearize), lin_values x E x q^3
   double* kwork = nullptr;     // adjoint BiCGStab: b, r, rhat, p, v, s, t (7 padded N)
   bool lin_valid = false;
-  int newton_lin = 0;          // Newton-CG: 0 matrix-free JVP, 1 stored linearisation
+  int newton_lin = 0;          // Newton-CG: 0 matrix-free JVP, 1 stored linearisation, 2 + Jacobi
+  double* jdiag = nullptr;     // Jacobi diagonal (Newton mode 2), N
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
 };
 
@@ -72,6 +73,7 @@ static void free_all(feod_op* h) {
   cudaFree(h->work);
   cudaFree(h->lin);
   cudaFree(h->kwork);
+  cudaFree(h->jdiag);
 }
 
 extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const feod_coeffs* coeffs,
@@ -380,8 +382,15 @@ extern "C" int feod_jvp_lin(feod_handle h, const double* v, double* Jv) {
 }
 
 extern "C" int feod_set_newton_linearization(feod_handle h, int stored) {
-  if (!h || (stored != 0 && stored != 1)) return fail(FEOD_EINVAL, "feod_set_newton_linearization: bad argument");
+  if (!h || stored < 0 || stored > 2) return fail(FEOD_EINVAL, "feod_set_newton_linearization: bad argument");
   h->newton_lin = stored;
+  return FEOD_OK;
+}
+
+extern "C" int feod_jacobi_diag(feod_handle h, double* diag) {
+  if (!h || !diag) return fail(FEOD_EINVAL, "feod_jacobi_diag: null argument");
+  if (!h->lin_valid) return fail(FEOD_EINVAL, "feod_jacobi_diag: no linearisation stored (call feod_linearize)");
+  CK(jacobi_diag_nd(h->nd, h->coeffs.model, h->P, h->T, diag, h->st), "feod_jacobi_diag");
   return FEOD_OK;
 }
 
@@ -443,6 +452,15 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
   for (int step = 0; step <= newton_steps; ++step) {
     int rc = h->newton_lin ? feod_linearize(h, u, F) : feod_residual(h, u, F);
     if (rc) return rc;
+    const double* pre = nullptr;
+    if (h->newton_lin == 2 && step < newton_steps) {
+      if (!h->jdiag && cudaMalloc(&h->jdiag, sizeof(double) * (size_t)N) != cudaSuccess) {
+        h->jdiag = nullptr;
+        return fail(FEOD_ENOMEM, "feod_newton_cg: Jacobi diagonal");
+      }
+      if ((rc = feod_jacobi_diag(h, h->jdiag))) return rc;
+      pre = h->jdiag;
+    }
     CK(dot_partial(F, F, N, part, h->st), "feod_newton_cg: norm");
     CK(reduce_final(part, sc + 3, h->st), "feod_newton_cg: norm");
     double ff = 0.0;
@@ -450,8 +468,8 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
     CK(cudaStreamSynchronize(h->st), "feod_newton_cg: sync");
     norms_host[step] = std::sqrt(ff);
     if (step == newton_steps) break;
-    CK(cg_init(F, r, p, d, N, h->st), "feod_newton_cg: init");
-    CK(dot_partial(r, r, N, part, h->st), "feod_newton_cg: rr");
+    CK(cg_init(F, r, p, d, N, h->st, pre), "feod_newton_cg: init");
+    CK(dot_partial(r, p, N, part, h->st), "feod_newton_cg: rz");   // p = z = M^{-1} r
     CK(reduce_final(part, sc + 0, h->st), "feod_newton_cg: rr");
     for (int it = 0; it < cg_iters; ++it) {
       double* rr_old = sc + ((it & 1) ? 2 : 0);
@@ -460,9 +478,9 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
       if (rc) return rc;
       CK(dot_partial(p, Ap, N, part, h->st), "feod_newton_cg: pAp");
       CK(reduce_final(part, sc + 1, h->st), "feod_newton_cg: pAp");
-      CK(cg_update(rr_old, sc + 1, p, Ap, d, r, N, part, bad, h->st), "feod_newton_cg: update");
+      CK(cg_update(rr_old, sc + 1, p, Ap, d, r, N, part, bad, h->st, pre), "feod_newton_cg: update");
       CK(reduce_final(part, rr_new, h->st), "feod_newton_cg: rr");
-      CK(cg_dir(rr_new, rr_old, r, p, N, h->st), "feod_newton_cg: direction");
+      CK(cg_dir(rr_new, rr_old, r, p, N, h->st, pre), "feod_newton_cg: direction");
     }
     CK(axpy1(u, d, N, h->st), "feod_newton_cg: u += d");
     int hbad = 0;

@@ -62,24 +62,26 @@ cudaError_t reduce_final(const double* partials, double* out, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// r = -F, p = r, d = 0
+// r = -F, p = z = M^{-1} r (M = diag, or the identity when diag == nullptr), d = 0
 __global__ void cg_init_kernel(const double* __restrict__ F, double* __restrict__ r, double* __restrict__ p,
-                               double* __restrict__ d, int64_t n) {
+                               double* __restrict__ d, const double* __restrict__ diag, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double v = -F[i];
     r[i] = v;
-    p[i] = v;
+    p[i] = diag ? v / diag[i] : v;
     d[i] = 0.0;
   }
 }
 
 // alpha = rr / pAp;  d += alpha p;  r -= alpha Ap;  partials of r.r (same fixed grid as dot_partial)
+// (with diag: the partials are of r . M^{-1} r, the preconditioned CG's rz)
 __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __restrict__ rr,
                                                                 const double* __restrict__ pAp,
                                                                 const double* __restrict__ p,
                                                                 const double* __restrict__ Ap, double* __restrict__ d,
                                                                 double* __restrict__ r, int64_t n,
-                                                                double* __restrict__ partials, int* __restrict__ bad) {
+                                                                double* __restrict__ partials, int* __restrict__ bad,
+                                                                const double* __restrict__ diag) {
   __shared__ double sh[kRedThreads];
   const double den = *pAp;
   if (blockIdx.x == 0 && threadIdx.x == 0 && !(den > 0.0)) *bad = 1;
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __
       d[j] = fma(alpha, pv[t], dv[t]);
       const double ri = fma(-alpha, av[t], rv[t]);
       r[j] = ri;
-      acc[t] = fma(ri, ri, acc[t]);
+      acc[t] = fma(ri, diag ? ri / diag[j] : ri, acc[t]);
     }
   }
 #pragma unroll
@@ -108,27 +110,31 @@ __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __
       d[i] = fma(alpha, p[i], d[i]);
       const double ri = fma(-alpha, Ap[i], r[i]);
       r[i] = ri;
-      acc[t] = fma(ri, ri, acc[t]);
+      acc[t] = fma(ri, diag ? ri / diag[i] : ri, acc[t]);
       i += kRedStride;
     }
   const double s = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]), sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
-// p = r + (rr_new / rr_old) p
+// p = z + (rz_new / rz_old) p,  z = M^{-1} r (z = r without preconditioner)
 __global__ void cg_dir_kernel(const double* __restrict__ rr_new, const double* __restrict__ rr_old,
-                              const double* __restrict__ r, double* __restrict__ p, int64_t n) {
+                              const double* __restrict__ r, double* __restrict__ p, int64_t n,
+                              const double* __restrict__ diag) {
   const double beta = *rr_new / *rr_old;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
     double pv[kUnroll], rv[kUnroll];
 #pragma unroll
-    for (int t = 0; t < kUnroll; ++t) { pv[t] = p[i + t * stride]; rv[t] = __ldcs(r + i + t * stride); }
+    for (int t = 0; t < kUnroll; ++t) {
+      pv[t] = p[i + t * stride];
+      rv[t] = diag ? __ldcs(r + i + t * stride) / diag[i + t * stride] : __ldcs(r + i + t * stride);
+    }
 #pragma unroll
     for (int t = 0; t < kUnroll; ++t) p[i + t * stride] = fma(beta, pv[t], rv[t]);
   }
-  for (; i < n; i += stride) p[i] = fma(beta, p[i], r[i]);
+  for (; i < n; i += stride) p[i] = fma(beta, p[i], diag ? r[i] / diag[i] : r[i]);
 }
 
 // u += d
@@ -142,18 +148,18 @@ static int grid_for(int64_t n) {
   return (int)(b < kRedBlocks ? (b > 0 ? b : 1) : kRedBlocks);
 }
 
-cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n, cudaStream_t st) {
-  cg_init_kernel<<<grid_for(n), 256, 0, st>>>(F, r, p, d, n);
+cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n, cudaStream_t st, const double* diag) {
+  cg_init_kernel<<<grid_for(n), 256, 0, st>>>(F, r, p, d, diag, n);
   return cudaGetLastError();
 }
 cudaError_t cg_update(const double* rr, const double* pAp, const double* p, const double* Ap, double* d, double* r,
-                      int64_t n, double* partials, int* bad, cudaStream_t st) {
-  cg_update_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(rr, pAp, p, Ap, d, r, n, partials, bad);
+                      int64_t n, double* partials, int* bad, cudaStream_t st, const double* diag) {
+  cg_update_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(rr, pAp, p, Ap, d, r, n, partials, bad, diag);
   return cudaGetLastError();
 }
 cudaError_t cg_dir(const double* rr_new, const double* rr_old, const double* r, double* p, int64_t n,
-                   cudaStream_t st) {
-  cg_dir_kernel<<<grid_for(n), 256, 0, st>>>(rr_new, rr_old, r, p, n);
+                   cudaStream_t st, const double* diag) {
+  cg_dir_kernel<<<grid_for(n), 256, 0, st>>>(rr_new, rr_old, r, p, n, diag);
   return cudaGetLastError();
 }
 cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st) {

@@ -1,0 +1,148 @@
+// K8 — diagonal of the stored linearisation's Jacobian (SURVEY §8(f) NEXT-3,
+// Jacobi preconditioning "from the PA diagonal"). With the stored per-point
+// linearisation A = dFh/dgh (symmetric) and b = dFh/du (feod_linearize), the
+// element Jacobian is K_e[i][j] = sum_q grad phi_i . (A grad phi_j + b phi_j)
+// (Eq. 2 / Eq. 3), so its diagonal at the tensor-product node (a, b, c) is
+//   sum_q [ A_xx G_a^2 B_b^2 B_c^2 + A_yy B_a^2 G_b^2 B_c^2 + A_zz B_a^2 B_b^2 G_c^2
+//         + 2 A_xy (GB)_a (BG)_b B_c^2 + 2 A_xz (GB)_a B_b^2 (BG)_c + 2 A_yz B_a^2 (GB)_b (GB)_c
+//         + b_x (GB)_a B_b^2 B_c^2 + b_y B_a^2 (GB)_b B_c^2 + b_z B_a^2 B_b^2 (GB)_c ]
+// with the 1D tables evaluated at the Gauss points (B = l_a(x_i), G = l_a'(x_i)):
+// every term is a sum-factorised contraction with squared / mixed 1D tables.
+// One CTA per element; G^T without atomics by 8 element colours (parity of
+// ex, ey, ez): elements of one colour share no DOF, the colours run in a fixed
+// order, so the assembled diagonal is bitwise reproducible. Dirichlet rows get
+// 1 (J's Dirichlet rows are zero; the preconditioner is the identity there).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace feod {
+
+constexpr int kDiagThreads = 128;
+
+template <int ND, int NT>
+__global__ void __launch_bounds__(kDiagThreads) diag_color_kernel(const OpParams P, const Tables T, int color,
+                                                                  double* __restrict__ diag) {
+  constexpr int NQ = ND, NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, NL = NT;
+  // per-term tables along x, y, z: 0 = B^2, 1 = G^2, 2 = G B
+  constexpr int TX[9] = {1, 0, 0, 2, 2, 0, 2, 0, 0};
+  constexpr int TY[9] = {0, 1, 0, 2, 0, 2, 0, 2, 0};
+  constexpr int TZ[9] = {0, 0, 1, 0, 2, 2, 0, 0, 2};
+  constexpr double WT[9] = {1, 1, 1, 2, 2, 2, 1, 1, 1};
+  extern __shared__ double dsm[];
+  double(*tab)[NQ][ND] = reinterpret_cast<double(*)[NQ][ND]>(dsm);                       // [3][NQ][ND]
+  double(*S0)[NQ3] = reinterpret_cast<double(*)[NQ3]>(dsm + 3 * NQ * ND);                 // A terms [l][j][i]
+  double(*S1)[NQ2 * ND] = reinterpret_cast<double(*)[NQ2 * ND]>(dsm + 3 * NQ * ND + NT * NQ3);   // [j][i][c]
+  double(*S2)[NQ * ND * ND] = reinterpret_cast<double(*)[NQ * ND * ND]>(dsm + 3 * NQ * ND);  // [i][b][c], over S0
+  const int tid = threadIdx.x;
+  // this CTA's element of the colour
+  const int hx = (P.nx + 1 - (color & 1)) / 2, hy = (P.ny + 1 - ((color >> 1) & 1)) / 2;
+  const int e = blockIdx.x;
+  const int ex = 2 * (e % hx) + (color & 1);
+  const int ey = 2 * ((e / hx) % hy) + ((color >> 1) & 1);
+  const int ez = 2 * (e / (hx * hy)) + ((color >> 2) & 1);
+  const int64_t eg = ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez);
+  for (int t = tid; t < NQ * ND; t += kDiagThreads) {
+    const int i = t / ND, a = t % ND;
+    const double b = T.B[i][a], g = T.G[i][a];
+    tab[0][i][a] = b * b;
+    tab[1][i][a] = g * g;
+    tab[2][i][a] = g * b;
+  }
+  const double* lin = P.lin + eg * (NL * NQ3);
+  for (int t = tid; t < NT * NQ3; t += kDiagThreads) {
+    const int term = t / NQ3, r = t % NQ3;   // r = (l, j, i) with i fastest
+    const int l = r / NQ2, ji = r % NQ2;
+    S0[term][r] = lin[l * NL * NQ2 + term * NQ2 + ji];
+  }
+  __syncthreads();
+  // contract l: S1[t][j][i][c] = sum_l S0[t][l][j][i] Z_t[l][c]
+  for (int t = tid; t < NT * NQ2 * ND; t += kDiagThreads) {
+    const int term = t / (NQ2 * ND), r = t % (NQ2 * ND), ji = r / ND, c = r % ND;
+    const int tz = TZ[term];
+    double s = 0.0;
+#pragma unroll
+    for (int l = 0; l < NQ; ++l) s = fma(S0[term][l * NQ2 + ji], tab[tz][l][c], s);
+    S1[term][r] = s;
+  }
+  __syncthreads();
+  // contract j: S2[t][i][b][c] = sum_j S1[t][j][i][c] Y_t[j][b]
+  for (int t = tid; t < NT * NQ * ND * ND; t += kDiagThreads) {
+    const int term = t / (NQ * ND * ND), r = t % (NQ * ND * ND);
+    const int i = r / (ND * ND), b = (r / ND) % ND, c = r % ND;
+    const int ty = TY[term];
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) s = fma(S1[term][(j * NQ + i) * ND + c], tab[ty][j][b], s);
+    S2[term][r] = s;
+  }
+  __syncthreads();
+  // contract i and sum the terms in a fixed order; add into the diagonal (colour-exclusive)
+  const int Mx = P.Mx, My = P.My;
+  for (int t = tid; t < ND * ND * ND; t += kDiagThreads) {
+    const int a = t % ND, b = (t / ND) % ND, c = t / (ND * ND);
+    double s = 0.0;
+#pragma unroll
+    for (int term = 0; term < NT; ++term) {
+      const int tx = TX[term];
+      double st = 0.0;
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) st = fma(S2[term][(i * ND + b) * ND + c], tab[tx][i][a], st);
+      s = fma(WT[term], st, s);
+    }
+    const int64_t g = (int64_t)((ND - 1) * ex + a) + (int64_t)Mx * (((ND - 1) * ey + b) + (int64_t)My * ((ND - 1) * ez + c));
+    diag[g] += s;
+  }
+}
+
+__global__ void diag_dirichlet_kernel(const OpParams P, double* __restrict__ diag) {
+  const int64_t n = (int64_t)P.Mx * P.My * P.Mz;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int X = (int)(i % P.Mx);
+    const int64_t yz = i / P.Mx;
+    const int Y = (int)(yz % P.My), Z = (int)(yz / P.My);
+    if (is_dirichlet(X, Y, Z, P.Mx, P.My, P.Mz, P.faces)) diag[i] = 1.0;
+  }
+}
+
+template <int ND, int NT>
+static cudaError_t diag_nd_t(const OpParams& P, const Tables& T, double* diag, cudaStream_t st) {
+  constexpr size_t smem = sizeof(double) * (3 * ND * ND + NT * ND * ND * ND + NT * ND * ND * ND);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(diag_color_kernel<ND, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  for (int color = 0; color < 8; ++color) {
+    const int hx = (P.nx + 1 - (color & 1)) / 2, hy = (P.ny + 1 - ((color >> 1) & 1)) / 2,
+              hz = (P.nz + 1 - ((color >> 2) & 1)) / 2;
+    const int64_t ne = (int64_t)hx * hy * hz;
+    if (ne == 0) continue;
+    diag_color_kernel<ND, NT><<<(unsigned)ne, kDiagThreads, smem, st>>>(P, T, color, diag);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t n = (int64_t)P.Mx * P.My * P.Mz;
+  const int64_t b = (n + 255) / 256;
+  diag_dirichlet_kernel<<<(unsigned)(b < kRedBlocks ? b : kRedBlocks), 256, 0, st>>>(P, diag);
+  return cudaGetLastError();
+}
+
+cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* diag, cudaStream_t st) {
+  const cudaError_t e = cudaMemsetAsync(diag, 0, sizeof(double) * (size_t)P.Mx * P.My * P.Mz, st);
+  if (e != cudaSuccess) return e;
+  const bool nine = lin_values(model) == 9;
+  switch (nd) {
+    case 2: return nine ? diag_nd_t<2, 9>(P, T, diag, st) : diag_nd_t<2, 6>(P, T, diag, st);
+    case 3: return nine ? diag_nd_t<3, 9>(P, T, diag, st) : diag_nd_t<3, 6>(P, T, diag, st);
+    case 4: return nine ? diag_nd_t<4, 9>(P, T, diag, st) : diag_nd_t<4, 6>(P, T, diag, st);
+    case 5: return nine ? diag_nd_t<5, 9>(P, T, diag, st) : diag_nd_t<5, 6>(P, T, diag, st);
+    case 6: return nine ? diag_nd_t<6, 9>(P, T, diag, st) : diag_nd_t<6, 6>(P, T, diag, st);
+    case 7: return nine ? diag_nd_t<7, 9>(P, T, diag, st) : diag_nd_t<7, 6>(P, T, diag, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace feod

@@ -60,11 +60,14 @@ cudaError_t reduce_final(const double* partials, double* out, cudaStream_t st);
 }  // namespace feod
 
 namespace feod {
-cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n, cudaStream_t st);
+cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n, cudaStream_t st,
+                    const double* diag = nullptr);
 cudaError_t cg_update(const double* rr, const double* pAp, const double* p, const double* Ap, double* d, double* r,
-                      int64_t n, double* partials, int* bad, cudaStream_t st);
+                      int64_t n, double* partials, int* bad, cudaStream_t st, const double* diag = nullptr);
 cudaError_t cg_dir(const double* rr_new, const double* rr_old, const double* r, double* p, int64_t n,
-                   cudaStream_t st);
+                   cudaStream_t st, const double* diag = nullptr);
+// Jacobi diagonal of the stored linearisation (diag.cu, K8)
+cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* diag, cudaStream_t st);
 cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st);
 // BiCGStab for the adjoint solve (krylov.cu)
 cudaError_t mask_dirichlet(double* x, const OpParams& P, cudaStream_t st);

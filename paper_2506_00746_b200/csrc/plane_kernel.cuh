@@ -39,6 +39,9 @@
 #include <cstdio>
 #endif
 
+#ifndef FEOD_MPD
+#define FEOD_MPD 0
+#endif
 #ifndef FEOD_MINB_OVERRIDE
 #define FEOD_MINB_OVERRIDE 0
 #endif
@@ -581,6 +584,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   // per-point global stream: the metric (stored-metric meshes) or the stored linearisation (MODE_PAJVP)
   constexpr int NSV = (MODE == MODE_PAJVP) ? lin_values(MODEL) : 6;
   constexpr bool STREAM = (MODE == MODE_PAJVP) || !AFFINE;
+  constexpr int MPD = FEOD_MPD > 0 ? FEOD_MPD : (ND == 2 ? 2 : 1);   // point rows of the stream in flight (Q1: 2, measured)
   double* const xe = xb + el * S::SE;   // this element's exchange slot
   const double wij = T.w[lic] * T.w[gr];
   const double iwij2 = T.wi2[lic] * T.wi2[gr];
@@ -610,12 +614,14 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     // per-point stream of this thread's points (i = li, j = gr, l), layout [E][l][NSV][j][i]:
     // the metric (NSV = 6) on stored-metric meshes, or the stored linearisation (MODE_PAJVP)
     const double* gm = nullptr;
-    double mnext[STREAM ? NSV : 1];
+    double mnext[STREAM ? MPD : 1][STREAM ? NSV : 1];   // rows l .. l+MPD-1 in flight
     if constexpr (STREAM) {
       const double* sb = (MODE == MODE_PAJVP) ? P.lin : P.geom;
       gm = sb + (evalid ? eg : 0) * (NSV * NQ3) + gr * NQ + lic;
 #pragma unroll
-      for (int c = 0; c < NSV; ++c) mnext[c] = ld_stream(gm + c * NQ2);
+      for (int r = 0; r < MPD; ++r)
+#pragma unroll
+        for (int c = 0; c < NSV; ++c) mnext[r][c] = r < NQ ? ld_stream(gm + r * NSV * NQ2 + c * NQ2) : 0.0;
       if (tid < byr && z + 1 < bzr) {   // L2 prefetch of the next layer's stream, one x-row of elements per y
         const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + tid) + (int64_t)P.ny * (ez0 + z + 1));
         prefetch_l2(sb + e1 * (NSV * NQ3), (uint32_t)(bxr * NSV * NQ3 * sizeof(double)));
@@ -728,10 +734,10 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       double sv[STREAM ? NSV : 1];   // this point's stream values
       if constexpr (STREAM) {
 #pragma unroll
-        for (int c = 0; c < NSV; ++c) sv[c] = mnext[c];
-        if (l + 1 < NQ) {
+        for (int c = 0; c < NSV; ++c) sv[c] = mnext[l % MPD][c];
+        if (l + MPD < NQ) {
 #pragma unroll
-          for (int c = 0; c < NSV; ++c) mnext[c] = ld_stream(gm + (l + 1) * NSV * NQ2 + c * NQ2);
+          for (int c = 0; c < NSV; ++c) mnext[l % MPD][c] = ld_stream(gm + (l + MPD) * NSV * NQ2 + c * NQ2);
         }
       }
       if constexpr (AFFINE || MODE == MODE_PAJVP) {

@@ -113,3 +113,24 @@ def test_adjoint_solve_fullsize_runs():
     op = operator(w, d)
     lam, norms = op.adjoint_solve(cuda(d["u"]), cuda(d["lam"]), iters=30)
     assert np.all(np.isfinite(host(lam))) and norms[-1] < 0.5 * norms[0]
+
+
+def test_newton_pcg_jacobi():
+    """Newton mode 2 (stored linearisation + Jacobi PCG, NEXT-3) free-running against the
+    oracle's Jacobi-preconditioned Newton-CG within 100x the oracle's own roundoff spread;
+    preconditioning must not be worse than plain CG on the final residual."""
+    w = W.C4.resized(2)
+    d = W.draw(w)
+    pr, op = problem(w, d), operator(w, d)
+    u0 = np.zeros(w.n_dofs)
+    u_ref, norms_ref = O.newton_cg(pr, u0, 5, 20, jacobi=True)
+    pert = 1e-15 * np.random.default_rng(9).uniform(-1, 1, w.n_dofs)
+    pert[W.dirichlet_dofs(w.n, w.k, w.faces)] = 0.0
+    u_p, norms_p = O.newton_cg(pr, pert, 5, 20, jacobi=True)
+    spread_n = np.max(np.abs(np.array(norms_p) - norms_ref) / np.array(norms_ref))
+    spread_u = rel_l2(u_p, u_ref)
+    op.set_newton_linearization(2)
+    u, norms = op.newton_cg(cuda(u0), 5, 20)
+    dev_n = np.max(np.abs(np.array(norms) - norms_ref) / np.array(norms_ref))
+    assert dev_n <= 100 * spread_n + 1e-12, (dev_n, spread_n)
+    assert rel_l2(host(u), u_ref) <= 100 * spread_u + 1e-12

@@ -77,3 +77,17 @@ def test_linearize_and_jvp_lin_parity(w, n):
     assert rel_l2(r, O.residual(pr, d["u"])) <= TOL
     Jv = host(op.jvp_lin(cuda(d["v"])))
     assert rel_l2(Jv, O.jvp(pr, d["u"], d["v"])) <= TOL
+
+
+DIAG_CASES = [(W.C1, 4), (W.C2, 11), (W.C3, 5), (W.C4, 3), (W.C5, 6), (W.C5, 9)]
+
+
+@pytest.mark.parametrize("w,n", DIAG_CASES, ids=[f"{w.name}n{n}" for w, n in DIAG_CASES])
+def test_jacobi_diag_parity(w, n):
+    """NEXT-3: feod_jacobi_diag (sum-factorised, colour-assembled diagonal of the stored
+    linearisation) against the oracle's scattered Eq. 3 element-tangent diagonal."""
+    ww, d = _case(w, n)
+    pr, op = problem(ww, d), operator(ww, d)
+    op.linearize(cuda(d["u"]))
+    got = host(op.jacobi_diag())
+    assert rel_l2(got, O.jacobi_diag(pr, d["u"])) <= TOL

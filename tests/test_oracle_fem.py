@@ -444,3 +444,34 @@ def test_bicgstab_fixed_solves_nonsymmetric():
     assert hist[-1] <= 1e-12 * hist[0]
     x5, h5 = O.bicgstab_fixed(lambda y: A @ y, b, 5)
     assert abs(np.linalg.norm(b - A @ x5) - h5[-1]) <= 1e-10 * h5[0]
+
+
+@pytest.mark.parametrize("c", CASES13, ids=lambda c: f"n{c['n']}k{c['k']}m{c['model']}")
+def test_jacobi_diag_is_dense_diagonal(c):
+    """NEXT-3: the scattered element-tangent diagonal equals the diagonal of the
+    FD-pinned dense Jacobian (T13) on free rows, 1 on Dirichlet rows."""
+    n = c["n"]
+    rho = np.random.default_rng(4).uniform(0.1, 1, n ** 3)
+    pr = prob(n, c["k"], model=c["model"], perturbed=c["perturbed"], faces=c["faces"],
+              p=c["p"], eps=c["eps"], rho=rho)
+    u = rand_free(pr, 11)
+    d = O.jacobi_diag(pr, u)
+    mask = O.dirichlet_mask(pr)
+    A = O.dense_jacobian(pr, u)
+    np.testing.assert_allclose(d[~mask], np.diag(A)[~mask], rtol=1e-13, atol=0)
+    assert np.all(d[mask] == 1.0)
+
+
+def test_pcg_fixed_reaches_solve():
+    """Pin for the Jacobi-preconditioned CG: on a badly scaled SPD matrix it reaches
+    numpy.linalg.solve's answer (and faster than plain CG)."""
+    rng = np.random.default_rng(6)
+    n = 50
+    Q = rng.uniform(-1, 1, (n, n))
+    S = np.diag(10.0 ** rng.uniform(-3, 3, n))
+    A = S @ (Q @ Q.T + n * np.eye(n)) @ S
+    b = rng.uniform(-1, 1, n)
+    x, _ = O.cg_fixed(lambda y: A @ y, b, 60, np.diag(A).copy())
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-9)
+    x0, _ = O.cg_fixed(lambda y: A @ y, b, 60)
+    assert np.linalg.norm(A @ x - b) < 1e-3 * np.linalg.norm(A @ x0 - b)
