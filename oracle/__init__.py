@@ -30,13 +30,13 @@ beyond roundoff growth is "parity unpinned" (T17).
 """
 from .rules import gauss_legendre01, gll_nodes01, lagrange_eval
 from .fem import Problem, residual, jvp, vjp, design_grad, element_tangent, dense_jacobian, adjoint_solve
-from .fem import residual_rows, jvp_rows, design_grad_elems, dirichlet_mask, dof_map
+from .fem import residual_rows, jvp_rows, vjp_rows, design_grad_elems, dirichlet_mask, dof_map
 from .flux import flux, flux_dg, flux_du, flux_drho
 from .newton import newton_cg, bicgstab_fixed, jacobi_diag, cg_fixed
 
 __all__ = [
     "gauss_legendre01", "gll_nodes01", "lagrange_eval", "Problem", "residual", "jvp", "vjp", "adjoint_solve",
-    "design_grad", "element_tangent", "dense_jacobian", "residual_rows", "jvp_rows",
+    "design_grad", "element_tangent", "dense_jacobian", "residual_rows", "jvp_rows", "vjp_rows",
     "design_grad_elems", "dirichlet_mask", "dof_map", "flux", "flux_dg", "flux_du",
     "flux_drho", "newton_cg", "bicgstab_fixed", "jacobi_diag", "cg_fixed",
 ]

@@ -322,6 +322,15 @@ def jvp_rows(pr: Problem, u, v, rows):
     return _assemble(pr, _jvp_elems(pr, np.asarray(u, float), np.asarray(v, float), el), pr.n_dofs)[rows]
 
 
+def vjp_rows(pr: Problem, u, w, rows):
+    """(J^T w)[rows], from only the elements that touch those rows (no row mask, A17)."""
+    el = _elems_touching(pr, rows)
+    parts = _vjp_elems(pr, np.asarray(u, float), w, el)
+    idx = np.concatenate([d.ravel() for d, _ in parts])
+    val = np.concatenate([v.ravel() for _, v in parts])
+    return np.bincount(idx, weights=val, minlength=pr.n_dofs)[rows]
+
+
 def design_grad_elems(pr: Problem, u, lam, elems):
     return _design_elems(pr, np.asarray(u, float), lam, np.asarray(elems))
 

@@ -23,7 +23,8 @@ def sample_rows(w, n_random=160, seed=0):
     m = w.k * w.n + 1
     rng = np.random.default_rng(seed)
     rows = list(rng.choice(m ** 3, n_random, replace=False))
-    bx, by, bz = {1: (8, 8, 16), 2: (4, 4, 16), 3: (2, 4, 8), 4: (4, 2, 8), 5: (2, 2, 8), 6: (2, 2, 8)}[w.k]
+    # the brick tiles of plane_kernel (PlaneTile<k+1>): faces, edges and corners of bricks
+    bx, by, bz = {1: (8, 4, 16), 2: (4, 3, 16), 3: (4, 2, 16), 4: (4, 2, 8), 5: (2, 2, 8), 6: (2, 2, 8)}[w.k]
     planes = sorted({0, 1, m - 2, m - 1} | {w.k * b * i for b in (bx, by, bz) for i in range(1, w.n // b + 1)
                                             if w.k * b * i < m})
     for _ in range(80):
@@ -110,3 +111,21 @@ def test_determinism_c2_repeated_jvp():
         assert torch.equal(out, ref)
     op2 = operator(w, d)
     assert torch.equal(op2.jvp(u, v), ref)
+
+
+def test_vjp_sampled(full):
+    """J^T w (NEXT-1) at full size on sampled rows (oracle from the touching elements)."""
+    w, d, pr, op = full
+    rows = sample_rows(w, seed=2)
+    JTw = host(op.vjp(cuda(d["u"]), cuda(d["v"])))
+    assert rel_l2(JTw[rows], O.vjp_rows(pr, d["u"], d["v"], rows)) <= TOL
+
+
+def test_linearize_jvp_lin_sampled(full):
+    """NEXT-2 at full size: F(u) from feod_linearize and J v from the stored linearisation."""
+    w, d, pr, op = full
+    rows = sample_rows(w, seed=3)
+    r = host(op.linearize(cuda(d["u"])))
+    assert rel_l2(r[rows], O.residual_rows(pr, d["u"], rows)) <= TOL
+    Jv = host(op.jvp_lin(cuda(d["v"])))
+    assert rel_l2(Jv[rows], O.jvp_rows(pr, d["u"], d["v"], rows)) <= TOL

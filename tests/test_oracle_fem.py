@@ -475,3 +475,10 @@ def test_pcg_fixed_reaches_solve():
     np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-9)
     x0, _ = O.cg_fixed(lambda y: A @ y, b, 60)
     assert np.linalg.norm(A @ x - b) < 1e-3 * np.linalg.norm(A @ x0 - b)
+
+
+def test_vjp_rows_match_full():
+    pr = prob(4, 2, model=HT, perturbed=True, faces=1, rho=np.random.default_rng(2).uniform(0.1, 1, 64))
+    u, w = rand_free(pr, 1), np.random.default_rng(3).uniform(-1, 1, pr.n_dofs)
+    rows = np.array([0, 5, 40, 100, pr.n_dofs - 1])
+    np.testing.assert_array_equal(O.vjp_rows(pr, u, w, rows), O.vjp(pr, u, w)[rows])
