@@ -26,9 +26,24 @@ static cudaError_t launch_one(int nbricks, const OpParams& P, const Tables& T, c
   }
   const int grid = nbricks < slots ? nbricks : slots;
   *grid_out = grid;
+#if FEOD_PDL_OPERATOR
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)S::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, plane_kernel<ND, MODE, MODEL, AFF>, P, T, p.in0, p.in1, p.out0, p.out1, p.shell0,
+                            p.shell1, p.gout);
+#else
   plane_kernel<ND, MODE, MODEL, AFF><<<grid, S::NT, smem, st>>>(P, T, p.in0, p.in1, p.out0, p.out1, p.shell0,
                                                                 p.shell1, p.gout);
   return cudaGetLastError();
+#endif
 }
 
 template <int ND, int NQ, int MODE, int MODEL, bool AFF>

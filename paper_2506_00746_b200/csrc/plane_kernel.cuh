@@ -39,6 +39,9 @@
 #include <cstdio>
 #endif
 
+#ifndef FEOD_PDL_OPERATOR
+#define FEOD_PDL_OPERATOR 1
+#endif
 #ifndef FEOD_MPD
 #define FEOD_MPD 0
 #endif
@@ -309,6 +312,11 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+#if FEOD_PDL_OPERATOR
+  // launched as a programmatic dependent of the previous call's fix-up: the table and
+  // barrier set-up above overlapped it; nothing global is read before this point
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 
   if (warp == S::NWC) {
     // =========================== IO warp ===================================
