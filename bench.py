@@ -435,6 +435,27 @@ def main():
         line["newton_cg"] = {"ms": statistics.median(tn), "ms_min": min(tn), "jvp_calls": n_jvp, "residual_calls": n_res,
                              "norms": norms, "op_share_ms": (n_jvp * t_jvp + n_res * t_res),
                              "note": "feod_newton_cg, device time incl. host syncs once per Newton step"}
+    if w.k <= 3 and world == 1:
+        # NEXT-4 (Table-1 analogue): element tangents K_e = B^T J_D B on the FP64 tensor cores,
+        # RES (integration-point AD) and ELM (element-level forward AD), on a bounded element range
+        nn, Qp = (w.k + 1) ** 3, w.q ** 3
+        ne = min(op.n_elems, 16384)
+        Ke = torch.empty((ne, nn, nn), dtype=torch.float64, device=u.device)
+        pw = {W.PLAPLACE: 35, W.NLDIFF: 19, W.HEAT: 19}[w.model] * (2 if w.perturbed else 1)   # dual flux flops
+        gemm = 2.0 * nn * nn * 3 * Qp
+        interp = 2.0 * 4 * Qp * nn
+        tab = {}
+        for elm in (False, True):
+            t_em = time_call(lambda: op.element_matrices(u, 0, ne, elm=elm, out=Ke), reps=5)
+            build = (Qp * nn * pw) if elm else (4 * Qp * pw + 2.0 * 4 * 3 * Qp * nn)
+            fl = gemm + interp + build
+            tab["ELM" if elm else "RES"] = {"ns_per_element": t_em * 1e6 / ne, "kflop_per_element": fl / 1e3,
+                                            "tflops": fl * ne / (t_em * 1e-3) / 1e12,
+                                            "gemm_share_of_flops": gemm / fl}
+        line["element_tangents"] = {"elements": ne, "nd3": nn, **tab,
+                                    "elm_over_res_flops": tab["ELM"]["kflop_per_element"] / tab["RES"]["kflop_per_element"],
+                                    "elm_over_res_time": tab["ELM"]["ns_per_element"] / tab["RES"]["ns_per_element"],
+                                    "note": "feod_element_matrices (DMMA m8n8k4 f64); peak 37 TF/s DMMA (tools/dmma_probe.cu)"}
     if w.model == W.HEAT and world == 1:
         # NEXT-1: adjoint solve, 50 BiCGStab iterations (2 J^T applications each), rhs = the recipe's lambda draw
         lam_rhs = torch.as_tensor(d["lam"]).cuda()

@@ -29,7 +29,8 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 # every symbol include/feod.h declares (checked by tests/test_abi.py)
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
-           "feod_set_newton_linearization", "feod_jacobi_diag", "feod_adjoint_solve", "feod_design_grad", "feod_apply_host", "feod_newton_cg",
+           "feod_set_newton_linearization", "feod_jacobi_diag", "feod_adjoint_solve", "feod_element_matrices",
+           "feod_design_grad", "feod_apply_host", "feod_newton_cg",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
@@ -79,6 +80,7 @@ def load_library(path: str = LIB_PATH):
     lib.feod_jvp_lin.argtypes = [vp, dp, dp]
     lib.feod_set_newton_linearization.argtypes = [vp, ctypes.c_int]
     lib.feod_jacobi_diag.argtypes = [vp, dp]
+    lib.feod_element_matrices.argtypes = [vp, dp, i64, i64, ctypes.c_int, dp]
     lib.feod_adjoint_solve.argtypes = [vp, dp, dp, dp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_apply_host.argtypes = [vp, ctypes.c_int, dp, dp, dp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
@@ -212,6 +214,16 @@ class Operator:
     def set_newton_linearization(self, stored):
         """0/False matrix-free, 1/True stored linearisation, 2 stored + Jacobi PCG."""
         _check(self.lib.feod_set_newton_linearization(self.h, int(stored)))
+
+    def element_matrices(self, u, e0=0, ne=None, elm=False, out=None):
+        """K_e = B^T J_D B for elements e0 .. e0+ne-1 (feod_element_matrices), shape (ne, nd^3, nd^3)."""
+        u = self._dev(u, self.n_dofs, "u")
+        ne = self.n_elems - e0 if ne is None else ne
+        nn = (self.order + 1) ** 3
+        Ke = out if out is not None else self._torch.empty((ne, nn, nn), dtype=self._torch.float64, device=self.device)
+        self._sync_stream()
+        _check(self.lib.feod_element_matrices(self.h, u.data_ptr(), int(e0), int(ne), 1 if elm else 0, Ke.data_ptr()))
+        return Ke
 
     def jacobi_diag(self, out=None):
         """Diagonal of J at the last linearize() (feod_jacobi_diag)."""

@@ -394,6 +394,19 @@ extern "C" int feod_jacobi_diag(feod_handle h, double* diag) {
   return FEOD_OK;
 }
 
+extern "C" int feod_element_matrices(feod_handle h, const double* u, int64_t e0, int64_t ne, int elm, double* Ke) {
+  if (!h || !u || !Ke) return fail(FEOD_EINVAL, "feod_element_matrices: null argument");
+  if (e0 < 0 || ne < 0 || e0 + ne > h->E || (elm != 0 && elm != 1))
+    return fail(FEOD_EINVAL, "feod_element_matrices: element range or mode out of bounds");
+  if (h->nd > 4) return fail(FEOD_EUNSUPPORTED, "feod_element_matrices: built for orders 1..3");
+  if (h->coeffs.model == FEOD_HEAT_DESIGN && !h->P.rho) return fail(FEOD_EINVAL, "feod_element_matrices: rho unset");
+  if (ne == 0) return FEOD_OK;
+  CK(element_matrices_nd(h->nd, h->coeffs.model, h->geom == nullptr, elm != 0, h->P, h->T, u, (int)e0, (int)ne, Ke,
+                         h->st),
+     "feod_element_matrices");
+  return FEOD_OK;
+}
+
 extern "C" int feod_design_grad(feod_handle h, const double* u, const double* lambda, double* g) {
   if (!h || !u || !lambda || !g) return fail(FEOD_EINVAL, "feod_design_grad: null argument");
   if (h->coeffs.model != FEOD_HEAT_DESIGN) return fail(FEOD_EINVAL, "feod_design_grad: model has no rho");

@@ -1,0 +1,250 @@
+// K9 — element tangent matrices K_e = B^T J_D(u_q) B (Eq. 3) on
+// the FP64 tensor cores: the hex analogue of Table 1 (SURVEY
+// §8(f) NEXT-4). With the per-point linearisation of D (A = dFh/dgh, b = dFh/du)
+//   K_e = M^T N,  M[(d,q)][i] = d_d phi_i(x_q),  N[(d,q)][j] = sum_d' A_dd'(q) d_d' phi_j(x_q) + b_d(q) phi_j(x_q),
+// a (nd^3 x 3Q) x (3Q x nd^3) product per element, run as 8x8x4 DMMA tiles
+// (mma.sync m8n8k4 f64: sm_100a executes it on the same FP64 pipe as DFMA, at
+// 37 TF/s measured vs 32 TF/s for DFMA — tools/dmma_probe.cu).
+//   RES (integration-point AD, the paper's approach): A and b from 4 dual
+//       evaluations of D per point, then N from the tables.
+//   ELM (element-level forward AD): every column j of N from one dual
+//       evaluation of D per point seeded with (phi_j, grad phi_j) — nd^3 dual
+//       evaluations per point, the cost that grows with the element's DOFs. The
+//       seeds are B e_j read from the tables: a forward-mode tool would form them by
+//       pushing width-nd^3 duals through B (8 Q nd^6 more flops).
+// One CTA (8 warps) per element, persistent over a range of elements. M^T and the
+// 1D tables are element-independent and built once per CTA in shared memory.
+#include "common.cuh"
+#include "dual.cuh"
+#include "kernels.h"
+#include "physics.cuh"
+
+namespace feod {
+
+constexpr int kEmThreads = 256;
+
+FEOD_DEV void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int ND>
+struct EmShape {
+  static constexpr int NQ = ND, Q = ND * ND * ND, NN = ND * ND * ND;
+  static constexpr int NP = (NN + 7) / 8 * 8;          // padded node count (DMMA m, n)
+  static constexpr int KD = (3 * Q + 3) / 4 * 4;       // padded inner dimension (DMMA k)
+  static constexpr int MT = NP * KD;                   // M^T [i][k]
+  static constexpr int NM = KD * NP;                   // N [k][j]
+  static constexpr size_t SMEM = sizeof(double) * (MT + NM + 9 * Q + 4 * Q + NN + 2 * NQ * ND + 3 * NQ);
+};
+
+template <int ND, int MODEL, bool AFFINE, bool ELM>
+__global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P, const Tables T,
+                                                               const double* __restrict__ u, int e0, int ne,
+                                                               double* __restrict__ Ke) {
+  using S = EmShape<ND>;
+  constexpr int NQ = S::NQ, Q = S::Q, NN = S::NN, NP = S::NP, KD = S::KD;
+  constexpr int K = ND - 1;
+  extern __shared__ double sm[];
+  double* MTs = sm;                      // [NP][KD]
+  double* Ns = MTs + S::MT;              // [KD][NP]
+  double* PW = Ns + S::NM;               // [9][Q]: A (xx yy zz xy xz yz), b
+  double* UQ = PW + 9 * Q;               // [4][Q]: u, gh_x, gh_y, gh_z at the points
+  double* UE = UQ + 4 * Q;               // [NN] element DOFs
+  double* Bt = UE + NN;                  // [NQ][ND]
+  double* Gt = Bt + NQ * ND;             // [NQ][ND]
+  double* Wt = Gt + NQ * ND;             // [NQ]
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+
+  for (int t = tid; t < NQ * ND; t += kEmThreads) {
+    Bt[t] = T.B[t / ND][t % ND];
+    Gt[t] = T.G[t / ND][t % ND];
+  }
+  for (int t = tid; t < NQ; t += kEmThreads) Wt[t] = T.w[t];
+  __syncthreads();
+  // shape-function tables: phi_d(q, i) from the 1D tables (d = 0 value, 1..3 x y z derivative)
+  auto phi = [&](int d, int q, int i) {
+    const int qx = q % NQ, qy = (q / NQ) % NQ, qz = q / (NQ * NQ);
+    const int ia = i % ND, ib = (i / ND) % ND, ic = i / (ND * ND);
+    const double fx = d == 1 ? Gt[qx * ND + ia] : Bt[qx * ND + ia];
+    const double fy = d == 2 ? Gt[qy * ND + ib] : Bt[qy * ND + ib];
+    const double fz = d == 3 ? Gt[qz * ND + ic] : Bt[qz * ND + ic];
+    return fx * fy * fz;
+  };
+  for (int t = tid; t < S::MT; t += kEmThreads) {   // M^T[i][k], k = d Q + q (zero padded)
+    const int i = t / KD, k = t % KD;
+    MTs[t] = (i < NN && k < 3 * Q) ? phi(1 + k / Q, k % Q, i) : 0.0;
+  }
+  __syncthreads();
+
+  for (int e = e0 + blockIdx.x; e < e0 + ne; e += gridDim.x) {
+    const int ex = e % P.nx, ey = (e / P.nx) % P.ny, ez = e / (P.nx * P.ny);
+    // G: element DOFs
+    for (int t = tid; t < NN; t += kEmThreads) {
+      const int ia = t % ND, ib = (t / ND) % ND, ic = t / (ND * ND);
+      UE[t] = u[(int64_t)(K * ex + ia) + (int64_t)P.Mx * ((K * ey + ib) + (int64_t)P.My * (K * ez + ic))];
+    }
+    __syncthreads();
+    // B: value and reference gradient of u at the points
+    for (int t = tid; t < 4 * Q; t += kEmThreads) {
+      const int d = t / Q, q = t % Q;
+      double s = 0.0;
+      if (d == 0) {
+        for (int i = 0; i < NN; ++i) s = fma(phi(0, q, i), UE[i], s);
+      } else {
+        for (int i = 0; i < NN; ++i) s = fma(MTs[i * KD + (d - 1) * Q + q], UE[i], s);
+      }
+      UQ[t] = s;
+    }
+    __syncthreads();
+    const double rho = (MODEL == HEAT) ? P.rho[e] : 1.0;
+    auto metric = [&](int q, Metric& M, double& W) {
+      const int qx = q % NQ, qy = (q / NQ) % NQ, qz = q / (NQ * NQ);
+      const double wq = Wt[qx] * Wt[qy] * Wt[qz];
+      if constexpr (AFFINE) {
+        M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
+        W = wq * P.vol;
+      } else {
+        const double* g = P.geom + (int64_t)e * (6 * Q) + qz * 6 * NQ * NQ + qy * NQ + qx;
+        M = {g[0], g[NQ * NQ], g[2 * NQ * NQ], g[3 * NQ * NQ], g[4 * NQ * NQ], g[5 * NQ * NQ]};
+        const double det = M.xx * (M.yy * M.zz - M.yz * M.yz) - M.xy * (M.xy * M.zz - M.yz * M.xz) +
+                           M.xz * (M.xy * M.yz - M.yy * M.xz);
+        W = det / (wq * wq);
+      }
+    };
+    using D = dual<double>;
+    if constexpr (!ELM) {
+      // RES: D's linearisation at each point (A from e_x, e_y, e_z seeds; b from the u seed)
+      for (int q = tid; q < Q; q += kEmThreads) {
+        Metric M;
+        double W;
+        metric(q, M, W);
+        const D ud(UQ[q]);
+        D Fh[3];
+        double A[3][3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const D gh[3] = {D(UQ[Q + q], k == 0 ? 1.0 : 0.0), D(UQ[2 * Q + q], k == 1 ? 1.0 : 0.0),
+                           D(UQ[3 * Q + q], k == 2 ? 1.0 : 0.0)};
+          flux_hat<MODEL>(ud, gh, M, W, rho, P, Fh);
+#pragma unroll
+          for (int m = 0; m < 3; ++m) A[m][k] = Fh[m].d;
+        }
+        const D uu(UQ[q], 1.0);
+        const D gu[3] = {D(UQ[Q + q]), D(UQ[2 * Q + q]), D(UQ[3 * Q + q])};
+        flux_hat<MODEL>(uu, gu, M, W, rho, P, Fh);
+        PW[0 * Q + q] = A[0][0]; PW[1 * Q + q] = A[1][1]; PW[2 * Q + q] = A[2][2];
+        PW[3 * Q + q] = A[0][1]; PW[4 * Q + q] = A[0][2]; PW[5 * Q + q] = A[1][2];
+        PW[6 * Q + q] = Fh[0].d; PW[7 * Q + q] = Fh[1].d; PW[8 * Q + q] = Fh[2].d;
+      }
+      __syncthreads();
+      for (int t = tid; t < S::NM; t += kEmThreads) {   // N[k][j]
+        const int k = t / NP, j = t % NP;
+        double v = 0.0;
+        if (k < 3 * Q && j < NN) {
+          const int d = k / Q, q = k % Q;
+          const double g0 = MTs[j * KD + q], g1 = MTs[j * KD + Q + q], g2 = MTs[j * KD + 2 * Q + q],
+                       p0 = phi(0, q, j);
+          const int r0 = d == 0 ? 0 : (d == 1 ? 3 : 4), r1 = d == 0 ? 3 : (d == 1 ? 1 : 5),
+                    r2 = d == 0 ? 4 : (d == 1 ? 5 : 2);
+          v = PW[r0 * Q + q] * g0 + PW[r1 * Q + q] * g1 + PW[r2 * Q + q] * g2 + PW[(6 + d) * Q + q] * p0;
+        }
+        Ns[t] = v;
+      }
+    } else {
+      // ELM: column j of N from a dual evaluation of D seeded with (phi_j, grad phi_j)
+      for (int t = tid; t < Q * NP; t += kEmThreads) {
+        const int q = t / NP, j = t % NP;
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+        if (j < NN) {
+          Metric M;
+          double W;
+          metric(q, M, W);
+          const D ud(UQ[q], phi(0, q, j));
+          const D gh[3] = {D(UQ[Q + q], MTs[j * KD + q]), D(UQ[2 * Q + q], MTs[j * KD + Q + q]),
+                           D(UQ[3 * Q + q], MTs[j * KD + 2 * Q + q])};
+          D Fh[3];
+          flux_hat<MODEL>(ud, gh, M, W, rho, P, Fh);
+          c0 = Fh[0].d; c1 = Fh[1].d; c2 = Fh[2].d;
+        }
+        Ns[(0 * Q + q) * NP + j] = c0;
+        Ns[(1 * Q + q) * NP + j] = c1;
+        Ns[(2 * Q + q) * NP + j] = c2;
+      }
+      for (int t = tid; t < (KD - 3 * Q) * NP; t += kEmThreads) Ns[3 * Q * NP + t] = 0.0;
+    }
+    __syncthreads();
+    // K = M^T N on the tensor cores: 8x8 output tiles, k-steps of 4
+    constexpr int TR = NP / 8, NT = TR * TR;
+    double* Ko = Ke + (int64_t)(e - e0) * NN * NN;
+    for (int tile = warp; tile < NT; tile += kEmThreads / 32) {
+      const int r8 = (tile / TR) * 8, c8 = (tile % TR) * 8;
+      double d0 = 0.0, d1 = 0.0;
+      const double* ap = MTs + (r8 + (lane >> 2)) * KD + (lane & 3);
+      const double* bp = Ns + (lane & 3) * NP + c8 + (lane >> 2);
+#pragma unroll 4
+      for (int k0 = 0; k0 < KD; k0 += 4) dmma884(d0, d1, ap[k0], bp[k0 * NP]);
+      const int i = r8 + (lane >> 2), j = c8 + 2 * (lane & 3);
+      if (i < NN && j < NN) Ko[(int64_t)i * NN + j] = d0;
+      if (i < NN && j + 1 < NN) Ko[(int64_t)i * NN + j + 1] = d1;
+    }
+    __syncthreads();   // Ns / UQ / PW reused by the next element
+  }
+}
+
+template <int ND, int MODEL, bool AFFINE, bool ELM>
+static cudaError_t elemat_launch(const OpParams& P, const Tables& T, const double* u, int e0, int ne, double* Ke,
+                                 cudaStream_t st) {
+  constexpr size_t smem = EmShape<ND>::SMEM;
+  static int grid = 0;
+  if (grid == 0) {
+    cudaError_t e = cudaFuncSetAttribute(elemat_kernel<ND, MODEL, AFFINE, ELM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, occ = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elemat_kernel<ND, MODEL, AFFINE, ELM>, kEmThreads,
+                                                           smem)) != cudaSuccess)
+      return e;
+    grid = sms * (occ > 0 ? occ : 1);
+  }
+  const int g = ne < grid ? ne : grid;
+  if (g <= 0) return cudaSuccess;
+  elemat_kernel<ND, MODEL, AFFINE, ELM><<<g, kEmThreads, smem, st>>>(P, T, u, e0, ne, Ke);
+  return cudaGetLastError();
+}
+
+template <int ND, int MODEL>
+static cudaError_t elemat_model(bool affine, bool elm, const OpParams& P, const Tables& T, const double* u, int e0,
+                                int ne, double* Ke, cudaStream_t st) {
+  if (affine) return elm ? elemat_launch<ND, MODEL, true, true>(P, T, u, e0, ne, Ke, st)
+                         : elemat_launch<ND, MODEL, true, false>(P, T, u, e0, ne, Ke, st);
+  return elm ? elemat_launch<ND, MODEL, false, true>(P, T, u, e0, ne, Ke, st)
+             : elemat_launch<ND, MODEL, false, false>(P, T, u, e0, ne, Ke, st);
+}
+
+template <int ND>
+static cudaError_t elemat_nd_t(int model, bool affine, bool elm, const OpParams& P, const Tables& T, const double* u,
+                               int e0, int ne, double* Ke, cudaStream_t st) {
+  switch (model) {
+    case PLAPLACE: return elemat_model<ND, PLAPLACE>(affine, elm, P, T, u, e0, ne, Ke, st);
+    case NLDIFF: return elemat_model<ND, NLDIFF>(affine, elm, P, T, u, e0, ne, Ke, st);
+    case HEAT: return elemat_model<ND, HEAT>(affine, elm, P, T, u, e0, ne, Ke, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t element_matrices_nd(int nd, int model, bool affine, bool elm, const OpParams& P, const Tables& T,
+                                const double* u, int e0, int ne, double* Ke, cudaStream_t st) {
+  switch (nd) {
+    case 2: return elemat_nd_t<2>(model, affine, elm, P, T, u, e0, ne, Ke, st);
+    case 3: return elemat_nd_t<3>(model, affine, elm, P, T, u, e0, ne, Ke, st);
+    case 4: return elemat_nd_t<4>(model, affine, elm, P, T, u, e0, ne, Ke, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+}  // namespace feod

@@ -91,3 +91,20 @@ def test_jacobi_diag_parity(w, n):
     op.linearize(cuda(d["u"]))
     got = host(op.jacobi_diag())
     assert rel_l2(got, O.jacobi_diag(pr, d["u"])) <= TOL
+
+
+EM_CASES = [(W.C1, 3), (W.C2, 5), (W.C3, 3), (W.C5, 3)]
+
+
+@pytest.mark.parametrize("elm", [False, True], ids=["RES", "ELM"])
+@pytest.mark.parametrize("w,n", EM_CASES, ids=[f"{w.name}n{n}" for w, n in EM_CASES])
+def test_element_matrices_parity(w, n, elm):
+    """NEXT-4 (Table-1 analogue): element tangents K_e = B^T J_D B on the FP64 tensor
+    cores, RES and ELM, against the oracle's Eq. 3 element tangents."""
+    ww, d = _case(w, n)
+    pr, op = problem(ww, d), operator(ww, d)
+    E = ww.n_elems
+    e0, ne = (1, E - 2) if E > 4 else (0, E)
+    got = host(op.element_matrices(cuda(d["u"]), e0, ne, elm=elm))
+    ref = O.element_tangent(pr, d["u"], np.arange(e0, e0 + ne))
+    assert rel_l2(got.ravel(), ref.ravel()) <= TOL
