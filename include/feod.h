@@ -171,7 +171,10 @@ FEOD_API int feod_design_grad(feod_handle h, const double* u, const double* lamb
 /* Same operations on HOST buffers: copies host->device, computes, copies
  * device->host and synchronises the stream before returning (the e2e path).
  * op: 0 residual(in0=u, out=r), 1 jvp(in0=u, in1=v, out=Jv),
- *     2 design_grad(in0=u, in1=lambda, out=g), 3 vjp(in0=u, in1=w, out=JTw).
+ *     2 design_grad(in0=u, in1=lambda, out=g), 3 vjp(in0=u, in1=w, out=JTw),
+ *     4 residual + jvp (in0=u, in1=v, out = [r | Jv], 2N doubles): the upload
+ *       of v overlaps the residual and the download of r overlaps the JVP
+ *       (a second, library-owned copy stream).
  * Host memory should be pinned. */
 FEOD_API int feod_apply_host(feod_handle h, int op, const double* in0, const double* in1, double* out);
 

@@ -247,7 +247,7 @@ class Operator:
     def apply_host(self, op, in0, in1=None, out=None):
         """Host-buffer path (feod_apply_host): H2D, compute, D2H, synchronise."""
         t = self._torch
-        n_out = self.n_elems if op == 2 else self.n_dofs
+        n_out = self.n_elems if op == 2 else (2 * self.n_dofs if op == 4 else self.n_dofs)
         a = in0 if isinstance(in0, t.Tensor) else t.as_tensor(np.asarray(in0, np.float64))
         b = None if in1 is None else (in1 if isinstance(in1, t.Tensor) else t.as_tensor(np.asarray(in1, np.float64)))
         for x, name in ((a, "in0"), (b, "in1")):

@@ -25,7 +25,10 @@ struct feod_op {
   int64_t N, E;
   double* geom = nullptr;
   double* shell = nullptr;     // 2 x nbricks x shell
-  double* stage = nullptr;     // host-API staging: 3 x max(N, E)
+  double* stage = nullptr;     // host-API staging: 4 x max(N, E)
+  cudaStream_t cst = nullptr;  // host-API upload stream (op 4 overlaps copies with the operator)
+  cudaStream_t dst = nullptr;  // host-API download stream (runs against the uploads: full duplex)
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double* red = nullptr;       // kRedBlocks partials, 24 scalars, kRedBlocks partials
   int* flag = nullptr;
   unsigned long long* sched = nullptr;   // dynamic brick scheduling ticket counter
@@ -65,6 +68,10 @@ static void free_all(feod_op* h) {
   cudaFree(h->geom);
   cudaFree(h->shell);
   cudaFree(h->stage);
+  for (cudaEvent_t& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->cst) cudaStreamDestroy(h->cst);
+  if (h->dst) cudaStreamDestroy(h->dst);
   cudaFree(h->red);
   cudaFree(h->flag);
   cudaFree(h->sched);
@@ -416,15 +423,47 @@ extern "C" int feod_design_grad(feod_handle h, const double* u, const double* la
 
 extern "C" int feod_apply_host(feod_handle h, int op, const double* in0, const double* in1, double* out) {
   if (!h || !in0 || !out || (op != 0 && !in1)) return fail(FEOD_EINVAL, "feod_apply_host: null argument");
-  if (op < 0 || op > 3) return fail(FEOD_EINVAL, "feod_apply_host: op must be 0, 1, 2 or 3");
+  if (op < 0 || op > 4) return fail(FEOD_EINVAL, "feod_apply_host: op must be 0 .. 4");
   const int64_t len = h->N > h->E ? h->N : h->E;
-  if (!h->stage && cudaMalloc(&h->stage, sizeof(double) * 3 * (size_t)len) != cudaSuccess) {
+  if (!h->stage && cudaMalloc(&h->stage, sizeof(double) * 4 * (size_t)len) != cudaSuccess) {
     h->stage = nullptr;
     return fail(FEOD_ENOMEM, "feod_apply_host: staging buffers");
   }
   double* d0 = h->stage;
   double* d1 = h->stage + len;
   double* d2 = h->stage + 2 * len;
+  if (op == 4) {
+    // r = F(u) and Jv = J(u) v with the copies on two more streams: v's upload
+    // overlaps the residual and r's download (opposite direction), which in turn
+    // overlaps the JVP
+    double* d3 = h->stage + 3 * len;
+    const size_t bytes = sizeof(double) * (size_t)h->N;
+    if (!h->cst) {
+      CK(cudaStreamCreateWithFlags(&h->cst, cudaStreamNonBlocking), "feod_apply_host: stream");
+      CK(cudaStreamCreateWithFlags(&h->dst, cudaStreamNonBlocking), "feod_apply_host: stream");
+      for (cudaEvent_t& e : h->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "feod_apply_host: event");
+    }
+    CK(cudaEventRecord(h->ev[3], h->st), "feod_apply_host");        // earlier work on the handle's stream
+    CK(cudaStreamWaitEvent(h->cst, h->ev[3], 0), "feod_apply_host");
+    CK(cudaMemcpyAsync(d0, in0, bytes, cudaMemcpyHostToDevice, h->cst), "feod_apply_host: H2D");
+    CK(cudaEventRecord(h->ev[0], h->cst), "feod_apply_host");
+    CK(cudaMemcpyAsync(d1, in1, bytes, cudaMemcpyHostToDevice, h->cst), "feod_apply_host: H2D");
+    CK(cudaEventRecord(h->ev[1], h->cst), "feod_apply_host");
+    CK(cudaStreamWaitEvent(h->st, h->ev[0], 0), "feod_apply_host");
+    int rc = feod_residual(h, d0, d2);
+    if (rc != FEOD_OK) return rc;
+    CK(cudaEventRecord(h->ev[2], h->st), "feod_apply_host");
+    CK(cudaStreamWaitEvent(h->st, h->ev[1], 0), "feod_apply_host");
+    rc = feod_jvp(h, d0, d1, d3);
+    if (rc != FEOD_OK) return rc;
+    CK(cudaStreamWaitEvent(h->dst, h->ev[2], 0), "feod_apply_host");
+    CK(cudaMemcpyAsync(out, d2, bytes, cudaMemcpyDeviceToHost, h->dst), "feod_apply_host: D2H");   // against v's upload
+    CK(cudaMemcpyAsync(out + h->N, d3, bytes, cudaMemcpyDeviceToHost, h->st), "feod_apply_host: D2H");
+    CK(cudaStreamSynchronize(h->st), "feod_apply_host: sync");
+    CK(cudaStreamSynchronize(h->cst), "feod_apply_host: sync");
+    CK(cudaStreamSynchronize(h->dst), "feod_apply_host: sync");
+    return FEOD_OK;
+  }
   CK(cudaMemcpyAsync(d0, in0, sizeof(double) * h->N, cudaMemcpyHostToDevice, h->st), "feod_apply_host: H2D");
   if (op != 0) CK(cudaMemcpyAsync(d1, in1, sizeof(double) * h->N, cudaMemcpyHostToDevice, h->st), "feod_apply_host: H2D");
   int rc = op == 0 ? feod_residual(h, d0, d2)

@@ -98,6 +98,10 @@ def test_host_buffer_path_matches_device():
     uh, vh = torch.as_tensor(d["u"]).pin_memory(), torch.as_tensor(d["v"]).pin_memory()
     assert torch.equal(op.apply_host(0, uh), op.residual(uh.cuda()).cpu())
     assert torch.equal(op.apply_host(1, uh, vh), op.jvp(uh.cuda(), vh.cuda()).cpu())
+    rj = op.apply_host(4, uh, vh)   # residual + JVP with overlapped copies
+    n = op.n_dofs
+    assert torch.equal(rj[:n], op.residual(uh.cuda()).cpu())
+    assert torch.equal(rj[n:], op.jvp(uh.cuda(), vh.cuda()).cpu())
 
 
 def test_error_paths():
