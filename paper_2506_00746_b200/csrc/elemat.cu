@@ -116,43 +116,46 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
     };
     using D = dual<double>;
     if constexpr (!ELM) {
-      // RES: D's linearisation at each point (A from e_x, e_y, e_z seeds; b from the u seed)
-      for (int q = tid; q < Q; q += kEmThreads) {
+      // RES: D's linearisation at each point, one dual evaluation per thread: seed s = 0..2
+      // along e_s gives column s of A (the upper triangle is kept), s = 3 along u gives b
+      for (int t = tid; t < 4 * Q; t += kEmThreads) {
+        const int q = t >> 2, sd = t & 3;
         Metric M;
         double W;
         metric(q, M, W);
-        const D ud(UQ[q]);
+        const D ud(UQ[q], sd == 3 ? 1.0 : 0.0);
+        const D gh[3] = {D(UQ[Q + q], sd == 0 ? 1.0 : 0.0), D(UQ[2 * Q + q], sd == 1 ? 1.0 : 0.0),
+                         D(UQ[3 * Q + q], sd == 2 ? 1.0 : 0.0)};
         D Fh[3];
-        double A[3][3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const D gh[3] = {D(UQ[Q + q], k == 0 ? 1.0 : 0.0), D(UQ[2 * Q + q], k == 1 ? 1.0 : 0.0),
-                           D(UQ[3 * Q + q], k == 2 ? 1.0 : 0.0)};
-          flux_hat<MODEL>(ud, gh, M, W, rho, P, Fh);
-#pragma unroll
-          for (int m = 0; m < 3; ++m) A[m][k] = Fh[m].d;
+        flux_hat<MODEL>(ud, gh, M, W, rho, P, Fh);
+        if (sd == 0) {
+          PW[0 * Q + q] = Fh[0].d;                                   // xx
+        } else if (sd == 1) {
+          PW[1 * Q + q] = Fh[1].d; PW[3 * Q + q] = Fh[0].d;          // yy, xy
+        } else if (sd == 2) {
+          PW[2 * Q + q] = Fh[2].d; PW[4 * Q + q] = Fh[0].d; PW[5 * Q + q] = Fh[1].d;   // zz, xz, yz
+        } else {
+          PW[6 * Q + q] = Fh[0].d; PW[7 * Q + q] = Fh[1].d; PW[8 * Q + q] = Fh[2].d;   // b
         }
-        const D uu(UQ[q], 1.0);
-        const D gu[3] = {D(UQ[Q + q]), D(UQ[2 * Q + q]), D(UQ[3 * Q + q])};
-        flux_hat<MODEL>(uu, gu, M, W, rho, P, Fh);
-        PW[0 * Q + q] = A[0][0]; PW[1 * Q + q] = A[1][1]; PW[2 * Q + q] = A[2][2];
-        PW[3 * Q + q] = A[0][1]; PW[4 * Q + q] = A[0][2]; PW[5 * Q + q] = A[1][2];
-        PW[6 * Q + q] = Fh[0].d; PW[7 * Q + q] = Fh[1].d; PW[8 * Q + q] = Fh[2].d;
       }
       __syncthreads();
-      for (int t = tid; t < S::NM; t += kEmThreads) {   // N[k][j]
-        const int k = t / NP, j = t % NP;
-        double v = 0.0;
-        if (k < 3 * Q && j < NN) {
-          const int d = k / Q, q = k % Q;
+      for (int t = tid; t < Q * NP; t += kEmThreads) {   // N[(d, q)][j], the three d rows per thread
+        const int q = t / NP, j = t % NP;
+        double n0 = 0.0, n1 = 0.0, n2 = 0.0;
+        if (j < NN) {
           const double g0 = MTs[j * KD + q], g1 = MTs[j * KD + Q + q], g2 = MTs[j * KD + 2 * Q + q],
                        p0 = phi(0, q, j);
-          const int r0 = d == 0 ? 0 : (d == 1 ? 3 : 4), r1 = d == 0 ? 3 : (d == 1 ? 1 : 5),
-                    r2 = d == 0 ? 4 : (d == 1 ? 5 : 2);
-          v = PW[r0 * Q + q] * g0 + PW[r1 * Q + q] * g1 + PW[r2 * Q + q] * g2 + PW[(6 + d) * Q + q] * p0;
+          const double axx = PW[q], ayy = PW[Q + q], azz = PW[2 * Q + q], axy = PW[3 * Q + q], axz = PW[4 * Q + q],
+                       ayz = PW[5 * Q + q];
+          n0 = axx * g0 + axy * g1 + axz * g2 + PW[6 * Q + q] * p0;
+          n1 = axy * g0 + ayy * g1 + ayz * g2 + PW[7 * Q + q] * p0;
+          n2 = axz * g0 + ayz * g1 + azz * g2 + PW[8 * Q + q] * p0;
         }
-        Ns[t] = v;
+        Ns[(0 * Q + q) * NP + j] = n0;
+        Ns[(1 * Q + q) * NP + j] = n1;
+        Ns[(2 * Q + q) * NP + j] = n2;
       }
+      for (int t = tid; t < (KD - 3 * Q) * NP; t += kEmThreads) Ns[3 * Q * NP + t] = 0.0;
     } else {
       // ELM: column j of N from a dual evaluation of D seeded with (phi_j, grad phi_j)
       for (int t = tid; t < Q * NP; t += kEmThreads) {
@@ -176,19 +179,30 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
       for (int t = tid; t < (KD - 3 * Q) * NP; t += kEmThreads) Ns[3 * Q * NP + t] = 0.0;
     }
     __syncthreads();
-    // K = M^T N on the tensor cores: 8x8 output tiles, k-steps of 4
-    constexpr int TR = NP / 8, NT = TR * TR;
+    // K = M^T N on the tensor cores: a warp owns one 8-row strip and all TR column
+    // tiles (TR independent accumulator chains; one A fragment per k-step reused TR times)
+    constexpr int TR = NP / 8;
     double* Ko = Ke + (int64_t)(e - e0) * NN * NN;
-    for (int tile = warp; tile < NT; tile += kEmThreads / 32) {
-      const int r8 = (tile / TR) * 8, c8 = (tile % TR) * 8;
-      double d0 = 0.0, d1 = 0.0;
+    for (int rt = warp; rt < TR; rt += kEmThreads / 32) {
+      const int r8 = rt * 8;
+      double acc[TR][2];
+#pragma unroll
+      for (int c = 0; c < TR; ++c) acc[c][0] = acc[c][1] = 0.0;
       const double* ap = MTs + (r8 + (lane >> 2)) * KD + (lane & 3);
-      const double* bp = Ns + (lane & 3) * NP + c8 + (lane >> 2);
-#pragma unroll 4
-      for (int k0 = 0; k0 < KD; k0 += 4) dmma884(d0, d1, ap[k0], bp[k0 * NP]);
-      const int i = r8 + (lane >> 2), j = c8 + 2 * (lane & 3);
-      if (i < NN && j < NN) Ko[(int64_t)i * NN + j] = d0;
-      if (i < NN && j + 1 < NN) Ko[(int64_t)i * NN + j + 1] = d1;
+      const double* bp = Ns + (lane & 3) * NP + (lane >> 2);
+#pragma unroll 2
+      for (int k0 = 0; k0 < KD; k0 += 4) {
+        const double a = ap[k0];
+#pragma unroll
+        for (int c = 0; c < TR; ++c) dmma884(acc[c][0], acc[c][1], a, bp[k0 * NP + 8 * c]);
+      }
+      const int i = r8 + (lane >> 2);
+#pragma unroll
+      for (int c = 0; c < TR; ++c) {
+        const int j = 8 * c + 2 * (lane & 3);
+        if (i < NN && j < NN) Ko[(int64_t)i * NN + j] = acc[c][0];
+        if (i < NN && j + 1 < NN) Ko[(int64_t)i * NN + j + 1] = acc[c][1];
+      }
     }
     __syncthreads();   // Ns / UQ / PW reused by the next element
   }
