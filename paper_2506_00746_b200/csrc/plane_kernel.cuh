@@ -39,6 +39,9 @@
 #include <cstdio>
 #endif
 
+#ifndef FEOD_NCH3_MIN
+#define FEOD_NCH3_MIN 6   // orders (ND) from which the exchange carries 3 channels
+#endif
 #ifndef FEOD_PDL_OPERATOR
 #define FEOD_PDL_OPERATOR 1
 #endif
@@ -153,7 +156,8 @@ struct PShape {
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
   // exchange channels: 2 ([W | Wy], x-derivative collocated over the lane group,
   // fewer FLOPs) up to Q4; 3 ([W | Wx | Wy], no cross-lane traffic) for Q5/Q6
-  static constexpr int NCH = ND >= 6 ? 3 : 2;
+  // (Q3 residual: 3 channels measured 1-2 % faster, the Q3 two-field modes 2 channels)
+  static constexpr int NCH = (ND >= FEOD_NCH3_MIN || (ND == 4 && MODE == MODE_RES)) ? 3 : 2;
   static constexpr XbPad XP = xb_pad(ND, NIN, NCH);
   static constexpr int SI = XP.SI, SJ = XP.SJ, SE = XP.SE, SF = ND * SJ;
   // element buffer (compute -> IO), per layer parity and output: [EL][b][a][c]
