@@ -171,3 +171,30 @@ def test_vjp_adjoint_identity_fullsize(name):
     mask = cuda(W.dirichlet_dofs(w.n, w.k, w.faces).astype(np.float64))
     a2 = a + 5.0 * mask
     assert torch.equal(op.vjp(u, a2), JTa)
+
+
+def test_two_handles_on_concurrent_streams_are_bitwise_reproducible():
+    """Two operators driven concurrently on two CUDA streams (per-handle ticket counters,
+    brick epochs and programmatic dependent launches must not interact) give bitwise
+    the results of the same calls run one after the other."""
+    import torch
+    import paper_2506_00746_b200 as fe
+    cases = []
+    for w, n in ((W.C3, 18), (W.C5, 17)):
+        ww = w.resized(n)
+        d = W.draw(ww)
+        rho = torch.as_tensor(d["rho"]).cuda() if "rho" in d else None
+        op = fe.from_workload(ww, verts=d["verts"], rho=rho)
+        cases.append((op, cuda(d["u"]), cuda(d["v"])))
+    ref = [(op.residual(u).clone(), op.jvp(u, v).clone(), op.vjp(u, v).clone()) for op, u, v in cases]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[], []]
+    for _ in range(6):
+        for k, (op, u, v) in enumerate(cases):
+            with torch.cuda.stream(streams[k]):
+                outs[k].append((op.residual(u), op.jvp(u, v), op.vjp(u, v)))
+    torch.cuda.synchronize()
+    for k in range(2):
+        for r, j, t in outs[k]:
+            assert torch.equal(r, ref[k][0]) and torch.equal(j, ref[k][1]) and torch.equal(t, ref[k][2])
