@@ -22,6 +22,14 @@
 namespace feod {
 
 constexpr int kEmThreads = 256;
+// M^T as a shared-memory table (Q1, Q2: measured faster) or rebuilt from the 1D tables
+// where used (Q3: the 96 KB table would leave one CTA per SM; without it, two —
+// RES 169 -> 123 ns/element); FEOD_EM_MT = 0 / 1 forces either for experiments
+#ifndef FEOD_EM_MT
+#define FEOD_EM_MT -1
+#endif
+template <int ND>
+constexpr bool em_table() { return FEOD_EM_MT >= 0 ? FEOD_EM_MT == 1 : ND <= 3; }
 
 FEOD_DEV void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -34,7 +42,7 @@ struct EmShape {
   static constexpr int NQ = ND, Q = ND * ND * ND, NN = ND * ND * ND;
   static constexpr int NP = (NN + 7) / 8 * 8;          // padded node count (DMMA m, n)
   static constexpr int KD = (3 * Q + 3) / 4 * 4;       // padded inner dimension (DMMA k)
-  static constexpr int MT = NP * KD;                   // M^T [i][k]
+  static constexpr int MT = em_table<ND>() ? NP * KD : 0;   // M^T [i][k]
   static constexpr int NM = KD * NP;                   // N [k][j]
   static constexpr size_t SMEM = sizeof(double) * (MT + NM + 9 * Q + 4 * Q + NN + 2 * NQ * ND + 3 * NQ);
 };
@@ -73,7 +81,12 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
     const double fz = d == 3 ? Gt[qz * ND + ic] : Bt[qz * ND + ic];
     return fx * fy * fz;
   };
-  for (int t = tid; t < S::MT; t += kEmThreads) {   // M^T[i][k], k = d Q + q (zero padded)
+  // M^T[i][k] = d_{k / Q} phi_i(x_{k % Q}), zero padded
+  auto mt = [&](int i, int k) {
+    if constexpr (em_table<ND>()) return MTs[i * KD + k];
+    else return (i < NN && k < 3 * Q) ? phi(1 + k / Q, k % Q, i) : 0.0;
+  };
+  for (int t = tid; t < S::MT; t += kEmThreads) {
     const int i = t / KD, k = t % KD;
     MTs[t] = (i < NN && k < 3 * Q) ? phi(1 + k / Q, k % Q, i) : 0.0;
   }
@@ -94,7 +107,7 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
       if (d == 0) {
         for (int i = 0; i < NN; ++i) s = fma(phi(0, q, i), UE[i], s);
       } else {
-        for (int i = 0; i < NN; ++i) s = fma(MTs[i * KD + (d - 1) * Q + q], UE[i], s);
+        for (int i = 0; i < NN; ++i) s = fma(mt(i, (d - 1) * Q + q), UE[i], s);
       }
       UQ[t] = s;
     }
@@ -143,8 +156,7 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
         const int q = t / NP, j = t % NP;
         double n0 = 0.0, n1 = 0.0, n2 = 0.0;
         if (j < NN) {
-          const double g0 = MTs[j * KD + q], g1 = MTs[j * KD + Q + q], g2 = MTs[j * KD + 2 * Q + q],
-                       p0 = phi(0, q, j);
+          const double g0 = mt(j, q), g1 = mt(j, Q + q), g2 = mt(j, 2 * Q + q), p0 = phi(0, q, j);
           const double axx = PW[q], ayy = PW[Q + q], azz = PW[2 * Q + q], axy = PW[3 * Q + q], axz = PW[4 * Q + q],
                        ayz = PW[5 * Q + q];
           n0 = axx * g0 + axy * g1 + axz * g2 + PW[6 * Q + q] * p0;
@@ -166,8 +178,7 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
           double W;
           metric(q, M, W);
           const D ud(UQ[q], phi(0, q, j));
-          const D gh[3] = {D(UQ[Q + q], MTs[j * KD + q]), D(UQ[2 * Q + q], MTs[j * KD + Q + q]),
-                           D(UQ[3 * Q + q], MTs[j * KD + 2 * Q + q])};
+          const D gh[3] = {D(UQ[Q + q], mt(j, q)), D(UQ[2 * Q + q], mt(j, Q + q)), D(UQ[3 * Q + q], mt(j, 2 * Q + q))};
           D Fh[3];
           flux_hat<MODEL>(ud, gh, M, W, rho, P, Fh);
           c0 = Fh[0].d; c1 = Fh[1].d; c2 = Fh[2].d;
@@ -188,11 +199,11 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
       double acc[TR][2];
 #pragma unroll
       for (int c = 0; c < TR; ++c) acc[c][0] = acc[c][1] = 0.0;
-      const double* ap = MTs + (r8 + (lane >> 2)) * KD + (lane & 3);
+      const int ai = r8 + (lane >> 2);
       const double* bp = Ns + (lane & 3) * NP + (lane >> 2);
 #pragma unroll 2
       for (int k0 = 0; k0 < KD; k0 += 4) {
-        const double a = ap[k0];
+        const double a = mt(ai, k0 + (lane & 3));
 #pragma unroll
         for (int c = 0; c < TR; ++c) dmma884(acc[c][0], acc[c][1], a, bp[k0 * NP + 8 * c]);
       }
