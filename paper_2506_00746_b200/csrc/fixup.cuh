@@ -27,6 +27,9 @@
 namespace feod {
 
 constexpr int kFixMaxThreads = 256;
+#ifndef FEOD_FIX_SLEEP_NS
+#define FEOD_FIX_SLEEP_NS 200   // back-off of a row waiting for its bricks
+#endif
 
 // box extent of brick b along an axis (the last brick may be ragged)
 template <int K, int B>
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P,
     for (int d = threadIdx.x; d < cnt; d += blockDim.x) {
       const int ix = d % cx, iy = (d / cx) % cy, iz = d / (cx * cy);
       const unsigned long long* f = P.bdone + ((x0 + ix) + (int64_t)P.nbx * ((y0 + iy) + (int64_t)P.nby * (z0 + iz)));
-      while (ld_acquire_u64(f) < epoch) __nanosleep(200);
+      while (ld_acquire_u64(f) < epoch) __nanosleep(FEOD_FIX_SLEEP_NS);
     }
     __syncthreads();
   }

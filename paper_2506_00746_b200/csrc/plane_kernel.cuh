@@ -39,6 +39,9 @@
 #include <cstdio>
 #endif
 
+#ifndef FEOD_PREFETCH
+#define FEOD_PREFETCH 1
+#endif
 #ifndef FEOD_NCH3_MIN
 #define FEOD_NCH3_MIN 6   // orders (ND) from which the exchange carries 3 channels
 #endif
@@ -640,9 +643,16 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       for (int r = 0; r < MPD; ++r)
 #pragma unroll
         for (int c = 0; c < NSV; ++c) mnext[r][c] = r < NQ ? ld_stream(gm + r * NSV * NQ2 + c * NQ2) : 0.0;
-      if (tid < byr && z + 1 < bzr) {   // L2 prefetch of the next layer's stream, one x-row of elements per y
-        const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + tid) + (int64_t)P.ny * (ez0 + z + 1));
-        prefetch_l2(sb + e1 * (NSV * NQ3), (uint32_t)(bxr * NSV * NQ3 * sizeof(double)));
+      // L2 prefetch of the stream FEOD_PREFETCH layers ahead (the first layer of a brick
+      // also requests the layers in between), one x-row of elements per y
+      if (FEOD_PREFETCH > 0 && tid < byr) {
+#pragma unroll
+        for (int a = (z == 0 ? 1 : FEOD_PREFETCH); a <= FEOD_PREFETCH; ++a) {
+          if (z + a < bzr) {
+            const int64_t e1 = (int64_t)ex0 + (int64_t)P.nx * ((ey0 + tid) + (int64_t)P.ny * (ez0 + z + a));
+            prefetch_l2(sb + e1 * (NSV * NQ3), (uint32_t)(bxr * NSV * NQ3 * sizeof(double)));
+          }
+        }
       }
     }
     double rho_e = 0.0;
