@@ -57,7 +57,13 @@
 namespace feod {
 
 template <int ND> struct PlaneTile;
-template <> struct PlaneTile<2> { static constexpr int BX = 8, BY = 4, BZ = 16; };
+#ifndef FEOD_Q1_BX
+#define FEOD_Q1_BX 8
+#endif
+#ifndef FEOD_Q1_BY
+#define FEOD_Q1_BY 4
+#endif
+template <> struct PlaneTile<2> { static constexpr int BX = FEOD_Q1_BX, BY = FEOD_Q1_BY, BZ = 16; };
 template <> struct PlaneTile<3> { static constexpr int BX = 4, BY = 3, BZ = 16; };
 template <> struct PlaneTile<4> { static constexpr int BX = 4, BY = 2, BZ = 16; };
 template <> struct PlaneTile<5> { static constexpr int BX = 4, BY = 2, BZ = 8; };
