@@ -153,7 +153,8 @@ struct PShape {
                                             MODE == MODE_PAJVP)) ||
                                (ND == 3 && (MODE == MODE_JVP || MODE == MODE_JVPRES || MODE == MODE_PAJVP));
   static constexpr int MINB = FEOD_MINB_OVERRIDE > 0 ? FEOD_MINB_OVERRIDE
-                              : (ND >= 6 && (MODE == MODE_JVP || MODE == MODE_JVPRES || MODE == MODE_VJP))
+                              : (ND >= 6 && (MODE == MODE_JVP || MODE == MODE_JVPRES || MODE == MODE_VJP ||
+                                             MODE == MODE_PAJVP))   // PAJVP: C4 jvp_lin 413 -> 358 us
                                     ? 1
                               : LEAN ? 4
                                      : ((65536 / (NT * 128)) < 1 ? 1 : (65536 / (NT * 128)));
