@@ -39,6 +39,9 @@
 #include <cstdio>
 #endif
 
+#ifndef FEOD_Q2_LEAN_MORE
+#define FEOD_Q2_LEAN_MORE 0
+#endif
 #ifndef FEOD_PREFETCH
 #define FEOD_PREFETCH 1
 #endif
@@ -151,7 +154,8 @@ struct PShape {
   // C5 JVP -2 %) for the modes that fit without spills
   static constexpr bool LEAN = (ND == 2 && (MODE == MODE_RES || MODE == MODE_JVP || MODE == MODE_JVPRES ||
                                             MODE == MODE_PAJVP)) ||
-                               (ND == 3 && (MODE == MODE_JVP || MODE == MODE_JVPRES || MODE == MODE_PAJVP));
+                               (ND == 3 && (MODE == MODE_JVP || MODE == MODE_JVPRES || MODE == MODE_PAJVP ||
+                                            (FEOD_Q2_LEAN_MORE && (MODE == MODE_DESIGN || MODE == MODE_VJP))));
   static constexpr int MINB = FEOD_MINB_OVERRIDE > 0 ? FEOD_MINB_OVERRIDE
                               : (ND >= 6 && (MODE == MODE_JVP || MODE == MODE_JVPRES || MODE == MODE_VJP ||
                                              MODE == MODE_PAJVP))   // PAJVP: C4 jvp_lin 413 -> 358 us
