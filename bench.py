@@ -168,6 +168,17 @@ def cpu_oracle_sample(w, d, target_s=15.0, S=None):
     return value, cores, sample, t
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args, w):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -188,7 +199,8 @@ def run_reference(args, w):
             "ms_per_step": 2 * w.n_dofs / (value * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(w),
-            "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -306,6 +318,21 @@ def main():
         return a.elapsed_time(b) / reps
     t_res = time_call(lambda: op.residual(u, out=r))
     t_jvp = time_call(lambda: op.jvp(u, v, out=Jv))
+
+    def each_call(fn, reps=20):
+        """R calls each bracketed by events on the stream -> (median, min) in ms."""
+        fn()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a_, b_ in evs:
+            a_.record(stream)
+            fn()
+            b_.record(stream)
+        torch.cuda.synchronize()
+        ts = [a_.elapsed_time(b_) for a_, b_ in evs]
+        return statistics.median(ts), min(ts)
+    res_med, res_min = each_call(lambda: op.residual(u, out=r))
+    jvp_med, jvp_min = each_call(lambda: op.jvp(u, v, out=Jv))
     JTw = torch.empty_like(u)
     t_vjp = time_call(lambda: op.vjp(u, v, out=JTw))   # NEXT-1 (diagnostic, not in the step)
     # NEXT-2 stored linearisation: one linearize (F(u) + D's linearisation) then J v from it
@@ -359,7 +386,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         val, cores, sample, _ = cpu_oracle_sample(w, d)
-        cpu = {"value": val, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = {"value": val, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "sample": sample,
+               "cpu_model": cpu_model()}
 
     fl_res, fl_jvp = algorithmic_flops(w, "residual"), algorithmic_flops(w, "jvp")
     by_res, by_jvp = algorithmic_bytes(w, "residual"), algorithmic_bytes(w, "jvp")
@@ -371,10 +399,12 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
             "gpu_launches": args.steps * 4,   # per call: the fused plane_kernel + the brick-face fixup_kernel
             "calls": {
-                "residual": {"us": t_res * 1e3, "gdof_s": N / (t_res * 1e-3) / 1e9,
+                "residual": {"us": t_res * 1e3, "us_median": res_med * 1e3, "us_min": res_min * 1e3,
+                             "gdof_s": N / (t_res * 1e-3) / 1e9,
                              "hbm_frac": by_res / (t_res * 1e-3) / 1e9 / peak,
                              "fp64_frac": fl_res / (t_res * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS},
-                "jvp": {"us": t_jvp * 1e3, "gdof_s": N / (t_jvp * 1e-3) / 1e9,
+                "jvp": {"us": t_jvp * 1e3, "us_median": jvp_med * 1e3, "us_min": jvp_min * 1e3,
+                        "gdof_s": N / (t_jvp * 1e-3) / 1e9,
                         "hbm_frac": by_jvp / (t_jvp * 1e-3) / 1e9 / peak,
                         "fp64_frac": fl_jvp / (t_jvp * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS,
                         "fused_kernel_us": jvp_kernel_ms * 1e3},
