@@ -334,7 +334,11 @@ def main():
     res_med, res_min = each_call(lambda: op.residual(u, out=r))
     jvp_med, jvp_min = each_call(lambda: op.jvp(u, v, out=Jv))
     JTw = torch.empty_like(u)
+    JTw_buf = torch.empty_like(u)
     t_vjp = time_call(lambda: op.vjp(u, v, out=JTw))   # NEXT-1 (diagnostic, not in the step)
+    # the fused entry point of SURVEY §8(b): r and J v from one dual pass (feod_jvp_res)
+    r2 = torch.empty_like(u)
+    t_jres = time_call(lambda: op.jvp_res(u, v, out=(r2, JTw_buf)))
     # NEXT-2 stored linearisation: one linearize (F(u) + D's linearisation) then J v from it
     t_lin = time_call(lambda: op.linearize(u, out=r))
     t_jlin = time_call(lambda: op.jvp_lin(v, out=JTw))
@@ -411,6 +415,8 @@ def main():
                 "linearize": {"us": t_lin * 1e3, "gdof_s": N / (t_lin * 1e-3) / 1e9},
                 "jvp_lin": {"us": t_jlin * 1e3, "gdof_s": N / (t_jlin * 1e-3) / 1e9},
                 "jacobi_diag": {"us": t_diag * 1e3},
+                "jvp_res": {"us": t_jres * 1e3, "gdof_s": 2 * N / (t_jres * 1e-3) / 1e9,
+                            "note": "r and J v from one dual pass (feod_jvp_res); 2 DOF applications per DOF"},
                 "vjp": {"us": t_vjp * 1e3, "gdof_s": N / (t_vjp * 1e-3) / 1e9,
                         "hbm_frac": algorithmic_bytes(w, "vjp") / (t_vjp * 1e-3) / 1e9 / peak,
                         "fp64_frac": algorithmic_flops(w, "vjp") / (t_vjp * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS},

@@ -170,9 +170,10 @@ class Operator:
         _check(self.lib.feod_jvp(self.h, u.data_ptr(), v.data_ptr(), Jv.data_ptr()))
         return Jv
 
-    def jvp_res(self, u, v):
+    def jvp_res(self, u, v, out=None):
+        """(F(u), J(u) v) from one dual pass (feod_jvp_res); out = (r, Jv) optional."""
         u, v = self._dev(u, self.n_dofs, "u"), self._dev(v, self.n_dofs, "v")
-        r, Jv = self._torch.empty_like(u), self._torch.empty_like(u)
+        r, Jv = out if out is not None else (self._torch.empty_like(u), self._torch.empty_like(u))
         self._sync_stream()
         _check(self.lib.feod_jvp_res(self.h, u.data_ptr(), v.data_ptr(), r.data_ptr(), Jv.data_ptr()))
         return r, Jv
