@@ -39,6 +39,9 @@
 #include <cstdio>
 #endif
 
+#ifndef FEOD_J_UNROLL3
+#define FEOD_J_UNROLL3 7
+#endif
 #ifndef FEOD_L_UNROLL3
 #define FEOD_L_UNROLL3 1   // point-row loop unroll with 3 exchange channels (Q5/Q6)
 #endif
@@ -621,6 +624,8 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   constexpr bool STREAM = (MODE == MODE_PAJVP) || !AFFINE;
   constexpr int MPD = FEOD_MPD > 0 ? FEOD_MPD : (ND == 2 ? 2 : 1);   // point rows of the stream in flight (Q1: 2, measured)
   double* const xe = xb + el * S::SE;   // this element's exchange slot
+  // node-phase y loops: rolled with 3 channels when FEOD_J_UNROLL3 says so (code size)
+  constexpr int JUNR = S::NCH == 3 ? FEOD_J_UNROLL3 : ND;
   const double wij = T.w[lic] * T.w[gr];
   const double iwij2 = T.wi2[lic] * T.wi2[gr];
 
@@ -698,7 +703,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         Vx[b] = accx;
       }
       double* xo = xe + f * S::SF + lic * S::SI + gr;
-#pragma unroll
+#pragma unroll(JUNR)
       for (int j = 0; j < ND; ++j) {
         double w = 0.0, wy = 0.0, wx = 0.0;
 #pragma unroll
@@ -977,7 +982,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         double Q[ND], QX[ND];
 #pragma unroll
         for (int b = 0; b < ND; ++b) Q[b] = QX[b] = 0.0;
-#pragma unroll
+#pragma unroll(JUNR)
         for (int j = 0; j < ND; ++j) {
           const double pz = xi[j * S::SJ], py = xi[j * S::SJ + ND];
 #pragma unroll
