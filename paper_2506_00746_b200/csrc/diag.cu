@@ -8,7 +8,8 @@
 //         + b_x (GB)_a B_b^2 B_c^2 + b_y B_a^2 (GB)_b B_c^2 + b_z B_a^2 B_b^2 (GB)_c ]
 // with the 1D tables evaluated at the Gauss points (B = l_a(x_i), G = l_a'(x_i)):
 // every term is a sum-factorised contraction with squared / mixed 1D tables.
-// One CTA per element; G^T without atomics by 8 element colours (parity of
+// Persistent CTAs per colour (the next element's values prefetched in registers);
+// G^T without atomics by 8 element colours (parity of
 // ex, ey, ez): elements of one colour share no DOF, the colours run in a fixed
 // order, so the assembled diagonal is bitwise reproducible. Dirichlet rows get
 // 1 (J's Dirichlet rows are zero; the preconditioner is the identity there).
@@ -34,13 +35,15 @@ __global__ void __launch_bounds__(kDiagThreads) diag_color_kernel(const OpParams
   double(*S1)[NQ2 * ND] = reinterpret_cast<double(*)[NQ2 * ND]>(dsm + 3 * NQ * ND + NT * NQ3);   // [j][i][c]
   double(*S2)[NQ * ND * ND] = reinterpret_cast<double(*)[NQ * ND * ND]>(dsm + 3 * NQ * ND);  // [i][b][c], over S0
   const int tid = threadIdx.x;
-  // this CTA's element of the colour
   const int hx = (P.nx + 1 - (color & 1)) / 2, hy = (P.ny + 1 - ((color >> 1) & 1)) / 2;
-  const int e = blockIdx.x;
-  const int ex = 2 * (e % hx) + (color & 1);
-  const int ey = 2 * ((e / hx) % hy) + ((color >> 1) & 1);
-  const int ez = 2 * (e / (hx * hy)) + ((color >> 2) & 1);
-  const int64_t eg = ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez);
+  const int hz = (P.nz + 1 - ((color >> 2) & 1)) / 2;
+  const int ne = hx * hy * hz;
+  auto elem = [&](int e, int& ex, int& ey, int& ez) {
+    ex = 2 * (e % hx) + (color & 1);
+    ey = 2 * ((e / hx) % hy) + ((color >> 1) & 1);
+    ez = 2 * (e / (hx * hy)) + ((color >> 2) & 1);
+    return (int64_t)ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez);
+  };
   for (int t = tid; t < NQ * ND; t += kDiagThreads) {
     const int i = t / ND, a = t % ND;
     const double b = T.B[i][a], g = T.G[i][a];
@@ -48,12 +51,33 @@ __global__ void __launch_bounds__(kDiagThreads) diag_color_kernel(const OpParams
     tab[1][i][a] = g * g;
     tab[2][i][a] = g * b;
   }
-  const double* lin = P.lin + eg * (NL * NQ3);
-  for (int t = tid; t < NT * NQ3; t += kDiagThreads) {
-    const int term = t / NQ3, r = t % NQ3;   // r = (l, j, i) with i fastest
-    const int l = r / NQ2, ji = r % NQ2;
-    S0[term][r] = lin[l * NL * NQ2 + term * NQ2 + ji];
+  // persistent over the colour's elements; the next element's linearisation is loaded
+  // into registers while the current one is contracted
+  constexpr int PF = (NT * NQ3 + kDiagThreads - 1) / kDiagThreads;
+  double pf[PF];
+  auto load = [&](int e) {
+    int ex, ey, ez;
+    const double* lin = P.lin + elem(e, ex, ey, ez) * (NL * NQ3);
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      const int t = tid + k * kDiagThreads;
+      if (t < NT * NQ3) {
+        const int term = t / NQ3, r = t % NQ3, l = r / NQ2, ji = r % NQ2;   // r = (l, j, i), i fastest
+        pf[k] = __ldcs(lin + l * NL * NQ2 + term * NQ2 + ji);
+      }
+    }
+  };
+  int e = blockIdx.x;
+  if (e < ne) load(e);
+  for (; e < ne; e += gridDim.x) {
+  int ex, ey, ez;
+  elem(e, ex, ey, ez);
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    const int t = tid + k * kDiagThreads;
+    if (t < NT * NQ3) S0[t / NQ3][t % NQ3] = pf[k];
   }
+  if (e + (int)gridDim.x < ne) load(e + gridDim.x);
   __syncthreads();
   // contract l: S1[t][j][i][c] = sum_l S0[t][l][j][i] Z_t[l][c]
   for (int t = tid; t < NT * NQ2 * ND; t += kDiagThreads) {
@@ -92,6 +116,8 @@ __global__ void __launch_bounds__(kDiagThreads) diag_color_kernel(const OpParams
     const int64_t g = (int64_t)((ND - 1) * ex + a) + (int64_t)Mx * (((ND - 1) * ey + b) + (int64_t)My * ((ND - 1) * ez + c));
     diag[g] += s;
   }
+  __syncthreads();   // S0 / S1 / S2 reused by the next element
+  }   // elements
 }
 
 __global__ void diag_dirichlet_kernel(const OpParams P, double* __restrict__ diag) {
@@ -120,7 +146,18 @@ static cudaError_t diag_nd_t(const OpParams& P, const Tables& T, double* diag, c
               hz = (P.nz + 1 - ((color >> 2) & 1)) / 2;
     const int64_t ne = (int64_t)hx * hy * hz;
     if (ne == 0) continue;
-    diag_color_kernel<ND, NT><<<(unsigned)ne, kDiagThreads, smem, st>>>(P, T, color, diag);
+    static int slots = 0;
+    if (slots == 0) {
+      int dev = 0, sms = 0, occ = 0;
+      cudaError_t e = cudaGetDevice(&dev);
+      if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, diag_color_kernel<ND, NT>, kDiagThreads, smem);
+      if (e != cudaSuccess) return e;
+      slots = sms * (occ > 0 ? occ : 1);
+    }
+    const int64_t grid = ne < slots ? ne : slots;
+    diag_color_kernel<ND, NT><<<(unsigned)grid, kDiagThreads, smem, st>>>(P, T, color, diag);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

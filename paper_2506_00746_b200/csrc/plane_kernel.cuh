@@ -766,7 +766,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     // with 3 channels (Q5/Q6) nothing is indexed by l, so it may stay rolled (code size)
     // (measured on C4: rolled, residual -15 %, JVP -8.5 %, linearize -30 %, J^T w -16 %;
     // jvp_lin is faster unrolled)
-    constexpr int LUNR = (S::NCH == 3 && MODE != MODE_PAJVP) ? FEOD_L_UNROLL3 : NQ;
+    constexpr int LUNR = (ND >= 6 && MODE != MODE_PAJVP) ? FEOD_L_UNROLL3 : NQ;   // (not the Q3 residual's 3 channels)
     double PZ[NO1][ND], PY[NO1][ND], FX[NO1][NB], PX[NO1][S::NCH == 3 ? ND : 1];
 #pragma unroll
     for (int o = 0; o < NO1; ++o)
