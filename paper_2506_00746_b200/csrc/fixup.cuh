@@ -94,7 +94,13 @@ __global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P,
     for (int d = threadIdx.x; d < cnt; d += blockDim.x) {
       const int ix = d % cx, iy = (d / cx) % cy, iz = d / (cx * cy);
       const unsigned long long* f = P.bdone + ((x0 + ix) + (int64_t)P.nbx * ((y0 + iy) + (int64_t)P.nby * (z0 + iz)));
-      while (ld_acquire_u64(f) < epoch) __nanosleep(FEOD_FIX_SLEEP_NS);
+      // bounded wait: a brick that never publishes (a fault upstream) ends in a trap
+      // (a reported launch error) instead of a hung GPU
+      const long long t0 = clock64();
+      while (ld_acquire_u64(f) < epoch) {
+        __nanosleep(FEOD_FIX_SLEEP_NS);
+        if (clock64() - t0 > (1ll << 35)) __trap();   // ~17 s at 2 GHz
+      }
     }
     __syncthreads();
   }
