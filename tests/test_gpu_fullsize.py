@@ -129,3 +129,30 @@ def test_linearize_jvp_lin_sampled(full):
     assert rel_l2(r[rows], O.residual_rows(pr, d["u"], rows)) <= TOL
     Jv = host(op.jvp_lin(cuda(d["v"])))
     assert rel_l2(Jv[rows], O.jvp_rows(pr, d["u"], d["v"], rows)) <= TOL
+
+
+def test_element_matrices_sampled(full):
+    """NEXT-4 at full size: element tangents of a few elements (first, middle, last)."""
+    w, d, pr, op = full
+    if w.k > 3:
+        pytest.skip("element tangents are built for orders 1..3")
+    E = w.n_elems
+    for e0 in (0, E // 2, E - 4):
+        got = host(op.element_matrices(cuda(d["u"]), e0, 4))
+        ref = O.element_tangent(pr, d["u"], np.arange(e0, e0 + 4))
+        assert rel_l2(got.ravel(), ref.ravel()) <= TOL
+
+
+def test_jacobi_diag_sampled(full):
+    """NEXT-3 at full size: the Jacobi diagonal on sampled rows (oracle: Eq. 3 element
+    tangents of the touching elements, diagonal entries scattered)."""
+    w, d, pr, op = full
+    rows = sample_rows(w, n_random=60, seed=4)
+    op.linearize(cuda(d["u"]))
+    got = host(op.jacobi_diag())[rows]
+    el = O.fem._elems_touching(pr, rows)
+    Ke = O.element_tangent(pr, d["u"], el)
+    dofs = O.dof_map(pr, el)
+    ref = np.bincount(dofs.ravel(), weights=np.einsum("eii->ei", Ke).ravel(), minlength=pr.n_dofs)
+    ref[O.dirichlet_mask(pr)] = 1.0
+    assert rel_l2(got, ref[rows]) <= TOL
