@@ -74,7 +74,10 @@ template <int ND> struct PlaneTile;
 #endif
 template <> struct PlaneTile<2> { static constexpr int BX = FEOD_Q1_BX, BY = FEOD_Q1_BY, BZ = 16; };
 template <> struct PlaneTile<3> { static constexpr int BX = 4, BY = 3, BZ = 16; };
-template <> struct PlaneTile<4> { static constexpr int BX = 4, BY = 2, BZ = 16; };
+#ifndef FEOD_Q3_BY
+#define FEOD_Q3_BY 2
+#endif
+template <> struct PlaneTile<4> { static constexpr int BX = 4, BY = FEOD_Q3_BY, BZ = 16; };
 template <> struct PlaneTile<5> { static constexpr int BX = 4, BY = 2, BZ = 8; };
 template <> struct PlaneTile<6> { static constexpr int BX = 2, BY = 2, BZ = 8; };
 template <> struct PlaneTile<7> { static constexpr int BX = 2, BY = 2, BZ = 8; };
