@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -23,6 +24,7 @@ struct feod_op {
   BrickInfo bi;
   int nbricks;
   int64_t N, E;
+  int64_t Epad;                // elements incl. the per-point stream interleave padding
   double* geom = nullptr;
   double* shell = nullptr;     // 2 x nbricks x shell
   double* stage = nullptr;     // host-API staging: 4 x max(N, E)
@@ -31,8 +33,11 @@ struct feod_op {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double* red = nullptr;       // kRedBlocks partials, 24 scalars, kRedBlocks partials
   int* flag = nullptr;
-  unsigned long long* sched = nullptr;   // dynamic brick scheduling ticket counter
+  DevState* ds = nullptr;                // device scheduler state: tickets, epoch (common.cuh)
   unsigned long long* bdone = nullptr;   // per-brick completion epochs (fix-up dependencies)
+  bool poisoned = false;                 // a launch failed after the operator kernel ran: the
+                                         // brick epochs no longer pair with the shell slab
+  cudaEvent_t sw = nullptr;              // stream switch (feod_set_stream orders old -> new)
   int2* fixrows = nullptr;               // fix-up rows in launch order
   double* work = nullptr;      // Newton-CG: F, r, p, Ap, d (5 N)
   double* lin = nullptr;       // stored linearisation (feod_linearize), lin_values x E x q^3
@@ -74,7 +79,8 @@ static void free_all(feod_op* h) {
   if (h->dst) cudaStreamDestroy(h->dst);
   cudaFree(h->red);
   cudaFree(h->flag);
-  cudaFree(h->sched);
+  cudaFree(h->ds);
+  if (h->sw) cudaEventDestroy(h->sw);
   cudaFree(h->bdone);
   cudaFree(h->fixrows);
   cudaFree(h->work);
@@ -131,10 +137,30 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   std::memset(&P, 0, sizeof(P));
   P.nx = mesh->nx; P.ny = mesh->ny; P.nz = mesh->nz;
   P.Mx = (int)Mx; P.My = (int)My; P.Mz = (int)Mz;
-  P.nbx = (mesh->nx + h->bi.BX - 1) / h->bi.BX;
-  P.nby = (mesh->ny + h->bi.BY - 1) / h->bi.BY;
-  P.nbz = (mesh->nz + h->bi.BZ - 1) / h->bi.BZ;
-  P.shell_stride = h->bi.shell;
+  P.tbx = h->bi.BX;
+  P.tby = h->bi.BY;
+  P.tbz = h->bi.BZ;
+  P.nbx = (mesh->nx + P.tbx - 1) / P.tbx;
+  P.nby = (mesh->ny + P.tby - 1) / P.tby;
+  if (h->bi.ptx > 1) {
+    // column kernel (Q1, Q2): the brick depth is a run-time choice; take the one whose
+    // bricks fill whole waves of resident CTAs best (dynamic scheduling evens out the rest)
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long slots = (long)sms * h->bi.minb;
+    double best = 1e300;
+    for (int bz : {4, 6, 8, 12, 16, 24, 32, 48, 64}) {
+      const long nb = (long)P.nbx * P.nby * ((mesh->nz + bz - 1) / bz);
+      const long waves = (nb + slots - 1) / slots;
+      const double cost = (double)waves * (std::min(bz, mesh->nz) + 1.0);
+      if (cost < best - 1e-9) { best = cost; P.tbz = bz; }
+    }
+    if (const char* env = std::getenv("FEOD_COL_BZ")) P.tbz = std::max(1, std::atoi(env));   // experiments
+  }
+  P.nbz = (mesh->nz + P.tbz - 1) / P.tbz;
+  P.ptx = h->bi.ptx;
+  P.pnbx = (mesh->nx + P.ptx - 1) / P.ptx;
+  P.shell_stride = shell_size(order * P.tbx + 1, order * P.tby + 1, order * P.tbz + 1);
   P.faces = mesh->dirichlet_faces;
   P.half_pm2 = 0.5 * (coeffs->p - 2.0);
   P.eps2 = coeffs->eps * coeffs->eps;
@@ -143,6 +169,8 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   P.cx = hy * hz / hx; P.cy = hx * hz / hy; P.cz = hx * hy / hz; P.vol = hx * hy * hz;
   P.rho = coeffs->rho;
   h->nbricks = P.nbx * P.nby * P.nbz;
+  // per-point streams (metric, stored linearisation) hold pnbx * ptx elements per row
+  h->Epad = (int64_t)P.pnbx * P.ptx * mesh->ny * mesh->nz;
 
   auto cleanup_fail = [&](int code) { free_all(h); delete h; return code; };
   cudaError_t e;
@@ -153,12 +181,11 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
     return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: reduction buffer"));
   if ((e = cudaMalloc(&h->flag, sizeof(int) * 2)) != cudaSuccess)
     return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: flag"));
-  if ((e = cudaMalloc(&h->sched, sizeof(unsigned long long))) != cudaSuccess)
-    return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: scheduler counter"));
-  if ((e = cudaMemsetAsync(h->sched, 0, sizeof(unsigned long long), h->st)) != cudaSuccess)
+  if ((e = cudaMalloc(&h->ds, sizeof(DevState))) != cudaSuccess)
+    return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: scheduler state"));
+  if ((e = cudaMemsetAsync(h->ds, 0, sizeof(DevState), h->st)) != cudaSuccess)
     return cleanup_fail(cuda_fail(e, "feod_create: memset"));
-  P.sched = h->sched;
-  P.sched_base = 0;
+  P.ds = h->ds;
   if ((e = cudaMalloc(&h->bdone, sizeof(unsigned long long) * (size_t)h->nbricks)) != cudaSuccess)
     return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: brick epochs"));
   if ((e = cudaMemsetAsync(h->bdone, 0, sizeof(unsigned long long) * (size_t)h->nbricks, h->st)) != cudaSuccess)
@@ -190,14 +217,14 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   if (mesh->vertices) {
     const size_t nv = (size_t)(mesh->nx + 1) * (mesh->ny + 1) * (mesh->nz + 1) * 3;
     double* dverts = nullptr;
-    const size_t ng = (size_t)h->E * 6 * qorder * qorder * qorder;
+    const size_t ng = (size_t)h->Epad * 6 * qorder * qorder * qorder;
     if (cudaMalloc(&dverts, sizeof(double) * nv) != cudaSuccess) return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: vertices"));
     if (cudaMalloc(&h->geom, sizeof(double) * ng) != cudaSuccess) {
       cudaFree(dverts);
       return cleanup_fail(fail(FEOD_ENOMEM, "feod_create: geometry (6 doubles per point)"));
     }
     e = cudaMemcpyAsync(dverts, mesh->vertices, sizeof(double) * nv, cudaMemcpyHostToDevice, h->st);
-    if (e == cudaSuccess) e = launch_geometry(dverts, mesh->nx, mesh->ny, mesh->nz, qorder, h->T, h->geom, h->flag, h->st);
+    if (e == cudaSuccess) e = launch_geometry(dverts, P, qorder, h->T, h->geom, h->flag, h->st);
     int bad = 0;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
@@ -222,7 +249,15 @@ extern "C" int feod_destroy(feod_handle h) {
 
 extern "C" int feod_set_stream(feod_handle h, void* cuda_stream) {
   if (!h) return fail(FEOD_EINVAL, "feod_set_stream: null handle");
-  h->st = (cudaStream_t)cuda_stream;
+  cudaStream_t ns = (cudaStream_t)cuda_stream;
+  if (ns != h->st) {
+    // the handle's scratch (tickets, shell slab, brick epochs) is shared by its calls:
+    // work on the new stream starts after everything already queued on the old one
+    if (!h->sw) CK(cudaEventCreateWithFlags(&h->sw, cudaEventDisableTiming), "feod_set_stream: event");
+    CK(cudaEventRecord(h->sw, h->st), "feod_set_stream");
+    CK(cudaStreamWaitEvent(ns, h->sw, 0), "feod_set_stream");
+    h->st = ns;
+  }
   return FEOD_OK;
 }
 
@@ -245,25 +280,26 @@ extern "C" int64_t feod_num_elems(feod_handle h) { return h ? h->E : -1; }
 
 static int run_op(feod_handle h, int mode, const double* in0, const double* in1, double* out0, double* out1,
                   double* gout, const char* name) {
+  if (h->poisoned) return fail(FEOD_ECUDA, std::string(name) + ": handle unusable after a failed launch");
   OpPtrs p{in0, in1, out0, out1, h->shell, h->shell + (size_t)h->nbricks * h->P.shell_stride, gout};
   cudaEvent_t pb = h->prof_begin, pe = h->prof_end;
   h->prof_begin = h->prof_end = nullptr;
   if (pb) cudaEventRecord(pb, h->st);
   int grid = 0;
-  const unsigned long long epoch = h->P.sched_base + 1;   // what the IO warps publish per finished brick
   // MODE_PAJVP reads the stored linearisation only, whatever the geometry
   const bool aff = mode == MODE_PAJVP ? true : h->geom == nullptr;
   cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, aff, h->nbricks, h->P, h->T, p, h->st, &grid);
-  // every CTA claims one ticket per brick it processes plus one that ends it
-  h->P.sched_base += (unsigned long long)h->nbricks + (unsigned long long)grid;
   if (pe) cudaEventRecord(pe, h->st);
   if (e != cudaSuccess) return cuda_fail(e, name);
   if (mode != MODE_DESIGN) {
     OpParams Pf = h->P;
     if (mode == MODE_VJP && h->P.vjp_keep_rows) Pf.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
-    e = fixup_nd(h->nd, Pf, epoch, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
+    e = fixup_nd(h->nd, Pf, p.shell0, out0, mode == MODE_JVPRES ? p.shell1 : nullptr,
                  mode == MODE_JVPRES ? out1 : nullptr, h->st);
-    if (e != cudaSuccess) return cuda_fail(e, name);
+    if (e != cudaSuccess) {
+      h->poisoned = true;
+      return cuda_fail(e, name);
+    }
   }
   return FEOD_OK;
 }
@@ -369,7 +405,7 @@ extern "C" int feod_linearize(feod_handle h, const double* u, double* r) {
   if (!h || !u || !r) return fail(FEOD_EINVAL, "feod_linearize: null argument");
   if ((const double*)r == u) return fail(FEOD_EINVAL, "feod_linearize: r aliases u");
   if (!h->lin) {
-    const size_t n = (size_t)lin_values(h->coeffs.model) * (size_t)h->E * h->q * h->q * h->q;
+    const size_t n = (size_t)lin_values(h->coeffs.model) * (size_t)h->Epad * h->q * h->q * h->q;
     if (cudaMalloc(&h->lin, sizeof(double) * n) != cudaSuccess) {
       h->lin = nullptr;
       return fail(FEOD_ENOMEM, "feod_linearize: linearisation buffer");

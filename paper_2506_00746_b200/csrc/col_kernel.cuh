@@ -1,0 +1,510 @@
+// Fused FEOD operator kernel for low orders (Q1, Q2): one thread per element
+// column, the whole sum factorisation of an element in registers.
+//
+// The chain is the paper's F(u) = P^T G^T B^T D(B G P u) (Eq. 1) and
+// its Jacobian action (Eq. 2), with AD confined to the pointwise D
+// (pointwise.cuh). At Q1/Q2 an element is small enough (8 / 27 nodes
+// and points) that one thread can hold its nodal values, its point values and its
+// transposed accumulators in registers, so B and B^T need no shuffles, no shared-
+// memory exchange and no barriers: every contraction is a chain of DFMAs with
+// compile-time table operands (constant bank). plane_kernel.cuh (Q3..Q6) splits an
+// element over ND^2 threads instead; for Q2 that left the FP64 pipe at ~25 %.
+//
+// CTA = a TX x TY tile of element columns, one thread each, sweeping the brick's
+// element layers along z (persistent CTAs, dynamic brick scheduling, DevState).
+//   G     the tile's DOF planes (u, and v / lambda / w) stream into a shared ring of
+//         RS planes, DPF layers ahead: one TMA bulk copy per tile row, issued by the
+//         lanes of warp 0, completion counted on the layer's mbarrier. The L-vector
+//         rows are 8 mod 16 bytes apart, so a row is copied from its 16-byte aligned
+//         start and stored at an odd virtual pitch VP (Mx odd): element (X, Y) of a
+//         plane sits at Y VP + X + s0, s0 the parity of the plane's first row
+//         (DESIGN.md §5). One __syncthreads per layer (element buffer, ring reuse).
+//   B     per field: x, y, z interpolation to the q^3 Gauss points (B (x) B (x) B),
+//         then the reference gradient by collocation, Ux = D_x U etc. (D = L'_m(x_i)
+//         on the Gauss points: exact for the degree-k interpolant, q = k+1)
+//   D     point_op<MODE, MODEL> at every point (double / dual<double>)
+//   B^T   R = D_x^T Fx + D_y^T Fy + D_z^T Fz + V at the points, then z first:
+//         S[c] = sum_l B[l][c] R[l]; the element's top plane S[K] is carried in
+//         registers to the next layer's element (z-sharing of G^T summed before the
+//         x-y transposed contraction, which runs once per shared DOF plane), and
+//         the finished planes go through B_y^T B_x^T to the nodes
+//   G^T   node values of the finished DOF planes -> shared buffer; after the layer's
+//         barrier every thread sums the <= 4 contributions of the nodes it owns in a
+//         fixed order (ascending element index) and stores them: interior DOFs to
+//         the output (P^T: Dirichlet rows 0), brick-face DOFs to the shell slab that
+//         fixup_kernel sums across bricks -> deterministic, no atomics
+//   a8    MODE_DESIGN: the element's g_e is one thread's sum, stored directly
+// Per-point streams (perturbed-mesh metric, stored linearisation) use the
+// interleaved layout OpParams::ptx = TX, so a warp reads 128-byte runs.
+#pragma once
+#include "common.cuh"
+#include "dual.cuh"
+#include "physics.cuh"
+#include "pointwise.cuh"
+
+namespace feod {
+
+template <int ND> struct ColTile;
+template <> struct ColTile<2> { static constexpr int TX = 32, TY = 4; };
+template <> struct ColTile<3> { static constexpr int TX = 16, TY = 8; };
+
+template <int ND, int MODE>
+struct CShape {
+  static constexpr int K = ND - 1;
+  static constexpr int TX = ColTile<ND>::TX, TY = ColTile<ND>::TY, NT = TX * TY, NW = NT / 32;
+  static constexpr int NIN = (MODE == MODE_RES || MODE == MODE_LIN || MODE == MODE_PAJVP) ? 1 : 2;
+  static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
+  static constexpr int PITCH = (K * TX + 2) / 2 * 2;         // even row pitch (doubles); VP = PITCH + (Mx & 1)
+  static constexpr int ROWS = K * TY + 1;
+  static constexpr int PLANE = (ROWS * (PITCH + 1) + 2 + 1) / 2 * 2;   // one ring slot (16-byte multiple)
+  static constexpr int DPF = 2;                              // layers prefetched ahead
+  static constexpr int RS = K * DPF + 2;                     // ring planes (one extra across a brick boundary)
+  static constexpr int ESTR = (ND * ND) | 1;                 // odd stride: conflict-free 8-byte accesses
+  static constexpr int EBP = NOUT == 2 ? 1 : 2;              // element-buffer parities
+  static constexpr int EB = (NOUT > 0 ? NOUT : 0) * (K + 1) * NT * ESTR;   // one parity
+  static constexpr int RING = NIN * RS * PLANE;
+  // + 2 mbarriers, the brick queue (8 x int4) and the plane shifts (NIN x RS ints)
+  static constexpr size_t SMEM_BYTES = sizeof(double) * (RING + EBP * EB) + 16 + 8 * 16 + ((NIN * RS * 4 + 15) / 16) * 16;
+  static constexpr int MINB = ND == 3 ? 2 : 4;
+  static_assert(NT % 32 == 0, "whole warps");
+  static constexpr int RCPY = (NIN * (K + 1) * ROWS + 31) / 32;   // row copies per lane of warp 0 (at most)
+};
+
+template <int ND, int MODE, int MODEL, bool AFFINE>
+__global__ void __launch_bounds__(CShape<ND, MODE>::NT, CShape<ND, MODE>::MINB)
+col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, const double* __restrict__ in1,
+           double* __restrict__ out0, double* __restrict__ out1, double* __restrict__ shell0,
+           double* __restrict__ shell1, double* __restrict__ gout) {
+  using S = CShape<ND, MODE>;
+  constexpr int K = S::K, NQ = ND, NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
+  constexpr int TX = S::TX, TY = S::TY, NT = S::NT, NIN = S::NIN, NOUT = S::NOUT, RS = S::RS;
+  constexpr int NO1 = NOUT > 0 ? NOUT : 1;
+  constexpr bool STREAM = (MODE == MODE_PAJVP) || !AFFINE;
+  constexpr int NSV = (MODE == MODE_PAJVP) ? lin_values(MODEL) : 6;
+  constexpr bool MASK1 = MODE == MODE_DESIGN || MODE == MODE_VJP;   // field 1 (lambda / w) Dirichlet-masked
+  extern __shared__ __align__(16) double smem[];
+  double* ring = smem;                                          // [NIN][RS][PLANE]
+  double* ebuf = smem + S::RING;                                // [EBP][NOUT][K+1][NT][ESTR]
+  uint64_t* mb = reinterpret_cast<uint64_t*>(ebuf + S::EBP * S::EB);   // [2] layer-slot mbarriers
+  int4* bq = reinterpret_cast<int4*>(mb + 2);                   // [8] (id, ex0, ey0, ez0) of the n-th brick
+  int* psh = reinterpret_cast<int*>(bq + 8);                    // [NIN][RS] s0 of the plane in each ring slot
+
+  // the fix-up kernel may launch now: it waits per brick on P.bdone, not on this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int tid = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+  const int tx = tid % TX, ty = tid / TX;
+  const int nbricks = P.nbx * P.nby * P.nbz;
+  const int BZ = P.tbz;
+  const int64_t MxMy = (int64_t)P.Mx * P.My;
+  const int VP = S::PITCH + (P.Mx & 1);   // virtual row pitch of the ring planes
+  auto claim = [&](int slot) {            // thread 0: claim a brick, publish (id, origin)
+    const int id = claim_brick(P.ds, nbricks);
+    int4 q = make_int4(-1, 0, 0, 0);
+    if (id >= 0) q = make_int4(id, (id % P.nbx) * TX, ((id / P.nbx) % P.nby) * TY, (id / (P.nbx * P.nby)) * BZ);
+    bq[slot & 7] = q;
+  };
+  if (tid == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // previous call's results are visible
+  const unsigned long long epoch = read_epoch(P.ds);
+  if (tid == 0) claim(0);
+  __syncthreads();
+
+  // ---- prefetch cursor: brick ordinal pn, its queue entry pq, layer pz, CTA-global plane
+  // base pbase, layer counter pL. The next brick is claimed only when the cursor has issued
+  // the current brick's last layer (late claiming: a CTA never holds a brick it is not about
+  // to stream), and read at the next step, after a layer barrier has published it.
+  int pn = 0, pz = 0, pbase = 0, pL = 0;
+  int4 pq = bq[0];
+  bool pend = false;
+  auto prefetch = [&]() {
+    if (pend) {
+      pq = bq[pn & 7];
+      pend = false;
+    }
+    if (pq.x >= 0) {
+      const int ex0 = pq.y, ey0 = pq.z, ez0 = pq.w;
+      const int LX = K * min(TX, P.nx - ex0) + 1, LY = K * min(TY, P.ny - ey0) + 1;
+      const int bzr = min(BZ, P.nz - ez0);
+      if (warp == 0) {
+        // one bulk copy per (field, plane, row) of the layer's new planes, spread over the lanes
+        uint64_t* bar = &mb[pL & 1];
+        const int p0 = pz == 0 ? 0 : K * pz + 1, np = K * pz + K - p0 + 1;
+        const int nrow = NIN * np * LY;
+#pragma unroll
+        for (int r0 = 0; r0 < S::RCPY * 32; r0 += 32) {
+          const int r = r0 + lane;
+          if (r < nrow) {
+            const int f = r / (np * LY), rem = r - f * (np * LY), pp = rem / LY, Y = rem - pp * LY;
+            const int p = p0 + pp, slot = (pbase + p) % RS;
+            const double* src = (f == 0 ? in0 : in1) + (int64_t)(K * ez0 + p) * MxMy + (int64_t)(K * ey0 + Y) * P.Mx + K * ex0;
+            const uint64_t ga = reinterpret_cast<uint64_t>(src);
+            const int sh = (int)((ga >> 3) & 1);           // this row's 8-byte phase
+            const int s0 = (int)(((ga >> 3) - (uint64_t)Y * P.Mx) & 1);   // the plane's first row's phase
+            if (Y == 0) psh[f * RS + slot] = s0;
+            const uint32_t bytes = (uint32_t)(((LX + sh) * 8 + 15) & ~15);
+            double* dst = ring + (f * RS + slot) * S::PLANE + (Y * VP + s0 - sh);
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(dst, reinterpret_cast<const void*>(ga & ~uint64_t(15)), bytes, bar);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar);
+      }
+      if constexpr (STREAM) {
+        // the layer's per-point stream into L2 (bulk engine), one contiguous chunk per tile row
+        const int byr = min(TY, P.ny - ey0);
+        if (tid >= 32 && tid - 32 < byr) {
+          const double* sb = (MODE == MODE_PAJVP) ? P.lin : P.geom;
+          prefetch_l2_bulk(sb + pt_base(P, ex0, ey0 + tid - 32, ez0 + pz, NSV * NQ3),
+                           (uint32_t)(sizeof(double) * NSV * NQ3 * TX));
+        }
+      }
+      ++pL;
+      if (++pz == bzr) {   // brick issued: claim the next one
+        pz = 0;
+        pbase += K * bzr + 1;
+        ++pn;
+        pend = true;
+        if (tid == 0) claim(pn);
+      }
+    }
+  };
+  static_assert(S::DPF == 2, "two layers in flight: mbarrier slot = layer & 1");
+  prefetch();
+  __syncthreads();   // a one-layer brick: the next brick written by thread 0 above
+  prefetch();
+
+  // ---- compute cursor
+  int cn = 0, cz = 0, cbase = 0;
+  double CS[NO1][NQ2];   // top plane of the previous element of the column, after B_z^T
+#pragma unroll
+  for (int o = 0; o < NO1; ++o)
+#pragma unroll
+    for (int t = 0; t < NQ2; ++t) CS[o][t] = 0.0;
+
+#pragma unroll 1
+  for (int L = 0;; ++L) {
+    const int4 cq = bq[cn & 7];
+    const int cid = cq.x;
+    if (cid < 0) break;
+    const int ex0 = cq.y, ey0 = cq.z, ez0 = cq.w;
+    const int bxr = min(TX, P.nx - ex0), byr = min(TY, P.ny - ey0), bzr = min(BZ, P.nz - ez0);
+    const bool ev = tx < bxr && ty < byr;
+    const bool last = cz == bzr - 1;
+    const int ex = ex0 + tx, ey = ey0 + ty, ez = ez0 + cz;
+    double rho_e = 1.0;
+    if constexpr (MODEL == HEAT && MODE != MODE_PAJVP)
+      if (ev) rho_e = __ldg(P.rho + ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez));
+    double* eb = ebuf + (S::EBP == 2 ? (L & 1) : 0) * S::EB;
+    if (S::EBP == 1 && NOUT > 0) __syncthreads();   // single element buffer: previous scatter done
+    mbar_wait(&mb[L & 1], (L >> 1) & 1);             // this layer's DOF planes landed
+
+    if (ev) {
+      // ---- gather the element's nodes from the ring; B: values at the q^3 points
+      double U[NIN][NQ3];
+#pragma unroll
+      for (int f = 0; f < NIN; ++f) {
+        double x[ND][ND][ND];   // [c][b][a]
+#pragma unroll
+        for (int c = 0; c < ND; ++c) {
+          const int slot = (cbase + K * cz + c) % RS;
+          const double* pl = ring + (f * RS + slot) * S::PLANE + psh[f * RS + slot] + K * ty * VP + K * tx;
+#pragma unroll
+          for (int b = 0; b < ND; ++b)
+#pragma unroll
+            for (int a = 0; a < ND; ++a) x[c][b][a] = pl[b * VP + a];
+        }
+        if (MASK1 && f == 1) {
+          // lambda's / w's Dirichlet entries are masked (readings A14, A17): only elements
+          // touching a Dirichlet face look at their nodes
+          const bool touch = ((P.faces & 1u) && ex == 0) || ((P.faces & 2u) && ex == P.nx - 1) ||
+                             ((P.faces & 4u) && ey == 0) || ((P.faces & 8u) && ey == P.ny - 1) ||
+                             ((P.faces & 16u) && ez == 0) || ((P.faces & 32u) && ez == P.nz - 1);
+          if (touch) {
+#pragma unroll
+            for (int c = 0; c < ND; ++c)
+#pragma unroll
+              for (int b = 0; b < ND; ++b)
+#pragma unroll
+                for (int a = 0; a < ND; ++a)
+                  if (is_dirichlet(K * ex + a, K * ey + b, K * ez + c, P.Mx, P.My, P.Mz, P.faces)) x[c][b][a] = 0.0;
+          }
+        }
+        double t1[ND][ND][NQ];   // x: [c][b][i]
+#pragma unroll
+        for (int c = 0; c < ND; ++c)
+#pragma unroll
+          for (int b = 0; b < ND; ++b)
+#pragma unroll
+            for (int i = 0; i < NQ; ++i) {
+              double s = T.B[i][0] * x[c][b][0];
+#pragma unroll
+              for (int a = 1; a < ND; ++a) s = fma(T.B[i][a], x[c][b][a], s);
+              t1[c][b][i] = s;
+            }
+        double t2[ND][NQ][NQ];   // y: [c][j][i]
+#pragma unroll
+        for (int c = 0; c < ND; ++c)
+#pragma unroll
+          for (int j = 0; j < NQ; ++j)
+#pragma unroll
+            for (int i = 0; i < NQ; ++i) {
+              double s = T.B[j][0] * t1[c][0][i];
+#pragma unroll
+              for (int b = 1; b < ND; ++b) s = fma(T.B[j][b], t1[c][b][i], s);
+              t2[c][j][i] = s;
+            }
+#pragma unroll
+        for (int l = 0; l < NQ; ++l)   // z: [l][j][i]
+#pragma unroll
+          for (int ji = 0; ji < NQ2; ++ji) {
+            double s = T.B[l][0] * t2[0][ji / NQ][ji % NQ];
+#pragma unroll
+            for (int c = 1; c < ND; ++c) s = fma(T.B[l][c], t2[c][ji / NQ][ji % NQ], s);
+            U[f][l * NQ2 + ji] = s;
+          }
+      }
+
+      // ---- D at every point, B^T's collocated part accumulated in R
+      double R[NO1][NQ3];
+#pragma unroll
+      for (int o = 0; o < NO1; ++o)
+#pragma unroll
+        for (int t = 0; t < NQ3; ++t) R[o][t] = 0.0;
+      double gpart = 0.0;
+      const double* gp = nullptr;   // this element's per-point stream (stride TX = ptx)
+      if constexpr (STREAM) {
+        const double* sb = (MODE == MODE_PAJVP) ? P.lin : P.geom;
+        gp = sb + pt_base(P, ex, ey, ez, NSV * NQ3);
+      }
+      double* lp = nullptr;
+      if constexpr (MODE == MODE_LIN) lp = P.lin + pt_base(P, ex, ey, ez, lin_values(MODEL) * NQ3);
+      // the point stream, MPD points ahead in registers (streaming loads, L2-prefetched a
+      // brick step earlier)
+      constexpr int MPD = ND == 2 ? 3 : 1;
+      double snext[STREAM ? MPD : 1][STREAM ? NSV : 1];
+      if constexpr (STREAM) {
+#pragma unroll
+        for (int r = 0; r < MPD; ++r)
+#pragma unroll
+          for (int c = 0; c < NSV; ++c)
+            snext[r][c] = ld_stream(gp + (((r / NQ2) * NSV + c) * NQ2 + r % NQ2) * TX);
+      }
+#pragma unroll
+      for (int l = 0; l < NQ; ++l)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j)
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) {
+            const int q = (l * NQ + j) * NQ + i;
+            const double wq = T.w[i] * T.w[j] * T.w[l];
+            double sv[STREAM ? NSV : 1];
+            if constexpr (STREAM) {
+              // layout [l][c][j][i] per element (as the geometry kernel writes it)
+#pragma unroll
+              for (int c = 0; c < NSV; ++c) sv[c] = snext[q % MPD][c];
+              if (q + MPD < NQ3) {
+                const int l1 = (q + MPD) / NQ2, ji1 = (q + MPD) % NQ2;
+#pragma unroll
+                for (int c = 0; c < NSV; ++c) snext[q % MPD][c] = ld_stream(gp + ((l1 * NSV + c) * NQ2 + ji1) * TX);
+              }
+            }
+            Metric M;
+            double W;
+            if constexpr (AFFINE || MODE == MODE_PAJVP) {
+              M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
+              W = wq * P.vol;
+            } else {
+              M = {sv[0], sv[1], sv[2], sv[3], sv[4], sv[5]};
+              const double det = M.xx * (M.yy * M.zz - M.yz * M.yz) - M.xy * (M.xy * M.zz - M.yz * M.xz) +
+                                 M.xz * (M.xy * M.yz - M.yy * M.xz);
+              W = det * (T.wi2[i] * T.wi2[j] * T.wi2[l]);   // W = w detJ = det(M) / w^2
+            }
+            double Ul[NIN], Uxl[NIN], Uyl[NIN], Uzl[NIN];
+#pragma unroll
+            for (int f = 0; f < NIN; ++f) {
+              Ul[f] = U[f][q];
+              double gx = T.D[i][0] * U[f][(l * NQ + j) * NQ];
+              double gy = T.D[j][0] * U[f][l * NQ2 + i];
+              double gz = T.D[l][0] * U[f][j * NQ + i];
+#pragma unroll
+              for (int m = 1; m < NQ; ++m) {
+                gx = fma(T.D[i][m], U[f][(l * NQ + j) * NQ + m], gx);
+                gy = fma(T.D[j][m], U[f][(l * NQ + m) * NQ + i], gy);
+                gz = fma(T.D[l][m], U[f][(m * NQ + j) * NQ + i], gz);
+              }
+              Uxl[f] = gx;
+              Uyl[f] = gy;
+              Uzl[f] = gz;
+            }
+            double F0[4], F1[4];
+            double lv[lin_values(MODEL)];
+            point_op<MODE, MODEL, AFFINE || MODE == MODE_PAJVP>(Ul, Uxl, Uyl, Uzl, M, W, rho_e, P, sv, F0, F1, gpart, lv);
+            if constexpr (MODE == MODE_LIN) {
+#pragma unroll
+              for (int c = 0; c < lin_values(MODEL); ++c) lp[((l * lin_values(MODEL) + c) * NQ2 + j * NQ + i) * TX] = lv[c];
+            }
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o) {
+              const double* Fo = o == 0 ? F0 : F1;
+              if (value_channel(MODE, o)) R[o][q] += Fo[3];
+#pragma unroll
+              for (int m = 0; m < NQ; ++m) {
+                R[o][(l * NQ + j) * NQ + m] = fma(T.D[i][m], Fo[0], R[o][(l * NQ + j) * NQ + m]);
+                R[o][(l * NQ + m) * NQ + i] = fma(T.D[j][m], Fo[1], R[o][(l * NQ + m) * NQ + i]);
+                R[o][(m * NQ + j) * NQ + i] = fma(T.D[l][m], Fo[2], R[o][(m * NQ + j) * NQ + i]);
+              }
+            }
+          }
+      if constexpr (MODE == MODE_DESIGN) gout[ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez)] = gpart;
+
+      // ---- B^T: z first, z-carry of the top plane, then y and x per finished DOF plane
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) {
+        double Sz[ND][NQ2];
+#pragma unroll
+        for (int c = 0; c < ND; ++c)
+#pragma unroll
+          for (int ji = 0; ji < NQ2; ++ji) {
+            double s = T.B[0][c] * R[o][ji];
+#pragma unroll
+            for (int l = 1; l < NQ; ++l) s = fma(T.B[l][c], R[o][l * NQ2 + ji], s);
+            Sz[c][ji] = s;
+          }
+        if (cz > 0) {
+#pragma unroll
+          for (int ji = 0; ji < NQ2; ++ji) Sz[0][ji] = CS[o][ji] + Sz[0][ji];
+        }
+#pragma unroll
+        for (int ji = 0; ji < NQ2; ++ji) CS[o][ji] = Sz[K][ji];
+#pragma unroll
+        for (int c = 0; c < ND; ++c) {
+          if (c == K && !last) break;
+          double sy[ND][NQ];   // [b][i]
+#pragma unroll
+          for (int b = 0; b < ND; ++b)
+#pragma unroll
+            for (int i = 0; i < NQ; ++i) {
+              double s = T.B[0][b] * Sz[c][i];
+#pragma unroll
+              for (int j = 1; j < NQ; ++j) s = fma(T.B[j][b], Sz[c][j * NQ + i], s);
+              sy[b][i] = s;
+            }
+          double* e = eb + ((o * (K + 1) + c) * NT + tid) * S::ESTR;
+#pragma unroll
+          for (int b = 0; b < ND; ++b)
+#pragma unroll
+            for (int a = 0; a < ND; ++a) {
+              double s = T.B[0][a] * sy[b][0];
+#pragma unroll
+              for (int i = 1; i < NQ; ++i) s = fma(T.B[i][a], sy[b][i], s);
+              e[b * ND + a] = s;
+            }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- G^T + P^T: the finished DOF planes of the layer (owner computes, fixed order).
+    // Thread (tx, ty) owns its element's nodes a, b < K (+ a = K on the tile's last column,
+    // b = K on its last row) and sums each node's <= 4 contributions in ascending element
+    // order: (ty-1, tx-1), (ty-1, tx), (ty, tx-1), (ty, tx).
+    if constexpr (NOUT > 0) {
+      if (ev) {
+        const int LX = K * bxr + 1, LY = K * byr + 1, LZ = K * bzr + 1;
+        const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx, lowY = ey0 > 0, highY = ey0 + byr < P.ny;
+        const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
+        const bool keep = MODE == MODE_VJP && P.vjp_keep_rows;   // J^T w keeps every row (reading A17)
+        const int nfp = last ? K + 1 : K;
+        const int64_t rowg = (int64_t)(K * (ey0 + ty)) * P.Mx + K * (ex0 + tx);   // in-plane index of node (0, 0)
+#pragma unroll
+        for (int c = 0; c < K + 1; ++c) {
+          if (c >= nfp) break;
+          const int lz = K * cz + c;
+          const int gz = K * ez0 + lz;
+          const bool zsh = (lz == 0 && lowZ) || (lz == LZ - 1 && highZ);
+          const bool zdir = !keep && (((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1));
+          // node (a, b) of output o: its contributions, then out / shell / Dirichlet zero
+          auto node = [&](int o, int a, int b, bool fast) {
+            const double* e = eb + (o * (K + 1) + c) * NT * S::ESTR;
+            double v;
+            if (fast) {   // all neighbours exist (tx, ty > 0) and the node is interior
+              v = 0.0;
+              if (b == 0) {
+                if (a == 0) v += e[(tid - TX - 1) * S::ESTR + K * ND + K];
+                v += e[(tid - TX) * S::ESTR + K * ND + a];
+              }
+              if (a == 0) v += e[(tid - 1) * S::ESTR + b * ND + K];
+              v += e[tid * S::ESTR + b * ND + a];
+              (o == 0 ? out0 : out1)[(int64_t)gz * MxMy + rowg + (int64_t)b * P.Mx + a] = v;
+              return;
+            }
+            v = 0.0;
+            if (b == 0 && ty > 0) {
+              if (a == 0 && tx > 0) v += e[(tid - TX - 1) * S::ESTR + K * ND + K];
+              v += e[(tid - TX) * S::ESTR + K * ND + a];
+            }
+            if (a == 0 && tx > 0) v += e[(tid - 1) * S::ESTR + b * ND + K];
+            v += e[tid * S::ESTR + b * ND + a];
+            const int X = K * tx + a, Y = K * ty + b;
+            const bool sh = zsh || (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) ||
+                            (Y == LY - 1 && highY);
+            if (sh) {
+              (o == 0 ? shell0 : shell1)[(int64_t)cid * P.shell_stride + shell_rank(X, Y, lz, LX, LY, LZ)] = v;
+            } else {
+              const int gx = K * ex0 + X, gy = K * ey0 + Y;
+              const bool dir = zdir || (!keep && (((P.faces & 1u) && gx == 0) || ((P.faces & 2u) && gx == P.Mx - 1) ||
+                                                  ((P.faces & 4u) && gy == 0) || ((P.faces & 8u) && gy == P.My - 1)));
+              (o == 0 ? out0 : out1)[(int64_t)gz * MxMy + (int64_t)gy * P.Mx + gx] = dir ? 0.0 : v;
+            }
+          };
+          // main nodes a, b < K: with tx, ty > 0 they lie on no brick face and no x / y
+          // Dirichlet face, so only the plane decides
+          const bool fast = tx > 0 && ty > 0 && !zsh && !zdir;
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+            for (int b = 0; b < K; ++b)
+#pragma unroll
+              for (int a = 0; a < K; ++a) {
+                if (fast) node(o, a, b, true);
+                else node(o, a, b, false);
+              }
+          // the tile's last column / row also owns a = K / b = K
+          if (tx == bxr - 1 || ty == byr - 1) {
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o) {
+              if (tx == bxr - 1) {
+#pragma unroll
+                for (int b = 0; b < K; ++b) node(o, K, b, false);
+              }
+              if (ty == byr - 1) {
+#pragma unroll
+                for (int a = 0; a < K; ++a) node(o, a, K, false);
+              }
+              if (tx == bxr - 1 && ty == byr - 1) node(o, K, K, false);
+            }
+          }
+        }
+      }
+      if (last) {   // brick done: publish its epoch to the fix-up rows that read it
+        __syncthreads();
+        if (tid == 0) publish_brick(P.bdone, cid, epoch + 1);
+      }
+    }
+
+    prefetch();
+    if (++cz == bzr) {
+      cz = 0;
+      cbase += K * bzr + 1;
+      ++cn;
+    }
+  }
+}
+
+}  // namespace feod

@@ -34,6 +34,20 @@ struct Tables {
   double x[kMaxNQ];
 };
 
+// Device-resident scheduler state of one handle.
+//   sched  ticket counter: the CTA that draws the last ticket of a launch (#bricks + grid
+//          tickets in all) resets it to 0, so every launch starts from 0
+//   epoch  calls completed by the scatter fix-up; the operator kernel publishes
+//          bdone[b] = epoch + 1, the fix-up waits for it, and the fix-up's last CTA
+//          advances epoch (the next operator kernel reads it after griddepcontrol.wait)
+//   fdone  fix-up CTAs finished in the current launch (reset by the last one)
+struct DevState {
+  unsigned long long sched;
+  unsigned long long epoch;
+  unsigned long long fdone;
+  unsigned long long pad;
+};
+
 // Everything a fused operator kernel needs besides the vectors.
 struct OpParams {
   int nx, ny, nz;        // elements per axis
@@ -51,16 +65,73 @@ struct OpParams {
   double* lin;           // [E][NQ][lin_values][NQ][NQ] stored linearisation (MODE_LIN writes, MODE_PAJVP reads)
   int vjp_keep_rows;     // MODE_VJP: 1 keeps every row of J^T w (feod_vjp), 0 applies P^T (adjoint solve)
   const double* rho;     // [E] (HEAT)
-  // dynamic brick scheduling: tickets atomicAdd(sched, 1) - sched_base < #bricks
-  // are bricks, the rest end a CTA; the host advances sched_base by #bricks + grid
-  unsigned long long* sched;
-  unsigned long long sched_base;
-  // fix-up dependencies: bdone[b] = sched_base + 1 of the last call whose IO warp
-  // finished brick b's stores (release); fixrows = the fix-up rows in launch order
+  // dynamic brick scheduling and the scatter fix-up's dependencies, all on the device
+  // (DevState): the kernel arguments do not change from call to call, so a sequence of
+  // calls can be captured in a CUDA graph
+  DevState* ds;
+  // bdone[b] = epoch + 1 of the last call whose operator kernel finished brick b's
+  // stores (release); fixrows = the fix-up rows in launch order
   unsigned long long* bdone;
   const int2* fixrows;
   int nfixrows;
+  // brick shape in elements (the fix-up reads it at run time; both kernel families)
+  int tbx, tby, tbz;
+  // per-point streams (metric, stored linearisation): element (ex, ey, ez) lives in
+  // chunk ((ez ny + ey) pnbx + ex / ptx), its values interleaved with the ptx - 1 other
+  // elements of the chunk: value w of the element at chunk * (nv q^3 ptx) + w ptx + ex % ptx.
+  // ptx = 1 (pnbx = nx) is plain element-major; the column kernel (Q1, Q2) uses ptx = its
+  // tile width, so that a warp's threads (consecutive elements) read consecutive doubles
+  int ptx, pnbx;
 };
+
+// Base index and stride of an element's per-point values (OpParams::ptx).
+FEOD_HD int64_t pt_base(const OpParams& P, int ex, int ey, int ez, int nvq3) {
+  const int64_t chunk = ((int64_t)ez * P.ny + ey) * P.pnbx + ex / P.ptx;
+  return chunk * (int64_t)nvq3 * P.ptx + ex % P.ptx;
+}
+
+#ifdef __CUDACC__
+FEOD_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Streaming load that the compiler may not sink toward its use (per-point streams).
+FEOD_DEV double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// mbarriers (shared memory, CTA scope)
+FEOD_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+FEOD_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+FEOD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+FEOD_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// 1D bulk copy global -> shared by the TMA engine, completion counted on bar
+// (16-byte aligned source, destination and size)
+FEOD_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// L2 prefetch of a contiguous byte range by the bulk-copy engine (no completion
+// tracking); start and size must be 16-byte multiples.
+FEOD_DEV void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+#endif
 
 FEOD_HD bool is_dirichlet(int X, int Y, int Z, int Mx, int My, int Mz, uint32_t faces) {
   return ((faces & 1u) && X == 0) || ((faces & 2u) && X == Mx - 1) ||
@@ -84,19 +155,5 @@ FEOD_HD int shell_rank(int X, int Y, int Z, int LX, int LY, int LZ) {
 FEOD_HD int shell_size(int LX, int LY, int LZ) {
   return LX * LY * LZ - (LX - 2) * (LY - 2) * (LZ - 2);
 }
-
-// Brick shape for order k = ND-1: a CTA owns a BX x BY tile of elements and
-// sweeps BZ element layers along z; one layer of BX*BY
-// elements is processed concurrently, NQ*NQ threads per element.
-// SB = sub-batches per layer: with SB = 2 the layer's even and odd element rows
-// (y) are processed one after the other by the same threads (half the threads
-// for twice the tile).
-template <int ND> struct BrickShape;
-template <> struct BrickShape<2> { static constexpr int BX = 8, BY = 8, BZ = 16, SB = 1; };
-template <> struct BrickShape<3> { static constexpr int BX = 4, BY = 4, BZ = 16, SB = 1; };
-template <> struct BrickShape<4> { static constexpr int BX = 4, BY = 4, BZ = 8, SB = 2; };
-template <> struct BrickShape<5> { static constexpr int BX = 4, BY = 2, BZ = 8, SB = 1; };
-template <> struct BrickShape<6> { static constexpr int BX = 2, BY = 2, BZ = 8, SB = 1; };
-template <> struct BrickShape<7> { static constexpr int BX = 2, BY = 2, BZ = 8, SB = 1; };
 
 }  // namespace feod

@@ -57,13 +57,15 @@ __global__ void __launch_bounds__(kDiagThreads) diag_color_kernel(const OpParams
   double pf[PF];
   auto load = [&](int e) {
     int ex, ey, ez;
-    const double* lin = P.lin + elem(e, ex, ey, ez) * (NL * NQ3);
+    elem(e, ex, ey, ez);
+    const int64_t px = P.ptx;   // interleaved per-point layout (pt_base, common.cuh)
+    const double* lin = P.lin + pt_base(P, ex, ey, ez, NL * NQ3);
 #pragma unroll
     for (int k = 0; k < PF; ++k) {
       const int t = tid + k * kDiagThreads;
       if (t < NT * NQ3) {
         const int term = t / NQ3, r = t % NQ3, l = r / NQ2, ji = r % NQ2;   // r = (l, j, i), i fastest
-        pf[k] = __ldcs(lin + l * NL * NQ2 + term * NQ2 + ji);
+        pf[k] = __ldcs(lin + (l * NL * NQ2 + term * NQ2 + ji) * px);
       }
     }
   };
@@ -134,28 +136,17 @@ __global__ void diag_dirichlet_kernel(const OpParams P, double* __restrict__ dia
 template <int ND, int NT>
 static cudaError_t diag_nd_t(const OpParams& P, const Tables& T, double* diag, cudaStream_t st) {
   constexpr size_t smem = sizeof(double) * (3 * ND * ND + NT * ND * ND * ND + NT * ND * ND * ND);
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(diag_color_kernel<ND, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e0 = cudaFuncSetAttribute(diag_color_kernel<ND, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem);
+  if (e0 != cudaSuccess) return e0;
+  int slots = 0;
+  if ((e0 = persistent_slots((const void*)diag_color_kernel<ND, NT>, kDiagThreads, smem, &slots)) != cudaSuccess)
+    return e0;
   for (int color = 0; color < 8; ++color) {
     const int hx = (P.nx + 1 - (color & 1)) / 2, hy = (P.ny + 1 - ((color >> 1) & 1)) / 2,
               hz = (P.nz + 1 - ((color >> 2) & 1)) / 2;
     const int64_t ne = (int64_t)hx * hy * hz;
     if (ne == 0) continue;
-    static int slots = 0;
-    if (slots == 0) {
-      int dev = 0, sms = 0, occ = 0;
-      cudaError_t e = cudaGetDevice(&dev);
-      if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, diag_color_kernel<ND, NT>, kDiagThreads, smem);
-      if (e != cudaSuccess) return e;
-      slots = sms * (occ > 0 ? occ : 1);
-    }
     const int64_t grid = ne < slots ? ne : slots;
     diag_color_kernel<ND, NT><<<(unsigned)grid, kDiagThreads, smem, st>>>(P, T, color, diag);
     cudaError_t e = cudaGetLastError();

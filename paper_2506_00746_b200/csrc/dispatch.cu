@@ -1,7 +1,32 @@
 // Order dispatch of the fused operator kernels.
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "kernels.h"
 
 namespace feod {
+
+cudaError_t persistent_slots(const void* kernel, int threads, size_t smem, int* slots) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;   // (kernel, device) -> SMs x occupancy
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({kernel, dev});
+    if (it != cache.end()) { *slots = it->second; return cudaSuccess; }
+  }
+  int sms = 0, occ = 0;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem)) != cudaSuccess) return e;
+  const int s = sms * (occ > 0 ? occ : 1);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[{kernel, dev}] = s;
+  *slots = s;
+  return cudaSuccess;
+}
 
 bool brick_info_nd(int nd, BrickInfo* bi) {
   switch (nd) {
@@ -40,15 +65,15 @@ cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const 
   return cudaErrorInvalidValue;
 }
 
-cudaError_t fixup_nd(int nd, const OpParams& P, unsigned long long epoch, const double* shell0, double* out0,
-                     const double* shell1, double* out1, cudaStream_t st) {
+cudaError_t fixup_nd(int nd, const OpParams& P, const double* shell0, double* out0, const double* shell1,
+                     double* out1, cudaStream_t st) {
   switch (nd) {
-    case 2: return fixup_order<2>(P, epoch, shell0, out0, shell1, out1, st);
-    case 3: return fixup_order<3>(P, epoch, shell0, out0, shell1, out1, st);
-    case 4: return fixup_order<4>(P, epoch, shell0, out0, shell1, out1, st);
-    case 5: return fixup_order<5>(P, epoch, shell0, out0, shell1, out1, st);
-    case 6: return fixup_order<6>(P, epoch, shell0, out0, shell1, out1, st);
-    case 7: return fixup_order<7>(P, epoch, shell0, out0, shell1, out1, st);
+    case 2: return fixup_order<2>(P, shell0, out0, shell1, out1, st);
+    case 3: return fixup_order<3>(P, shell0, out0, shell1, out1, st);
+    case 4: return fixup_order<4>(P, shell0, out0, shell1, out1, st);
+    case 5: return fixup_order<5>(P, shell0, out0, shell1, out1, st);
+    case 6: return fixup_order<6>(P, shell0, out0, shell1, out1, st);
+    case 7: return fixup_order<7>(P, shell0, out0, shell1, out1, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -120,8 +120,9 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
         M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
         W = wq * P.vol;
       } else {
-        const double* g = P.geom + (int64_t)e * (6 * Q) + qz * 6 * NQ * NQ + qy * NQ + qx;
-        M = {g[0], g[NQ * NQ], g[2 * NQ * NQ], g[3 * NQ * NQ], g[4 * NQ * NQ], g[5 * NQ * NQ]};
+        const int64_t px = P.ptx;   // interleaved per-point layout (pt_base, common.cuh)
+        const double* g = P.geom + pt_base(P, ex, ey, ez, 6 * Q) + (qz * 6 * NQ * NQ + qy * NQ + qx) * px;
+        M = {g[0], g[NQ * NQ * px], g[2 * NQ * NQ * px], g[3 * NQ * NQ * px], g[4 * NQ * NQ * px], g[5 * NQ * NQ * px]};
         const double det = M.xx * (M.yy * M.zz - M.yz * M.yz) - M.xy * (M.xy * M.zz - M.yz * M.xz) +
                            M.xz * (M.xy * M.yz - M.yy * M.xz);
         W = det / (wq * wq);
@@ -223,19 +224,14 @@ template <int ND, int MODEL, bool AFFINE, bool ELM>
 static cudaError_t elemat_launch(const OpParams& P, const Tables& T, const double* u, int e0, int ne, double* Ke,
                                  cudaStream_t st) {
   constexpr size_t smem = EmShape<ND>::SMEM;
-  static int grid = 0;
-  if (grid == 0) {
-    cudaError_t e = cudaFuncSetAttribute(elemat_kernel<ND, MODEL, AFFINE, ELM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, occ = 0;
-    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elemat_kernel<ND, MODEL, AFFINE, ELM>, kEmThreads,
-                                                           smem)) != cudaSuccess)
-      return e;
-    grid = sms * (occ > 0 ? occ : 1);
-  }
+  // per call (a handle may live on any device): the attribute, then the cached occupancy
+  cudaError_t e = cudaFuncSetAttribute(elemat_kernel<ND, MODEL, AFFINE, ELM>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int grid = 0;
+  if ((e = persistent_slots((const void*)elemat_kernel<ND, MODEL, AFFINE, ELM>, kEmThreads, smem, &grid)) !=
+      cudaSuccess)
+    return e;
   const int g = ne < grid ? ne : grid;
   if (g <= 0) return cudaSuccess;
   elemat_kernel<ND, MODEL, AFFINE, ELM><<<g, kEmThreads, smem, st>>>(P, T, u, e0, ne, Ke);

@@ -23,6 +23,7 @@
 // the operator kernel.
 #pragma once
 #include "common.cuh"
+#include "pointwise.cuh"
 
 namespace feod {
 
@@ -32,8 +33,7 @@ constexpr int kFixMaxThreads = 256;
 #endif
 
 // box extent of brick b along an axis (the last brick may be ragged)
-template <int K, int B>
-FEOD_HD int box_len(int b, int ne) { return K * min(B, ne - b * B) + 1; }
+FEOD_HD int box_len(int K, int B, int b, int ne) { return K * min(B, ne - b * B) + 1; }
 
 // contributors of global DOF index g along one axis: brick b[.] and local index l[.]
 // (two when g lies on an interior brick plane: the low brick first)
@@ -58,11 +58,17 @@ FEOD_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
 //   0 < lz < LZ-1, ly = 0:     lx + LX (LY + 2(lz-1))      + 2(lz-1)(LY-2)
 //   0 < lz < LZ-1, ly = LY-1:  lx + LX (LY + 2(lz-1) + 1)  + 2(lz-1)(LY-2)
 // so each contributor costs one IMAD per DOF: offset = U + C LX + (bx stride + lx).
-template <int K, int BX, int BY, int BZ, bool TWO>
-__global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P, unsigned long long epoch,
+// The brick shape (BX, BY, BZ elements) is read from P.tbx / tby / tbz: both kernel
+// families (plane_kernel, col_kernel) write the same shell layout for their own bricks.
+template <int K, bool TWO>
+__global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P,
                                                                const double* __restrict__ shell0, double* __restrict__ out0,
                                                                const double* __restrict__ shell1, double* __restrict__ out1) {
-  constexpr int PX = K * BX, PY = K * BY, PZ = K * BZ;
+  const int BX = P.tbx, BY = P.tby, BZ = P.tbz;
+  const int PX = K * BX, PY = K * BY, PZ = K * BZ;
+  // this call's epoch: the previous fix-up grid completed before this one launched
+  // (its primary, the operator kernel, starts only after it), so the value is current
+  const unsigned long long epoch = read_epoch(P.ds) + 1;
   const int2 rw = P.fixrows[blockIdx.x];
   const int set = rw.x >> 24, m = rw.x & 0xffffff, coord = rw.y;
   const int64_t bstride = P.shell_stride;
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P,
         const int q = 2 * cz + cy;
         U[q] = 0; C[q] = 0;
         if (cz < nz && cy < ny) {
-          const int LY = box_len<K, BY>(bya[cy], P.ny), LZ = box_len<K, BZ>(bza[cz], P.nz);
+          const int LY = box_len(K, BY, bya[cy], P.ny), LZ = box_len(K, BZ, bza[cz], P.nz);
           const int ly = lya[cy], lz = lza[cz];
           int A, Cc;
           if (lz == 0) { A = 0; Cc = ly; }
@@ -155,14 +161,14 @@ __global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P,
       if constexpr (TWO) out1[g0 + x] = dir ? 0.0 : s1;
     }
   } else {
-    const int LXa[2] = {PX + 1, box_len<K, BX>(m, P.nx)};
-    const int LZa[2] = {box_len<K, BZ>(bza[0], P.nz), box_len<K, BZ>(nz == 2 ? bza[1] : bza[0], P.nz)};
+    const int LXa[2] = {PX + 1, box_len(K, BX, m, P.nx)};
+    const int LZa[2] = {box_len(K, BZ, bza[0], P.nz), box_len(K, BZ, nz == 2 ? bza[1] : bza[0], P.nz)};
     const bool dxz = ((P.faces & 1u) && X == 0) || ((P.faces & 2u) && X == P.Mx - 1) ||
                      ((P.faces & 16u) && Z == 0) || ((P.faces & 32u) && Z == P.Mz - 1);
     for (int y = threadIdx.x; y < P.My; y += blockDim.x) {
       int byt[2], lyt[2], nyt;
       axis_contrib(y, PY, P.nby, byt, lyt, nyt);
-      const int LYa[2] = {box_len<K, BY>(byt[0], P.ny), box_len<K, BY>(nyt == 2 ? byt[1] : byt[0], P.ny)};
+      const int LYa[2] = {box_len(K, BY, byt[0], P.ny), box_len(K, BY, nyt == 2 ? byt[1] : byt[0], P.ny)};
       double v0[8], v1[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -191,13 +197,23 @@ __global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P,
   }
   // the fix-up grid must not complete before its primary (the operator kernel)
   if (blockIdx.x == gridDim.x - 1) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the last CTA to finish advances the epoch for the next call (all CTAs have read it)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&P.ds->fdone, 1ull) == (unsigned long long)gridDim.x - 1) {
+      P.ds->fdone = 0;
+      __threadfence();
+      atomicAdd(&P.ds->epoch, 1ull);
+    }
+  }
 }
 
 // Host: the fix-up rows, keyed by the largest brick index (= ticket) they read.
 // Entry: x = set << 24 | m, y = the row's fixed coordinate.
-template <int K, int BX, int BY, int BZ>
+template <int K>
 int fixup_rows(const OpParams& P, int2* rows, unsigned long long* keys) {
-  constexpr int PY = K * BY, PZ = K * BZ;
+  const int PY = K * P.tby, PZ = K * P.tbz;
   int c = 0;
   auto bmax = [](int g, int PS, int nb) { int b[2], l[2], k; axis_contrib(g, PS, nb, b, l, k); return b[k - 1]; };
   for (int m = 1; m < P.nby; ++m)
@@ -228,9 +244,9 @@ int fixup_rows(const OpParams& P, int2* rows, unsigned long long* keys) {
   return c;
 }
 
-template <int K, int BX, int BY, int BZ>
-cudaError_t launch_fixup_t(const OpParams& P, unsigned long long epoch, const double* shell0, double* out0,
-                           const double* shell1, double* out1, cudaStream_t st) {
+template <int K>
+cudaError_t launch_fixup_t(const OpParams& P, const double* shell0, double* out0, const double* shell1, double* out1,
+                           cudaStream_t st) {
   if (P.nfixrows == 0) return cudaSuccess;
   const int len = max(P.Mx, P.My);
   cudaLaunchConfig_t cfg = {};
@@ -252,9 +268,8 @@ cudaError_t launch_fixup_t(const OpParams& P, unsigned long long epoch, const do
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (shell1)
-    return cudaLaunchKernelEx(&cfg, fixup_kernel<K, BX, BY, BZ, true>, P, epoch, shell0, out0, shell1, out1);
-  return cudaLaunchKernelEx(&cfg, fixup_kernel<K, BX, BY, BZ, false>, P, epoch, shell0, out0,
-                            (const double*)nullptr, (double*)nullptr);
+    return cudaLaunchKernelEx(&cfg, fixup_kernel<K, true>, P, shell0, out0, shell1, out1);
+  return cudaLaunchKernelEx(&cfg, fixup_kernel<K, false>, P, shell0, out0, (const double*)nullptr, (double*)nullptr);
 }
 
 }  // namespace feod

@@ -3,16 +3,19 @@
 // of the trilinear map of each hexahedron (the linear,
 // solution-independent part of B that PAPER.md:25 keeps "excluded from the
 // differentiation loop"). One thread per (element, point); components xx yy zz
-// xy xz yz; layout [E][l][6][j][i] (component-major within each z-row l of points, x
-// fastest): the ND*ND threads that own an element's points in plane_kernel read
-// one contiguous 128-byte run per (row, component).
+// xy xz yz; per element [l][6][j][i] (component-major within each z-row l of points,
+// x fastest), elements interleaved by OpParams::ptx (pt_base, common.cuh): with
+// ptx = 1 (plane kernel) the ND*ND threads that own an element's points read one
+// contiguous run per (row, component); with ptx = TX (column kernel) the threads of
+// a tile row, one element each, read consecutive doubles.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace feod {
 
-__global__ void geometry_kernel(const double* __restrict__ verts, int nx, int ny, int nz, int nq, Tables T,
+__global__ void geometry_kernel(const double* __restrict__ verts, const OpParams P, int nq, Tables T,
                                 double* __restrict__ geom, int* __restrict__ bad) {
+  const int nx = P.nx, ny = P.ny, nz = P.nz;
   const int nq3 = nq * nq * nq;
   const int64_t total = (int64_t)nx * ny * nz * nq3;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -58,24 +61,25 @@ __global__ void geometry_kernel(const double* __restrict__ verts, int nx, int ny
     if (!(det > 0.0)) atomicExch(bad, 1);
     const double s = T.w[i] * T.w[j] * T.w[l] / det;
     const int nq2 = nq * nq;
-    double* g = geom + e * 6 * nq3 + l * 6 * nq2 + j * nq + i;
+    const int64_t px = P.ptx;
+    double* g = geom + pt_base(P, ex, ey, ez, 6 * nq3) + (l * 6 * nq2 + j * nq + i) * px;
     auto dot = [&](int r, int c) { return A[r][0] * A[c][0] + A[r][1] * A[c][1] + A[r][2] * A[c][2]; };
-    g[0 * nq2] = s * dot(0, 0);
-    g[1 * nq2] = s * dot(1, 1);
-    g[2 * nq2] = s * dot(2, 2);
-    g[3 * nq2] = s * dot(0, 1);
-    g[4 * nq2] = s * dot(0, 2);
-    g[5 * nq2] = s * dot(1, 2);
+    g[0 * nq2 * px] = s * dot(0, 0);
+    g[1 * nq2 * px] = s * dot(1, 1);
+    g[2 * nq2 * px] = s * dot(2, 2);
+    g[3 * nq2 * px] = s * dot(0, 1);
+    g[4 * nq2 * px] = s * dot(0, 2);
+    g[5 * nq2 * px] = s * dot(1, 2);
   }
 }
 
-cudaError_t launch_geometry(const double* verts, int nx, int ny, int nz, int nq, const Tables& T, double* geom,
-                            int* bad, cudaStream_t st) {
-  const int64_t total = (int64_t)nx * ny * nz * nq * nq * nq;
+cudaError_t launch_geometry(const double* verts, const OpParams& P, int nq, const Tables& T, double* geom, int* bad,
+                            cudaStream_t st) {
+  const int64_t total = (int64_t)P.nx * P.ny * P.nz * nq * nq * nq;
   const int threads = 256;
   const int64_t want = (total + threads - 1) / threads;
   const int blocks = (int)(want < 148 * 64 ? (want > 0 ? want : 1) : 148 * 64);
-  geometry_kernel<<<blocks, threads, 0, st>>>(verts, nx, ny, nz, nq, T, geom, bad);
+  geometry_kernel<<<blocks, threads, 0, st>>>(verts, P, nq, T, geom, bad);
   return cudaGetLastError();
 }
 

@@ -1,3 +1,3 @@
-// Fused operator kernels for Q1 (ND = NQ = 2).
+// Fused operator kernels for Q1 (ND = NQ = 2): the column kernel.
 #define FEOD_ND 2
-#include "inst.cuh"
+#include "inst_col.cuh"

@@ -1,3 +1,3 @@
-// Fused operator kernels for Q2 (ND = NQ = 3).
+// Fused operator kernels for Q2 (ND = NQ = 3): the column kernel.
 #define FEOD_ND 3
-#include "inst.cuh"
+#include "inst_col.cuh"

@@ -1,3 +1,3 @@
-// Fused operator kernels for Q3 (ND = NQ = 4).
+// Fused operator kernels for Q3 (ND = NQ = 4): the plane kernel.
 #define FEOD_ND 4
-#include "inst.cuh"
+#include "inst_plane.cuh"

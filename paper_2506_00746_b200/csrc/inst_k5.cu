@@ -1,3 +1,3 @@
-// Fused operator kernels for Q5 (ND = NQ = 6).
+// Fused operator kernels for Q5 (ND = NQ = 6): the plane kernel.
 #define FEOD_ND 6
-#include "inst.cuh"
+#include "inst_plane.cuh"

@@ -1,4 +1,4 @@
-// Instantiation of the fused operator kernel for one order (ND = k+1 nodes,
+// Instantiation of the plane kernel (Q3..Q6) for one order (ND = k+1 nodes,
 // NQ = k+1 points per axis): 7 modes x 3 models x {affine, stored metric}.
 #pragma once
 #include "kernels.h"
@@ -14,16 +14,9 @@ static cudaError_t launch_one(int nbricks, const OpParams& P, const Tables& T, c
                               int* grid_out) {
   using S = PShape<ND, MODE>;
   const size_t smem = S::SMEM_BYTES;
-  static int slots = 0;   // per instantiation; one device per process (replicas)
-  if (slots == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plane_kernel<ND, MODE, MODEL, AFF>, S::NT, smem);
-    if (e != cudaSuccess) return e;
-    slots = sms * (occ > 0 ? occ : 1);
-  }
+  int slots = 0;
+  cudaError_t e = persistent_slots((const void*)plane_kernel<ND, MODE, MODEL, AFF>, S::NT, smem, &slots);
+  if (e != cudaSuccess) return e;
   const int grid = nbricks < slots ? nbricks : slots;
   *grid_out = grid;
 #if FEOD_PDL_OPERATOR
@@ -81,7 +74,7 @@ static cudaError_t prep_mode() {
 template <>
 bool brick_info<FEOD_ND>(BrickInfo* bi) {
   using S = PShape<FEOD_ND, MODE_RES>;
-  bi->BX = S::BX; bi->BY = S::BY; bi->BZ = S::BZ; bi->threads = S::NT; bi->shell = S::SHELL;
+  bi->BX = S::BX; bi->BY = S::BY; bi->BZ = S::BZ; bi->threads = S::NT; bi->ptx = 1; bi->minb = S::MINB;
   bi->smem[MODE_RES] = PShape<FEOD_ND, MODE_RES>::SMEM_BYTES;
   bi->smem[MODE_JVP] = PShape<FEOD_ND, MODE_JVP>::SMEM_BYTES;
   bi->smem[MODE_JVPRES] = PShape<FEOD_ND, MODE_JVPRES>::SMEM_BYTES;
@@ -120,16 +113,14 @@ cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int grid, const
 }
 
 template <>
-cudaError_t fixup_order<FEOD_ND>(const OpParams& P, unsigned long long epoch, const double* shell0, double* out0,
-                                 const double* shell1, double* out1, cudaStream_t st) {
-  using S = PShape<FEOD_ND, MODE_RES>;
-  return launch_fixup_t<S::K, S::BX, S::BY, S::BZ>(P, epoch, shell0, out0, shell1, out1, st);
+cudaError_t fixup_order<FEOD_ND>(const OpParams& P, const double* shell0, double* out0, const double* shell1,
+                                 double* out1, cudaStream_t st) {
+  return launch_fixup_t<FEOD_ND - 1>(P, shell0, out0, shell1, out1, st);
 }
 
 template <>
 int fixup_rows_order<FEOD_ND>(const OpParams& P, int2* rows, unsigned long long* keys) {
-  using S = PShape<FEOD_ND, MODE_RES>;
-  return fixup_rows<S::K, S::BX, S::BY, S::BZ>(P, rows, keys);
+  return fixup_rows<FEOD_ND - 1>(P, rows, keys);
 }
 
 }  // namespace feod

@@ -15,18 +15,25 @@ struct OpPtrs {
   double* gout;
 };
 
-struct BrickInfo { int BX, BY, BZ, threads, shell; size_t smem[kModes]; };
+// Brick shape (elements) and kernel family of one order: ptx = per-point stream
+// interleave (OpParams::ptx: the column kernel's tile width, 1 for the plane kernel),
+// minb = resident CTAs per SM the kernel is built for.
+struct BrickInfo { int BX, BY, BZ, threads, ptx, minb; size_t smem[kModes]; };
 
-cudaError_t launch_geometry(const double* verts, int nx, int ny, int nz, int nq, const Tables& T, double* geom,
-                            int* bad, cudaStream_t st);
+// Resident CTAs of a persistent kernel on the current device (SMs x occupancy),
+// cached per (kernel, device) (dispatch.cu).
+cudaError_t persistent_slots(const void* kernel, int threads, size_t smem, int* slots);
+
+cudaError_t launch_geometry(const double* verts, const OpParams& P, int nq, const Tables& T, double* geom, int* bad,
+                            cudaStream_t st);
 
 // Per-order entry points (inst_kN.cu), ND = k+1, NQ = k+1.
 template <int ND> bool brick_info(BrickInfo* bi);
 template <int ND> cudaError_t prepare_order();
 template <int ND> cudaError_t launch_order(int mode, int model, bool affine, int grid, const OpParams& P,
                                            const Tables& T, const OpPtrs& p, cudaStream_t st, int* grid_out);
-template <int ND> cudaError_t fixup_order(const OpParams& P, unsigned long long epoch, const double* shell0,
-                                          double* out0, const double* shell1, double* out1, cudaStream_t st);
+template <int ND> cudaError_t fixup_order(const OpParams& P, const double* shell0, double* out0,
+                                          const double* shell1, double* out1, cudaStream_t st);
 template <int ND> int fixup_rows_order(const OpParams& P, int2* rows, unsigned long long* keys);
 
 #define FEOD_DECLARE_ORDER(ND)                                                                    \
@@ -34,8 +41,8 @@ template <int ND> int fixup_rows_order(const OpParams& P, int2* rows, unsigned l
   template <> cudaError_t prepare_order<ND>();                                                    \
   template <> cudaError_t launch_order<ND>(int mode, int model, bool affine, int grid, const OpParams& P, \
                                            const Tables& T, const OpPtrs& p, cudaStream_t st, int* grid_out); \
-  template <> cudaError_t fixup_order<ND>(const OpParams& P, unsigned long long epoch, const double* shell0, \
-                                          double* out0, const double* shell1, double* out1, cudaStream_t st); \
+  template <> cudaError_t fixup_order<ND>(const OpParams& P, const double* shell0, double* out0, \
+                                          const double* shell1, double* out1, cudaStream_t st); \
   template <> int fixup_rows_order<ND>(const OpParams& P, int2* rows, unsigned long long* keys);
 FEOD_DECLARE_ORDER(2)
 FEOD_DECLARE_ORDER(3)
@@ -48,8 +55,8 @@ bool brick_info_nd(int nd, BrickInfo* bi);
 cudaError_t prepare_nd(int nd);
 cudaError_t launch_nd(int nd, int mode, int model, bool affine, int grid, const OpParams& P, const Tables& T,
                       const OpPtrs& p, cudaStream_t st, int* grid_out);
-cudaError_t fixup_nd(int nd, const OpParams& P, unsigned long long epoch, const double* shell0, double* out0,
-                     const double* shell1, double* out1, cudaStream_t st);
+cudaError_t fixup_nd(int nd, const OpParams& P, const double* shell0, double* out0, const double* shell1,
+                     double* out1, cudaStream_t st);
 int fixup_rows_nd(int nd, const OpParams& P, int2* rows, unsigned long long* keys);
 
 // BLAS-1 (blas1.cu): deterministic fixed-grid two-stage reductions.

@@ -17,13 +17,22 @@ namespace feod {
 
 struct Metric { double xx, yy, zz, xy, xz, yz; };
 
-template <int MODEL, class T, class R>
+// DIAG: the metric is diagonal (uniform affine grid: M = w_q diag(cx, cy, cz)), so the
+// off-diagonal products are skipped (they are exact zeros; IEEE arithmetic would not
+// let the compiler drop x * 0.0 on its own).
+template <int MODEL, bool DIAG = false, class T, class R>
 FEOD_DEV void flux_hat(const T& u, const T gh[3], const Metric& M, double W, const R& rho,
                        const OpParams& P, T Fh[3]) {
   T a[3];
-  a[0] = gh[0] * M.xx + gh[1] * M.xy + gh[2] * M.xz;
-  a[1] = gh[0] * M.xy + gh[1] * M.yy + gh[2] * M.yz;
-  a[2] = gh[0] * M.xz + gh[1] * M.yz + gh[2] * M.zz;
+  if constexpr (DIAG) {
+    a[0] = gh[0] * M.xx;
+    a[1] = gh[1] * M.yy;
+    a[2] = gh[2] * M.zz;
+  } else {
+    a[0] = gh[0] * M.xx + gh[1] * M.xy + gh[2] * M.xz;
+    a[1] = gh[0] * M.xy + gh[1] * M.yy + gh[2] * M.yz;
+    a[2] = gh[0] * M.xz + gh[1] * M.yz + gh[2] * M.zz;
+  }
   T kappa;
   if constexpr (MODEL == PLAPLACE) {
     T s = (gh[0] * a[0] + gh[1] * a[1] + gh[2] * a[2]) * (1.0 / W) + P.eps2;

@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "dual.cuh"
 #include "physics.cuh"
+#include "pointwise.cuh"
 #if defined(FEOD_PROFILE_IO) || defined(FEOD_PROFILE_TAIL)
 #include <cstdio>
 #endif
@@ -200,7 +201,6 @@ struct PShape {
 };
 
 // ---- async copies and mbarriers (PTX) -----------------------------------------
-FEOD_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 // 8-byte asynchronous global -> shared copy (LDGSTS). The L-vector row pitch
 // 8(kn+1) B is not 16-byte aligned, so TMA tensor maps cannot describe it.
 FEOD_DEV void cp_async8(double* smem_dst, const double* gsrc) {
@@ -210,27 +210,6 @@ FEOD_DEV void cp_async8(double* smem_dst, const double* gsrc) {
 FEOD_DEV void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-FEOD_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-FEOD_DEV void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-FEOD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// Streaming metric load that the compiler may not sink toward its use.
-FEOD_DEV double ld_stream(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-
 // L2 prefetch of a contiguous byte range (bulk-copy engine; no completion tracking).
 // The bulk engine needs a 16-byte aligned start and a multiple of 16 bytes: the
 // range is widened to that (odd per-element strides, e.g. 9 x 27 doubles, exist).
@@ -349,6 +328,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
     // =========================== IO warp ===================================
     // loader cursor (brick lb, layer lz, ring base of the brick) and storer cursor
     // (brick sb, layer sz); tile-plane positions of this lane: idx = lane + 32 m
+    const unsigned long long epoch = read_epoch(P.ds);   // after griddepcontrol.wait: this call's epoch
     Brick gl, gs;
     int lz = 0, sz = 0, lbase = 0, ln = 0, sn = 0;   // loader / storer brick ordinals
     bool ldone = false;
@@ -452,8 +432,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       if (lz == 0) {   // claim the next brick and publish it
         int id = -1;
         if (lane == 0) {
-          const unsigned long long t = atomicAdd(P.sched, 1ull) - P.sched_base;
-          id = t < (unsigned long long)nbricks ? (int)t : -1;
+          id = claim_brick(P.ds, nbricks);
           bq[ln & 7] = id;
         }
         id = __shfl_sync(0xffffffffu, id, 0);
@@ -585,11 +564,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         sz = 0;
         if constexpr (S::NOUT > 0) {   // brick done: publish its epoch to the fix-up rows that read it
           __syncwarp();
-          if (lane == 0) {
-            __threadfence();
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(P.bdone + gs.b), "l"(P.sched_base + 1)
-                         : "memory");
-          }
+          if (lane == 0) publish_brick(P.bdone, gs.b, epoch + 1);
         }
       }
     }
@@ -829,92 +804,15 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         }
       }
       double F0[4], F1[4];   // Fx, Fy, Fz, V of output 0 (and 1)
-      if constexpr (MODE == MODE_RES) {
-        const double gh[3] = {Uxl[0], Uyl[0], Uzl[0]};
-        double Fh[3];
-        flux_hat<MODEL>(Ul[0], gh, M, W, rho_e, P, Fh);
-        F0[0] = Fh[0]; F0[1] = Fh[1]; F0[2] = Fh[2];
-        F0[3] = -P.f * W;
-      } else if constexpr (MODE == MODE_JVP || MODE == MODE_JVPRES) {
-        using D = dual<double>;
-        const D ud(Ul[0], Ul[1]);
-        const D gh[3] = {D(Uxl[0], Uxl[1]), D(Uyl[0], Uyl[1]), D(Uzl[0], Uzl[1])};
-        D Fh[3];
-        flux_hat<MODEL>(ud, gh, M, W, rho_e, P, Fh);
-        F0[0] = Fh[0].d; F0[1] = Fh[1].d; F0[2] = Fh[2].d;
-        F0[3] = 0.0;
-        if constexpr (MODE == MODE_JVPRES) {
-          F1[0] = Fh[0].v; F1[1] = Fh[1].v; F1[2] = Fh[2].v;
-          F1[3] = -P.f * W;
-        }
-      } else if constexpr (MODE == MODE_VJP) {
-        // J^T w at the point (field 1 is w): value channel gw . dFh/du, flux channel
-        // (dFh/dgh)^T gw. For the three models dFh/dgh = kappa M + c (M gh)(M gh)^T is
-        // symmetric (kappa depends on gh only through gh . M gh), so the transpose is the
-        // forward derivative along (0, gw); dFh/du is the one along (1, 0) (DESIGN.md §2 A17)
-        using D = dual<double>;
-        const D uw(Ul[0]);
-        const D gw[3] = {D(Uxl[0], Uxl[1]), D(Uyl[0], Uyl[1]), D(Uzl[0], Uzl[1])};
-        D Fg[3];
-        flux_hat<MODEL>(uw, gw, M, W, rho_e, P, Fg);
-        const D uu(Ul[0], 1.0);
-        const D gu[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
-        D Fu[3];
-        flux_hat<MODEL>(uu, gu, M, W, rho_e, P, Fu);
-        F0[0] = Fg[0].d; F0[1] = Fg[1].d; F0[2] = Fg[2].d;
-        F0[3] = Uxl[1] * Fu[0].d + Uyl[1] * Fu[1].d + Uzl[1] * Fu[2].d;
-      } else if constexpr (MODE == MODE_LIN) {
-        // r = F(u) as MODE_RES, and the linearisation of D at the point for MODE_PAJVP:
-        // A = dFh/dgh from three dual evaluations along e_x, e_y, e_z (symmetric,
-        // reading A17; the upper triangle is stored), b = dFh/du along (1, 0)
-        using D = dual<double>;
-        const D ud(Ul[0]);
-        double A[3][3];
-        D Fh[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const D gh[3] = {D(Uxl[0], k == 0 ? 1.0 : 0.0), D(Uyl[0], k == 1 ? 1.0 : 0.0), D(Uzl[0], k == 2 ? 1.0 : 0.0)};
-          flux_hat<MODEL>(ud, gh, M, W, rho_e, P, Fh);
-#pragma unroll
-          for (int m = 0; m < 3; ++m) A[m][k] = Fh[m].d;
-        }
-        F0[0] = Fh[0].v; F0[1] = Fh[1].v; F0[2] = Fh[2].v;
-        F0[3] = -P.f * W;
+      double lv[lin_values(MODEL)];
+      point_op<MODE, MODEL, AFFINE || MODE == MODE_PAJVP>(Ul, Uxl, Uyl, Uzl, M, W, rho_e, P, sv, F0, F1, gpart, lv);
+      if constexpr (MODE == MODE_LIN) {
         constexpr int NL = lin_values(MODEL);
-        double lv[NL];
-        lv[0] = A[0][0]; lv[1] = A[1][1]; lv[2] = A[2][2]; lv[3] = A[0][1]; lv[4] = A[0][2]; lv[5] = A[1][2];
-        if constexpr (NL == 9) {
-          const D uu(Ul[0], 1.0);
-          const D gu[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
-          D Fu[3];
-          flux_hat<MODEL>(uu, gu, M, W, rho_e, P, Fu);
-          lv[6] = Fu[0].d; lv[7] = Fu[1].d; lv[8] = Fu[2].d;
-        }
         if (evalid) {
-          double* lp = P.lin + eg * (NL * NQ3) + l * NL * NQ2 + gr * NQ + lic;
+          double* lp = P.lin + eg * (NL * NQ3) + l * NL * NQ2 + gr * NQ + lic;   // ptx = 1 (plane kernel)
 #pragma unroll
           for (int c = 0; c < NL; ++c) lp[c * NQ2] = lv[c];
         }
-      } else if constexpr (MODE == MODE_PAJVP) {
-        // J(u0) v from the stored linearisation: F' = A gh_v + b v (field 0 is v)
-        const double g0 = Uxl[0], g1 = Uyl[0], g2 = Uzl[0];
-        F0[0] = sv[0] * g0 + sv[3] * g1 + sv[4] * g2;
-        F0[1] = sv[3] * g0 + sv[1] * g1 + sv[5] * g2;
-        F0[2] = sv[4] * g0 + sv[5] * g1 + sv[2] * g2;
-        if constexpr (NSV == 9) {
-          F0[0] = fma(sv[6], Ul[0], F0[0]);
-          F0[1] = fma(sv[7], Ul[0], F0[1]);
-          F0[2] = fma(sv[8], Ul[0], F0[2]);
-        }
-        F0[3] = 0.0;
-      } else {   // MODE_DESIGN: seed d/drho; field 1 is lambda
-        using D = dual<double>;
-        const D ud(Ul[0]);
-        const D gh[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
-        const D rd(rho_e, 1.0);
-        D Fh[3];
-        flux_hat<MODEL>(ud, gh, M, W, rd, P, Fh);
-        gpart -= Uxl[1] * Fh[0].d + Uyl[1] * Fh[1].d + Uzl[1] * Fh[2].d;
       }
       // transposed z-contraction of the y, z and value channels at the point;
       // the x channel is kept for the batched transposed x-derivative below
@@ -926,7 +824,8 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         for (int c = 0; c < ND; ++c) {
           if constexpr (S::NCH == 3) PX[o][c] = fma(T.B[l][c], Fo[0], PX[o][c]);
           PY[o][c] = fma(T.B[l][c], Fo[1], PY[o][c]);
-          PZ[o][c] = fma(T.G[l][c], Fo[2], fma(T.B[l][c], Fo[3], PZ[o][c]));
+          if (value_channel(MODE, o)) PZ[o][c] = fma(T.G[l][c], Fo[2], fma(T.B[l][c], Fo[3], PZ[o][c]));
+          else PZ[o][c] = fma(T.G[l][c], Fo[2], PZ[o][c]);
         }
       }
     }
@@ -1038,7 +937,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   {
     unsigned long long tail_t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tail_t1));
-    if (tid == 0) printf("TAIL %d %llu %d %d %llu %llu\n", MODE, P.sched_base, blockIdx.x, L, tail_t0, tail_t1);
+    if (tid == 0) printf("TAIL %d %llu %d %d %llu %llu\n", MODE, 0ull, blockIdx.x, L, tail_t0, tail_t1);
   }
 #endif
 #ifdef FEOD_PROFILE_IO
