@@ -21,7 +21,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfeod.so")
+LIB_PATH = os.environ.get("FEOD_LIB") or os.path.join(HERE, "libfeod.so")   # FEOD_LIB: experiment builds
 
 PLAPLACE, NLDIFF, HEAT_DESIGN = 0, 1, 2
 FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3, -4

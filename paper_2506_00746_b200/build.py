@@ -37,18 +37,31 @@ def _stale(obj, src, hdrs):
     return any(os.path.getmtime(p) > t for p in [src] + hdrs)
 
 
-def build(verbose: bool = False, jobs: int | None = None, extra: list[str] | None = None) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, jobs: int | None = None, extra: list[str] | None = None,
+          lib: str | None = None) -> str:
+    """Compile and link libfeod. ``extra`` nvcc flags (experiment variants) build into
+    their own object directory (keyed by a hash of the flags) and, unless ``lib`` says
+    otherwise, link to abtest/libfeod_<hash>.so -- never over the default build."""
+    import hashlib
+    build_dir, out_lib = BUILD, LIB
+    if extra:
+        tag = hashlib.sha1(" ".join(extra).encode()).hexdigest()[:10]
+        build_dir = BUILD + "_" + tag
+        out_lib = os.path.join(ROOT, "abtest", f"libfeod_{tag}.so")
+    if lib:
+        out_lib = lib
+    os.makedirs(build_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(out_lib), exist_ok=True)
     cu, cpp, hdrs = _sources()
     cmds = []
     objs = []
     for f in cu:
-        src, obj = os.path.join(CSRC, f), os.path.join(BUILD, f + ".o")
+        src, obj = os.path.join(CSRC, f), os.path.join(build_dir, f + ".o")
         objs.append(obj)
         if _stale(obj, src, hdrs):
             cmds.append([NVCC, *ARCH, *NVFLAGS, *(extra or []), "-c", src, "-o", obj])
     for f in cpp:
-        src, obj = os.path.join(CSRC, f), os.path.join(BUILD, f + ".o")
+        src, obj = os.path.join(CSRC, f), os.path.join(build_dir, f + ".o")
         objs.append(obj)
         if _stale(obj, src, hdrs):
             cmds.append(["g++", "-O2", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-c", src, "-o", obj])
@@ -63,14 +76,14 @@ def build(verbose: bool = False, jobs: int | None = None, extra: list[str] | Non
                 sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
             if res.returncode:
                 raise RuntimeError(f"compile failed: {cmd[-3]}")
-    if cmds or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static", "-Xcompiler", "-fPIC"]
+    if cmds or not os.path.exists(out_lib) or any(os.path.getmtime(o) > os.path.getmtime(out_lib) for o in objs):
+        link = [NVCC, *ARCH, "-shared", "-o", out_lib, *objs, "-cudart", "static", "-Xcompiler", "-fPIC"]
         res = subprocess.run(link, capture_output=True, text=True)
         if verbose or res.returncode:
             sys.stderr.write(" ".join(link) + "\n" + res.stdout + res.stderr)
         if res.returncode:
             raise RuntimeError("link failed")
-    return LIB
+    return out_lib
 
 
 if __name__ == "__main__":

@@ -44,9 +44,18 @@
 
 namespace feod {
 
+#ifndef FEOD_COL_MINB_Q1
+#define FEOD_COL_MINB_Q1 4
+#endif
+#ifndef FEOD_COL_MINB_Q2
+#define FEOD_COL_MINB_Q2 2
+#endif
+#ifndef FEOD_COL_TY_Q2
+#define FEOD_COL_TY_Q2 8
+#endif
 template <int ND> struct ColTile;
-template <> struct ColTile<2> { static constexpr int TX = 32, TY = 4; };
-template <> struct ColTile<3> { static constexpr int TX = 16, TY = 8; };
+template <> struct ColTile<2> { static constexpr int TX = 32, TY = 4, MINB = FEOD_COL_MINB_Q1; };
+template <> struct ColTile<3> { static constexpr int TX = 16, TY = FEOD_COL_TY_Q2, MINB = FEOD_COL_MINB_Q2; };
 
 template <int ND, int MODE>
 struct CShape {
@@ -65,9 +74,8 @@ struct CShape {
   static constexpr int RING = NIN * RS * PLANE;
   // + 2 mbarriers, the brick queue (8 x int4) and the plane shifts (NIN x RS ints)
   static constexpr size_t SMEM_BYTES = sizeof(double) * (RING + EBP * EB) + 16 + 8 * 16 + ((NIN * RS * 4 + 15) / 16) * 16;
-  static constexpr int MINB = ND == 3 ? 2 : 4;
+  static constexpr int MINB = ColTile<ND>::MINB;
   static_assert(NT % 32 == 0, "whole warps");
-  static constexpr int RCPY = (NIN * (K + 1) * ROWS + 31) / 32;   // row copies per lane of warp 0 (at most)
 };
 
 template <int ND, int MODE, int MODEL, bool AFFINE>
@@ -130,37 +138,36 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
       const int ex0 = pq.y, ey0 = pq.z, ez0 = pq.w;
       const int LX = K * min(TX, P.nx - ex0) + 1, LY = K * min(TY, P.ny - ey0) + 1;
       const int bzr = min(BZ, P.nz - ez0);
-      if (warp == 0) {
-        // one bulk copy per (field, plane, row) of the layer's new planes, spread over the lanes
+      if (warp == S::NW - 1) {
+        // one bulk copy per (field, plane, row) of the layer's new planes: lane = row
+        // (the last warp: it has no perimeter work in the scatter)
         uint64_t* bar = &mb[pL & 1];
-        const int p0 = pz == 0 ? 0 : K * pz + 1, np = K * pz + K - p0 + 1;
-        const int nrow = NIN * np * LY;
+        const int p0 = pz == 0 ? 0 : K * pz + 1;
 #pragma unroll
-        for (int r0 = 0; r0 < S::RCPY * 32; r0 += 32) {
-          const int r = r0 + lane;
-          if (r < nrow) {
-            const int f = r / (np * LY), rem = r - f * (np * LY), pp = rem / LY, Y = rem - pp * LY;
-            const int p = p0 + pp, slot = (pbase + p) % RS;
-            const double* src = (f == 0 ? in0 : in1) + (int64_t)(K * ez0 + p) * MxMy + (int64_t)(K * ey0 + Y) * P.Mx + K * ex0;
-            const uint64_t ga = reinterpret_cast<uint64_t>(src);
-            const int sh = (int)((ga >> 3) & 1);           // this row's 8-byte phase
-            const int s0 = (int)(((ga >> 3) - (uint64_t)Y * P.Mx) & 1);   // the plane's first row's phase
-            if (Y == 0) psh[f * RS + slot] = s0;
-            const uint32_t bytes = (uint32_t)(((LX + sh) * 8 + 15) & ~15);
-            double* dst = ring + (f * RS + slot) * S::PLANE + (Y * VP + s0 - sh);
-            mbar_expect_tx(bar, bytes);
-            bulk_g2s(dst, reinterpret_cast<const void*>(ga & ~uint64_t(15)), bytes, bar);
+        for (int f = 0; f < NIN; ++f)
+          for (int p = p0; p <= K * pz + K; ++p) {
+            const int slot = (pbase + p) % RS;
+            for (int Y = lane; Y < LY; Y += 32) {
+              const double* src = (f == 0 ? in0 : in1) + (int64_t)(K * ez0 + p) * MxMy + (int64_t)(K * ey0 + Y) * P.Mx + K * ex0;
+              const uint64_t ga = reinterpret_cast<uint64_t>(src);
+              const int sh = (int)((ga >> 3) & 1);                            // this row's 8-byte phase
+              const int s0 = (int)(((ga >> 3) - (uint64_t)Y * P.Mx) & 1);     // the plane's first row's phase
+              if (Y == 0) psh[f * RS + slot] = s0;
+              const uint32_t bytes = (uint32_t)(((LX + sh) * 8 + 15) & ~15);
+              double* dst = ring + (f * RS + slot) * S::PLANE + (Y * VP + s0 - sh);
+              mbar_expect_tx(bar, bytes);
+              bulk_g2s(dst, reinterpret_cast<const void*>(ga & ~uint64_t(15)), bytes, bar);
+            }
           }
-        }
         __syncwarp();
         if (lane == 0) mbar_arrive(bar);
       }
       if constexpr (STREAM) {
         // the layer's per-point stream into L2 (bulk engine), one contiguous chunk per tile row
         const int byr = min(TY, P.ny - ey0);
-        if (tid >= 32 && tid - 32 < byr) {
+        if (tid < byr) {
           const double* sb = (MODE == MODE_PAJVP) ? P.lin : P.geom;
-          prefetch_l2_bulk(sb + pt_base(P, ex0, ey0 + tid - 32, ez0 + pz, NSV * NQ3),
+          prefetch_l2_bulk(sb + pt_base(P, ex0, ey0 + tid, ez0 + pz, NSV * NQ3),
                            (uint32_t)(sizeof(double) * NSV * NQ3 * TX));
         }
       }
@@ -199,7 +206,7 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
     const int ex = ex0 + tx, ey = ey0 + ty, ez = ez0 + cz;
     double rho_e = 1.0;
     if constexpr (MODEL == HEAT && MODE != MODE_PAJVP)
-      if (ev) rho_e = __ldg(P.rho + ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez));
+      if (ev) rho_e = ld_stream(P.rho + ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez));   // issued early (volatile)
     double* eb = ebuf + (S::EBP == 2 ? (L & 1) : 0) * S::EB;
     if (S::EBP == 1 && NOUT > 0) __syncthreads();   // single element buffer: previous scatter done
     mbar_wait(&mb[L & 1], (L >> 1) & 1);             // this layer's DOF planes landed
@@ -410,84 +417,84 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
     }
     __syncthreads();
 
-    // ---- G^T + P^T: the finished DOF planes of the layer (owner computes, fixed order).
-    // Thread (tx, ty) owns its element's nodes a, b < K (+ a = K on the tile's last column,
-    // b = K on its last row) and sums each node's <= 4 contributions in ascending element
-    // order: (ty-1, tx-1), (ty-1, tx), (ty, tx-1), (ty, tx).
+    // ---- G^T + P^T: the finished DOF planes of the layer, each node's <= 4 contributions
+    // summed in ascending element order (ty-1, tx-1), (ty-1, tx), (ty, tx-1), (ty, tx).
+    //  main pass      thread (tx, ty) owns its element's nodes a, b < K that are not on the
+    //                 tile plane's perimeter: never on an x / y brick face or Dirichlet face,
+    //                 so only the plane decides the destination (output row, the shell's
+    //                 z-face plane at rank X + LX Y, or a Dirichlet zero)
+    //  perimeter      thread p < 2(LX + LY) - 4 owns perimeter node p in the shell's ring
+    //  pass           order (row Y = 0, row Y = LY-1, then (X = 0, X = LX-1) per middle row)
     if constexpr (NOUT > 0) {
-      if (ev) {
-        const int LX = K * bxr + 1, LY = K * byr + 1, LZ = K * bzr + 1;
-        const bool lowX = ex0 > 0, highX = ex0 + bxr < P.nx, lowY = ey0 > 0, highY = ey0 + byr < P.ny;
-        const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
-        const bool keep = MODE == MODE_VJP && P.vjp_keep_rows;   // J^T w keeps every row (reading A17)
-        const int nfp = last ? K + 1 : K;
-        const int64_t rowg = (int64_t)(K * (ey0 + ty)) * P.Mx + K * (ex0 + tx);   // in-plane index of node (0, 0)
+      const int LX = K * bxr + 1, LY = K * byr + 1, LZ = K * bzr + 1;
+      const bool lowZ = ez0 > 0, highZ = ez0 + bzr < P.nz;
+      const bool keep = MODE == MODE_VJP && P.vjp_keep_rows;   // J^T w keeps every row (reading A17)
+      const int nfp = last ? K + 1 : K;
+      const int ring_len = 2 * LX + 2 * (LY - 2);
+      const int np = 2 * (LX + LY) - 4;   // perimeter nodes
 #pragma unroll
-        for (int c = 0; c < K + 1; ++c) {
-          if (c >= nfp) break;
-          const int lz = K * cz + c;
-          const int gz = K * ez0 + lz;
-          const bool zsh = (lz == 0 && lowZ) || (lz == LZ - 1 && highZ);
-          const bool zdir = !keep && (((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1));
-          // node (a, b) of output o: its contributions, then out / shell / Dirichlet zero
-          auto node = [&](int o, int a, int b, bool fast) {
-            const double* e = eb + (o * (K + 1) + c) * NT * S::ESTR;
-            double v;
-            if (fast) {   // all neighbours exist (tx, ty > 0) and the node is interior
-              v = 0.0;
-              if (b == 0) {
-                if (a == 0) v += e[(tid - TX - 1) * S::ESTR + K * ND + K];
-                v += e[(tid - TX) * S::ESTR + K * ND + a];
-              }
-              if (a == 0) v += e[(tid - 1) * S::ESTR + b * ND + K];
-              v += e[tid * S::ESTR + b * ND + a];
-              (o == 0 ? out0 : out1)[(int64_t)gz * MxMy + rowg + (int64_t)b * P.Mx + a] = v;
-              return;
-            }
-            v = 0.0;
-            if (b == 0 && ty > 0) {
-              if (a == 0 && tx > 0) v += e[(tid - TX - 1) * S::ESTR + K * ND + K];
-              v += e[(tid - TX) * S::ESTR + K * ND + a];
-            }
-            if (a == 0 && tx > 0) v += e[(tid - 1) * S::ESTR + b * ND + K];
-            v += e[tid * S::ESTR + b * ND + a];
-            const int X = K * tx + a, Y = K * ty + b;
-            const bool sh = zsh || (X == 0 && lowX) || (X == LX - 1 && highX) || (Y == 0 && lowY) ||
-                            (Y == LY - 1 && highY);
-            if (sh) {
-              (o == 0 ? shell0 : shell1)[(int64_t)cid * P.shell_stride + shell_rank(X, Y, lz, LX, LY, LZ)] = v;
-            } else {
-              const int gx = K * ex0 + X, gy = K * ey0 + Y;
-              const bool dir = zdir || (!keep && (((P.faces & 1u) && gx == 0) || ((P.faces & 2u) && gx == P.Mx - 1) ||
-                                                  ((P.faces & 4u) && gy == 0) || ((P.faces & 8u) && gy == P.My - 1)));
-              (o == 0 ? out0 : out1)[(int64_t)gz * MxMy + (int64_t)gy * P.Mx + gx] = dir ? 0.0 : v;
-            }
-          };
-          // main nodes a, b < K: with tx, ty > 0 they lie on no brick face and no x / y
-          // Dirichlet face, so only the plane decides
-          const bool fast = tx > 0 && ty > 0 && !zsh && !zdir;
+      for (int c = 0; c < K + 1; ++c) {
+        if (c >= nfp) break;
+        const int lz = K * cz + c;
+        const int gz = K * ez0 + lz;
+        const bool zlo = lz == 0 && lowZ, zhi = lz == LZ - 1 && highZ;
+        const bool zdir = !keep && (((P.faces & 16u) && gz == 0) || ((P.faces & 32u) && gz == P.Mz - 1));
+        // z-face planes go to the shell whole: rank X + LX Y (+ the top plane's offset)
+        const int64_t zsh_off = (int64_t)cid * P.shell_stride + (zhi ? LX * LY + (LZ - 2) * ring_len : 0);
 #pragma unroll
-          for (int o = 0; o < NOUT; ++o)
+        for (int o = 0; o < NOUT; ++o) {
+          const double* e = eb + (o * (K + 1) + c) * NT * S::ESTR;
+          double* outo = o == 0 ? out0 : out1;
+          double* sho = o == 0 ? shell0 : shell1;
+          if (ev) {
 #pragma unroll
             for (int b = 0; b < K; ++b)
 #pragma unroll
               for (int a = 0; a < K; ++a) {
-                if (fast) node(o, a, b, true);
-                else node(o, a, b, false);
+                if ((a == 0 && tx == 0) || (b == 0 && ty == 0)) continue;   // perimeter node
+                double v = 0.0;
+                if (b == 0) {
+                  if (a == 0) v += e[(tid - TX - 1) * S::ESTR + K * ND + K];
+                  v += e[(tid - TX) * S::ESTR + K * ND + a];
+                }
+                if (a == 0) v += e[(tid - 1) * S::ESTR + b * ND + K];
+                v += e[tid * S::ESTR + b * ND + a];
+                const int X = K * tx + a, Y = K * ty + b;
+                if (zlo || zhi) sho[zsh_off + X + LX * Y] = v;
+                else outo[(int64_t)gz * MxMy + (int64_t)(K * ey0 + Y) * P.Mx + K * ex0 + X] = zdir ? 0.0 : v;
               }
-          // the tile's last column / row also owns a = K / b = K
-          if (tx == bxr - 1 || ty == byr - 1) {
-#pragma unroll
-            for (int o = 0; o < NOUT; ++o) {
-              if (tx == bxr - 1) {
-#pragma unroll
-                for (int b = 0; b < K; ++b) node(o, K, b, false);
-              }
-              if (ty == byr - 1) {
-#pragma unroll
-                for (int a = 0; a < K; ++a) node(o, a, K, false);
-              }
-              if (tx == bxr - 1 && ty == byr - 1) node(o, K, K, false);
+          }
+          // perimeter pass (threads 0 .. np-1)
+          for (int pp = tid; pp < np; pp += NT) {
+            int X, Y;
+            if (pp < LX) { X = pp; Y = 0; }
+            else if (pp < 2 * LX) { X = pp - LX; Y = LY - 1; }
+            else { const int r = pp - 2 * LX; Y = 1 + (r >> 1); X = (r & 1) ? LX - 1 : 0; }
+            // contributing elements along x and y (the low one first), and local node indices
+            const int cx1 = min(X / K, bxr - 1), cy1 = min(Y / K, byr - 1);
+            const int ax1 = X - K * cx1, ay1 = Y - K * cy1;
+            const bool two_x = ax1 == 0 && cx1 > 0, two_y = ay1 == 0 && cy1 > 0;
+            double v = 0.0;
+            if (two_y) {
+              if (two_x) v += e[((cy1 - 1) * TX + cx1 - 1) * S::ESTR + K * ND + K];
+              v += e[((cy1 - 1) * TX + cx1) * S::ESTR + K * ND + ax1];
+            }
+            if (two_x) v += e[(cy1 * TX + cx1 - 1) * S::ESTR + ay1 * ND + K];
+            v += e[(cy1 * TX + cx1) * S::ESTR + ay1 * ND + ax1];
+            const bool xyface = (X == 0 && ex0 > 0) || (X == LX - 1 && ex0 + bxr < P.nx) || (Y == 0 && ey0 > 0) ||
+                                (Y == LY - 1 && ey0 + byr < P.ny);
+            if (zlo || zhi) {
+              sho[zsh_off + X + LX * Y] = v;
+            } else if (xyface) {   // common.cuh shell_rank: the ring (rank pp) on middle planes
+              const int rk = lz == 0 ? X + LX * Y
+                             : lz == LZ - 1 ? LX * LY + (LZ - 2) * ring_len + X + LX * Y
+                                            : LX * LY + (lz - 1) * ring_len + pp;
+              sho[(int64_t)cid * P.shell_stride + rk] = v;
+            } else {
+              const int gx = K * ex0 + X, gy = K * ey0 + Y;
+              const bool dir = zdir || (!keep && (((P.faces & 1u) && gx == 0) || ((P.faces & 2u) && gx == P.Mx - 1) ||
+                                                  ((P.faces & 4u) && gy == 0) || ((P.faces & 8u) && gy == P.My - 1)));
+              outo[(int64_t)gz * MxMy + (int64_t)gy * P.Mx + gx] = dir ? 0.0 : v;
             }
           }
         }

@@ -1,6 +1,7 @@
 #!/bin/bash
-# A/B the abtest/libfeod_<v>.so variants (VARIANTS) on WL workloads via exp_variants.py.
+# A/B the abtest/libfeod_<v>.so variants (VARIANTS, "base" = the in-tree build) on the
+# WL workloads and CALLS (tools/kt.py); the in-tree library is never overwritten.
 for v in ${VARIANTS:-base}; do
-  cp abtest/libfeod_$v.so paper_2506_00746_b200/libfeod.so
-  echo "== $v"; ONLY=${ONLY:-} timeout 200 python tools/exp_variants.py ${WL:-C3 C2} | grep label
+  lib=abtest/libfeod_$v.so; [ "$v" = base ] && lib=paper_2506_00746_b200/libfeod.so
+  for w in ${WL:-C5}; do echo "== $v"; FEOD_LIB=$PWD/$lib timeout 300 python tools/kt.py $w ${CALLS:-jvp residual}; done
 done
