@@ -113,8 +113,8 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
     bq[slot & 7] = q;
   };
   if (tid == 0) {
-    mbar_init(&mb[0], 1);
-    mbar_init(&mb[1], 1);
+    mbar_init(&mb[0], S::NW);   // one arrival per warp (each issues its share of the row copies)
+    mbar_init(&mb[1], S::NW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");   // previous call's results are visible
@@ -138,27 +138,26 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
       const int ex0 = pq.y, ey0 = pq.z, ez0 = pq.w;
       const int LX = K * min(TX, P.nx - ex0) + 1, LY = K * min(TY, P.ny - ey0) + 1;
       const int bzr = min(BZ, P.nz - ez0);
-      if (warp == S::NW - 1) {
-        // one bulk copy per (field, plane, row) of the layer's new planes: lane = row
-        // (the last warp: it has no perimeter work in the scatter)
+      {
+        // one bulk copy per (field, plane, row) of the layer's new planes: warp w takes the
+        // (field, plane) pairs w, w + NW, ..., lane = row; every warp's lane 0 arrives
         uint64_t* bar = &mb[pL & 1];
-        const int p0 = pz == 0 ? 0 : K * pz + 1;
-#pragma unroll
-        for (int f = 0; f < NIN; ++f)
-          for (int p = p0; p <= K * pz + K; ++p) {
-            const int slot = (pbase + p) % RS;
-            for (int Y = lane; Y < LY; Y += 32) {
-              const double* src = (f == 0 ? in0 : in1) + (int64_t)(K * ez0 + p) * MxMy + (int64_t)(K * ey0 + Y) * P.Mx + K * ex0;
-              const uint64_t ga = reinterpret_cast<uint64_t>(src);
-              const int sh = (int)((ga >> 3) & 1);                            // this row's 8-byte phase
-              const int s0 = (int)(((ga >> 3) - (uint64_t)Y * P.Mx) & 1);     // the plane's first row's phase
-              if (Y == 0) psh[f * RS + slot] = s0;
-              const uint32_t bytes = (uint32_t)(((LX + sh) * 8 + 15) & ~15);
-              double* dst = ring + (f * RS + slot) * S::PLANE + (Y * VP + s0 - sh);
-              mbar_expect_tx(bar, bytes);
-              bulk_g2s(dst, reinterpret_cast<const void*>(ga & ~uint64_t(15)), bytes, bar);
-            }
+        const int p0 = pz == 0 ? 0 : K * pz + 1, npl = K * pz + K - p0 + 1;
+        for (int fp = warp; fp < NIN * npl; fp += S::NW) {
+          const int f = fp / npl, p = p0 + fp - f * npl;
+          const int slot = (pbase + p) % RS;
+          for (int Y = lane; Y < LY; Y += 32) {
+            const double* src = (f == 0 ? in0 : in1) + (int64_t)(K * ez0 + p) * MxMy + (int64_t)(K * ey0 + Y) * P.Mx + K * ex0;
+            const uint64_t ga = reinterpret_cast<uint64_t>(src);
+            const int sh = (int)((ga >> 3) & 1);                            // this row's 8-byte phase
+            const int s0 = (int)(((ga >> 3) - (uint64_t)Y * P.Mx) & 1);     // the plane's first row's phase
+            if (Y == 0) psh[f * RS + slot] = s0;
+            const uint32_t bytes = (uint32_t)(((LX + sh) * 8 + 15) & ~15);
+            double* dst = ring + (f * RS + slot) * S::PLANE + (Y * VP + s0 - sh);
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(dst, reinterpret_cast<const void*>(ga & ~uint64_t(15)), bytes, bar);
           }
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(bar);
       }
@@ -188,11 +187,7 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
 
   // ---- compute cursor
   int cn = 0, cz = 0, cbase = 0;
-  double CS[NO1][NQ2];   // top plane of the previous element of the column, after B_z^T
-#pragma unroll
-  for (int o = 0; o < NO1; ++o)
-#pragma unroll
-    for (int t = 0; t < NQ2; ++t) CS[o][t] = 0.0;
+  double rho_nx = 1.0;   // HEAT: rho of this thread's element one layer ahead
 
 #pragma unroll 1
   for (int L = 0;; ++L) {
@@ -205,8 +200,17 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
     const bool last = cz == bzr - 1;
     const int ex = ex0 + tx, ey = ey0 + ty, ez = ez0 + cz;
     double rho_e = 1.0;
-    if constexpr (MODEL == HEAT && MODE != MODE_PAJVP)
-      if (ev) rho_e = ld_stream(P.rho + ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez));   // issued early (volatile)
+    if constexpr (MODEL == HEAT && MODE != MODE_PAJVP) {
+      // rho one layer ahead: this layer's value came with the previous layer; request the next
+      // layer's (the next brick's first layer is claimed by now: the prefetch cursor is ahead)
+      rho_e = rho_nx;
+      if (L == 0 && ev) rho_e = ld_stream(P.rho + ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez));
+      int4 nq = cq;
+      int nz_ = cz + 1;
+      if (nz_ == bzr) { nq = bq[(cn + 1) & 7]; nz_ = 0; }
+      if (nq.x >= 0 && nq.y + tx < P.nx && nq.z + ty < P.ny && nq.w + nz_ < P.nz)
+        rho_nx = ld_stream(P.rho + (nq.y + tx) + (int64_t)P.nx * ((nq.z + ty) + (int64_t)P.ny * (nq.w + nz_)));
+    }
     double* eb = ebuf + (S::EBP == 2 ? (L & 1) : 0) * S::EB;
     if (S::EBP == 1 && NOUT > 0) __syncthreads();   // single element buffer: previous scatter done
     mbar_wait(&mb[L & 1], (L >> 1) & 1);             // this layer's DOF planes landed
@@ -383,12 +387,19 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
             for (int l = 1; l < NQ; ++l) s = fma(T.B[l][c], R[o][l * NQ2 + ji], s);
             Sz[c][ji] = s;
           }
+        // z-carry of the column's top plane (after B_z^T, before B_y^T B_x^T), parked in the
+        // element buffer's plane-K slot of the layer's parity, which only the brick's last
+        // layer uses for nodes: read from the previous layer's slot, written to this one's
         if (cz > 0) {
+          const double* cp = ebuf + (S::EBP == 2 ? ((L - 1) & 1) : 0) * S::EB + ((o * (K + 1) + K) * NT + tid) * S::ESTR;
 #pragma unroll
-          for (int ji = 0; ji < NQ2; ++ji) Sz[0][ji] = CS[o][ji] + Sz[0][ji];
+          for (int ji = 0; ji < NQ2; ++ji) Sz[0][ji] = cp[ji] + Sz[0][ji];
         }
+        if (!last) {
+          double* cp = eb + ((o * (K + 1) + K) * NT + tid) * S::ESTR;
 #pragma unroll
-        for (int ji = 0; ji < NQ2; ++ji) CS[o][ji] = Sz[K][ji];
+          for (int ji = 0; ji < NQ2; ++ji) cp[ji] = Sz[K][ji];
+        }
 #pragma unroll
         for (int c = 0; c < ND; ++c) {
           if (c == K && !last) break;
@@ -464,8 +475,8 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
                 else outo[(int64_t)gz * MxMy + (int64_t)(K * ey0 + Y) * P.Mx + K * ex0 + X] = zdir ? 0.0 : v;
               }
           }
-          // perimeter pass (threads 0 .. np-1)
-          for (int pp = tid; pp < np; pp += NT) {
+          // perimeter pass: threads rotated by a warp per plane, so that every warp gets a share
+          for (int pp = (tid + NT - 32 * ((c + o) % S::NW)) % NT; pp < np; pp += NT) {
             int X, Y;
             if (pp < LX) { X = pp; Y = 0; }
             else if (pp < 2 * LX) { X = pp - LX; Y = LY - 1; }
