@@ -163,6 +163,7 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   P.shell_stride = shell_size(order * P.tbx + 1, order * P.tby + 1, order * P.tbz + 1);
   P.faces = mesh->dirichlet_faces;
   P.half_pm2 = 0.5 * (coeffs->p - 2.0);
+  P.pcase = P.half_pm2 == 0.0 ? 0 : P.half_pm2 == 1.0 ? 1 : P.half_pm2 == 0.5 ? 2 : 3;
   P.eps2 = coeffs->eps * coeffs->eps;
   P.f = coeffs->f;
   const double hx = 1.0 / mesh->nx, hy = 1.0 / mesh->ny, hz = 1.0 / mesh->nz;

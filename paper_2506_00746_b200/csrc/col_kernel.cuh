@@ -45,22 +45,34 @@
 namespace feod {
 
 #ifndef FEOD_COL_MINB_Q1
-#define FEOD_COL_MINB_Q1 4
+#define FEOD_COL_MINB_Q1 0   // 0: per mode (residual 4 CTAs per SM, the two-field / linearising modes 3)
 #endif
 #ifndef FEOD_COL_MINB_Q2
 #define FEOD_COL_MINB_Q2 2
 #endif
+#ifndef FEOD_COL_MPD_Q1
+#define FEOD_COL_MPD_Q1 0   // Q1: per-point stream loads in flight (points ahead); 0: 3 at 4 CTAs, 4 at 3 CTAs
+#endif
 #ifndef FEOD_COL_TY_Q2
 #define FEOD_COL_TY_Q2 8
 #endif
-template <int ND> struct ColTile;
-template <> struct ColTile<2> { static constexpr int TX = 32, TY = 4, MINB = FEOD_COL_MINB_Q1; };
-template <> struct ColTile<3> { static constexpr int TX = 16, TY = FEOD_COL_TY_Q2, MINB = FEOD_COL_MINB_Q2; };
+// Tile (TX x TY element columns, one thread each) and resident CTAs per SM by order and
+// mode. Q1 (measured on C2): the residual at 4 CTAs per SM (128 registers), the heavier
+// modes at 3 (168 registers, no spills; JVP -3 %, J^T w -12 %, linearise -10 %).
+template <int ND, int MODE> struct ColTile;
+template <int MODE> struct ColTile<2, MODE> {
+  static constexpr int TX = 32, TY = 4;
+  static constexpr int MINB = FEOD_COL_MINB_Q1 > 0 ? FEOD_COL_MINB_Q1 : (MODE == MODE_RES ? 4 : 3);
+  static constexpr int MPD = FEOD_COL_MPD_Q1 > 0 ? FEOD_COL_MPD_Q1 : (MINB >= 4 ? 3 : 4);
+};
+template <int MODE> struct ColTile<3, MODE> {
+  static constexpr int TX = 16, TY = FEOD_COL_TY_Q2, MINB = FEOD_COL_MINB_Q2, MPD = 1;
+};
 
 template <int ND, int MODE>
 struct CShape {
   static constexpr int K = ND - 1;
-  static constexpr int TX = ColTile<ND>::TX, TY = ColTile<ND>::TY, NT = TX * TY, NW = NT / 32;
+  static constexpr int TX = ColTile<ND, MODE>::TX, TY = ColTile<ND, MODE>::TY, NT = TX * TY, NW = NT / 32;
   static constexpr int NIN = (MODE == MODE_RES || MODE == MODE_LIN || MODE == MODE_PAJVP) ? 1 : 2;
   static constexpr int NOUT = (MODE == MODE_DESIGN) ? 0 : (MODE == MODE_JVPRES ? 2 : 1);
   static constexpr int PITCH = (K * TX + 2) / 2 * 2;         // even row pitch (doubles); VP = PITCH + (Mx & 1)
@@ -74,7 +86,7 @@ struct CShape {
   static constexpr int RING = NIN * RS * PLANE;
   // + 2 mbarriers, the brick queue (8 x int4) and the plane shifts (NIN x RS ints)
   static constexpr size_t SMEM_BYTES = sizeof(double) * (RING + EBP * EB) + 16 + 8 * 16 + ((NIN * RS * 4 + 15) / 16) * 16;
-  static constexpr int MINB = ColTile<ND>::MINB;
+  static constexpr int MINB = ColTile<ND, MODE>::MINB, MPD = ColTile<ND, MODE>::MPD;
   static_assert(NT % 32 == 0, "whole warps");
 };
 
@@ -297,7 +309,7 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
       if constexpr (MODE == MODE_LIN) lp = P.lin + pt_base(P, ex, ey, ez, lin_values(MODEL) * NQ3);
       // the point stream, MPD points ahead in registers (streaming loads, L2-prefetched a
       // brick step earlier)
-      constexpr int MPD = ND == 2 ? 3 : 1;
+      constexpr int MPD = S::MPD;
       double snext[STREAM ? MPD : 1][STREAM ? NSV : 1];
       if constexpr (STREAM) {
 #pragma unroll

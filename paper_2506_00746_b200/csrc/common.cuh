@@ -57,6 +57,7 @@ struct OpParams {
   uint32_t faces;        // Dirichlet face bits
   // physics
   double half_pm2;       // (p-2)/2 (PLAPLACE)
+  int pcase;             // half_pm2 == 0 / 1 / 0.5 / other: 0 / 1 / 2 / 3 (dual.cuh pow_case)
   double eps2;           // eps^2
   double f;              // source
   // geometry: uniform grid (geom == nullptr): M = w_q diag(cx, cy, cz), W = w_q * vol

@@ -68,6 +68,22 @@ FEOD_HD double pow_special(double a, double e) {
 }
 template <class T> FEOD_HD dual<T> pow_special(dual<T> a, T e) { return pow(a, e); }
 
+// The same with the exponent's special case decided once per handle (OpParams::pcase:
+// 0 -> e = 0, 1 -> e = 1, 2 -> e = 0.5, 3 -> general): one integer test per point.
+FEOD_HD double pow_case(double a, double e, int pc) {
+  if (pc == 1) return a;
+  if (pc == 2) return ::sqrt(a);
+  if (pc == 0) return 1.0;
+  return ::pow(a, e);
+}
+template <class T> FEOD_HD dual<T> pow_case(dual<T> a, T e, int pc) {
+  if (pc == 1) return a;
+  if (pc == 2) return sqrt(a);
+  if (pc == 0) return {T(1), T(0)};
+  const T pv = ::pow(a.v, e);
+  return {pv, e * pv * a.d / a.v};
+}
+
 FEOD_HD double value(double a) { return a; }
 template <class T> FEOD_HD T value(dual<T> a) { return a.v; }
 

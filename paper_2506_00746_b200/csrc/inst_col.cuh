@@ -65,7 +65,7 @@ static cudaError_t prep_col_mode() {
 template <>
 bool brick_info<FEOD_ND>(BrickInfo* bi) {
   using S = CShape<FEOD_ND, MODE_RES>;
-  bi->BX = S::TX; bi->BY = S::TY; bi->BZ = 16; bi->threads = S::NT; bi->ptx = S::TX; bi->minb = S::MINB;
+  bi->BX = S::TX; bi->BY = S::TY; bi->BZ = 16; bi->threads = S::NT; bi->ptx = S::TX; bi->minb = CShape<FEOD_ND, MODE_JVP>::MINB;   // brick-depth choice: the JVP's residency
   bi->smem[MODE_RES] = CShape<FEOD_ND, MODE_RES>::SMEM_BYTES;
   bi->smem[MODE_JVP] = CShape<FEOD_ND, MODE_JVP>::SMEM_BYTES;
   bi->smem[MODE_JVPRES] = CShape<FEOD_ND, MODE_JVPRES>::SMEM_BYTES;

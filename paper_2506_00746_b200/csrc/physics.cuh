@@ -36,7 +36,7 @@ FEOD_DEV void flux_hat(const T& u, const T gh[3], const Metric& M, double W, con
   T kappa;
   if constexpr (MODEL == PLAPLACE) {
     T s = (gh[0] * a[0] + gh[1] * a[1] + gh[2] * a[2]) * (1.0 / W) + P.eps2;
-    kappa = pow_special(s, P.half_pm2);
+    kappa = pow_case(s, P.half_pm2, P.pcase);
   } else if constexpr (MODEL == NLDIFF) {
     kappa = u * u + 1.0;
   } else {
