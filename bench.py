@@ -91,46 +91,64 @@ def traffic_from_profiles(workload_name):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle reasons sampled DURING the timed region (B200_PROFILING.md clocks line).
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NVML (nvidia-ml-py) polled from a background thread every ~2 ms, so even a 10 ms
+    region gets several samples; only samples whose host timestamps fall between
+    mark_begin() and mark_end() count. nvidia-smi is the fallback (100 ms cadence)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
-        self.proc = None
+        self.samples = []
+        self.t_begin = self.t_end = None
+        self._stop = False
+        self._thr = None
+        self.max_mhz = None
 
     def start(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
         except Exception:
-            self.proc = None
+            self._thr = None
+            return
+
+        def run():
+            while not self._stop:
+                try:
+                    mhz = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    rs = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                except Exception:
+                    break
+                self.samples.append((time.perf_counter(), mhz, rs))
+                time.sleep(0.002)
+        self._thr = threading.Thread(target=run, daemon=True)
+        self._thr.start()
+
+    def mark_begin(self):
+        self.t_begin = time.perf_counter()
+
+    def mark_end(self):
+        self.t_end = time.perf_counter()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v == "Active":
-                    reasons.add(nm)
-        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        self._stop = True
+        if self._thr is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["nvml unavailable"]}
+        self._thr.join(timeout=5)
+        inside = [s for s in self.samples if self.t_begin is not None and self.t_begin <= s[0] <= self.t_end]
+        reasons = sorted({nm for _, _, rs in inside for nm, bit in self.REASONS.items() if rs & bit})
+        mhz = [m for _, m, _ in inside]
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "samples": len(inside), "source": "NVML, ~2 ms cadence, samples inside the timed region only",
+                "region_s": (self.t_end - self.t_begin) if self.t_begin is not None else None,
+                "reasons": reasons}
 
 
 def _oracle_step(pr, d, el):
@@ -152,7 +170,11 @@ def oracle_sample_size(pr, d, E, target_s):
 
 
 def cpu_oracle_sample(w, d, target_s=15.0, S=None):
-    """Oracle residual + JVP on a bounded element sample of w; returns GDOF/s, cores, sample, seconds."""
+    """Oracle residual + JVP on a bounded element sample of w (the first S elements).
+
+    Returns (rate, cores, sample, seconds, fraction): rate = the DOF applications the
+    sample accounts for (2 N S / E) / the measured seconds of that sample. Nothing is
+    extrapolated in time: the seconds are the sample's own wall time."""
     import oracle as O
     pr = O.Problem.from_workload(w, verts=d["verts"], rho=d.get("rho"))
     cores = len(os.sched_getaffinity(0))
@@ -164,8 +186,9 @@ def cpu_oracle_sample(w, d, target_s=15.0, S=None):
     frac = S / E
     value = 2 * w.n_dofs * frac / t / 1e9
     sample = (f"oracle residual+JVP (dense element matrices, numpy fp64) on the first {S} of {E} elements "
-              f"of {w.name} ({100 * frac:.3f} %), {t:.2f} s, throughput scaled by the element fraction")
-    return value, cores, sample, t
+              f"of {w.name} ({100 * frac:.3f} %, {t:.2f} s measured); rate = 2 N x {frac:.5f} DOF applications / "
+              f"that time")
+    return value, cores, sample, t, frac
 
 
 def cpu_model():
@@ -180,25 +203,32 @@ def cpu_model():
 
 
 def run_reference(args, w):
+    """The reference arm (tier rules: the CPU oracle, as it stands, on the host cores).
+
+    A step = one oracle residual + JVP over a bounded element sample of the workload,
+    sized so the whole --warmup W --steps K run ends within a few minutes. ms_per_step is
+    the measured time of one such step (the driver's clock sees exactly that); value is
+    the DOF applications the sample accounts for per second."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     d = W.draw(w)
     import oracle as O
     pr = O.Problem.from_workload(w, verts=d["verts"], rho=d.get("rho"))
-    per_step = min(20.0, 150.0 / max(1, args.steps + args.warmup))
+    per_step = min(10.0, 120.0 / max(1, args.steps + args.warmup))
     S = oracle_sample_size(pr, d, w.n_elems, per_step)
-    vals = []
+    ts = []
     for s in range(args.warmup + args.steps):
-        v, cores, sample, t = cpu_oracle_sample(w, d, S=S)
+        v, cores, sample, t, frac = cpu_oracle_sample(w, d, S=S)
         if s >= args.warmup:
-            vals.append(v)
-    value = statistics.median(vals)
+            ts.append(t)
+    t_step = statistics.mean(ts)
+    value = 2 * w.n_dofs * frac / t_step / 1e9
     line = {"impl": "reference", "metric": "residual+JVP throughput (GDOF/s, fp64)", "value": value,
             "unit": "GDOF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 2 * w.n_dofs / (value * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_of(w),
+            "config": config_of(w), "extrapolated": False, "sample_fraction": frac,
             "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "sample": sample,
                              "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -233,7 +263,7 @@ def config_of(w):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=1000)   # ~0.5 s timed region at C3
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="feod", choices=["feod", "reference"])
     ap.add_argument("--workload", default="C3", choices=list(W.CONFIGS))
@@ -285,17 +315,19 @@ def main():
     torch.cuda.synchronize()
     clocks = Clocks(local)
     clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.05)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark_begin()
     t0.record(stream)
     for s in range(args.steps):
         step(prof=ev[s])
     t1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark_end()
     if world > 1:
         dist.barrier()
     ck = clocks.stop()
@@ -346,7 +378,8 @@ def main():
     t_des = None
     if w.model == W.HEAT:
         g = torch.empty(op.n_elems, dtype=torch.float64, device=u.device)
-        t_des = time_call(lambda: op.design_grad(u, v, out=g))
+        lam = torch.as_tensor(d["lam"]).cuda()   # the recipe's lambda draw
+        t_des = time_call(lambda: op.design_grad(u, lam, out=g))
 
     # e2e through the C-ABI host-buffer path
     e2e = None
@@ -389,9 +422,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        val, cores, sample, _ = cpu_oracle_sample(w, d)
+        val, cores, sample, t_s, frac = cpu_oracle_sample(w, d)
         cpu = {"value": val, "unit": "GDOF/s", "cores": cores, "kind": "oracle", "sample": sample,
-               "cpu_model": cpu_model()}
+               "seconds": t_s, "sample_fraction": frac, "extrapolated": False, "cpu_model": cpu_model()}
 
     fl_res, fl_jvp = algorithmic_flops(w, "residual"), algorithmic_flops(w, "jvp")
     by_res, by_jvp = algorithmic_bytes(w, "residual"), algorithmic_bytes(w, "jvp")

@@ -109,8 +109,6 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
   int4* bq = reinterpret_cast<int4*>(mb + 2);                   // [8] (id, ex0, ey0, ez0) of the n-th brick
   int* psh = reinterpret_cast<int*>(bq + 8);                    // [NIN][RS] s0 of the plane in each ring slot
 
-  // the fix-up kernel may launch now: it waits per brick on P.bdone, not on this grid
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int tx = tid % TX, ty = tid / TX;
@@ -118,8 +116,11 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
   const int BZ = P.tbz;
   const int64_t MxMy = (int64_t)P.Mx * P.My;
   const int VP = S::PITCH + (P.Mx & 1);   // virtual row pitch of the ring planes
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // previous call's results are visible
+  // this call's epoch; the fix-up kernel may launch from here on (it waits per brick on P.bdone)
+  const unsigned long long epoch = call_begin(P.ds);
   auto claim = [&](int slot) {            // thread 0: claim a brick, publish (id, origin)
-    const int id = claim_brick(P.ds, nbricks);
+    const int id = claim_brick(P.ds, nbricks, epoch);
     int4 q = make_int4(-1, 0, 0, 0);
     if (id >= 0) q = make_int4(id, (id % P.nbx) * TX, ((id / P.nbx) % P.nby) * TY, (id / (P.nbx * P.nby)) * BZ);
     bq[slot & 7] = q;
@@ -129,8 +130,6 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
     mbar_init(&mb[1], S::NW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // previous call's results are visible
-  const unsigned long long epoch = read_epoch(P.ds);
   if (tid == 0) claim(0);
   __syncthreads();
 

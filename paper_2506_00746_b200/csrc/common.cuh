@@ -37,14 +37,13 @@ struct Tables {
 // Device-resident scheduler state of one handle.
 //   sched  ticket counter: the CTA that draws the last ticket of a launch (#bricks + grid
 //          tickets in all) resets it to 0, so every launch starts from 0
-//   epoch  calls completed by the scatter fix-up; the operator kernel publishes
-//          bdone[b] = epoch + 1, the fix-up waits for it, and the fix-up's last CTA
-//          advances epoch (the next operator kernel reads it after griddepcontrol.wait)
-//   fdone  fix-up CTAs finished in the current launch (reset by the last one)
+//   epoch  operator calls completed; a call's bricks publish bdone[b] = epoch + 1, and the
+//          same last-ticket CTA advances it (pointwise.cuh claim_brick)
+//   cur    epoch + 1 of the running call, for its scatter fix-up (pointwise.cuh call_begin)
 struct DevState {
   unsigned long long sched;
   unsigned long long epoch;
-  unsigned long long fdone;
+  unsigned long long cur;
   unsigned long long pad;
 };
 

@@ -28,6 +28,7 @@
 namespace feod {
 
 constexpr int kFixMaxThreads = 256;
+
 #ifndef FEOD_FIX_SLEEP_NS
 #define FEOD_FIX_SLEEP_NS 200   // back-off of a row waiting for its bricks
 #endif
@@ -58,17 +59,18 @@ FEOD_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
 //   0 < lz < LZ-1, ly = 0:     lx + LX (LY + 2(lz-1))      + 2(lz-1)(LY-2)
 //   0 < lz < LZ-1, ly = LY-1:  lx + LX (LY + 2(lz-1) + 1)  + 2(lz-1)(LY-2)
 // so each contributor costs one IMAD per DOF: offset = U + C LX + (bx stride + lx).
-// The brick shape (BX, BY, BZ elements) is read from P.tbx / tby / tbz: both kernel
-// families (plane_kernel, col_kernel) write the same shell layout for their own bricks.
-template <int K, bool TWO>
+// The brick shape: BX, BY are compile-time (the inner loops divide by them), the depth
+// BZ is read from P.tbz (the column kernel chooses it per mesh). Both kernel families
+// (plane_kernel, col_kernel) write the same shell layout for their own bricks.
+template <int K, int BX, int BY, bool TWO>
 __global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P,
                                                                const double* __restrict__ shell0, double* __restrict__ out0,
                                                                const double* __restrict__ shell1, double* __restrict__ out1) {
-  const int BX = P.tbx, BY = P.tby, BZ = P.tbz;
-  const int PX = K * BX, PY = K * BY, PZ = K * BZ;
-  // this call's epoch: the previous fix-up grid completed before this one launched
-  // (its primary, the operator kernel, starts only after it), so the value is current
-  const unsigned long long epoch = read_epoch(P.ds) + 1;
+  const int BZ = P.tbz;
+  constexpr int PX = K * BX, PY = K * BY;
+  const int PZ = K * BZ;
+  // the value this call's bricks publish (set by the operator kernel before it let this grid launch)
+  const unsigned long long epoch = ld_acquire_u64(&P.ds->cur);
   const int2 rw = P.fixrows[blockIdx.x];
   const int set = rw.x >> 24, m = rw.x & 0xffffff, coord = rw.y;
   const int64_t bstride = P.shell_stride;
@@ -197,17 +199,8 @@ __global__ void __launch_bounds__(kFixMaxThreads) fixup_kernel(const OpParams P,
   }
   // the fix-up grid must not complete before its primary (the operator kernel)
   if (blockIdx.x == gridDim.x - 1) asm volatile("griddepcontrol.wait;" ::: "memory");
-  // the last CTA to finish advances the epoch for the next call (all CTAs have read it)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&P.ds->fdone, 1ull) == (unsigned long long)gridDim.x - 1) {
-      P.ds->fdone = 0;
-      __threadfence();
-      atomicAdd(&P.ds->epoch, 1ull);
-    }
-  }
 }
+
 
 // Host: the fix-up rows, keyed by the largest brick index (= ticket) they read.
 // Entry: x = set << 24 | m, y = the row's fixed coordinate.
@@ -244,7 +237,7 @@ int fixup_rows(const OpParams& P, int2* rows, unsigned long long* keys) {
   return c;
 }
 
-template <int K>
+template <int K, int BX, int BY>
 cudaError_t launch_fixup_t(const OpParams& P, const double* shell0, double* out0, const double* shell1, double* out1,
                            cudaStream_t st) {
   if (P.nfixrows == 0) return cudaSuccess;
@@ -267,9 +260,13 @@ cudaError_t launch_fixup_t(const OpParams& P, const double* shell0, double* out0
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  cudaError_t e;
   if (shell1)
-    return cudaLaunchKernelEx(&cfg, fixup_kernel<K, true>, P, shell0, out0, shell1, out1);
-  return cudaLaunchKernelEx(&cfg, fixup_kernel<K, false>, P, shell0, out0, (const double*)nullptr, (double*)nullptr);
+    e = cudaLaunchKernelEx(&cfg, fixup_kernel<K, BX, BY, true>, P, shell0, out0, shell1, out1);
+  else
+    e = cudaLaunchKernelEx(&cfg, fixup_kernel<K, BX, BY, false>, P, shell0, out0, (const double*)nullptr,
+                           (double*)nullptr);
+  return e;
 }
 
 }  // namespace feod

@@ -106,7 +106,7 @@ cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int nbricks, co
 template <>
 cudaError_t fixup_order<FEOD_ND>(const OpParams& P, const double* shell0, double* out0, const double* shell1,
                                  double* out1, cudaStream_t st) {
-  return launch_fixup_t<FEOD_ND - 1>(P, shell0, out0, shell1, out1, st);
+  return launch_fixup_t<FEOD_ND - 1, CShape<FEOD_ND, MODE_RES>::TX, CShape<FEOD_ND, MODE_RES>::TY>(P, shell0, out0, shell1, out1, st);
 }
 
 template <>

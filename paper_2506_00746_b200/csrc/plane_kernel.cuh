@@ -61,6 +61,10 @@
 #ifndef FEOD_MPD
 #define FEOD_MPD 0
 #endif
+#ifndef FEOD_PLANE_VALUE_ALWAYS
+#define FEOD_PLANE_VALUE_ALWAYS 1   // the tangent modes' zero value channel kept: dropping it measured
+                                    // slower (C3 JVP 247 -> 257 us; schedule, not FLOPs)
+#endif
 #ifndef FEOD_MINB_OVERRIDE
 #define FEOD_MINB_OVERRIDE 0
 #endif
@@ -276,8 +280,6 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   uint64_t* e_empty = bars + 6;             // [2] layer z's element results consumed (IO -> compute)
   int* bq = reinterpret_cast<int*>(bars + 8);   // [8] claimed brick of the CTA's n-th brick (-1: done)
 
-  // the fix-up kernel may launch now: it waits per brick on P.bdone, not on this grid
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // warp-uniform: lets the compiler keep table constants in uniform registers
@@ -323,12 +325,13 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
   // barrier set-up above overlapped it; nothing global is read before this point
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
+  // this call's epoch; the fix-up kernel may launch from here on (it waits per brick on P.bdone)
+  const unsigned long long epoch = call_begin(P.ds);
 
   if (warp == S::NWC) {
     // =========================== IO warp ===================================
     // loader cursor (brick lb, layer lz, ring base of the brick) and storer cursor
     // (brick sb, layer sz); tile-plane positions of this lane: idx = lane + 32 m
-    const unsigned long long epoch = read_epoch(P.ds);   // after griddepcontrol.wait: this call's epoch
     Brick gl, gs;
     int lz = 0, sz = 0, lbase = 0, ln = 0, sn = 0;   // loader / storer brick ordinals
     bool ldone = false;
@@ -432,7 +435,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
       if (lz == 0) {   // claim the next brick and publish it
         int id = -1;
         if (lane == 0) {
-          id = claim_brick(P.ds, nbricks);
+          id = claim_brick(P.ds, nbricks, epoch);
           bq[ln & 7] = id;
         }
         id = __shfl_sync(0xffffffffu, id, 0);
@@ -824,7 +827,7 @@ plane_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, c
         for (int c = 0; c < ND; ++c) {
           if constexpr (S::NCH == 3) PX[o][c] = fma(T.B[l][c], Fo[0], PX[o][c]);
           PY[o][c] = fma(T.B[l][c], Fo[1], PY[o][c]);
-          if (value_channel(MODE, o)) PZ[o][c] = fma(T.G[l][c], Fo[2], fma(T.B[l][c], Fo[3], PZ[o][c]));
+          if (FEOD_PLANE_VALUE_ALWAYS || value_channel(MODE, o)) PZ[o][c] = fma(T.G[l][c], Fo[2], fma(T.B[l][c], Fo[3], PZ[o][c]));
           else PZ[o][c] = fma(T.G[l][c], Fo[2], PZ[o][c]);
         }
       }

@@ -116,10 +116,14 @@ FEOD_DEV void point_op(const double* Ul, const double* Uxl, const double* Uyl, c
 }
 
 // Brick tickets (DevState): the CTA that draws the launch's last ticket resets the
-// counter, so the next launch starts from 0 whatever happened on the host.
-FEOD_DEV int claim_brick(DevState* ds, int nbricks) {
+// counter (so the next launch starts from 0 whatever happened on the host) and advances
+// the epoch: every CTA of the launch read it before its first claim.
+FEOD_DEV int claim_brick(DevState* ds, int nbricks, unsigned long long epoch) {
   const unsigned long long t = atomicAdd(&ds->sched, 1ull);
-  if (t == (unsigned long long)nbricks + gridDim.x - 1) atomicExch(&ds->sched, 0ull);
+  if (t == (unsigned long long)nbricks + gridDim.x - 1) {
+    atomicExch(&ds->sched, 0ull);
+    atomicExch(&ds->epoch, epoch + 1);
+  }
   return t < (unsigned long long)nbricks ? (int)t : -1;
 }
 
@@ -127,6 +131,21 @@ FEOD_DEV unsigned long long read_epoch(const DevState* ds) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&ds->epoch) : "memory");
   return v;
+}
+
+// Start of an operator call, after griddepcontrol.wait (the previous call is complete):
+// read this call's epoch E; CTA 0 hands E + 1 (the value the bricks will publish) to the
+// scatter fix-up through DevState::cur, then the CTA lets its dependents launch (the
+// fence orders the store before the trigger, so the fix-up reads the current value).
+FEOD_DEV unsigned long long call_begin(DevState* ds) {
+  const unsigned long long e = read_epoch(ds);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(&ds->cur), "l"(e + 1) : "memory");
+    __threadfence();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  return e;
 }
 
 FEOD_DEV void publish_brick(unsigned long long* bdone, int b, unsigned long long value) {
