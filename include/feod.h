@@ -114,6 +114,11 @@ FEOD_API int feod_set_stream(feod_handle h, void* cuda_stream);
 FEOD_API int feod_set_rho(feod_handle h, const double* rho);
 FEOD_API int64_t feod_num_dofs(feod_handle h);
 FEOD_API int64_t feod_num_elems(feod_handle h);
+/* Diagnostic: the brick shape (elements per brick along x, y, z) the operator kernels
+ * tile the mesh with (their scatter seams: brick faces go through the fix-up kernel).
+ * Q1/Q2 use the column kernel (the depth bz is chosen per mesh), Q3..Q6 the plane
+ * kernel. Any of the pointers may be NULL. FEOD_EINVAL on a null handle. */
+FEOD_API int feod_brick_shape(feod_handle h, int* bx, int* by, int* bz);
 
 /* r = F(u)                               (Eq. 1)          */
 FEOD_API int feod_residual(feod_handle h, const double* u, double* r);

@@ -9,6 +9,9 @@ Models (BASELINE.json configs; SPEC.md lines 304, 313, 330 for the forms):
 * PLAPLACE (p-Laplacian, line 164):  D = k g,  k = (eps^2 + |g|^2)^((p-2)/2)
       dD/dg = k I + (p-2) s^((p-4)/2) g g^T ,  dD/du = 0
       p == 2: k = 1 and the second term is 0 (reading A12).
+      eps == 0 and g == 0 (s == 0), p > 2: dD/dg = 0, the limit of both terms as
+      g -> 0 (k ~ |g|^(p-2), (p-2) s^((p-4)/2) g g^T ~ |g|^(p-2)); written out so that
+      0 * inf does not produce NaN (reading A20).
 * NLDIFF (nonlinear diffusion):      D = (1+u^2) g
       dD/dg = (1+u^2) I ,  dD/du = 2 u g
 * HEAT (design problem):             D = rho^3 (1+u^2) g
@@ -48,7 +51,8 @@ def flux_dg(model, U, g, p=2.0, eps=0.0, rho=None):
             return np.broadcast_to(eye, g.shape + (3,)).copy()
         s = _s(g, eps)
         k = s ** ((p - 2.0) / 2.0)
-        c = (p - 2.0) * s ** ((p - 4.0) / 2.0)
+        pos = s > 0.0
+        c = np.where(pos, (p - 2.0) * np.where(pos, s, 1.0) ** ((p - 4.0) / 2.0), 0.0)   # A20 at s == 0
         return k[..., None, None] * eye + c[..., None, None] * g[..., :, None] * g[..., None, :]
     if model == NLDIFF:
         return (1.0 + U * U)[..., None, None] * eye

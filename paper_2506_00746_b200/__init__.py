@@ -29,7 +29,7 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 # every symbol include/feod.h declares (checked by tests/test_abi.py)
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
-           "feod_set_newton_linearization", "feod_jacobi_diag", "feod_adjoint_solve", "feod_element_matrices",
+           "feod_set_newton_linearization", "feod_brick_shape", "feod_jacobi_diag", "feod_adjoint_solve", "feod_element_matrices",
            "feod_design_grad", "feod_apply_host", "feod_newton_cg",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
@@ -71,6 +71,8 @@ def load_library(path: str = LIB_PATH):
     lib.feod_num_dofs.restype = i64
     lib.feod_num_elems.argtypes = [vp]
     lib.feod_num_elems.restype = i64
+    lib.feod_brick_shape.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                     ctypes.POINTER(ctypes.c_int)]
     lib.feod_residual.argtypes = [vp, dp, dp]
     lib.feod_jvp.argtypes = [vp, dp, dp, dp]
     lib.feod_jvp_res.argtypes = [vp, dp, dp, dp, dp]
@@ -144,7 +146,25 @@ class Operator:
             raise FeodError(FEOD_EINVAL, f"{name} must have {n} entries, got {x.numel()}")
         if x.device.type != "cuda":
             x = x.to(self.device)
+        elif x.device != self._cuda_device():
+            raise FeodError(FEOD_EINVAL, f"{name} lives on {x.device}, the operator on {self._cuda_device()}")
         return x.contiguous().view(-1)
+
+    def _cuda_device(self):
+        t = self._torch
+        d = self.device
+        return d if d.index is not None else t.device("cuda", t.cuda.current_device())
+
+    def _out(self, out, n, name="out", shape=None):
+        """Validate a caller-supplied output: float64, exactly n entries, this device, contiguous."""
+        t = self._torch
+        if out is None:
+            return t.empty(shape if shape is not None else (n,), dtype=t.float64, device=self._cuda_device())
+        if not isinstance(out, t.Tensor) or out.dtype != t.float64 or out.numel() != n:
+            raise FeodError(FEOD_EINVAL, f"{name} must be a float64 tensor with {n} entries")
+        if out.device != self._cuda_device() or not out.is_contiguous():
+            raise FeodError(FEOD_EINVAL, f"{name} must be contiguous on {self._cuda_device()}")
+        return out
 
     def _sync_stream(self):
         _check(self.lib.feod_set_stream(self.h, self._stream()))
@@ -158,14 +178,14 @@ class Operator:
     # ------------------------------------------------------------------ operations
     def residual(self, u, out=None):
         u = self._dev(u, self.n_dofs, "u")
-        r = out if out is not None else self._torch.empty_like(u)
+        r = self._out(out, self.n_dofs)
         self._sync_stream()
         _check(self.lib.feod_residual(self.h, u.data_ptr(), r.data_ptr()))
         return r
 
     def jvp(self, u, v, out=None):
         u, v = self._dev(u, self.n_dofs, "u"), self._dev(v, self.n_dofs, "v")
-        Jv = out if out is not None else self._torch.empty_like(u)
+        Jv = self._out(out, self.n_dofs)
         self._sync_stream()
         _check(self.lib.feod_jvp(self.h, u.data_ptr(), v.data_ptr(), Jv.data_ptr()))
         return Jv
@@ -173,7 +193,8 @@ class Operator:
     def jvp_res(self, u, v, out=None):
         """(F(u), J(u) v) from one dual pass (feod_jvp_res); out = (r, Jv) optional."""
         u, v = self._dev(u, self.n_dofs, "u"), self._dev(v, self.n_dofs, "v")
-        r, Jv = out if out is not None else (self._torch.empty_like(u), self._torch.empty_like(u))
+        r, Jv = (None, None) if out is None else out
+        r, Jv = self._out(r, self.n_dofs, "out[0]"), self._out(Jv, self.n_dofs, "out[1]")
         self._sync_stream()
         _check(self.lib.feod_jvp_res(self.h, u.data_ptr(), v.data_ptr(), r.data_ptr(), Jv.data_ptr()))
         return r, Jv
@@ -181,7 +202,7 @@ class Operator:
     def vjp(self, u, w, out=None):
         """J(u)^T w (feod_vjp): w's Dirichlet entries ignored, every row kept."""
         u, w = self._dev(u, self.n_dofs, "u"), self._dev(w, self.n_dofs, "w")
-        JTw = out if out is not None else self._torch.empty_like(u)
+        JTw = self._out(out, self.n_dofs)
         self._sync_stream()
         _check(self.lib.feod_vjp(self.h, u.data_ptr(), w.data_ptr(), JTw.data_ptr()))
         return JTw
@@ -189,7 +210,7 @@ class Operator:
     def linearize(self, u, out=None):
         """r = F(u), and store the pointwise linearisation at u (feod_linearize)."""
         u = self._dev(u, self.n_dofs, "u")
-        r = out if out is not None else self._torch.empty_like(u)
+        r = self._out(out, self.n_dofs)
         self._sync_stream()
         _check(self.lib.feod_linearize(self.h, u.data_ptr(), r.data_ptr()))
         return r
@@ -197,7 +218,7 @@ class Operator:
     def jvp_lin(self, v, out=None):
         """J(u) v at the u of the last linearize() (feod_jvp_lin)."""
         v = self._dev(v, self.n_dofs, "v")
-        Jv = out if out is not None else self._torch.empty_like(v)
+        Jv = self._out(out, self.n_dofs)
         self._sync_stream()
         _check(self.lib.feod_jvp_lin(self.h, v.data_ptr(), Jv.data_ptr()))
         return Jv
@@ -221,25 +242,32 @@ class Operator:
         u = self._dev(u, self.n_dofs, "u")
         ne = self.n_elems - e0 if ne is None else ne
         nn = (self.order + 1) ** 3
-        Ke = out if out is not None else self._torch.empty((ne, nn, nn), dtype=self._torch.float64, device=self.device)
+        if ne < 0 or e0 < 0 or e0 + ne > self.n_elems:
+            raise FeodError(FEOD_EINVAL, "element range out of bounds")
+        Ke = self._out(out, ne * nn * nn, shape=(ne, nn, nn))
         self._sync_stream()
         _check(self.lib.feod_element_matrices(self.h, u.data_ptr(), int(e0), int(ne), 1 if elm else 0, Ke.data_ptr()))
         return Ke
 
     def jacobi_diag(self, out=None):
         """Diagonal of J at the last linearize() (feod_jacobi_diag)."""
-        d = out if out is not None else self._torch.empty(self.n_dofs, dtype=self._torch.float64, device=self.device)
+        d = self._out(out, self.n_dofs)
         self._sync_stream()
         _check(self.lib.feod_jacobi_diag(self.h, d.data_ptr()))
         return d
 
     def design_grad(self, u, lam, out=None):
         u, lam = self._dev(u, self.n_dofs, "u"), self._dev(lam, self.n_dofs, "lam")
-        g = out if out is not None else self._torch.empty(self.n_elems, dtype=self._torch.float64,
-                                                           device=self.device)
+        g = self._out(out, self.n_elems)
         self._sync_stream()
         _check(self.lib.feod_design_grad(self.h, u.data_ptr(), lam.data_ptr(), g.data_ptr()))
         return g
+
+    def brick_shape(self):
+        """(bx, by, bz): elements per brick of the operator kernels (feod_brick_shape)."""
+        b = [ctypes.c_int() for _ in range(3)]
+        _check(self.lib.feod_brick_shape(self.h, *[ctypes.byref(x) for x in b]))
+        return tuple(x.value for x in b)
 
     def set_rho(self, rho):
         self._rho = self._dev(rho, self.n_elems, "rho")
@@ -254,7 +282,13 @@ class Operator:
         for x, name in ((a, "in0"), (b, "in1")):
             if x is not None and (x.device.type != "cpu" or x.dtype != t.float64 or x.numel() != self.n_dofs):
                 raise FeodError(FEOD_EINVAL, f"{name}: host float64 vector of length N expected")
-        res = out if out is not None else t.empty(n_out, dtype=t.float64, pin_memory=True)
+        if out is None:
+            res = t.empty(n_out, dtype=t.float64, pin_memory=True)
+        else:
+            res = out
+            if (not isinstance(res, t.Tensor) or res.device.type != "cpu" or res.dtype != t.float64
+                    or res.numel() != n_out or not res.is_contiguous()):
+                raise FeodError(FEOD_EINVAL, f"out: contiguous host float64 tensor of {n_out} entries expected")
         self._sync_stream()
         _check(self.lib.feod_apply_host(self.h, int(op), a.data_ptr(), 0 if b is None else b.data_ptr(),
                                         res.data_ptr()))
@@ -273,7 +307,9 @@ class Operator:
                                           ctypes.c_void_p(ev_end.cuda_event)))
 
     def dot(self, x, y):
-        x, y = self._dev(x, x.numel(), "x"), self._dev(y, y.numel(), "y")
+        if x.numel() != y.numel():
+            raise FeodError(FEOD_EINVAL, f"dot: x has {x.numel()} entries, y {y.numel()}")
+        x, y = self._dev(x, x.numel(), "x"), self._dev(y, x.numel(), "y")
         out = self._torch.empty(1, dtype=self._torch.float64, device=self.device)
         self._sync_stream()
         _check(self.lib.feod_dot(self.h, x.data_ptr(), y.data_ptr(), x.numel(), out.data_ptr()))

@@ -279,6 +279,14 @@ extern "C" int feod_profile_next(feod_handle h, void* ev_begin, void* ev_end) {
 extern "C" int64_t feod_num_dofs(feod_handle h) { return h ? h->N : -1; }
 extern "C" int64_t feod_num_elems(feod_handle h) { return h ? h->E : -1; }
 
+extern "C" int feod_brick_shape(feod_handle h, int* bx, int* by, int* bz) {
+  if (!h) return fail(FEOD_EINVAL, "feod_brick_shape: null handle");
+  if (bx) *bx = h->P.tbx;
+  if (by) *by = h->P.tby;
+  if (bz) *bz = h->P.tbz;
+  return FEOD_OK;
+}
+
 static int run_op(feod_handle h, int mode, const double* in0, const double* in1, double* out0, double* out1,
                   double* gout, const char* name) {
   if (h->poisoned) return fail(FEOD_ECUDA, std::string(name) + ": handle unusable after a failed launch");

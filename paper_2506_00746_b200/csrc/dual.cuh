@@ -45,9 +45,11 @@ template <class T> FEOD_HD dual<T> operator*(T a, dual<T> b) { return {a * b.v, 
 template <class T> FEOD_HD dual<T> operator/(dual<T> a, T b) { return {a.v / b, a.d / b}; }
 template <class T> FEOD_HD dual<T>& operator+=(dual<T>& a, dual<T> b) { a = a + b; return a; }
 
+// At a.v == 0 the derivative is taken as 0: the only way to reach it is the p-Laplacian
+// with eps = 0 at a zero gradient, where the flux tangent's limit is 0 (reading A20).
 template <class T> FEOD_HD dual<T> sqrt(dual<T> a) {
   const T s = ::sqrt(a.v);
-  return {s, a.d / (T(2) * s)};
+  return {s, s > T(0) ? a.d / (T(2) * s) : T(0)};
 }
 
 // pow with a real exponent; the special cases keep p = 2, 3, 4 exact and cheap.
@@ -56,7 +58,7 @@ template <class T> FEOD_HD dual<T> pow(dual<T> a, T e) {
   if (e == T(1)) return a;
   if (e == T(0.5)) return sqrt(a);
   const T pv = ::pow(a.v, e);
-  return {pv, e * pv * a.d / a.v};
+  return {pv, a.v != T(0) ? e * pv * a.d / a.v : T(0)};   // a.v == 0: reading A20
 }
 
 // Plain-double versions so the same flux template instantiates with T = double.
@@ -81,7 +83,7 @@ template <class T> FEOD_HD dual<T> pow_case(dual<T> a, T e, int pc) {
   if (pc == 2) return sqrt(a);
   if (pc == 0) return {T(1), T(0)};
   const T pv = ::pow(a.v, e);
-  return {pv, e * pv * a.d / a.v};
+  return {pv, a.v != T(0) ? e * pv * a.d / a.v : T(0)};   // a.v == 0: reading A20
 }
 
 FEOD_HD double value(double a) { return a; }

@@ -18,13 +18,13 @@ TOL = 1e-11
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "load_sums.json")))
 
 
-def sample_rows(w, n_random=160, seed=0):
+def sample_rows(w, n_random=160, seed=0, op=None):
     """Random rows + rows on brick boundaries, domain faces, edges and corners."""
     m = w.k * w.n + 1
     rng = np.random.default_rng(seed)
     rows = list(rng.choice(m ** 3, n_random, replace=False))
-    # the brick tiles of plane_kernel (PlaneTile<k+1>): faces, edges and corners of bricks
-    bx, by, bz = {1: (8, 4, 16), 2: (4, 3, 16), 3: (4, 2, 16), 4: (4, 2, 8), 5: (2, 2, 8), 6: (2, 2, 8)}[w.k]
+    # the operator kernels' bricks (feod_brick_shape): faces, edges and corners of bricks
+    bx, by, bz = op.brick_shape() if op is not None else (4, 2, 16)
     planes = sorted({0, 1, m - 2, m - 1} | {w.k * b * i for b in (bx, by, bz) for i in range(1, w.n // b + 1)
                                             if w.k * b * i < m})
     for _ in range(80):
@@ -48,14 +48,14 @@ def full(request):
 
 def test_residual_sampled(full):
     w, d, pr, op = full
-    rows = sample_rows(w)
+    rows = sample_rows(w, op=op)
     r = host(op.residual(cuda(d["u"])))
     assert rel_l2(r[rows], O.residual_rows(pr, d["u"], rows)) <= TOL
 
 
 def test_jvp_sampled(full):
     w, d, pr, op = full
-    rows = sample_rows(w, seed=1)
+    rows = sample_rows(w, seed=1, op=op)
     Jv = host(op.jvp(cuda(d["u"]), cuda(d["v"])))
     assert rel_l2(Jv[rows], O.jvp_rows(pr, d["u"], d["v"], rows)) <= TOL
     assert np.all(np.isfinite(Jv))
@@ -116,7 +116,7 @@ def test_determinism_c2_repeated_jvp():
 def test_vjp_sampled(full):
     """J^T w (NEXT-1) at full size on sampled rows (oracle from the touching elements)."""
     w, d, pr, op = full
-    rows = sample_rows(w, seed=2)
+    rows = sample_rows(w, seed=2, op=op)
     JTw = host(op.vjp(cuda(d["u"]), cuda(d["v"])))
     assert rel_l2(JTw[rows], O.vjp_rows(pr, d["u"], d["v"], rows)) <= TOL
 
@@ -124,7 +124,7 @@ def test_vjp_sampled(full):
 def test_linearize_jvp_lin_sampled(full):
     """NEXT-2 at full size: F(u) from feod_linearize and J v from the stored linearisation."""
     w, d, pr, op = full
-    rows = sample_rows(w, seed=3)
+    rows = sample_rows(w, seed=3, op=op)
     r = host(op.linearize(cuda(d["u"])))
     assert rel_l2(r[rows], O.residual_rows(pr, d["u"], rows)) <= TOL
     Jv = host(op.jvp_lin(cuda(d["v"])))
@@ -147,7 +147,7 @@ def test_jacobi_diag_sampled(full):
     """NEXT-3 at full size: the Jacobi diagonal on sampled rows (oracle: Eq. 3 element
     tangents of the touching elements, diagonal entries scattered)."""
     w, d, pr, op = full
-    rows = sample_rows(w, n_random=60, seed=4)
+    rows = sample_rows(w, n_random=60, seed=4, op=op)
     op.linearize(cuda(d["u"]))
     got = host(op.jacobi_diag())[rows]
     el = O.fem._elems_touching(pr, rows)

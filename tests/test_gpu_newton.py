@@ -134,3 +134,26 @@ def test_newton_pcg_jacobi():
     dev_n = np.max(np.abs(np.array(norms) - norms_ref) / np.array(norms_ref))
     assert dev_n <= 100 * spread_n + 1e-12, (dev_n, spread_n)
     assert rel_l2(host(u), u_ref) <= 100 * spread_u + 1e-12
+
+
+def test_newton_cg_fullsize_state_synchronised_rows():
+    """Full-size C4 (A15): after one and two GPU Newton steps from u0 = 0, the GPU
+    iterate is checked state-synchronised on sampled rows -- F(u_k) and J(u_{k-1}) delta_k
+    against the oracle at the same state -- and the driver's reported ||F|| against the
+    norm of the GPU residual (the trajectory itself is parity-unpinned, T17)."""
+    from test_gpu_fullsize import sample_rows
+    w = W.C4
+    d = W.draw(w)
+    pr, op = problem(w, d), operator(w, d)
+    rows = sample_rows(w, n_random=80, seed=11, op=op)
+    u_prev = np.zeros(w.n_dofs)
+    for steps in (1, 2):
+        u, norms = op.newton_cg(cuda(np.zeros(w.n_dofs)), steps, 20)
+        uh = host(u)
+        r = host(op.residual(u))
+        assert rel_l2(r[rows], O.residual_rows(pr, uh, rows)) <= 1e-11
+        delta = uh - u_prev
+        Jd = host(op.jvp(cuda(u_prev), cuda(delta)))
+        assert rel_l2(Jd[rows], O.jvp_rows(pr, u_prev, delta, rows)) <= 1e-11
+        assert abs(norms[steps] - np.linalg.norm(r)) <= 1e-10 * norms[steps]
+        u_prev = uh

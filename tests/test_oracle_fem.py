@@ -482,3 +482,41 @@ def test_vjp_rows_match_full():
     u, w = rand_free(pr, 1), np.random.default_rng(3).uniform(-1, 1, pr.n_dofs)
     rows = np.array([0, 5, 40, 100, pr.n_dofs - 1])
     np.testing.assert_array_equal(O.vjp_rows(pr, u, w, rows), O.vjp(pr, u, w)[rows])
+
+
+# ------------------------------------------------------------------ reading A20 (eps = 0, grad u = 0)
+@pytest.mark.parametrize("p", [2.5, 3.0, 3.5, 4.0])
+def test_a20_eps0_zero_gradient_limit(p):
+    """p-Laplacian with eps = 0 where grad u vanishes identically (u = 0 away from one
+    node): the JVP is finite, exactly 0 on rows whose elements all have grad u = 0 (the
+    limit of dD/dg ~ |g|^(p-2) -> 0), and central FD of the residual tends to it at the
+    rate h^(p-2) (a wrong limit -- NaN, or k I with k != 0 -- fails)."""
+    pr = prob(3, 2, PL, perturbed=False, p=p, eps=0.0)
+    u = np.zeros(pr.n_dofs)
+    m = 2 * 3 + 1
+    c = 2 + m * (2 + m * 2)                 # an interior node: (2, 2, 2)
+    u[c] = 1.0
+    v = rand_free(pr, 5)
+    Jv = O.jvp(pr, u, v)
+    assert np.all(np.isfinite(Jv))
+    # rows coupled to node c only through elements with grad u != 0
+    hot = O.jvp(pr, u, np.where(np.arange(pr.n_dofs) == c, 1.0, 0.0)) != 0.0
+    X = np.arange(pr.n_dofs) % m
+    Y = (np.arange(pr.n_dofs) // m) % m
+    Z = np.arange(pr.n_dofs) // (m * m)
+    touched = (np.abs(X - 2) <= 2) & (np.abs(Y - 2) <= 2) & (np.abs(Z - 2) <= 2)   # rows of the elements at c
+    cold = ~touched & ~O.dirichlet_mask(pr)
+    assert cold.any() and hot.any()
+    assert np.all(Jv[cold] == 0.0)
+    F = lambda x: O.residual(pr, x)
+    errs, errs_all = [], []
+    for h in (1e-2, 1e-4):
+        fd = (F(u + h * v) - F(u - h * v)) / (2 * h)
+        errs.append(np.max(np.abs(fd[cold])))
+        errs_all.append(np.max(np.abs(fd - Jv)))
+    # FD on the cold rows decays like h^(p-2) to the limit 0 (h ratio 100); on all rows
+    # the FD error decays at least that fast (second order where the flux is smooth)
+    rate = 100.0 ** (-min(p - 2.0, 2.0))
+    assert errs[1] <= errs[0] * rate * 4.0 + 1e-13
+    assert errs_all[1] <= errs_all[0] * rate * 4.0 + 1e-12
+    assert np.isfinite(errs_all).all() and errs_all[1] < errs_all[0]
