@@ -375,11 +375,13 @@ def main():
     t_lin = time_call(lambda: op.linearize(u, out=r))
     t_jlin = time_call(lambda: op.jvp_lin(v, out=JTw))
     t_diag = time_call(lambda: op.jacobi_diag(out=JTw))
-    t_des = None
+    t_des = t_rg = None
     if w.model == W.HEAT:
         g = torch.empty(op.n_elems, dtype=torch.float64, device=u.device)
         lam = torch.as_tensor(d["lam"]).cuda()   # the recipe's lambda draw
         t_des = time_call(lambda: op.design_grad(u, lam, out=g))
+        r3 = torch.empty_like(u)
+        t_rg = time_call(lambda: op.res_design_grad(u, lam, out=(r3, g)))   # SURVEY §8(d) "C5 r+g fused"
 
     # e2e through the C-ABI host-buffer path
     e2e = None
@@ -535,6 +537,13 @@ def main():
         line["adjoint_solve"] = {"ms": a_.elapsed_time(b_), "iters": 50, "vjp_calls": 100,
                                  "res_first": hist[0], "res_last": hist[-1],
                                  "note": "feod_adjoint_solve, unpreconditioned BiCGStab on P^T J^T (device time)"}
+    if t_rg is not None:
+        by = 8 * (2 * N + N) + 16 * w.n_elems + (48 * w.q ** 3 * w.n_elems if w.perturbed else 0)
+        fl = 2 * 3 * w.n_elems * (w.q * (w.k + 1) ** 3 + w.q ** 2 * (w.k + 1) ** 2 + w.q ** 3 * (w.k + 1) + 3 * w.q ** 4) \
+            + 23 * w.n_elems * w.q ** 3
+        line["calls"]["res_design_grad"] = {"us": t_rg * 1e3, "hbm_frac": by / (t_rg * 1e-3) / 1e9 / peak,
+                                            "fp64_frac": fl / (t_rg * 1e-3) / 1e12 / FP64_MEASURED_TFLOPS,
+                                            "note": "feod_res_design_grad: r and g from one dual pass seeded along rho"}
     if t_des is not None:
         line["calls"]["design_grad"] = {"us": t_des * 1e3, "gdof_s": N / (t_des * 1e-3) / 1e9,
                                         "hbm_frac": algorithmic_bytes(w, "design") / (t_des * 1e-3) / 1e9 / peak,

@@ -172,6 +172,13 @@ FEOD_API int feod_jvp_lin(feod_handle h, const double* v, double* Jv);
 /* g_e = -lambda^T dF/drho_e, lambda's Dirichlet entries ignored          *
  * (A14); HEAT_DESIGN only (others: FEOD_EINVAL)           */
 FEOD_API int feod_design_grad(feod_handle h, const double* u, const double* lambda, double* g);
+/* r = F(u) and g_e = -sum_{i free} lambda_i dF_i/drho_e together (SURVEY §8(b) optional
+ * fused entry point; the adjoint-load use of PAPER.md:199): one dual evaluation of D per
+ * point seeded along rho gives the residual flux (value part) and dF/drho (tangent part).
+ * Same conventions as feod_residual and feod_design_grad (HEAT_DESIGN only; r length N,
+ * g length E, no output may alias an input or the other output). Q1/Q2: one fused
+ * kernel; Q3..Q6: the two calls. */
+FEOD_API int feod_res_design_grad(feod_handle h, const double* u, const double* lambda, double* r, double* g);
 
 /* Same operations on HOST buffers: copies host->device, computes, copies
  * device->host and synchronises the stream before returning (the e2e path).

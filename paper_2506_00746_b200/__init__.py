@@ -30,7 +30,7 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
            "feod_set_newton_linearization", "feod_brick_shape", "feod_jacobi_diag", "feod_adjoint_solve", "feod_element_matrices",
-           "feod_design_grad", "feod_apply_host", "feod_newton_cg",
+           "feod_design_grad", "feod_res_design_grad", "feod_apply_host", "feod_newton_cg",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH):
     lib.feod_jvp.argtypes = [vp, dp, dp, dp]
     lib.feod_jvp_res.argtypes = [vp, dp, dp, dp, dp]
     lib.feod_design_grad.argtypes = [vp, dp, dp, dp]
+    lib.feod_res_design_grad.argtypes = [vp, dp, dp, dp, dp]
     lib.feod_vjp.argtypes = [vp, dp, dp, dp]
     lib.feod_linearize.argtypes = [vp, dp, dp]
     lib.feod_jvp_lin.argtypes = [vp, dp, dp]
@@ -268,6 +269,15 @@ class Operator:
         b = [ctypes.c_int() for _ in range(3)]
         _check(self.lib.feod_brick_shape(self.h, *[ctypes.byref(x) for x in b]))
         return tuple(x.value for x in b)
+
+    def res_design_grad(self, u, lam, out=None):
+        """(r, g): F(u) and the design gradient from one dual pass (feod_res_design_grad)."""
+        u, lam = self._dev(u, self.n_dofs, "u"), self._dev(lam, self.n_dofs, "lam")
+        r, g = (None, None) if out is None else out
+        r, g = self._out(r, self.n_dofs, "out[0]"), self._out(g, self.n_elems, "out[1]")
+        self._sync_stream()
+        _check(self.lib.feod_res_design_grad(self.h, u.data_ptr(), lam.data_ptr(), r.data_ptr(), g.data_ptr()))
+        return r, g
 
     def set_rho(self, rho):
         self._rho = self._dev(rho, self.n_elems, "rho")

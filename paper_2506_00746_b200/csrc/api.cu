@@ -466,6 +466,18 @@ extern "C" int feod_design_grad(feod_handle h, const double* u, const double* la
   return run_op(h, MODE_DESIGN, u, lambda, nullptr, nullptr, g, "feod_design_grad");
 }
 
+extern "C" int feod_res_design_grad(feod_handle h, const double* u, const double* lambda, double* r, double* g) {
+  if (!h || !u || !lambda || !r || !g) return fail(FEOD_EINVAL, "feod_res_design_grad: null argument");
+  if (h->coeffs.model != FEOD_HEAT_DESIGN) return fail(FEOD_EINVAL, "feod_res_design_grad: model has no rho");
+  if ((const double*)r == u || (const double*)r == lambda || (const double*)g == u || (const double*)g == lambda ||
+      r == g)
+    return fail(FEOD_EINVAL, "feod_res_design_grad: an output aliases another argument");
+  if (h->bi.ptx > 1)   // column kernel: one dual pass gives both
+    return run_op(h, MODE_RESDES, u, lambda, r, nullptr, g, "feod_res_design_grad");
+  const int rc = feod_residual(h, u, r);   // plane-kernel orders: the two calls
+  return rc ? rc : feod_design_grad(h, u, lambda, g);
+}
+
 extern "C" int feod_apply_host(feod_handle h, int op, const double* in0, const double* in1, double* out) {
   if (!h || !in0 || !out || (op != 0 && !in1)) return fail(FEOD_EINVAL, "feod_apply_host: null argument");
   if (op < 0 || op > 4) return fail(FEOD_EINVAL, "feod_apply_host: op must be 0 .. 4");

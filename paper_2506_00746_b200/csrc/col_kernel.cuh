@@ -101,7 +101,7 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
   constexpr int NO1 = NOUT > 0 ? NOUT : 1;
   constexpr bool STREAM = (MODE == MODE_PAJVP) || !AFFINE;
   constexpr int NSV = (MODE == MODE_PAJVP) ? lin_values(MODEL) : 6;
-  constexpr bool MASK1 = MODE == MODE_DESIGN || MODE == MODE_VJP;   // field 1 (lambda / w) Dirichlet-masked
+  constexpr bool MASK1 = MODE == MODE_DESIGN || MODE == MODE_VJP || MODE == MODE_RESDES;   // field 1 (lambda / w) masked
   extern __shared__ __align__(16) double smem[];
   double* ring = smem;                                          // [NIN][RS][PLANE]
   double* ebuf = smem + S::RING;                                // [EBP][NOUT][K+1][NT][ESTR]
@@ -383,7 +383,7 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
               }
             }
           }
-      if constexpr (MODE == MODE_DESIGN) gout[ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez)] = gpart;
+      if constexpr (MODE == MODE_DESIGN || MODE == MODE_RESDES) gout[ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez)] = gpart;
 
       // ---- B^T: z first, z-carry of the top plane, then y and x per finished DOF plane
 #pragma unroll

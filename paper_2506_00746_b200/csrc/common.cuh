@@ -8,8 +8,11 @@
 
 namespace feod {
 
-enum Mode { MODE_RES = 0, MODE_JVP = 1, MODE_JVPRES = 2, MODE_DESIGN = 3, MODE_VJP = 4, MODE_LIN = 5, MODE_PAJVP = 6 };
-constexpr int kModes = 7;
+// MODE_RESDES: r = F(u) and g_e = -lambda^T dF/drho_e from one dual pass (feod_res_design_grad;
+// column kernel only -- the plane-kernel orders compose it from MODE_RES and MODE_DESIGN)
+enum Mode { MODE_RES = 0, MODE_JVP = 1, MODE_JVPRES = 2, MODE_DESIGN = 3, MODE_VJP = 4, MODE_LIN = 5, MODE_PAJVP = 6,
+            MODE_RESDES = 7 };
+constexpr int kModes = 8;
 enum Model { PLAPLACE = 0, NLDIFF = 1, HEAT = 2 };
 constexpr int kMaxNQ = 8;
 

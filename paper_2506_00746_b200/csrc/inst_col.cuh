@@ -73,6 +73,7 @@ bool brick_info<FEOD_ND>(BrickInfo* bi) {
   bi->smem[MODE_VJP] = CShape<FEOD_ND, MODE_VJP>::SMEM_BYTES;
   bi->smem[MODE_LIN] = CShape<FEOD_ND, MODE_LIN>::SMEM_BYTES;
   bi->smem[MODE_PAJVP] = CShape<FEOD_ND, MODE_PAJVP>::SMEM_BYTES;
+  bi->smem[MODE_RESDES] = CShape<FEOD_ND, MODE_RESDES>::SMEM_BYTES;
   return true;
 }
 
@@ -85,6 +86,8 @@ cudaError_t prepare_order<FEOD_ND>() {
   if ((e = prep_col_mode<FEOD_ND, MODE_DESIGN>()) != cudaSuccess) return e;
   if ((e = prep_col_mode<FEOD_ND, MODE_VJP>()) != cudaSuccess) return e;
   if ((e = prep_col_mode<FEOD_ND, MODE_LIN>()) != cudaSuccess) return e;
+  if ((e = prep_col<FEOD_ND, MODE_RESDES, HEAT, true>()) != cudaSuccess) return e;
+  if ((e = prep_col<FEOD_ND, MODE_RESDES, HEAT, false>()) != cudaSuccess) return e;
   return prep_col_mode<FEOD_ND, MODE_PAJVP>();
 }
 
@@ -99,6 +102,10 @@ cudaError_t launch_order<FEOD_ND>(int mode, int model, bool aff, int nbricks, co
     case MODE_VJP: return launch_col_mode<FEOD_ND, MODE_VJP>(model, aff, nbricks, P, T, p, st, grid_out);
     case MODE_LIN: return launch_col_mode<FEOD_ND, MODE_LIN>(model, aff, nbricks, P, T, p, st, grid_out);
     case MODE_PAJVP: return launch_col_mode<FEOD_ND, MODE_PAJVP>(model, aff, nbricks, P, T, p, st, grid_out);
+    case MODE_RESDES:   // HEAT only (the only model with a design variable)
+      if (model != HEAT) return cudaErrorInvalidValue;
+      return aff ? launch_col<FEOD_ND, MODE_RESDES, HEAT, true>(nbricks, P, T, p, st, grid_out)
+                 : launch_col<FEOD_ND, MODE_RESDES, HEAT, false>(nbricks, P, T, p, st, grid_out);
   }
   return cudaErrorInvalidValue;
 }

@@ -23,7 +23,7 @@ namespace feod {
 // Does output o of MODE carry a value channel (test function phi_i itself, not its
 // gradient)? Modes without one skip its transposed contraction entirely.
 FEOD_HD constexpr bool value_channel(int mode, int o) {
-  return mode == MODE_RES || mode == MODE_LIN || mode == MODE_VJP || (mode == MODE_JVPRES && o == 1);
+  return mode == MODE_RES || mode == MODE_LIN || mode == MODE_VJP || mode == MODE_RESDES || (mode == MODE_JVPRES && o == 1);
 }
 
 template <int MODE, int MODEL, bool DIAG = false>
@@ -104,6 +104,18 @@ FEOD_DEV void point_op(const double* Ul, const double* Uxl, const double* Uyl, c
       F0[2] = fma(sv[8], Ul[0], F0[2]);
     }
     F0[3] = 0.0;
+  } else if constexpr (MODE == MODE_RESDES) {
+    // r and the design derivative from ONE dual evaluation seeded along rho: the value
+    // part is the residual's flux, the tangent part dF/drho; field 1 is lambda
+    using D = dual<double>;
+    const D ud(Ul[0]);
+    const D gh[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
+    const D rd(rho_e, 1.0);
+    D Fh[3];
+    flux_hat<MODEL, DIAG>(ud, gh, M, W, rd, P, Fh);
+    F0[0] = Fh[0].v; F0[1] = Fh[1].v; F0[2] = Fh[2].v;
+    F0[3] = -P.f * W;
+    gpart -= Uxl[1] * Fh[0].d + Uyl[1] * Fh[1].d + Uzl[1] * Fh[2].d;
   } else {   // MODE_DESIGN: seed d/drho (PAPER.md:199 adjoint loads); field 1 is lambda
     using D = dual<double>;
     const D ud(Ul[0]);

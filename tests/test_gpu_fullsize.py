@@ -77,6 +77,14 @@ def test_design_grad_sampled_and_euler():
     lm[W.dirichlet_dofs(w.n, w.k, w.faces)] = 0.0
     lhs, rhs = d["rho"] @ g, -3.0 * (lm @ (F - F0))
     assert abs(lhs - rhs) <= 1e-11 * np.sum(np.abs(d["rho"] * g))
+    # the fused entry point (one dual pass, feod_res_design_grad) at full size: sampled
+    # elements and rows against the oracle, and the same Euler identity
+    r2, g2 = op.res_design_grad(u, lam)
+    r2, g2 = host(r2), host(g2)
+    assert rel_l2(g2[el], O.design_grad_elems(pr, d["u"], d["lam"], el)) <= TOL
+    rows = sample_rows(w, seed=5, op=op)
+    assert rel_l2(r2[rows], O.residual_rows(pr, d["u"], rows)) <= TOL
+    assert abs(d["rho"] @ g2 + 3.0 * (lm @ (r2 - F0))) <= 1e-11 * np.sum(np.abs(d["rho"] * g2))
 
 
 @pytest.mark.parametrize("name,n,k,faces", [("C4", 32, 6, 63), ("C5", 96, 2, 1), ("C1", 4, 2, 63), ("C2", 128, 1, 63)])

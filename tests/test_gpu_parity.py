@@ -5,6 +5,8 @@ seeded inputs, for r = F(u), J(u)v and the design gradient g.
 Full vectors at reduced sizes spanning several bricks with ragged tails; the
 full BASELINE sizes are covered by sampled rows in test_gpu_fullsize.py.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -55,6 +57,21 @@ def test_design_grad_parity(n):
     g_ref = O.design_grad(pr, d["u"], d["lam"])
     g = host(op.design_grad(cuda(d["u"]), cuda(d["lam"])))
     assert rel_l2(g, g_ref) <= TOL
+
+
+RG_CASES = [(W.C5, 6), (W.C5, 9), (W.C5, 17), (dataclasses.replace(W.C5, k=1, q=2, perturbed=True), 11),
+            (dataclasses.replace(W.C5, k=3, q=4), 5)]
+
+
+@pytest.mark.parametrize("w,n", RG_CASES, ids=[f"Q{w.k}n{n}" for w, n in RG_CASES])
+def test_res_design_grad_parity(w, n):
+    """feod_res_design_grad (SURVEY §8(b) fused r + g; one dual pass on Q1/Q2, the two
+    calls on Q3+) against the oracle's Eq. 1 residual and design gradient."""
+    ww, d = _case(w, n)
+    pr, op = problem(ww, d), operator(ww, d)
+    r, g = op.res_design_grad(cuda(d["u"]), cuda(d["lam"]))
+    assert rel_l2(host(r), O.residual(pr, d["u"])) <= TOL
+    assert rel_l2(host(g), O.design_grad(pr, d["u"], d["lam"])) <= TOL
 
 
 @pytest.mark.parametrize("w,n", CASES, ids=[f"{w.name}n{n}" for w, n in CASES])

@@ -33,6 +33,7 @@ def main():
         "jvp_res": lambda: op.jvp_res(u, v, out=(out2, out)),
         "vjp": lambda: op.vjp(u, v, out=out),
         "design": lambda: op.design_grad(u, lam, out=g),
+        "res_design": lambda: op.res_design_grad(u, lam, out=(out, g)),
         "linearize": lambda: op.linearize(u, out=out),
         "jvp_lin": lambda: op.jvp_lin(v, out=out),
     }
