@@ -132,6 +132,12 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
     lagrange01(qorder, pts, qorder, pts, id, &h->T.D[0][0], kMaxNQ);
   }
   for (int i = 0; i < qorder; ++i) { h->T.w[i] = wts[i]; h->T.wi2[i] = 1.0 / (wts[i] * wts[i]); h->T.x[i] = pts[i]; }
+  if (qorder % 2 == 1 && std::fabs(h->T.D[qorder / 2][qorder / 2]) < 1e-12)
+    h->T.D[qorder / 2][qorder / 2] = 0.0;   // symmetric points: L_mid'(x_mid) = 0 (col_kernel skips it)
+  for (int i = 0; i < qorder; ++i)
+    for (int m = 0; m < qorder; ++m) h->T.Dh[i][m] = h->T.D[i][m] * wts[i] / wts[m];
+  for (int i = 0; i < qorder; ++i)
+    for (int a = 0; a < h->nd; ++a) h->T.Bw[i][a] = wts[i] * h->T.B[i][a];
 
   OpParams& P = h->P;
   std::memset(&P, 0, sizeof(P));
@@ -149,7 +155,7 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const long slots = (long)sms * h->bi.minb;
     double best = 1e300;
-    for (int bz : {4, 6, 8, 12, 16, 24, 32, 48, 64}) {
+    for (int bz : {1, 2, 4, 6, 8, 12, 16, 24, 32, 48, 64}) {
       const long nb = (long)P.nbx * P.nby * ((mesh->nz + bz - 1) / bz);
       const long waves = (nb + slots - 1) / slots;
       const double cost = (double)waves * (std::min(bz, mesh->nz) + 1.0);

@@ -84,8 +84,11 @@ struct CShape {
   static constexpr int EBP = NOUT == 2 ? 1 : 2;              // element-buffer parities
   static constexpr int EB = (NOUT > 0 ? NOUT : 0) * (K + 1) * NT * ESTR;   // one parity
   static constexpr int RING = NIN * RS * PLANE;
-  // + 2 mbarriers, the brick queue (8 x int4) and the plane shifts (NIN x RS ints)
-  static constexpr size_t SMEM_BYTES = sizeof(double) * (RING + EBP * EB) + 16 + 8 * 16 + ((NIN * RS * 4 + 15) / 16) * 16;
+  // + 2 mbarriers, the brick queue (8 x int4), the plane shifts (NIN x RS ints, padded to 16 B)
+  // and the affine metric table (q^3 x 4 doubles)
+  static constexpr int PSH = (NIN * RS + 3) / 4 * 4;
+  static constexpr size_t SMEM_BYTES =
+      sizeof(double) * (RING + EBP * EB) + 16 + 8 * 16 + PSH * 4 + sizeof(double) * 4 * ND * ND * ND;
   static constexpr int MINB = ColTile<ND, MODE>::MINB, MPD = ColTile<ND, MODE>::MPD;
   static_assert(NT % 32 == 0, "whole warps");
 };
@@ -101,6 +104,12 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
   constexpr int NO1 = NOUT > 0 ? NOUT : 1;
   constexpr bool STREAM = (MODE == MODE_PAJVP) || !AFFINE;
   constexpr int NSV = (MODE == MODE_PAJVP) ? lin_values(MODEL) : 6;
+  constexpr int MID = (NQ % 2 == 1) ? NQ / 2 : -1;   // middle Gauss point (odd q)
+  // FOLD (affine meshes, the modes whose outputs are plain B^T of the point fluxes): the
+  // weight w_q of M = w_q diag(c) and W = w_q vol is folded into the transposed tables
+  // (Tables::Dh, Bw), so the points work with M = diag(c), W = vol -- the p-Laplacian's
+  // s = gh.M gh / W is unchanged (w_q cancels), every flux is F = w_q Ft
+  constexpr bool FOLD = AFFINE && (MODE == MODE_RES || MODE == MODE_JVP || MODE == MODE_JVPRES || MODE == MODE_VJP);
   constexpr bool MASK1 = MODE == MODE_DESIGN || MODE == MODE_VJP || MODE == MODE_RESDES;   // field 1 (lambda / w) masked
   extern __shared__ __align__(16) double smem[];
   double* ring = smem;                                          // [NIN][RS][PLANE]
@@ -108,6 +117,7 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
   uint64_t* mb = reinterpret_cast<uint64_t*>(ebuf + S::EBP * S::EB);   // [2] layer-slot mbarriers
   int4* bq = reinterpret_cast<int4*>(mb + 2);                   // [8] (id, ex0, ey0, ez0) of the n-th brick
   int* psh = reinterpret_cast<int*>(bq + 8);                    // [NIN][RS] s0 of the plane in each ring slot
+  double* wc = reinterpret_cast<double*>(psh + S::PSH);         // [q^3][4] affine metric: w_q (cx, cy, cz, vol)
 
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
@@ -125,6 +135,15 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
     if (id >= 0) q = make_int4(id, (id % P.nbx) * TX, ((id / P.nbx) % P.nby) * TY, (id / (P.nbx * P.nby)) * BZ);
     bq[slot & 7] = q;
   };
+  if constexpr (AFFINE || MODE == MODE_PAJVP) {
+    for (int t = tid; t < NQ3; t += NT) {
+      const double wq = T.w[t % NQ] * T.w[(t / NQ) % NQ] * T.w[t / NQ2];
+      wc[4 * t + 0] = wq * P.cx;
+      wc[4 * t + 1] = wq * P.cy;
+      wc[4 * t + 2] = wq * P.cz;
+      wc[4 * t + 3] = wq * P.vol;
+    }
+  }
   if (tid == 0) {
     mbar_init(&mb[0], S::NW);   // one arrival per warp (each issues its share of the row copies)
     mbar_init(&mb[1], S::NW);
@@ -324,7 +343,6 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
 #pragma unroll
           for (int i = 0; i < NQ; ++i) {
             const int q = (l * NQ + j) * NQ + i;
-            const double wq = T.w[i] * T.w[j] * T.w[l];
             double sv[STREAM ? NSV : 1];
             if constexpr (STREAM) {
               // layout [l][c][j][i] per element (as the geometry kernel writes it)
@@ -338,9 +356,14 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
             }
             Metric M;
             double W;
-            if constexpr (AFFINE || MODE == MODE_PAJVP) {
-              M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
-              W = wq * P.vol;
+            if constexpr (FOLD) {
+              M = {P.cx, P.cy, P.cz, 0.0, 0.0, 0.0};
+              W = P.vol;
+            } else if constexpr (AFFINE || MODE == MODE_PAJVP) {
+              const double2 m01 = *reinterpret_cast<const double2*>(wc + 4 * q);
+              const double2 m23 = *reinterpret_cast<const double2*>(wc + 4 * q + 2);
+              M = {m01.x, m01.y, m23.x, 0.0, 0.0, 0.0};
+              W = m23.y;
             } else {
               M = {sv[0], sv[1], sv[2], sv[3], sv[4], sv[5]};
               const double det = M.xx * (M.yy * M.zz - M.yz * M.yz) - M.xy * (M.xy * M.zz - M.yz * M.xz) +
@@ -356,9 +379,10 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
               double gz = T.D[l][0] * U[f][j * NQ + i];
 #pragma unroll
               for (int m = 1; m < NQ; ++m) {
-                gx = fma(T.D[i][m], U[f][(l * NQ + j) * NQ + m], gx);
-                gy = fma(T.D[j][m], U[f][(l * NQ + m) * NQ + i], gy);
-                gz = fma(T.D[l][m], U[f][(m * NQ + j) * NQ + i], gz);
+                // D[mid][mid] = 0 on the symmetric Gauss points (odd q; set exactly at create)
+                if (!(i == MID && m == MID)) gx = fma(T.D[i][m], U[f][(l * NQ + j) * NQ + m], gx);
+                if (!(j == MID && m == MID)) gy = fma(T.D[j][m], U[f][(l * NQ + m) * NQ + i], gy);
+                if (!(l == MID && m == MID)) gz = fma(T.D[l][m], U[f][(m * NQ + j) * NQ + i], gz);
               }
               Uxl[f] = gx;
               Uyl[f] = gy;
@@ -377,9 +401,10 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
               if (value_channel(MODE, o)) R[o][q] += Fo[3];
 #pragma unroll
               for (int m = 0; m < NQ; ++m) {
-                R[o][(l * NQ + j) * NQ + m] = fma(T.D[i][m], Fo[0], R[o][(l * NQ + j) * NQ + m]);
-                R[o][(l * NQ + m) * NQ + i] = fma(T.D[j][m], Fo[1], R[o][(l * NQ + m) * NQ + i]);
-                R[o][(m * NQ + j) * NQ + i] = fma(T.D[l][m], Fo[2], R[o][(m * NQ + j) * NQ + i]);
+                const auto& DT = FOLD ? T.Dh : T.D;
+                if (!(i == MID && m == MID)) R[o][(l * NQ + j) * NQ + m] = fma(DT[i][m], Fo[0], R[o][(l * NQ + j) * NQ + m]);
+                if (!(j == MID && m == MID)) R[o][(l * NQ + m) * NQ + i] = fma(DT[j][m], Fo[1], R[o][(l * NQ + m) * NQ + i]);
+                if (!(l == MID && m == MID)) R[o][(m * NQ + j) * NQ + i] = fma(DT[l][m], Fo[2], R[o][(m * NQ + j) * NQ + i]);
               }
             }
           }
@@ -393,9 +418,10 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
         for (int c = 0; c < ND; ++c)
 #pragma unroll
           for (int ji = 0; ji < NQ2; ++ji) {
-            double s = T.B[0][c] * R[o][ji];
+            const auto& BT = FOLD ? T.Bw : T.B;
+            double s = BT[0][c] * R[o][ji];
 #pragma unroll
-            for (int l = 1; l < NQ; ++l) s = fma(T.B[l][c], R[o][l * NQ2 + ji], s);
+            for (int l = 1; l < NQ; ++l) s = fma(BT[l][c], R[o][l * NQ2 + ji], s);
             Sz[c][ji] = s;
           }
         // z-carry of the column's top plane (after B_z^T, before B_y^T B_x^T), parked in the
@@ -419,9 +445,10 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
           for (int b = 0; b < ND; ++b)
 #pragma unroll
             for (int i = 0; i < NQ; ++i) {
-              double s = T.B[0][b] * Sz[c][i];
+              const auto& BT = FOLD ? T.Bw : T.B;
+              double s = BT[0][b] * Sz[c][i];
 #pragma unroll
-              for (int j = 1; j < NQ; ++j) s = fma(T.B[j][b], Sz[c][j * NQ + i], s);
+              for (int j = 1; j < NQ; ++j) s = fma(BT[j][b], Sz[c][j * NQ + i], s);
               sy[b][i] = s;
             }
           double* e = eb + ((o * (K + 1) + c) * NT + tid) * S::ESTR;
@@ -429,9 +456,10 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
           for (int b = 0; b < ND; ++b)
 #pragma unroll
             for (int a = 0; a < ND; ++a) {
-              double s = T.B[0][a] * sy[b][0];
+              const auto& BT = FOLD ? T.Bw : T.B;
+              double s = BT[0][a] * sy[b][0];
 #pragma unroll
-              for (int i = 1; i < NQ; ++i) s = fma(T.B[i][a], sy[b][i], s);
+              for (int i = 1; i < NQ; ++i) s = fma(BT[i][a], sy[b][i], s);
               e[b * ND + a] = s;
             }
         }

@@ -35,6 +35,12 @@ struct Tables {
   double w[kMaxNQ];
   double wi2[kMaxNQ];   // 1 / w[i]^2
   double x[kMaxNQ];
+  // weight-folded tables of the affine column kernel (col_kernel.cuh FOLD): with
+  // M = w_q diag(c) and F = w_q Ft, the quadrature weight w_q = w_i w_j w_l moves out of
+  // the per-point work into the transposed 1D operators:
+  //   Dh[i][m] = D[i][m] w_i / w_m  (R = w_q Rt at the points),  Bw[i][a] = w_i B[i][a]
+  double Dh[kMaxNQ][kMaxNQ];
+  double Bw[kMaxNQ][kMaxNQ];
 };
 
 // Device-resident scheduler state of one handle.

@@ -24,7 +24,9 @@ template <int MODEL, bool DIAG = false, class T, class R>
 FEOD_DEV void flux_hat(const T& u, const T gh[3], const Metric& M, double W, const R& rho,
                        const OpParams& P, T Fh[3]) {
   T a[3];
-  if constexpr (DIAG) {
+  if constexpr (DIAG && MODEL != PLAPLACE) {
+    // a is not needed (see below)
+  } else if constexpr (DIAG) {
     a[0] = gh[0] * M.xx;
     a[1] = gh[1] * M.yy;
     a[2] = gh[2] * M.zz;
@@ -43,9 +45,17 @@ FEOD_DEV void flux_hat(const T& u, const T gh[3], const Metric& M, double W, con
     auto r3 = rho * rho * rho;
     kappa = r3 * (u * u + 1.0);
   }
-  Fh[0] = kappa * a[0];
-  Fh[1] = kappa * a[1];
-  Fh[2] = kappa * a[2];
+  if constexpr (DIAG && MODEL != PLAPLACE) {
+    // kappa does not depend on gh: (kappa gh_d) M_dd, the metric applied last (one
+    // multiply per component; the same value as kappa (M_dd gh_d) up to rounding order)
+    Fh[0] = (kappa * gh[0]) * M.xx;
+    Fh[1] = (kappa * gh[1]) * M.yy;
+    Fh[2] = (kappa * gh[2]) * M.zz;
+  } else {
+    Fh[0] = kappa * a[0];
+    Fh[1] = kappa * a[1];
+    Fh[2] = kappa * a[2];
+  }
 }
 
 }  // namespace feod
