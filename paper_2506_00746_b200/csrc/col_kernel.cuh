@@ -218,6 +218,11 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
   // ---- compute cursor
   int cn = 0, cz = 0, cbase = 0;
   double rho_nx = 1.0;   // HEAT: rho of this thread's element one layer ahead
+  if constexpr (MODEL == HEAT && MODE != MODE_PAJVP) {
+    const int4 q0 = bq[0];   // the first layer's element
+    if (q0.x >= 0 && q0.y + tx < P.nx && q0.z + ty < P.ny)
+      rho_nx = ld_stream(P.rho + (q0.y + tx) + (int64_t)P.nx * ((q0.z + ty) + (int64_t)P.ny * q0.w));
+  }
 
 #pragma unroll 1
   for (int L = 0;; ++L) {
@@ -233,8 +238,7 @@ col_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, con
     if constexpr (MODEL == HEAT && MODE != MODE_PAJVP) {
       // rho one layer ahead: this layer's value came with the previous layer; request the next
       // layer's (the next brick's first layer is claimed by now: the prefetch cursor is ahead)
-      rho_e = rho_nx;
-      if (L == 0 && ev) rho_e = ld_stream(P.rho + ex + (int64_t)P.nx * (ey + (int64_t)P.ny * ez));
+      rho_e = rho_nx;   // (no predicated load into rho_e: its scoreboard would stall the first use)
       int4 nq = cq;
       int nz_ = cz + 1;
       if (nz_ == bzr) { nq = bq[(cn + 1) & 7]; nz_ = 0; }
