@@ -42,7 +42,18 @@ sys.path.insert(0, ROOT)
 import workloads as W  # noqa: E402
 
 HBM_FALLBACK_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
-FP64_MEASURED_TFLOPS = 33.0  # profiles/r01_peaks_fp64.json (tools/fp64_peak.cu on a B200)
+def _fp64_peaks():
+    """DFMA rate measured by tools/peaks.py (profiles/r02_peaks_fp64.json, NVML clock record:
+    1965 MHz, no throttle reason) and the nominal 148 SMs x 64 FMA/clk x 2 x clock."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_peaks_fp64.json")) as f:
+            pk = json.load(f)
+        return float(pk["fp64_tflops_burst"]), float(pk["fp64_tflops_nominal_at_max_clock"])
+    except Exception:
+        return 33.0, 37.2
+
+
+FP64_MEASURED_TFLOPS, FP64_NOMINAL_TFLOPS = _fp64_peaks()
 
 
 def algorithmic_bytes(w, call):
@@ -411,7 +422,8 @@ def main():
     jvp_bytes = algorithmic_bytes(w, "jvp")
     achieved = jvp_bytes / (jvp_kernel_ms * 1e-3) / 1e9
     traffic = traffic_from_profiles(w.name)
-    roofline = {"bound": "hbm" if w.perturbed else "alu", "kernel": f"plane_kernel<JVP> (fused G-B-D-B^T-G^T, {w.name})",
+    kname = "col_kernel<JVP> (one thread per element column, Q1/Q2)" if w.k <= 2 else "plane_kernel<JVP>"
+    roofline = {"bound": "hbm" if w.perturbed else "alu", "kernel": f"{kname}: fused G-B-D-B^T-G^T, {w.name}",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": jvp_bytes, "kernel_ms": jvp_kernel_ms}
@@ -419,8 +431,11 @@ def main():
         fl = algorithmic_flops(w, "jvp")
         ach = fl / (jvp_kernel_ms * 1e-3) / 1e12
         roofline.update({"achieved": ach, "peak": FP64_MEASURED_TFLOPS, "unit": "TFLOP/s",
-                         "frac": ach / FP64_MEASURED_TFLOPS,
-                         "peak_source": "measured DFMA rate, profiles/r01_peaks_fp64.json"})
+                         "frac": ach / FP64_MEASURED_TFLOPS, "frac_of_nominal": ach / FP64_NOMINAL_TFLOPS,
+                         "peak_nominal": FP64_NOMINAL_TFLOPS,
+                         "peak_source": "measured DFMA rate at 1965 MHz, no throttle (profiles/r02_peaks_fp64.json); "
+                                        "nominal = 148 SMs x 64 FMA/clk x 2 x 1.965 GHz (reached only by DMMA)",
+                         "algorithmic_flops_per_launch": fl})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
