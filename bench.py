@@ -515,9 +515,23 @@ def main():
         line["newton_pcg_jacobi"] = {"ms": statistics.median(tj), "ms_min": min(tj), "norms": norms_j,
                                      "note": "feod_set_newton_linearization(2): + feod_jacobi_diag per step, "
                                              "Jacobi-preconditioned CG (NEXT-3)"}
+        op.set_cg_graphs(False)
+        op.newton_cg(u0, 5, 20)
+        torch.cuda.synchronize()
+        tg = []
+        for _ in range(3):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            op.newton_cg(u0, 5, 20)
+            b_.record(stream)
+            torch.cuda.synchronize()
+            tg.append(a_.elapsed_time(b_))
+        op.set_cg_graphs(True)
         line["newton_cg"] = {"ms": statistics.median(tn), "ms_min": min(tn), "jvp_calls": n_jvp, "residual_calls": n_res,
                              "norms": norms, "op_share_ms": (n_jvp * t_jvp + n_res * t_res),
-                             "note": "feod_newton_cg, device time incl. host syncs once per Newton step"}
+                             "ms_without_graphs": statistics.median(tg),
+                             "note": "feod_newton_cg: CG iterations as a replayed CUDA graph (5 launches per iteration, "
+                                     "alpha/beta reduced in-kernel), host sync once per Newton step"}
     if w.k <= 3 and world == 1:
         # NEXT-4 (Table-1 analogue): element tangents K_e = B^T J_D B on the FP64 tensor cores,
         # RES (integration-point AD) and ELM (element-level forward AD), on a bounded element range

@@ -197,6 +197,13 @@ FEOD_API int feod_apply_host(feod_handle h, int op, const double* in0, const dou
  * ||F|| before each step and after the last. Returns FEOD_EINVAL if
  * p^T J p <= 0 occurs (CG breakdown). Synchronises the stream. */
 FEOD_API int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg_iters, double* norms_host);
+/* Newton-CG option: capture each Newton step's CG iterations as a
+ * CUDA graph on an internal stream and replay it (default on; the captured kernels take
+ * the same arguments every step, the per-call scheduling state lives on the device).
+ * enable: 0 or 1. A capture that fails falls back to direct launches. */
+FEOD_API int feod_set_cg_graphs(feod_handle h, int enable);
+/* Number of CG graph replays so far (diagnostic; -1 on a null handle). */
+FEOD_API int64_t feod_cg_graph_launches(feod_handle h);
 /* Newton-CG Jacobian: 0 (default) matrix-free feod_jvp at the current u;   *
  * 1 feod_linearize once per Newton step (it also yields F) and            *
  * feod_jvp_lin in every CG iteration; 2 as 1 plus Jacobi preconditioning   *

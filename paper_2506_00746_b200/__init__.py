@@ -31,6 +31,7 @@ EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "fe
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
            "feod_set_newton_linearization", "feod_brick_shape", "feod_jacobi_diag", "feod_adjoint_solve", "feod_element_matrices",
            "feod_design_grad", "feod_res_design_grad", "feod_apply_host", "feod_newton_cg",
+           "feod_set_cg_graphs", "feod_cg_graph_launches",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
@@ -87,6 +88,9 @@ def load_library(path: str = LIB_PATH):
     lib.feod_adjoint_solve.argtypes = [vp, dp, dp, dp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_apply_host.argtypes = [vp, ctypes.c_int, dp, dp, dp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    lib.feod_set_cg_graphs.argtypes = [vp, ctypes.c_int]
+    lib.feod_cg_graph_launches.argtypes = [vp]
+    lib.feod_cg_graph_launches.restype = i64
     lib.feod_dot.argtypes = [vp, dp, dp, i64, dp]
     lib.feod_profile_next.argtypes = [vp, vp, vp]
     lib.feod_last_error.restype = ctypes.c_char_p
@@ -310,6 +314,13 @@ class Operator:
         self._sync_stream()
         _check(self.lib.feod_newton_cg(self.h, u.data_ptr(), int(newton_steps), int(cg_iters), norms))
         return u, list(norms)
+
+    def set_cg_graphs(self, enable):
+        """Capture the CG iterations of feod_newton_cg as a CUDA graph (default on)."""
+        _check(self.lib.feod_set_cg_graphs(self.h, 1 if enable else 0))
+
+    def cg_graph_launches(self):
+        return int(self.lib.feod_cg_graph_launches(self.h))
 
     def profile_next(self, ev_begin, ev_end):
         """Time the fused kernel of the next call with two torch.cuda.Event(enable_timing=True)."""

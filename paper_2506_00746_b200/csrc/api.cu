@@ -46,6 +46,13 @@ struct feod_op {
   int newton_lin = 0;          // Newton-CG: 0 matrix-free JVP, 1 stored linearisation, 2 + Jacobi
   double* jdiag = nullptr;     // Jacobi diagonal (Newton mode 2), N
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
+  // Newton-CG: the CG iterations captured as a CUDA graph (on gst), replayed per step
+  bool cg_graphs = true, cg_graph_failed = false;
+  cudaGraphExec_t cg_exec = nullptr;
+  uint64_t cg_key = 0;
+  cudaStream_t gst = nullptr;
+  cudaEvent_t ev_g[2] = {nullptr, nullptr};
+  int64_t cg_graph_launches = 0;
 };
 
 static thread_local std::string g_err;
@@ -80,6 +87,10 @@ static void free_all(feod_op* h) {
   cudaFree(h->red);
   cudaFree(h->flag);
   cudaFree(h->ds);
+  if (h->cg_exec) cudaGraphExecDestroy(h->cg_exec);
+  if (h->gst) cudaStreamDestroy(h->gst);
+  for (cudaEvent_t& e : h->ev_g)
+    if (e) cudaEventDestroy(e);
   if (h->sw) cudaEventDestroy(h->sw);
   cudaFree(h->bdone);
   cudaFree(h->fixrows);
@@ -560,10 +571,32 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
   double* p = r + N;
   double* Ap = p + N;
   double* d = Ap + N;
-  double* part = h->red;
-  double* sc = h->red + kRedBlocks;   // sc[0], sc[2]: rr ping-pong; sc[1]: pAp; sc[3]: ||F||^2
+  double* part = h->red;                       // pAp partials (dot_partial)
+  double* part2 = h->red + kRedBlocks + 32;    // r.z partials (cg_update)
+  double* sc = h->red + kRedBlocks;   // sc[0], sc[2]: rz ping-pong; sc[1]: pAp; sc[3]: ||F||^2
   int* bad = h->flag + 1;
   CK(cudaMemsetAsync(bad, 0, sizeof(int), h->st), "feod_newton_cg");
+  // The CG iterations of a Newton step: 5 launches each (operator + fix-up, p.Ap partials,
+  // the update with alpha reduced in-kernel and the r.z partials, the direction with beta
+  // reduced in-kernel). Every kernel argument is fixed for the handle, u and the
+  // preconditioner (DevState holds the per-call scheduling state), so the loop is captured
+  // once as a CUDA graph on an internal stream and replayed every Newton step.
+  auto cg_body = [&](cudaStream_t st, const double* pre) -> int {
+    cudaStream_t keep = h->st;
+    h->st = st;
+    for (int it = 0; it < cg_iters; ++it) {
+      double* rr_old = sc + ((it & 1) ? 2 : 0);
+      double* rr_new = sc + ((it & 1) ? 0 : 2);
+      const int rc = h->newton_lin ? feod_jvp_lin(h, p, Ap) : feod_jvp(h, u, p, Ap);
+      if (rc) { h->st = keep; return rc; }
+      cudaError_t e = dot_partial(p, Ap, N, part, st);
+      if (e == cudaSuccess) e = cg_update(rr_old, part, sc + 1, p, Ap, d, r, N, part2, bad, st, pre);
+      if (e == cudaSuccess) e = cg_dir(part2, rr_new, rr_old, r, p, N, st, pre);
+      if (e != cudaSuccess) { h->st = keep; return cuda_fail(e, "feod_newton_cg: CG"); }
+    }
+    h->st = keep;
+    return FEOD_OK;
+  };
   for (int step = 0; step <= newton_steps; ++step) {
     int rc = h->newton_lin ? feod_linearize(h, u, F) : feod_residual(h, u, F);
     if (rc) return rc;
@@ -586,16 +619,39 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
     CK(cg_init(F, r, p, d, N, h->st, pre), "feod_newton_cg: init");
     CK(dot_partial(r, p, N, part, h->st), "feod_newton_cg: rz");   // p = z = M^{-1} r
     CK(reduce_final(part, sc + 0, h->st), "feod_newton_cg: rr");
-    for (int it = 0; it < cg_iters; ++it) {
-      double* rr_old = sc + ((it & 1) ? 2 : 0);
-      double* rr_new = sc + ((it & 1) ? 0 : 2);
-      rc = h->newton_lin ? feod_jvp_lin(h, p, Ap) : feod_jvp(h, u, p, Ap);
-      if (rc) return rc;
-      CK(dot_partial(p, Ap, N, part, h->st), "feod_newton_cg: pAp");
-      CK(reduce_final(part, sc + 1, h->st), "feod_newton_cg: pAp");
-      CK(cg_update(rr_old, sc + 1, p, Ap, d, r, N, part, bad, h->st, pre), "feod_newton_cg: update");
-      CK(reduce_final(part, rr_new, h->st), "feod_newton_cg: rr");
-      CK(cg_dir(rr_new, rr_old, r, p, N, h->st, pre), "feod_newton_cg: direction");
+    if (cg_iters > 0) {
+      const bool want_graph = h->cg_graphs && !h->cg_graph_failed;
+      const uint64_t key = (reinterpret_cast<uint64_t>(u) ^ (reinterpret_cast<uint64_t>(pre) << 1)) * 31 +
+                           (uint64_t)(h->newton_lin * 1000003 + cg_iters);
+      if (want_graph && (!h->cg_exec || h->cg_key != key)) {
+        if (h->cg_exec) { cudaGraphExecDestroy(h->cg_exec); h->cg_exec = nullptr; }
+        if (!h->gst) {
+          CK(cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking), "feod_newton_cg: stream");
+          for (cudaEvent_t& ev : h->ev_g) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "feod_newton_cg: event");
+        }
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(h->gst, cudaStreamCaptureModeThreadLocal);
+        int crc = e == cudaSuccess ? cg_body(h->gst, pre) : FEOD_ECUDA;
+        cudaError_t e2 = cudaStreamEndCapture(h->gst, &g);
+        if (e == cudaSuccess && crc == FEOD_OK && e2 == cudaSuccess && g)
+          e = cudaGraphInstantiate(&h->cg_exec, g, 0);
+        else
+          e = cudaErrorStreamCaptureInvalidated;
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();   // a failed capture leaves no sticky error
+        if (e != cudaSuccess) { h->cg_exec = nullptr; h->cg_graph_failed = true; }
+        else h->cg_key = key;
+      }
+      if (want_graph && h->cg_exec) {
+        CK(cudaEventRecord(h->ev_g[0], h->st), "feod_newton_cg");
+        CK(cudaStreamWaitEvent(h->gst, h->ev_g[0], 0), "feod_newton_cg");
+        CK(cudaGraphLaunch(h->cg_exec, h->gst), "feod_newton_cg: graph");
+        CK(cudaEventRecord(h->ev_g[1], h->gst), "feod_newton_cg");
+        CK(cudaStreamWaitEvent(h->st, h->ev_g[1], 0), "feod_newton_cg");
+        ++h->cg_graph_launches;
+      } else if ((rc = cg_body(h->st, pre))) {
+        return rc;
+      }
     }
     CK(axpy1(u, d, N, h->st), "feod_newton_cg: u += d");
     int hbad = 0;
@@ -605,3 +661,12 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
   }
   return FEOD_OK;
 }
+
+extern "C" int feod_set_cg_graphs(feod_handle h, int enable) {
+  if (!h || enable < 0 || enable > 1) return fail(FEOD_EINVAL, "feod_set_cg_graphs: bad argument");
+  h->cg_graphs = enable != 0;
+  h->cg_graph_failed = false;
+  return FEOD_OK;
+}
+
+extern "C" int64_t feod_cg_graph_launches(feod_handle h) { return h ? h->cg_graph_launches : -1; }

@@ -73,18 +73,34 @@ __global__ void cg_init_kernel(const double* __restrict__ F, double* __restrict_
   }
 }
 
-// alpha = rr / pAp;  d += alpha p;  r -= alpha Ap;  partials of r.r (same fixed grid as dot_partial)
+// The final stage of a dot product, done redundantly by every CTA of the kernel that
+// needs the scalar: the same thread mapping and tree as reduce_final_kernel, so every
+// CTA (and reduce_final) gets the same bits -- one launch less per scalar.
+FEOD_DEV double reduce_partials(const double* __restrict__ partials, double* sh) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += kRedThreads) acc += partials[i];
+  const double s = block_sum(acc, sh);
+  __syncthreads();   // sh reused by the caller
+  return s;
+}
+
+// alpha = rr / pAp (pAp reduced here from dot_partial's partials; CTA 0 keeps it in
+// *pAp);  d += alpha p;  r -= alpha Ap;  partials of r.r (same fixed grid as dot_partial)
 // (with diag: the partials are of r . M^{-1} r, the preconditioned CG's rz)
 __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __restrict__ rr,
-                                                                const double* __restrict__ pAp,
+                                                                const double* __restrict__ pAp_partials,
+                                                                double* __restrict__ pAp,
                                                                 const double* __restrict__ p,
                                                                 const double* __restrict__ Ap, double* __restrict__ d,
                                                                 double* __restrict__ r, int64_t n,
                                                                 double* __restrict__ partials, int* __restrict__ bad,
                                                                 const double* __restrict__ diag) {
   __shared__ double sh[kRedThreads];
-  const double den = *pAp;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && !(den > 0.0)) *bad = 1;
+  const double den = reduce_partials(pAp_partials, sh);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *pAp = den;
+    if (!(den > 0.0)) *bad = 1;
+  }
   const double alpha = *rr / den;
   double acc[kUnroll] = {};
   int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
@@ -117,11 +133,18 @@ __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
-// p = z + (rz_new / rz_old) p,  z = M^{-1} r (z = r without preconditioner)
-__global__ void cg_dir_kernel(const double* __restrict__ rr_new, const double* __restrict__ rr_old,
-                              const double* __restrict__ r, double* __restrict__ p, int64_t n,
-                              const double* __restrict__ diag) {
-  const double beta = *rr_new / *rr_old;
+// p = z + (rz_new / rz_old) p,  z = M^{-1} r (z = r without preconditioner); rz_new is
+// reduced here from cg_update's partials (CTA 0 stores it for the next iteration, the
+// other slot of the ping-pong than the rz_old read here)
+__global__ void __launch_bounds__(kRedThreads) cg_dir_kernel(const double* __restrict__ rr_partials,
+                                                             double* __restrict__ rr_new,
+                                                             const double* __restrict__ rr_old,
+                                                             const double* __restrict__ r, double* __restrict__ p,
+                                                             int64_t n, const double* __restrict__ diag) {
+  __shared__ double sh[kRedThreads];
+  const double rn = reduce_partials(rr_partials, sh);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *rr_new = rn;
+  const double beta = rn / *rr_old;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
@@ -152,14 +175,15 @@ cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n,
   cg_init_kernel<<<grid_for(n), 256, 0, st>>>(F, r, p, d, diag, n);
   return cudaGetLastError();
 }
-cudaError_t cg_update(const double* rr, const double* pAp, const double* p, const double* Ap, double* d, double* r,
-                      int64_t n, double* partials, int* bad, cudaStream_t st, const double* diag) {
-  cg_update_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(rr, pAp, p, Ap, d, r, n, partials, bad, diag);
+cudaError_t cg_update(const double* rr, const double* pAp_partials, double* pAp, const double* p, const double* Ap,
+                      double* d, double* r, int64_t n, double* partials, int* bad, cudaStream_t st,
+                      const double* diag) {
+  cg_update_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(rr, pAp_partials, pAp, p, Ap, d, r, n, partials, bad, diag);
   return cudaGetLastError();
 }
-cudaError_t cg_dir(const double* rr_new, const double* rr_old, const double* r, double* p, int64_t n,
-                   cudaStream_t st, const double* diag) {
-  cg_dir_kernel<<<grid_for(n), 256, 0, st>>>(rr_new, rr_old, r, p, n, diag);
+cudaError_t cg_dir(const double* rr_partials, double* rr_new, const double* rr_old, const double* r, double* p,
+                   int64_t n, cudaStream_t st, const double* diag) {
+  cg_dir_kernel<<<grid_for(n), kRedThreads, 0, st>>>(rr_partials, rr_new, rr_old, r, p, n, diag);
   return cudaGetLastError();
 }
 cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st) {

@@ -157,3 +157,24 @@ def test_newton_cg_fullsize_state_synchronised_rows():
         assert rel_l2(Jd[rows], O.jvp_rows(pr, u_prev, delta, rows)) <= 1e-11
         assert abs(norms[steps] - np.linalg.norm(r)) <= 1e-10 * norms[steps]
         u_prev = uh
+
+
+@pytest.mark.parametrize("stored", [0, 1, 2])
+def test_newton_cg_graph_replay_bitwise(stored):
+    """NEXT-3: the CG iterations captured as a CUDA graph and replayed per Newton step give
+    the same bits as direct launches (deterministic kernels, device-side scheduling state)."""
+    import torch
+    w = W.C4.resized(3)
+    d = W.draw(w)
+    op = operator(w, d)
+    op.set_newton_linearization(stored)
+    u0 = cuda(np.zeros(w.n_dofs))
+    op.set_cg_graphs(False)
+    u_direct, n_direct = op.newton_cg(u0, 3, 20)
+    assert op.cg_graph_launches() == 0
+    op.set_cg_graphs(True)
+    u_graph, n_graph = op.newton_cg(u0, 3, 20)
+    assert op.cg_graph_launches() == 3
+    assert torch.equal(u_graph, u_direct) and n_graph == n_direct
+    u_again, _ = op.newton_cg(u0, 3, 20)   # replays the cached graph
+    assert op.cg_graph_launches() == 6 and torch.equal(u_again, u_direct)
