@@ -542,17 +542,26 @@ def main():
         gemm = 2.0 * nn * nn * 3 * Qp
         interp = 2.0 * 4 * Qp * nn
         tab = {}
+        per_pass = w.q * (w.k + 1) ** 3 + w.q ** 2 * (w.k + 1) ** 2 + w.q ** 3 * (w.k + 1) + 3 * w.q ** 4
         for elm in (False, True):
             t_em = time_call(lambda: op.element_matrices(u, 0, ne, elm=elm, out=Ke), reps=5)
-            build = (Qp * nn * pw) if elm else (4 * Qp * pw + 2.0 * 4 * 3 * Qp * nn)
-            fl = gemm + interp + build
+            if elm:
+                # value pass (dense B3 + collocated gradients) once, then per seed column: the
+                # tangent through B (forward) and B^T (transposed), and Q dual flux evaluations
+                fl = 2.0 * Qp * nn + 2.0 * 3 * Qp * w.q + nn * (2.0 * 2 * per_pass + Qp * pw)
+            else:
+                fl = gemm + interp + (4 * Qp * pw + 2.0 * 4 * 3 * Qp * nn)
             tab["ELM" if elm else "RES"] = {"ns_per_element": t_em * 1e6 / ne, "kflop_per_element": fl / 1e3,
                                             "tflops": fl * ne / (t_em * 1e-3) / 1e12,
-                                            "gemm_share_of_flops": gemm / fl}
+                                            "dual_flux_evaluations_per_point": nn if elm else 4}
         line["element_tangents"] = {"elements": ne, "nd3": nn, **tab,
                                     "elm_over_res_flops": tab["ELM"]["kflop_per_element"] / tab["RES"]["kflop_per_element"],
                                     "elm_over_res_time": tab["ELM"]["ns_per_element"] / tab["RES"]["ns_per_element"],
-                                    "note": "feod_element_matrices (DMMA m8n8k4 f64); peak 37 TF/s DMMA (tools/dmma_probe.cu)"}
+                                    "elm_over_res_dual_flux_evaluations": nn / 4,
+                                    "table1_fwd_elm_over_res_flops_context": {"Tet1": 2.5, "Tet2": 5.4, "Tet3": 9.4},
+                                    "note": "feod_element_matrices: RES = 4 dual evaluations of D per point + K_e = M^T N "
+                                            "on DMMA m8n8k4 f64; ELM = element-level forward AD, one dual pass of "
+                                            "B^T D(B u_e) per seed column (B inside the differentiation loop)"}
     if w.model == W.HEAT and world == 1:
         # NEXT-1: adjoint solve, 50 BiCGStab iterations (2 J^T applications each), rhs = the recipe's lambda draw
         lam_rhs = torch.as_tensor(d["lam"]).cuda()

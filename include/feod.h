@@ -134,11 +134,14 @@ FEOD_API int feod_jvp_res(feod_handle h, const double* u, const double* v, doubl
 FEOD_API int feod_vjp(feod_handle h, const double* u, const double* w, double* JTw);
 /* Element tangent matrices K_e = B^T J_D(u_q) B (Eq. 3;    *
  * the hex analogue of Table 1) for elements             *
- * e0 .. e0+ne-1 (lexicographic), on the FP64 tensor cores (DMMA 8x8x4).      *
- * Ke (device) gets ne x nd^3 x nd^3 doubles, Ke[e][i][j] = d r_e,i / d u_e,j, *
- * local nodes a + nd (b + nd c). elm = 0: RES, J_D from 4 dual evaluations   *
- * per point (integration-point AD, the paper's approach); elm = 1: ELM,      *
- * element-level forward AD, one dual evaluation per point and trial node.    *
+ * e0 .. e0+ne-1 (lexicographic). Ke (device) gets ne x nd^3 x nd^3 doubles,  *
+ * Ke[e][i][j] = d r_e,i / d u_e,j, local nodes a + nd (b + nd c).            *
+ * elm = 0: RES (integration-point AD, the paper's approach): J_D from 4 dual *
+ *   evaluations per point, then K_e = M^T N on the FP64 tensor cores (DMMA). *
+ * elm = 1: ELM (element-level forward AD, Table 1's other column): column j  *
+ *   is the tangent of the element residual B^T D(B u_e) along e_j, the dual  *
+ *   pushed through the sum-factorised B, D and B^T -- nd^3 dual evaluations  *
+ *   of D per point.                                       *
  * No Dirichlet handling (element level). Orders 1..3 (FEOD_EUNSUPPORTED      *
  * above: an element matrix no longer fits one CTA's shared memory).          */
 FEOD_API int feod_element_matrices(feod_handle h, const double* u, int64_t e0, int64_t ne, int elm, double* Ke);

@@ -470,9 +470,13 @@ extern "C" int feod_element_matrices(feod_handle h, const double* u, int64_t e0,
   if (h->nd > 4) return fail(FEOD_EUNSUPPORTED, "feod_element_matrices: built for orders 1..3");
   if (h->coeffs.model == FEOD_HEAT_DESIGN && !h->P.rho) return fail(FEOD_EINVAL, "feod_element_matrices: rho unset");
   if (ne == 0) return FEOD_OK;
-  CK(element_matrices_nd(h->nd, h->coeffs.model, h->geom == nullptr, elm != 0, h->P, h->T, u, (int)e0, (int)ne, Ke,
-                         h->st),
-     "feod_element_matrices");
+  if (elm)   // element-level forward AD through B, D, B^T (Table 1's ELM), elm.cu
+    CK(element_matrices_elm_nd(h->nd, h->coeffs.model, h->geom == nullptr, h->P, h->T, u, (int)e0, (int)ne, Ke, h->st),
+       "feod_element_matrices");
+  else       // integration-point AD + K_e = M^T N on the FP64 tensor cores (Table 1's RES), elemat.cu
+    CK(element_matrices_nd(h->nd, h->coeffs.model, h->geom == nullptr, false, h->P, h->T, u, (int)e0, (int)ne, Ke,
+                           h->st),
+       "feod_element_matrices");
   return FEOD_OK;
 }
 

@@ -7,11 +7,7 @@
 // 37 TF/s measured vs 32 TF/s for DFMA — tools/dmma_probe.cu).
 //   RES (integration-point AD, the paper's approach): A and b from 4 dual
 //       evaluations of D per point, then N from the tables.
-//   ELM (element-level forward AD): every column j of N from one dual
-//       evaluation of D per point seeded with (phi_j, grad phi_j) — nd^3 dual
-//       evaluations per point, the cost that grows with the element's DOFs. The
-//       seeds are B e_j read from the tables: a forward-mode tool would form them by
-//       pushing width-nd^3 duals through B (8 Q nd^6 more flops).
+//   ELM (element-level forward AD, B inside the differentiation loop): elm.cu (K10).
 // One CTA (8 warps) per element, persistent over a range of elements. M^T and the
 // 1D tables are element-independent and built once per CTA in shared memory.
 #include "common.cuh"
@@ -241,10 +237,10 @@ static cudaError_t elemat_launch(const OpParams& P, const Tables& T, const doubl
 template <int ND, int MODEL>
 static cudaError_t elemat_model(bool affine, bool elm, const OpParams& P, const Tables& T, const double* u, int e0,
                                 int ne, double* Ke, cudaStream_t st) {
-  if (affine) return elm ? elemat_launch<ND, MODEL, true, true>(P, T, u, e0, ne, Ke, st)
-                         : elemat_launch<ND, MODEL, true, false>(P, T, u, e0, ne, Ke, st);
-  return elm ? elemat_launch<ND, MODEL, false, true>(P, T, u, e0, ne, Ke, st)
-             : elemat_launch<ND, MODEL, false, false>(P, T, u, e0, ne, Ke, st);
+  // RES only: the element-level AD variant (Table 1's ELM) is elm.cu (K10)
+  if (elm) return cudaErrorInvalidValue;
+  return affine ? elemat_launch<ND, MODEL, true, false>(P, T, u, e0, ne, Ke, st)
+                : elemat_launch<ND, MODEL, false, false>(P, T, u, e0, ne, Ke, st);
 }
 
 template <int ND>

@@ -77,6 +77,9 @@ cudaError_t cg_dir(const double* rr_partials, double* rr_new, const double* rr_o
 // element tangent matrices on the FP64 tensor cores (elemat.cu, K9): nd = 2..4
 cudaError_t element_matrices_nd(int nd, int model, bool affine, bool elm, const OpParams& P, const Tables& T,
                                 const double* u, int e0, int ne, double* Ke, cudaStream_t st);
+// element tangents by element-level forward AD through B, D and B^T (elm.cu, K10; Table 1's ELM)
+cudaError_t element_matrices_elm_nd(int nd, int model, bool affine, const OpParams& P, const Tables& T,
+                                    const double* u, int e0, int ne, double* Ke, cudaStream_t st);
 // Jacobi diagonal of the stored linearisation (diag.cu, K8)
 cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* diag, cudaStream_t st);
 cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st);
