@@ -122,6 +122,102 @@ __global__ void __launch_bounds__(kDiagThreads) diag_color_kernel(const OpParams
   }   // elements
 }
 
+// Q1 / Q2: one thread per element of the colour, the element's diagonal sum-factorised in
+// registers (the same 9 terms), then added into the colour-exclusive DOFs -- no shared
+// memory and no block barriers (the per-element CTA version above is latency-bound at
+// low order: C5 2.3 ms).
+template <int ND, int NT>
+__global__ void __launch_bounds__(128) diag_elem_kernel(const OpParams P, const Tables T, int color,
+                                                        double* __restrict__ diag) {
+  constexpr int NQ = ND, NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, NL = NT;
+  constexpr int TX[9] = {1, 0, 0, 2, 2, 0, 2, 0, 0};
+  constexpr int TY[9] = {0, 1, 0, 2, 0, 2, 0, 2, 0};
+  constexpr int TZ[9] = {0, 0, 1, 0, 2, 2, 0, 0, 2};
+  constexpr double WT[9] = {1, 1, 1, 2, 2, 2, 1, 1, 1};
+  const int hx = (P.nx + 1 - (color & 1)) / 2, hy = (P.ny + 1 - ((color >> 1) & 1)) / 2;
+  const int hz = (P.nz + 1 - ((color >> 2) & 1)) / 2;
+  const int64_t ne = (int64_t)hx * hy * hz;
+  // 1D factor tables: 0 = B^2, 1 = G^2, 2 = G B
+  auto tab = [&](int k, int i, int a) {
+    const double b = T.B[i][a], g = T.G[i][a];
+    return k == 0 ? b * b : k == 1 ? g * g : g * b;
+  };
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const int ex = 2 * (int)(e % hx) + (color & 1);
+    const int ey = 2 * (int)((e / hx) % hy) + ((color >> 1) & 1);
+    const int ez = 2 * (int)(e / ((int64_t)hx * hy)) + ((color >> 2) & 1);
+    const int64_t px = P.ptx;
+    const double* lin = P.lin + pt_base(P, ex, ey, ez, NL * NQ3);
+    double dg[ND * ND * ND];
+#pragma unroll
+    for (int n = 0; n < ND * ND * ND; ++n) dg[n] = 0.0;
+#pragma unroll
+    for (int term = 0; term < NT; ++term) {
+      double S0[NQ3];
+#pragma unroll
+      for (int q = 0; q < NQ3; ++q) S0[q] = __ldcs(lin + ((q / NQ2) * NL * NQ2 + term * NQ2 + q % NQ2) * px);
+      double S1[ND][NQ2];   // [c][j i]
+#pragma unroll
+      for (int c = 0; c < ND; ++c)
+#pragma unroll
+        for (int ji = 0; ji < NQ2; ++ji) {
+          double s = 0.0;
+#pragma unroll
+          for (int l = 0; l < NQ; ++l) s = fma(S0[l * NQ2 + ji], tab(TZ[term], l, c), s);
+          S1[c][ji] = s;
+        }
+      double S2[ND][ND][NQ];   // [c][b][i]
+#pragma unroll
+      for (int c = 0; c < ND; ++c)
+#pragma unroll
+        for (int b = 0; b < ND; ++b)
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) s = fma(S1[c][j * NQ + i], tab(TY[term], j, b), s);
+            S2[c][b][i] = s;
+          }
+#pragma unroll
+      for (int c = 0; c < ND; ++c)
+#pragma unroll
+        for (int b = 0; b < ND; ++b)
+#pragma unroll
+          for (int a = 0; a < ND; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < NQ; ++i) s = fma(S2[c][b][i], tab(TX[term], i, a), s);
+            dg[a + ND * (b + ND * c)] = fma(WT[term], s, dg[a + ND * (b + ND * c)]);
+          }
+    }
+    const int K = ND - 1;
+#pragma unroll
+    for (int c = 0; c < ND; ++c)
+#pragma unroll
+      for (int b = 0; b < ND; ++b)
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+          const int64_t g = (int64_t)(K * ex + a) + (int64_t)P.Mx * ((K * ey + b) + (int64_t)P.My * (K * ez + c));
+          diag[g] += dg[a + ND * (b + ND * c)];
+        }
+  }
+}
+
+template <int ND, int NT>
+static cudaError_t diag_elem_t(const OpParams& P, const Tables& T, double* diag, cudaStream_t st) {
+  for (int color = 0; color < 8; ++color) {
+    const int hx = (P.nx + 1 - (color & 1)) / 2, hy = (P.ny + 1 - ((color >> 1) & 1)) / 2,
+              hz = (P.nz + 1 - ((color >> 2) & 1)) / 2;
+    const int64_t ne = (int64_t)hx * hy * hz;
+    if (ne == 0) continue;
+    const int64_t b = (ne + 127) / 128;
+    diag_elem_kernel<ND, NT><<<(unsigned)(b < 148 * 32 ? b : 148 * 32), 128, 0, st>>>(P, T, color, diag);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 __global__ void diag_dirichlet_kernel(const OpParams P, double* __restrict__ diag) {
   const int64_t n = (int64_t)P.Mx * P.My * P.Mz;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -163,8 +259,16 @@ cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T
   if (e != cudaSuccess) return e;
   const bool nine = lin_values(model) == 9;
   switch (nd) {
-    case 2: return nine ? diag_nd_t<2, 9>(P, T, diag, st) : diag_nd_t<2, 6>(P, T, diag, st);
-    case 3: return nine ? diag_nd_t<3, 9>(P, T, diag, st) : diag_nd_t<3, 6>(P, T, diag, st);
+    case 2:
+    case 3: {
+      cudaError_t e2 = nd == 2 ? (nine ? diag_elem_t<2, 9>(P, T, diag, st) : diag_elem_t<2, 6>(P, T, diag, st))
+                               : (nine ? diag_elem_t<3, 9>(P, T, diag, st) : diag_elem_t<3, 6>(P, T, diag, st));
+      if (e2 != cudaSuccess) return e2;
+      const int64_t n = (int64_t)P.Mx * P.My * P.Mz;
+      const int64_t b = (n + 255) / 256;
+      diag_dirichlet_kernel<<<(unsigned)(b < kRedBlocks ? b : kRedBlocks), 256, 0, st>>>(P, diag);
+      return cudaGetLastError();
+    }
     case 4: return nine ? diag_nd_t<4, 9>(P, T, diag, st) : diag_nd_t<4, 6>(P, T, diag, st);
     case 5: return nine ? diag_nd_t<5, 9>(P, T, diag, st) : diag_nd_t<5, 6>(P, T, diag, st);
     case 6: return nine ? diag_nd_t<6, 9>(P, T, diag, st) : diag_nd_t<6, 6>(P, T, diag, st);
