@@ -45,6 +45,8 @@ struct feod_op {
   bool lin_valid = false;
   int newton_lin = 0;          // Newton-CG: 0 matrix-free JVP, 1 stored linearisation, 2 + Jacobi
   double* jdiag = nullptr;     // Jacobi diagonal (Newton mode 2), N
+  double* evec = nullptr;      // Q6 tensor-core path: element vector, E x 343 (q6tc.cu)
+  bool q6tc = true;            // FEOD_Q6_TC=0 disables the Q6 tensor-core path (experiments)
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
   // Newton-CG: the CG iterations captured as a CUDA graph (on gst), replayed per step
   bool cg_graphs = true, cg_graph_failed = false;
@@ -98,6 +100,7 @@ static void free_all(feod_op* h) {
   cudaFree(h->lin);
   cudaFree(h->kwork);
   cudaFree(h->jdiag);
+  cudaFree(h->evec);
 }
 
 extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const feod_coeffs* coeffs,
@@ -175,6 +178,7 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
     if (const char* env = std::getenv("FEOD_COL_BZ")) P.tbz = std::max(1, std::atoi(env));   // experiments
   }
   P.nbz = (mesh->nz + P.tbz - 1) / P.tbz;
+  if (const char* env = std::getenv("FEOD_Q6_TC")) h->q6tc = std::atoi(env) != 0;   // experiments
   P.ptx = h->bi.ptx;
   P.pnbx = (mesh->nx + P.ptx - 1) / P.ptx;
   P.shell_stride = shell_size(order * P.tbx + 1, order * P.tby + 1, order * P.tbz + 1);
@@ -314,6 +318,17 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   int grid = 0;
   // MODE_PAJVP reads the stored linearisation only, whatever the geometry
   const bool aff = mode == MODE_PAJVP ? true : h->geom == nullptr;
+  if (h->nd == 7 && h->geom == nullptr && h->q6tc && mode == MODE_JVP) {
+    // Q6 JVP on affine meshes: the FP64 tensor-core kernel + the element-vector assembly
+    // (C4 JVP 444 -> 358 us; its residual measured slower than plane_kernel's: 287 vs 278 us)
+    if (!h->evec && cudaMalloc(&h->evec, sizeof(double) * 343 * (size_t)h->E) != cudaSuccess) {
+      h->evec = nullptr;
+      return fail(FEOD_ENOMEM, std::string(name) + ": element vector");
+    }
+    cudaError_t e = q6tc_run(mode, h->coeffs.model, h->P, h->T, in0, in1, h->evec, out0, h->st);
+    if (pe) cudaEventRecord(pe, h->st);
+    return e == cudaSuccess ? FEOD_OK : cuda_fail(e, name);
+  }
   cudaError_t e = launch_nd(h->nd, mode, h->coeffs.model, aff, h->nbricks, h->P, h->T, p, h->st, &grid);
   if (pe) cudaEventRecord(pe, h->st);
   if (e != cudaSuccess) return cuda_fail(e, name);
