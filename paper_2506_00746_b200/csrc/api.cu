@@ -47,6 +47,7 @@ struct feod_op {
   double* jdiag = nullptr;     // Jacobi diagonal (Newton mode 2), N
   double* evec = nullptr;      // Q6 tensor-core path: element vector, E x 343 (q6tc.cu)
   bool q6tc = true;            // FEOD_Q6_TC=0 disables the Q6 tensor-core path (experiments)
+  bool q6tc_res = true;        // FEOD_Q6_TC_RES=0: the residual on plane_kernel (experiments)
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
   // Newton-CG: the CG iterations captured as a CUDA graph (on gst), replayed per step
   bool cg_graphs = true, cg_graph_failed = false;
@@ -179,6 +180,7 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   }
   P.nbz = (mesh->nz + P.tbz - 1) / P.tbz;
   if (const char* env = std::getenv("FEOD_Q6_TC")) h->q6tc = std::atoi(env) != 0;   // experiments
+  if (const char* env = std::getenv("FEOD_Q6_TC_RES")) h->q6tc_res = std::atoi(env) != 0;
   P.ptx = h->bi.ptx;
   P.pnbx = (mesh->nx + P.ptx - 1) / P.ptx;
   P.shell_stride = shell_size(order * P.tbx + 1, order * P.tby + 1, order * P.tbz + 1);
@@ -189,6 +191,7 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   P.f = coeffs->f;
   const double hx = 1.0 / mesh->nx, hy = 1.0 / mesh->ny, hz = 1.0 / mesh->nz;
   P.cx = hy * hz / hx; P.cy = hx * hz / hy; P.cz = hx * hy / hz; P.vol = hx * hy * hz;
+  P.cxv = P.cx / P.vol; P.cyv = P.cy / P.vol; P.czv = P.cz / P.vol;
   P.rho = coeffs->rho;
   h->nbricks = P.nbx * P.nby * P.nbz;
   // per-point streams (metric, stored linearisation) hold pnbx * ptx elements per row
@@ -318,9 +321,9 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   int grid = 0;
   // MODE_PAJVP reads the stored linearisation only, whatever the geometry
   const bool aff = mode == MODE_PAJVP ? true : h->geom == nullptr;
-  if (h->nd == 7 && h->geom == nullptr && h->q6tc && mode == MODE_JVP) {
-    // Q6 JVP on affine meshes: the FP64 tensor-core kernel + the element-vector assembly
-    // (C4 JVP 444 -> 358 us; its residual measured slower than plane_kernel's: 287 vs 278 us)
+  if (h->nd == 7 && h->geom == nullptr && h->q6tc && q6tc_supports(mode) && (mode != MODE_RES || h->q6tc_res)) {
+    // Q6 on affine meshes (residual, JVP, J^T w, linearisation, stored-linearisation JVP):
+    // the FP64 tensor-core kernel + the assembly of its discontinuous L-vector (q6tc.cu)
     if (!h->evec && cudaMalloc(&h->evec, sizeof(double) * 343 * (size_t)h->E) != cudaSuccess) {
       h->evec = nullptr;
       return fail(FEOD_ENOMEM, std::string(name) + ": element vector");

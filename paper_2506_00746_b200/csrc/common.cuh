@@ -70,6 +70,7 @@ struct OpParams {
   double f;              // source
   // geometry: uniform grid (geom == nullptr): M = w_q diag(cx, cy, cz), W = w_q * vol
   double cx, cy, cz, vol;
+  double cxv, cyv, czv;  // cx / vol, cy / vol, cz / vol: |grad u|^2 = sum_d c_d gh_d^2 / vol on such grids
   const double* geom;    // [E][NQ][6][NQ][NQ] metric, components xx yy zz xy xz yz
   double* lin;           // [E][NQ][lin_values][NQ][NQ] stored linearisation (MODE_LIN writes, MODE_PAJVP reads)
   int vjp_keep_rows;     // MODE_VJP: 1 keeps every row of J^T w (feod_vjp), 0 applies P^T (adjoint solve)

@@ -78,9 +78,20 @@ FEOD_HD double pow_case(double a, double e, int pc) {
   if (pc == 0) return 1.0;
   return ::pow(a, e);
 }
+// sqrt of a dual through one reciprocal square root (device): s = a r, s' = a' r / 2 with
+// r = 1/sqrt(a) -- no division on the derivative; a == 0 gives (0, 0) (reading A20)
+template <class T> FEOD_HD dual<T> sqrt_rs(dual<T> a) {
+#ifdef __CUDA_ARCH__
+  const T r = ::rsqrt(a.v);
+  const bool pos = a.v > T(0);
+  return {pos ? a.v * r : T(0), pos ? (T(0.5) * a.d) * r : T(0)};
+#else
+  return sqrt(a);
+#endif
+}
 template <class T> FEOD_HD dual<T> pow_case(dual<T> a, T e, int pc) {
   if (pc == 1) return a;
-  if (pc == 2) return sqrt(a);
+  if (pc == 2) return sqrt_rs(a);
   if (pc == 0) return {T(1), T(0)};
   const T pv = ::pow(a.v, e);
   return {pv, a.v != T(0) ? e * pv * a.d / a.v : T(0)};   // a.v == 0: reading A20

@@ -36,7 +36,12 @@ FEOD_DEV void flux_hat(const T& u, const T gh[3], const Metric& M, double W, con
     a[2] = gh[0] * M.xz + gh[1] * M.yz + gh[2] * M.zz;
   }
   T kappa;
-  if constexpr (MODEL == PLAPLACE) {
+  if constexpr (MODEL == PLAPLACE && DIAG) {
+    // M = s diag(c), W = s vol: |grad u|^2 = gh . M gh / W = sum_d (c_d / vol) gh_d^2 --
+    // the same quantity without the per-point reciprocal of W
+    T s = gh[0] * (gh[0] * P.cxv) + gh[1] * (gh[1] * P.cyv) + gh[2] * (gh[2] * P.czv) + P.eps2;
+    kappa = pow_case(s, P.half_pm2, P.pcase);
+  } else if constexpr (MODEL == PLAPLACE) {
     T s = (gh[0] * a[0] + gh[1] * a[1] + gh[2] * a[2]) * (1.0 / W) + P.eps2;
     kappa = pow_case(s, P.half_pm2, P.pcase);
   } else if constexpr (MODEL == NLDIFF) {

@@ -20,6 +20,8 @@
 // of its FMAs useful. The element's node results go to an element vector (E x 343); the
 // assembly kernel sums each DOF's <= 8 contributions in a fixed order and applies P^T
 // -- deterministic, no atomics.
+#include <algorithm>
+
 #include "common.cuh"
 #include "dual.cuh"
 #include "kernels.h"
@@ -68,15 +70,20 @@ FEOD_DEV Frag transpose(const Frag& m, int lane) {
 #ifndef FEOD_Q6_MINB_RES
 #define FEOD_Q6_MINB_RES 3
 #endif
+// modes: RES (F(u)), JVP (J(u) v), VJP (J(u)^T w, w's Dirichlet entries masked, reading
+// A17), LIN (F(u) and the point linearisation written to P.lin), PAJVP (J(u0) v from P.lin)
+template <int MODE> constexpr int q6_nin() { return (MODE == MODE_JVP || MODE == MODE_VJP) ? 2 : 1; }
+
 template <int MODE, int MODEL>
-__global__ void __launch_bounds__(32 * q6::WARPS, MODE == MODE_RES ? FEOD_Q6_MINB_RES : FEOD_Q6_MINB_JVP)
+__global__ void __launch_bounds__(32 * q6::WARPS, q6_nin<MODE>() == 1 ? FEOD_Q6_MINB_RES : FEOD_Q6_MINB_JVP)
 q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, const double* __restrict__ in1,
             double* __restrict__ ev) {
   using namespace q6;
-  constexpr int NIN = MODE == MODE_RES ? 1 : 2;
+  constexpr int NIN = q6_nin<MODE>();
+  constexpr int NL = lin_values(MODEL);   // stored linearisation values per point (LIN, PAJVP)
   // two-field modes: the first field's four point channels are parked in shared memory
   // (lane-interleaved, conflict-free), so only one field's 56 doubles are live in registers
-  extern __shared__ double q6sm[];
+  extern __shared__ __align__(16) double q6sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* park = q6sm + (size_t)wid * (4 * 7 * 2 * 32);   // [channel][plane][t][lane]
   auto pk = [&](int ch, int l, int t) -> double& { return park[((ch * 7 + l) * 2 + t) * 32 + lane]; };
@@ -96,13 +103,18 @@ q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, co
 
   // B and the collocated gradients of one field: nodes z = c in fragment c (rows y,
   // columns x) -> U, Ux, Uy, Uz at the points, plane l, fragment [i][j]
-  auto forward = [&](const double* __restrict__ src, int ex, int ey, int ez, Frag* U, Frag* Ux, Frag* Uy, Frag* Uz) {
+  auto forward = [&](const double* __restrict__ src, int ex, int ey, int ez, bool mask, Frag* U, Frag* Ux, Frag* Uy,
+                     Frag* Uz) {
     Frag X[7];
 #pragma unroll
     for (int c = 0; c < 7; ++c) {
       const int64_t row = (int64_t)(K * ex) + (int64_t)P.Mx * ((K * ey + r) + (int64_t)P.My * (K * ez + c));
 #pragma unroll
-      for (int t = 0; t < 2; ++t) X[c].v[t] = (rowv && colv[t]) ? __ldg(src + row + 2 * q + t) : 0.0;
+      for (int t = 0; t < 2; ++t) {
+        double x = (rowv && colv[t]) ? __ldg(src + row + 2 * q + t) : 0.0;
+        if (mask && is_dirichlet(K * ex + 2 * q + t, K * ey + r, K * ez + c, P.Mx, P.My, P.Mz, P.faces)) x = 0.0;
+        X[c].v[t] = x;
+      }
     }
     Frag Ep[7];   // after x and y: [i][j] per node plane c
 #pragma unroll
@@ -133,11 +145,39 @@ q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, co
     }
   };
 
+  // PAJVP with 16-byte sized element records (p-Laplacian, 6 values per point): each warp
+  // stages its element's stored linearisation in shared memory by one TMA bulk copy,
+  // issued right after the previous element's pointwise phase (it lands during that
+  // element's B^T and this element's B)
+  constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
+  constexpr uint32_t LIN_BYTES = NL * 343 * sizeof(double);
+  double* const lbuf = q6sm + (size_t)wid * (NL * 343);
+  uint64_t* const lbar = reinterpret_cast<uint64_t*>(q6sm + (size_t)WARPS * (NL * 343)) + wid;
+  uint32_t lphase = 0;
+  auto issue_lin = [&](int64_t en) {
+    if constexpr (TMA_LIN) {
+      if (lane == 0 && en < E) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(lbar, LIN_BYTES);
+        mbar_arrive(lbar);
+        bulk_g2s(lbuf, P.lin + en * (NL * 343), LIN_BYTES, lbar);
+      }
+    }
+  };
+  if constexpr (TMA_LIN) {
+    if (lane == 0) {
+      mbar_init(lbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    issue_lin((int64_t)blockIdx.x * WARPS + wid);
+  }
+
   for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
     const int ex = (int)(e % P.nx), ey = (int)((e / P.nx) % P.ny), ez = (int)(e / ((int64_t)P.nx * P.ny));
     Frag U[7], Ux[7], Uy[7], Uz[7];   // the last field's channels (the fluxes overwrite Ux, Uy, Uz)
     if constexpr (NIN == 2) {
-      forward(in0, ex, ey, ez, U, Ux, Uy, Uz);
+      forward(in0, ex, ey, ez, false, U, Ux, Uy, Uz);
 #pragma unroll
       for (int l = 0; l < 7; ++l)
 #pragma unroll
@@ -148,15 +188,45 @@ q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, co
           pk(3, l, t) = Uz[l].v[t];
         }
       __syncwarp();
-      forward(in1, ex, ey, ez, U, Ux, Uy, Uz);
+      forward(in1, ex, ey, ez, MODE == MODE_VJP, U, Ux, Uy, Uz);
     } else {
-      forward(in0, ex, ey, ez, U, Ux, Uy, Uz);
+      forward(in0, ex, ey, ez, false, U, Ux, Uy, Uz);
     }
     // ---- D at the points (slot (i = r, j = 2q + t) of plane l); fluxes over Ux / Uy / Uz
-    const double rho_e = (MODEL == HEAT) ? __ldg(P.rho + e) : 1.0;
+    const double rho_e = (MODEL == HEAT && MODE != MODE_PAJVP) ? __ldg(P.rho + e) : 1.0;
+    // the element's stored linearisation, [l][NL][j][i] (the plane kernel's layout, ptx = 1)
+    double* const linp = (MODE == MODE_LIN || MODE == MODE_PAJVP) ? P.lin + e * (NL * 343) : nullptr;
+    if constexpr (MODE == MODE_PAJVP && !TMA_LIN) {   // next element's values into L2 while this one computes
+      const int64_t en = e + (int64_t)gridDim.x * WARPS;
+      if (lane == 0 && en < E) prefetch_l2_bulk(P.lin + en * (NL * 343), NL * 343 * sizeof(double));
+    }
+    if constexpr (TMA_LIN) {
+      mbar_wait(lbar, lphase);
+      lphase ^= 1u;
+    }
+    constexpr int NSV = MODE == MODE_PAJVP ? NL : 1;
+    double svn[2][NSV];   // PAJVP: plane l's stored values, requested one plane ahead
+    auto load_sv = [&](int l, double (*dst)[NSV]) {
+      if constexpr (MODE == MODE_PAJVP) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int c = 0; c < NL; ++c)
+            dst[t][c] = !(rowv && colv[t]) ? 0.0
+                        : TMA_LIN ? lbuf[(l * NL + c) * 49 + (2 * q + t) * 7 + r]
+                                  : ld_stream(linp + (l * NL + c) * 49 + (2 * q + t) * 7 + r);
+      }
+    };
+    load_sv(0, svn);
     Frag V[7];   // value channel (residual: the load term)
 #pragma unroll
-    for (int l = 0; l < 7; ++l)
+    for (int l = 0; l < 7; ++l) {
+      double sv[2][NSV];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int c = 0; c < NSV; ++c) sv[t][c] = svn[t][c];
+      if (l + 1 < 7) load_sv(l + 1, svn);
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int j = 2 * q + t;
@@ -173,15 +243,24 @@ q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, co
           Uxl[NIN - 1] = Ux[l].v[t];
           Uyl[NIN - 1] = Uy[l].v[t];
           Uzl[NIN - 1] = Uz[l].v[t];
-          double gpart = 0.0, lv[9];
-          point_op<MODE, MODEL, true>(Ul, Uxl, Uyl, Uzl, M, W, rho_e, P, nullptr, F0, F1, gpart, lv);
+          double gpart = 0.0, lv[NL];
+          point_op<MODE, MODEL, true>(Ul, Uxl, Uyl, Uzl, M, W, rho_e, P, sv[t], F0, F1, gpart, lv);
+          if constexpr (MODE == MODE_LIN) {
+#pragma unroll
+            for (int c = 0; c < NL; ++c) linp[(l * NL + c) * 49 + j * 7 + r] = lv[c];
+          }
         }
         Ux[l].v[t] = F0[0];
         Uy[l].v[t] = F0[1];
         Uz[l].v[t] = F0[2];
         V[l].v[t] = value_channel(MODE, 0) ? F0[3] : 0.0;
       }
+    }
     if constexpr (NIN == 2) __syncwarp();   // park reads done before the next element's writes
+    if constexpr (TMA_LIN) {                // buffer reads done: stage the next element's values
+      __syncwarp();
+      issue_lin(e + (int64_t)gridDim.x * WARPS);
+    }
     // ---- B^T: R = Dx^T Fx + Dy^T Fy + Dz^T Fz + V at the points, then z, y, x to the nodes
     Frag R[7];
 #pragma unroll
@@ -201,7 +280,11 @@ q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, co
       acc.v[1] += rx.v[1];
       R[l] = contract_cols(Uy[l], WDt, acc);   // + Dy^T Fy
     }
-    double* out = ev + e * NN;
+    // element node (a, b, c) -> the discontinuous L-vector (7 nx) x (7 ny) x (7 nz), x fastest:
+    // an element's 7-node x-rows are contiguous and neighbours' rows adjacent, so the
+    // assembly reads it row by row, coalesced
+    const int64_t LXd = 7 * (int64_t)P.nx, LYd = 7 * (int64_t)P.ny;
+    double* out = ev + ((int64_t)(7 * ez) * LYd + 7 * ey) * LXd + 7 * ex;
 #pragma unroll
     for (int c = 0; c < 7; ++c) {
       Frag S;
@@ -215,88 +298,331 @@ q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, co
       const Frag ty = contract_cols(S, WBt, zero);                      // [i][b]
       const Frag nd = contract_cols(transpose(ty, lane), WBt, zero);    // [b][a]
       if (rowv) {
+        double* o = out + ((int64_t)c * LYd + r) * LXd;
 #pragma unroll
         for (int t = 0; t < 2; ++t)
-          if (colv[t]) out[c * 49 + r * 7 + 2 * q + t] = nd.v[t];
+          if (colv[t]) o[2 * q + t] = nd.v[t];
       }
     }
   }
 }
 
-// G^T + P^T from the element vector: each DOF sums its <= 8 element contributions in
-// ascending element order (z, y, x), Dirichlet rows 0 -- deterministic. One CTA row per
-// DOF row (Y, Z): the y / z contributors are row-uniform, the x ones come from K = 6
-// (compile-time division); consecutive threads read consecutive element-vector entries.
-__global__ void __launch_bounds__(256) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
-                                                             double* __restrict__ out) {
-  constexpr int K = q6::K, ND = q6::ND;
-  auto axis = [&](int G, int ne, int* c, int* a) {
-    int nc = 0;
-    const int hi = min(G / K, ne - 1);
-    if (G - K * hi == 0 && hi > 0) { c[nc] = hi - 1; a[nc] = K; ++nc; }
-    c[nc] = hi; a[nc] = G - K * hi; ++nc;
-    return nc;
+// Per-point-plane variant (FEOD_Q6_PERL, default): after x and y, each field keeps only
+// its 7 node-plane fragments Ep[c] ([i][j]); point plane l is then formed, differentiated,
+// passed through D and transposed back in one step -- U_l = sum_c B[l][c] Ep[c] and
+// Uz_l = sum_c G[l][c] Ep[c] (DFMA), Uy_l / Ux_l by DMMA; after D,
+// R_l = V_l + Dy^T Fy_l + Dx^T Fx_l (DMMA) and the z-transpose accumulates
+// S[c] += B[l][c] R_l + G[l][c] Fz_l (DFMA). The same contractions as above (G = D B
+// exactly, k <= q - 1), with 7 fragments per field and 7 accumulators live instead of
+// 4 x 7 point channels: no shared-memory parking, fewer registers.
+#ifndef FEOD_Q6_PERL
+#define FEOD_Q6_PERL 1
+#endif
+#ifndef FEOD_Q6P_MINB1   // residual (measured C4: 4 CTAs of 4 warps per SM, 128 registers)
+#define FEOD_Q6P_MINB1 4
+#endif
+#ifndef FEOD_Q6P_MINB2   // two-field modes and PAJVP (3 CTAs, 168 registers; PAJVP spills at 128)
+#define FEOD_Q6P_MINB2 3
+#endif
+template <int MODE, int MODEL>
+__global__ void __launch_bounds__(32 * q6::WARPS,
+                                  (q6_nin<MODE>() == 2 || MODE == MODE_PAJVP) ? FEOD_Q6P_MINB2 : FEOD_Q6P_MINB1)
+q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, const double* __restrict__ in1,
+                 double* __restrict__ ev) {
+  using namespace q6;
+  constexpr int NIN = q6_nin<MODE>();
+  constexpr int NL = lin_values(MODEL);
+  extern __shared__ __align__(16) double q6sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  const int64_t E = (int64_t)P.nx * P.ny * P.nz;
+  auto tab = [&](int kind, int s) {   // 0: B[n][c] 1: D[n][c] 2: B[c][n] 3: D[c][n]
+    const int c = 2 * q + s, n = r;
+    if (c >= 7 || n >= 7) return 0.0;
+    return kind == 0 ? T.B[n][c] : kind == 1 ? T.D[n][c] : kind == 2 ? T.B[c][n] : T.D[c][n];
   };
+  const double WB[2] = {tab(0, 0), tab(0, 1)}, WD[2] = {tab(1, 0), tab(1, 1)};
+  const double WBt[2] = {tab(2, 0), tab(2, 1)}, WDt[2] = {tab(3, 0), tab(3, 1)};
+  const bool rowv = r < 7;
+  const bool colv[2] = {2 * q < 7, 2 * q + 1 < 7};
+  const Frag zero = {{0.0, 0.0}};
+
+  // x and y of one field: node plane c (rows y, columns x) -> Ep[c] = [i][j]
+  auto nodes_xy = [&](const double* __restrict__ src, int ex, int ey, int ez, bool mask, Frag* Ep) {
+    Frag X[7];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      const int64_t row = (int64_t)(K * ex) + (int64_t)P.Mx * ((K * ey + r) + (int64_t)P.My * (K * ez + c));
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        double x = (rowv && colv[t]) ? __ldg(src + row + 2 * q + t) : 0.0;
+        if (mask && is_dirichlet(K * ex + 2 * q + t, K * ey + r, K * ez + c, P.Mx, P.My, P.Mz, P.faces)) x = 0.0;
+        X[c].v[t] = x;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 7; ++c) Ep[c] = contract_cols(transpose(contract_cols(X[c], WB, zero), lane), WB, zero);
+  };
+
+  constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
+  constexpr uint32_t LIN_BYTES = NL * 343 * sizeof(double);
+  double* const lbuf = q6sm + (size_t)wid * (NL * 343);
+  uint64_t* const lbar = reinterpret_cast<uint64_t*>(q6sm + (size_t)WARPS * (NL * 343)) + wid;
+  uint32_t lphase = 0;
+  auto issue_lin = [&](int64_t en) {
+    if constexpr (TMA_LIN) {
+      if (lane == 0 && en < E) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(lbar, LIN_BYTES);
+        mbar_arrive(lbar);
+        bulk_g2s(lbuf, P.lin + en * (NL * 343), LIN_BYTES, lbar);
+      }
+    }
+  };
+  if constexpr (TMA_LIN) {
+    if (lane == 0) {
+      mbar_init(lbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    issue_lin((int64_t)blockIdx.x * WARPS + wid);
+  }
+
+  for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
+    const int ex = (int)(e % P.nx), ey = (int)((e / P.nx) % P.ny), ez = (int)(e / ((int64_t)P.nx * P.ny));
+    Frag Ep[NIN][7];
+    nodes_xy(in0, ex, ey, ez, false, Ep[0]);
+    if constexpr (NIN == 2) nodes_xy(in1, ex, ey, ez, MODE == MODE_VJP, Ep[NIN - 1]);
+    const double rho_e = (MODEL == HEAT && MODE != MODE_PAJVP) ? __ldg(P.rho + e) : 1.0;
+    double* const linp = (MODE == MODE_LIN || MODE == MODE_PAJVP) ? P.lin + e * (NL * 343) : nullptr;
+    if constexpr (MODE == MODE_PAJVP && !TMA_LIN) {
+      const int64_t en = e + (int64_t)gridDim.x * WARPS;
+      if (lane == 0 && en < E) prefetch_l2_bulk(P.lin + en * (NL * 343), NL * 343 * sizeof(double));
+    }
+    if constexpr (TMA_LIN) {
+      mbar_wait(lbar, lphase);
+      lphase ^= 1u;
+    }
+    Frag S[7];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) S[c] = zero;
+#pragma unroll
+    for (int l = 0; l < 7; ++l) {
+      // point plane l of each field: value, collocated x / y derivatives, z derivative
+      Frag Ul[NIN], Uxl[NIN], Uyl[NIN], Uzl[NIN];
+#pragma unroll
+      for (int f = 0; f < NIN; ++f) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          double a = T.B[l][0] * Ep[f][0].v[t], b = T.G[l][0] * Ep[f][0].v[t];
+#pragma unroll
+          for (int c = 1; c < 7; ++c) {
+            a = fma(T.B[l][c], Ep[f][c].v[t], a);
+            b = fma(T.G[l][c], Ep[f][c].v[t], b);
+          }
+          Ul[f].v[t] = a;
+          Uzl[f].v[t] = b;
+        }
+        Uyl[f] = contract_cols(Ul[f], WD, zero);                                   // d/dy: [i][j']
+        Uxl[f] = transpose(contract_cols(transpose(Ul[f], lane), WD, zero), lane);   // d/dx: [i'][j]
+      }
+      Frag Fx, Fy, Fz, V;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int j = 2 * q + t;
+        double F0[4] = {0.0, 0.0, 0.0, 0.0}, F1[4];
+        if (rowv && colv[t]) {
+          const double wq = T.w[r] * T.w[j] * T.w[l];
+          const Metric M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
+          const double W = wq * P.vol;
+          double u0[NIN], gx[NIN], gy[NIN], gz[NIN];
+#pragma unroll
+          for (int f = 0; f < NIN; ++f) {
+            u0[f] = Ul[f].v[t]; gx[f] = Uxl[f].v[t]; gy[f] = Uyl[f].v[t]; gz[f] = Uzl[f].v[t];
+          }
+          double sv[MODE == MODE_PAJVP ? NL : 1];
+          if constexpr (MODE == MODE_PAJVP) {
+#pragma unroll
+            for (int c = 0; c < NL; ++c) {
+              const int o = (l * NL + c) * 49 + j * 7 + r;
+              sv[c] = TMA_LIN ? lbuf[o] : ld_stream(linp + o);
+            }
+          }
+          double gpart = 0.0, lv[NL];
+          point_op<MODE, MODEL, true>(u0, gx, gy, gz, M, W, rho_e, P, sv, F0, F1, gpart, lv);
+          if constexpr (MODE == MODE_LIN) {
+#pragma unroll
+            for (int c = 0; c < NL; ++c) linp[(l * NL + c) * 49 + j * 7 + r] = lv[c];
+          }
+        }
+        Fx.v[t] = F0[0];
+        Fy.v[t] = F0[1];
+        Fz.v[t] = F0[2];
+        V.v[t] = value_channel(MODE, 0) ? F0[3] : 0.0;
+      }
+      // B^T at plane l: R_l = V + Dx^T Fx + Dy^T Fy, then z into the node-plane accumulators
+      Frag R = transpose(contract_cols(transpose(Fx, lane), WDt, zero), lane);
+      R.v[0] += V.v[0];
+      R.v[1] += V.v[1];
+      R = contract_cols(Fy, WDt, R);
+#pragma unroll
+      for (int c = 0; c < 7; ++c)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) S[c].v[t] = fma(T.B[l][c], R.v[t], fma(T.G[l][c], Fz.v[t], S[c].v[t]));
+    }
+    if constexpr (TMA_LIN) {   // buffer reads done: stage the next element's values
+      __syncwarp();
+      issue_lin(e + (int64_t)gridDim.x * WARPS);
+    }
+    const int64_t LXd = 7 * (int64_t)P.nx, LYd = 7 * (int64_t)P.ny;
+    double* out = ev + ((int64_t)(7 * ez) * LYd + 7 * ey) * LXd + 7 * ex;
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      const Frag ty = contract_cols(S[c], WBt, zero);                      // [i][b]
+      const Frag nd = contract_cols(transpose(ty, lane), WBt, zero);       // [b][a]
+      if (rowv) {
+        double* o = out + ((int64_t)c * LYd + r) * LXd;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (colv[t]) o[2 * q + t] = nd.v[t];
+      }
+    }
+  }
+}
+
+// G^T + P^T from the discontinuous L-vector: DOF X of an axis is node a = X - 6 e of
+// element e (X' = 7e + a = X + e); an element-boundary DOF (X = 6 e, 0 < e < n) has the
+// two candidates X' = 7e - 1 and 7e (ascending element order). A CTA per DOF row (Y, Z):
+// stage 1 sums, for every X' of the row, its <= 4 source rows (the row-uniform y / z
+// candidates, z then y ascending) into shared memory with coalesced loads; stage 2 gives
+// each DOF its one or two X' sums (left element first) and applies P^T. Deterministic,
+// no atomics.
+FEOD_DEV int q6_cands(int G, int ne, int* c) {
+  if (G % 6 == 0 && G > 0 && G < 6 * ne) {
+    c[0] = 7 * (G / 6) - 1;
+    c[1] = 7 * (G / 6);
+    return 2;
+  }
+  const int e = min(G / 6, ne - 1);
+  c[0] = 7 * e + (G - 6 * e);
+  return 1;
+}
+
+constexpr int kAsmThreads = 256;
+constexpr int kAsmUnroll = 8;   // X' loads per lane issued together
+
+// A warp per DOF row (Y, Z) with a shared-memory row buffer of its own: stage 1 sums
+// each X' of the row over the row's <= 4 source rows (lanes over X', coalesced, the
+// loads of kAsmUnroll X' in flight together), stage 2 gives each DOF X its one or two
+// X' sums (left element first) and applies P^T.
+__global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
+                                                                     double* __restrict__ out) {
+  extern __shared__ __align__(16) double asm_sm[];
+  const int LX = 7 * P.nx;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* const t = asm_sm + (size_t)wid * LX;
+  const int64_t LYd = 7 * (int64_t)P.ny;
   const int rows = P.My * P.Mz;
-  // a warp per DOF row (Y, Z): its y / z contributors are row-uniform, the x ones come
-  // from K = 6 (compile-time division); the lanes read consecutive element-vector entries
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int YZ = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); YZ < rows; YZ += warps) {
+  const int warps = gridDim.x * (kAsmThreads / 32);
+  for (int YZ = blockIdx.x * (kAsmThreads / 32) + wid; YZ < rows; YZ += warps) {
     const int Y = YZ % P.My, Z = YZ / P.My;
-    int cy[2], ay[2], cz[2], az[2];
-    const int nyc = axis(Y, P.ny, cy, ay), nzc = axis(Z, P.nz, cz, az);
+    int cy[2], cz[2];
+    const int nyc = q6_cands(Y, P.ny, cy), nzc = q6_cands(Z, P.nz, cz);
+    const double* src[4] = {ev, ev, ev, ev};
+    int ns = 0;
+    for (int kz = 0; kz < nzc; ++kz)
+      for (int ky = 0; ky < nyc; ++ky) src[ns++] = ev + ((int64_t)cz[kz] * LYd + cy[ky]) * LX;
+    for (int X0 = 0; X0 < LX; X0 += 32 * kAsmUnroll) {
+      double v[kAsmUnroll][4];
+#pragma unroll
+      for (int m = 0; m < kAsmUnroll; ++m) {
+        const int Xp = X0 + 32 * m + lane;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[m][k] = (k < ns && Xp < LX) ? __ldcs(src[k] + Xp) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < kAsmUnroll; ++m) {
+        const int Xp = X0 + 32 * m + lane;
+        if (Xp < LX) t[Xp] = ((v[m][0] + v[m][1]) + v[m][2]) + v[m][3];   // absent sources add +0.0
+      }
+    }
+    __syncwarp();
     const bool dyz = ((P.faces & 4u) && Y == 0) || ((P.faces & 8u) && Y == P.My - 1) ||
                      ((P.faces & 16u) && Z == 0) || ((P.faces & 32u) && Z == P.Mz - 1);
-    const int64_t row = (int64_t)P.Mx * (Y + (int64_t)P.My * Z);
-    for (int X = threadIdx.x & 31; X < P.Mx; X += 32) {
-      int cx[2], ax[2];
-      const int nxc = axis(X, P.nx, cx, ax);
-      double s = 0.0;
-      for (int kz = 0; kz < nzc; ++kz)
-        for (int ky = 0; ky < nyc; ++ky) {
-          const int64_t e0 = (int64_t)P.nx * (cy[ky] + (int64_t)P.ny * cz[kz]);
-          const int off = az[kz] * ND * ND + ay[ky] * ND;
-          for (int kx = 0; kx < nxc; ++kx) s += __ldcs(ev + (e0 + cx[kx]) * q6::NN + off + ax[kx]);
-        }
+    double* orow = out + (int64_t)P.Mx * YZ;
+    for (int X = lane; X < P.Mx; X += 32) {
+      const int e = X / 6, a = X - 6 * e;
+      double s;
+      if (a == 0 && e > 0 && e < P.nx) s = t[7 * e - 1] + t[7 * e];   // left element first
+      else s = t[X + min(e, P.nx - 1)];   // X = 6 nx: the last element's node 6, X' = 7 nx - 1
       const bool dir = dyz || ((P.faces & 1u) && X == 0) || ((P.faces & 2u) && X == P.Mx - 1);
-      out[row + X] = dir ? 0.0 : s;
+      orow[X] = dir ? 0.0 : s;
     }
+    __syncwarp();
   }
 }
 
 template <int MODE, int MODEL>
 static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double* in0, const double* in1, double* ev,
                                double* out, cudaStream_t st) {
-  constexpr size_t smem = MODE == MODE_RES ? 0 : sizeof(double) * q6::WARPS * 4 * 7 * 2 * 32;
-  cudaError_t e = cudaFuncSetAttribute(q6tc_kernel<MODE, MODEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  constexpr int NL = lin_values(MODEL);
+  constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
+#if FEOD_Q6_PERL
+  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS : 0;
+  const void* kfn = (const void*)q6tc_perl_kernel<MODE, MODEL>;
+#else
+  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS
+                          : q6_nin<MODE>() == 1 ? 0 : sizeof(double) * q6::WARPS * 4 * 7 * 2 * 32;
+  const void* kfn = (const void*)q6tc_kernel<MODE, MODEL>;
+#endif
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int slots = 0;
-  if ((e = persistent_slots((const void*)q6tc_kernel<MODE, MODEL>, 32 * q6::WARPS, smem, &slots)) != cudaSuccess) return e;
+  if ((e = persistent_slots(kfn, 32 * q6::WARPS, smem, &slots)) != cudaSuccess) return e;
   const int64_t E = (int64_t)P.nx * P.ny * P.nz;
   const int64_t want = (E + q6::WARPS - 1) / q6::WARPS;
-  q6tc_kernel<MODE, MODEL><<<(unsigned)(want < slots ? want : slots), 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev);
+  const unsigned grid = (unsigned)(want < slots ? want : slots);
+#if FEOD_Q6_PERL
+  q6tc_perl_kernel<MODE, MODEL><<<grid, 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev);
+#else
+  q6tc_kernel<MODE, MODEL><<<grid, 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev);
+#endif
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int rows = P.My * P.Mz, wpb = 8;
-  const int blocks = (rows + wpb - 1) / wpb;
-  evec_assemble_kernel<<<blocks < 148 * 8 ? blocks : 148 * 8, 32 * wpb, 0, st>>>(P, ev, out);
+  const int rows = P.My * P.Mz;
+  const size_t asm_smem = sizeof(double) * 7 * (size_t)P.nx * (kAsmThreads / 32);
+  if (asm_smem > 48 * 1024) return cudaErrorInvalidValue;   // nx <= 109
+  OpParams Pa = P;
+  if (MODE == MODE_VJP && P.vjp_keep_rows) Pa.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
+  const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
+  evec_assemble_kernel<<<(unsigned)(ctas < 148 * 8 ? ctas : 148 * 8), kAsmThreads, asm_smem, st>>>(Pa, ev, out);
   return cudaGetLastError();
 }
 
-// C4's path: Q6, affine, residual or JVP (other modes / perturbed meshes use plane_kernel)
+// C4's path: Q6 on affine meshes, the modes above (other modes / perturbed meshes use plane_kernel)
+template <int MODE>
+static cudaError_t q6tc_mode(int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
+                             double* ev, double* out, cudaStream_t st) {
+  switch (model) {
+    case PLAPLACE: return q6tc_launch<MODE, PLAPLACE>(P, T, in0, in1, ev, out, st);
+    case NLDIFF: return q6tc_launch<MODE, NLDIFF>(P, T, in0, in1, ev, out, st);
+    case HEAT: return q6tc_launch<MODE, HEAT>(P, T, in0, in1, ev, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// MODE_LIN stays on plane_kernel (measured C4: 343 us there, 415 us here -- three dual
+// evaluations per point spill at this kernel's 168 registers); both write the same layout
+bool q6tc_supports(int mode) {
+  return mode == MODE_RES || mode == MODE_JVP || mode == MODE_VJP || mode == MODE_PAJVP;
+}
+
 cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
                      double* ev, double* out, cudaStream_t st) {
-  if (mode == MODE_RES) {
-    switch (model) {
-      case PLAPLACE: return q6tc_launch<MODE_RES, PLAPLACE>(P, T, in0, in1, ev, out, st);
-      case NLDIFF: return q6tc_launch<MODE_RES, NLDIFF>(P, T, in0, in1, ev, out, st);
-      case HEAT: return q6tc_launch<MODE_RES, HEAT>(P, T, in0, in1, ev, out, st);
-    }
-  } else if (mode == MODE_JVP) {
-    switch (model) {
-      case PLAPLACE: return q6tc_launch<MODE_JVP, PLAPLACE>(P, T, in0, in1, ev, out, st);
-      case NLDIFF: return q6tc_launch<MODE_JVP, NLDIFF>(P, T, in0, in1, ev, out, st);
-      case HEAT: return q6tc_launch<MODE_JVP, HEAT>(P, T, in0, in1, ev, out, st);
-    }
+  switch (mode) {
+    case MODE_RES: return q6tc_mode<MODE_RES>(model, P, T, in0, in1, ev, out, st);
+    case MODE_JVP: return q6tc_mode<MODE_JVP>(model, P, T, in0, in1, ev, out, st);
+    case MODE_VJP: return q6tc_mode<MODE_VJP>(model, P, T, in0, in1, ev, out, st);
+    case MODE_PAJVP: return q6tc_mode<MODE_PAJVP>(model, P, T, in0, in1, ev, out, st);
   }
   return cudaErrorInvalidValue;
 }
