@@ -48,6 +48,11 @@ struct feod_op {
   double* evec = nullptr;      // Q6 tensor-core path: element vector, E x 343 (q6tc.cu)
   bool q6tc = true;            // FEOD_Q6_TC=0 disables the Q6 tensor-core path (experiments)
   bool q6tc_res = true;        // FEOD_Q6_TC_RES=0: the residual on plane_kernel (experiments)
+  // Newton-CG: when set, the next operator call also forms the partials of dot_x . out
+  // into dot_part (q6tc assembly) and sets dot_fused; cleared by the call
+  const double* dot_x = nullptr;
+  double* dot_part = nullptr;
+  bool dot_fused = false;
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
   // Newton-CG: the CG iterations captured as a CUDA graph (on gst), replayed per step
   bool cg_graphs = true, cg_graph_failed = false;
@@ -328,7 +333,10 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
       h->evec = nullptr;
       return fail(FEOD_ENOMEM, std::string(name) + ": element vector");
     }
-    cudaError_t e = q6tc_run(mode, h->coeffs.model, h->P, h->T, in0, in1, h->evec, out0, h->st);
+    cudaError_t e = q6tc_run(mode, h->coeffs.model, h->P, h->T, in0, in1, h->evec, out0, h->dot_x, h->dot_part, h->st);
+    h->dot_fused = h->dot_x != nullptr;
+    h->dot_x = nullptr;
+    h->dot_part = nullptr;
     if (pe) cudaEventRecord(pe, h->st);
     return e == cudaSuccess ? FEOD_OK : cuda_fail(e, name);
   }
@@ -609,9 +617,16 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
     for (int it = 0; it < cg_iters; ++it) {
       double* rr_old = sc + ((it & 1) ? 2 : 0);
       double* rr_new = sc + ((it & 1) ? 0 : 2);
+      // p.Ap: fused into the operator's assembly where the path has one (Q6), else a pass
+      h->dot_x = p;
+      h->dot_part = part;
+      h->dot_fused = false;
       const int rc = h->newton_lin ? feod_jvp_lin(h, p, Ap) : feod_jvp(h, u, p, Ap);
+      const bool fused = h->dot_fused;
+      h->dot_x = nullptr;
+      h->dot_part = nullptr;
       if (rc) { h->st = keep; return rc; }
-      cudaError_t e = dot_partial(p, Ap, N, part, st);
+      cudaError_t e = fused ? cudaSuccess : dot_partial(p, Ap, N, part, st);
       if (e == cudaSuccess) e = cg_update(rr_old, part, sc + 1, p, Ap, d, r, N, part2, bad, st, pre);
       if (e == cudaSuccess) e = cg_dir(part2, rr_new, rr_old, r, p, N, st, pre);
       if (e != cudaSuccess) { h->st = keep; return cuda_fail(e, "feod_newton_cg: CG"); }

@@ -81,7 +81,7 @@ cudaError_t element_matrices_nd(int nd, int model, bool affine, bool elm, const 
 // vector (q6tc.cu, K11); out gets the assembled L-vector
 bool q6tc_supports(int mode);
 cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
-                     double* ev, double* out, cudaStream_t st);
+                     double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st);
 // element tangents by element-level forward AD through B, D and B^T (elm.cu, K10; Table 1's ELM)
 cudaError_t element_matrices_elm_nd(int nd, int model, bool affine, const OpParams& P, const Tables& T,
                                     const double* u, int e0, int ne, double* Ke, cudaStream_t st);

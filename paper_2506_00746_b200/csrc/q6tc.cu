@@ -318,6 +318,9 @@ q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, co
 #ifndef FEOD_Q6_PERL
 #define FEOD_Q6_PERL 1
 #endif
+#ifndef FEOD_Q6_FSTAGE   // shared-memory staging of the input fields (measured C4: JVP 304 -> 336 us
+#define FEOD_Q6_FSTAGE 0   // with it, residual 225 -> 255; the L2 prefetch alone is kept)
+#endif
 #ifndef FEOD_Q6P_MINB1   // residual (measured C4: 4 CTAs of 4 warps per SM, 128 registers)
 #define FEOD_Q6P_MINB1 4
 #endif
@@ -347,15 +350,17 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
   const bool colv[2] = {2 * q < 7, 2 * q + 1 < 7};
   const Frag zero = {{0.0, 0.0}};
 
-  // x and y of one field: node plane c (rows y, columns x) -> Ep[c] = [i][j]
-  auto nodes_xy = [&](const double* __restrict__ src, int ex, int ey, int ez, bool mask, Frag* Ep) {
+  // x and y of one field: node plane c (rows y, columns x) -> Ep[c] = [i][j]; the nodes come
+  // from the warp's shared-memory copy of the element (fb, staged one element ahead) or,
+  // when that space holds the stored linearisation (PAJVP), from global memory
+  auto nodes_xy = [&](const double* __restrict__ src, const double* fb, int ex, int ey, int ez, bool mask, Frag* Ep) {
     Frag X[7];
 #pragma unroll
     for (int c = 0; c < 7; ++c) {
       const int64_t row = (int64_t)(K * ex) + (int64_t)P.Mx * ((K * ey + r) + (int64_t)P.My * (K * ez + c));
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        double x = (rowv && colv[t]) ? __ldg(src + row + 2 * q + t) : 0.0;
+        double x = !(rowv && colv[t]) ? 0.0 : fb ? fb[c * 49 + r * 7 + 2 * q + t] : __ldg(src + row + 2 * q + t);
         if (mask && is_dirichlet(K * ex + 2 * q + t, K * ey + r, K * ez + c, P.Mx, P.My, P.Mz, P.faces)) x = 0.0;
         X[c].v[t] = x;
       }
@@ -387,12 +392,49 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
     __syncwarp();
     issue_lin((int64_t)blockIdx.x * WARPS + wid);
   }
+  // the next element's input fields: prefetched into L2 right after this element's x-y
+  // phase (49 node rows per field); FEOD_Q6_FSTAGE=1 stages them in shared memory by
+  // 8-byte cp.async instead (measured slower)
+  constexpr bool FSTAGE = FEOD_Q6_FSTAGE && !TMA_LIN;
+  constexpr int FB = 344;
+  double* const fbuf = q6sm + (size_t)wid * (NIN * FB);
+  auto stage_fields = [&](int64_t en) {
+    if (en >= E) return;
+    const int ex = (int)(en % P.nx), ey = (int)((en / P.nx) % P.ny), ez = (int)(en / ((int64_t)P.nx * P.ny));
+    const int64_t base = (int64_t)(K * ex) + (int64_t)P.Mx * ((K * ey) + (int64_t)P.My * (K * ez));
+    if constexpr (FSTAGE) {
+      for (int idx = lane; idx < 343; idx += 32) {
+        const int c = idx / 49, rem = idx - 49 * c, y = rem / 7, x = rem - 7 * y;
+        const int64_t g = base + x + (int64_t)P.Mx * (y + (int64_t)P.My * c);
+#pragma unroll
+        for (int f = 0; f < NIN; ++f)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(fbuf + f * FB + idx)),
+                       "l"((f == 0 ? in0 : in1) + g)
+                       : "memory");
+      }
+    } else if (lane < 49) {
+      const int c = lane / 7, y = lane - 7 * c;
+      const int64_t o = base + (int64_t)P.Mx * (y + (int64_t)P.My * c);
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(in0 + o));   // (field 1 too: measured no better)
+    }
+  };
+  if constexpr (FSTAGE) {
+    stage_fields((int64_t)blockIdx.x * WARPS + wid);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
 
   for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
     const int ex = (int)(e % P.nx), ey = (int)((e / P.nx) % P.ny), ez = (int)(e / ((int64_t)P.nx * P.ny));
     Frag Ep[NIN][7];
-    nodes_xy(in0, ex, ey, ez, false, Ep[0]);
-    if constexpr (NIN == 2) nodes_xy(in1, ex, ey, ez, MODE == MODE_VJP, Ep[NIN - 1]);
+    if constexpr (FSTAGE) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+    }
+    nodes_xy(in0, FSTAGE ? fbuf : nullptr, ex, ey, ez, false, Ep[0]);
+    if constexpr (NIN == 2) nodes_xy(in1, FSTAGE ? fbuf + FB : nullptr, ex, ey, ez, MODE == MODE_VJP, Ep[NIN - 1]);
+    if constexpr (FSTAGE) __syncwarp();   // buffer consumed
+    stage_fields(e + (int64_t)gridDim.x * WARPS);
+    if constexpr (FSTAGE) asm volatile("cp.async.commit_group;" ::: "memory");
     const double rho_e = (MODEL == HEAT && MODE != MODE_PAJVP) ? __ldg(P.rho + e) : 1.0;
     double* const linp = (MODE == MODE_LIN || MODE == MODE_PAJVP) ? P.lin + e * (NL * 343) : nullptr;
     if constexpr (MODE == MODE_PAJVP && !TMA_LIN) {
@@ -515,9 +557,16 @@ constexpr int kAsmUnroll = 8;   // X' loads per lane issued together
 // each X' of the row over the row's <= 4 source rows (lanes over X', coalesced, the
 // loads of kAsmUnroll X' in flight together), stage 2 gives each DOF X its one or two
 // X' sums (left element first) and applies P^T.
+// With dotx != nullptr (Newton-CG, feod_newton_cg) the kernel also forms the partial sums
+// of dotx . out per CTA (rows in the warp's order, warps in order) into dpart[blockIdx.x]:
+// a fixed grid of kRedBlocks CTAs, so the CG's p.Ap needs no pass of its own and stays
+// bitwise reproducible (reduce_partials in blas1.cu finishes it).
 __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
-                                                                     double* __restrict__ out) {
+                                                                     double* __restrict__ out,
+                                                                     const double* __restrict__ dotx,
+                                                                     double* __restrict__ dpart) {
   extern __shared__ __align__(16) double asm_sm[];
+  double acc = 0.0;
   const int LX = 7 * P.nx;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* const t = asm_sm + (size_t)wid * LX;
@@ -556,19 +605,34 @@ __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpPara
       if (a == 0 && e > 0 && e < P.nx) s = t[7 * e - 1] + t[7 * e];   // left element first
       else s = t[X + min(e, P.nx - 1)];   // X = 6 nx: the last element's node 6, X' = 7 nx - 1
       const bool dir = dyz || ((P.faces & 1u) && X == 0) || ((P.faces & 2u) && X == P.Mx - 1);
-      orow[X] = dir ? 0.0 : s;
+      const double o = dir ? 0.0 : s;
+      orow[X] = o;
+      if (dotx) acc = fma(__ldcs(dotx + (int64_t)P.Mx * YZ + X), o, acc);
     }
     __syncwarp();
+  }
+  if (dotx) {   // fixed-order CTA sum: lanes by a butterfly, then the warps in order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __syncthreads();   // the row buffers are free: reuse for the warp sums
+    if (lane == 0) asm_sm[wid] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < kAsmThreads / 32; ++w) sum += asm_sm[w];
+      dpart[blockIdx.x] = sum;
+    }
   }
 }
 
 template <int MODE, int MODEL>
 static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double* in0, const double* in1, double* ev,
-                               double* out, cudaStream_t st) {
+                               double* out, const double* dotx, double* dpart, cudaStream_t st) {
   constexpr int NL = lin_values(MODEL);
   constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
 #if FEOD_Q6_PERL
-  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS : 0;
+  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS
+                                  : FEOD_Q6_FSTAGE ? sizeof(double) * q6_nin<MODE>() * 344 * q6::WARPS : 0;
   const void* kfn = (const void*)q6tc_perl_kernel<MODE, MODEL>;
 #else
   constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS
@@ -594,18 +658,19 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
   OpParams Pa = P;
   if (MODE == MODE_VJP && P.vjp_keep_rows) Pa.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
   const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
-  evec_assemble_kernel<<<(unsigned)(ctas < 148 * 8 ? ctas : 148 * 8), kAsmThreads, asm_smem, st>>>(Pa, ev, out);
+  const unsigned agrid = dotx ? (unsigned)kRedBlocks : (unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks);
+  evec_assemble_kernel<<<agrid, kAsmThreads, asm_smem, st>>>(Pa, ev, out, dotx, dpart);
   return cudaGetLastError();
 }
 
 // C4's path: Q6 on affine meshes, the modes above (other modes / perturbed meshes use plane_kernel)
 template <int MODE>
 static cudaError_t q6tc_mode(int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
-                             double* ev, double* out, cudaStream_t st) {
+                             double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st) {
   switch (model) {
-    case PLAPLACE: return q6tc_launch<MODE, PLAPLACE>(P, T, in0, in1, ev, out, st);
-    case NLDIFF: return q6tc_launch<MODE, NLDIFF>(P, T, in0, in1, ev, out, st);
-    case HEAT: return q6tc_launch<MODE, HEAT>(P, T, in0, in1, ev, out, st);
+    case PLAPLACE: return q6tc_launch<MODE, PLAPLACE>(P, T, in0, in1, ev, out, dotx, dpart, st);
+    case NLDIFF: return q6tc_launch<MODE, NLDIFF>(P, T, in0, in1, ev, out, dotx, dpart, st);
+    case HEAT: return q6tc_launch<MODE, HEAT>(P, T, in0, in1, ev, out, dotx, dpart, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -617,12 +682,12 @@ bool q6tc_supports(int mode) {
 }
 
 cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
-                     double* ev, double* out, cudaStream_t st) {
+                     double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st) {
   switch (mode) {
-    case MODE_RES: return q6tc_mode<MODE_RES>(model, P, T, in0, in1, ev, out, st);
-    case MODE_JVP: return q6tc_mode<MODE_JVP>(model, P, T, in0, in1, ev, out, st);
-    case MODE_VJP: return q6tc_mode<MODE_VJP>(model, P, T, in0, in1, ev, out, st);
-    case MODE_PAJVP: return q6tc_mode<MODE_PAJVP>(model, P, T, in0, in1, ev, out, st);
+    case MODE_RES: return q6tc_mode<MODE_RES>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
+    case MODE_JVP: return q6tc_mode<MODE_JVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
+    case MODE_VJP: return q6tc_mode<MODE_VJP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
+    case MODE_PAJVP: return q6tc_mode<MODE_PAJVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
   }
   return cudaErrorInvalidValue;
 }

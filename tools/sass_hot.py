@@ -17,7 +17,7 @@ for b in txt.split('"Kernel Name"')[1:]:
     h = rows[0]
     ix = {k: h.index(k) for k in ["Source", "Warp Stall Sampling (All Samples)", "Instructions Executed",
                                  "L1 Wavefronts Shared", "L1 Wavefronts Shared Ideal", "stall_wait", "stall_barrier",
-                                 "stall_long_sb", "stall_short_sb", "stall_mio", "stall_math"]}
+                                 "stall_long_sb", "stall_short_sb", "stall_mio", "stall_math"] if k in h}
     agg = collections.defaultdict(lambda: collections.Counter())
     for r in rows[1:]:
         if len(r) < len(h):
@@ -34,7 +34,7 @@ for b in txt.split('"Kernel Name"')[1:]:
             if k == "Source":
                 continue
             try:
-                agg[base][k] += float(r[ix[k]] or 0)
+                agg[base][k] += float(r[ix[k]] or 0) if k in ix else 0.0
             except ValueError:
                 pass
     tot = sum(v["Warp Stall Sampling (All Samples)"] for v in agg.values())
