@@ -422,7 +422,9 @@ def main():
     jvp_bytes = algorithmic_bytes(w, "jvp")
     achieved = jvp_bytes / (jvp_kernel_ms * 1e-3) / 1e9
     traffic = traffic_from_profiles(w.name)
-    kname = "col_kernel<JVP> (one thread per element column, Q1/Q2)" if w.k <= 2 else "plane_kernel<JVP>"
+    kname = ("col_kernel<JVP> (one thread per element column, Q1/Q2)" if w.k <= 2 else
+             "q6tc_perl_kernel<JVP> + evec_assemble_kernel (FP64 tensor cores, Q6 affine)"
+             if w.k == 6 and not w.perturbed else "plane_kernel<JVP>")
     roofline = {"bound": "hbm" if w.perturbed else "alu", "kernel": f"{kname}: fused G-B-D-B^T-G^T, {w.name}",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src,
@@ -451,7 +453,7 @@ def main():
             "data": "synthetic (seeded workloads/ recipe, SURVEY.md §8(d))", "config": config_of(w),
             "parallelism": f"replicas x{world} (no data-path collective; DESIGN.md §Multi-GPU)",
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
-            "gpu_launches": args.steps * 4,   # per call: the fused plane_kernel + the brick-face fixup_kernel
+            "gpu_launches": args.steps * 4,   # per call: the fused operator kernel + the fix-up / assembly kernel
             "calls": {
                 "residual": {"us": t_res * 1e3, "us_median": res_med * 1e3, "us_min": res_min * 1e3,
                              "gdof_s": N / (t_res * 1e-3) / 1e9,
