@@ -485,6 +485,14 @@ extern "C" int feod_set_newton_linearization(feod_handle h, int stored) {
 extern "C" int feod_jacobi_diag(feod_handle h, double* diag) {
   if (!h || !diag) return fail(FEOD_EINVAL, "feod_jacobi_diag: null argument");
   if (!h->lin_valid) return fail(FEOD_EINVAL, "feod_jacobi_diag: no linearisation stored (call feod_linearize)");
+  if (h->nd == 7 && h->geom == nullptr && h->q6tc) {   // Q6 affine: the tensor-core diagonal (q6tc.cu)
+    if (!h->evec && cudaMalloc(&h->evec, sizeof(double) * 343 * (size_t)h->E) != cudaSuccess) {
+      h->evec = nullptr;
+      return fail(FEOD_ENOMEM, "feod_jacobi_diag: element vector");
+    }
+    CK(q6tc_diag(h->coeffs.model, h->P, h->T, h->evec, diag, h->st), "feod_jacobi_diag");
+    return FEOD_OK;
+  }
   CK(jacobi_diag_nd(h->nd, h->coeffs.model, h->P, h->T, diag, h->st), "feod_jacobi_diag");
   return FEOD_OK;
 }

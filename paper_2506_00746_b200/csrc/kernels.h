@@ -79,6 +79,8 @@ cudaError_t element_matrices_nd(int nd, int model, bool affine, bool elm, const 
                                 const double* u, int e0, int ne, double* Ke, cudaStream_t st);
 // Q6 residual / JVP on the FP64 tensor cores, one warp per element, through an element
 // vector (q6tc.cu, K11); out gets the assembled L-vector
+// Jacobi diagonal of the stored linearisation at Q6 on affine meshes (q6tc.cu, K12)
+cudaError_t q6tc_diag(int model, const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st);
 bool q6tc_supports(int mode);
 cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
                      double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st);

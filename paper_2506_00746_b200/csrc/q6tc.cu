@@ -564,7 +564,7 @@ constexpr int kAsmUnroll = 8;   // X' loads per lane issued together
 __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
                                                                      double* __restrict__ out,
                                                                      const double* __restrict__ dotx,
-                                                                     double* __restrict__ dpart) {
+                                                                     double* __restrict__ dpart, double dirval) {
   extern __shared__ __align__(16) double asm_sm[];
   double acc = 0.0;
   const int LX = 7 * P.nx;
@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpPara
       if (a == 0 && e > 0 && e < P.nx) s = t[7 * e - 1] + t[7 * e];   // left element first
       else s = t[X + min(e, P.nx - 1)];   // X = 6 nx: the last element's node 6, X' = 7 nx - 1
       const bool dir = dyz || ((P.faces & 1u) && X == 0) || ((P.faces & 2u) && X == P.Mx - 1);
-      const double o = dir ? 0.0 : s;
+      const double o = dir ? dirval : s;
       orow[X] = o;
       if (dotx) acc = fma(__ldcs(dotx + (int64_t)P.Mx * YZ + X), o, acc);
     }
@@ -659,7 +659,7 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
   if (MODE == MODE_VJP && P.vjp_keep_rows) Pa.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
   const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
   const unsigned agrid = dotx ? (unsigned)kRedBlocks : (unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks);
-  evec_assemble_kernel<<<agrid, kAsmThreads, asm_smem, st>>>(Pa, ev, out, dotx, dpart);
+  evec_assemble_kernel<<<agrid, kAsmThreads, asm_smem, st>>>(Pa, ev, out, dotx, dpart, 0.0);
   return cudaGetLastError();
 }
 
@@ -690,6 +690,151 @@ cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, co
     case MODE_PAJVP: return q6tc_mode<MODE_PAJVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
   }
   return cudaErrorInvalidValue;
+}
+
+
+// K12 -- Jacobi diagonal of the stored linearisation at Q6 on the
+// FP64 tensor cores: the diagonal of K_e = B^T J_D B at node (a, b, c) is
+//   sum_terms w_t sum_{i,j,l} TX_t[i][a] TY_t[j][b] TZ_t[l][c] A_t(i, j, l)
+// (the nine terms of diag.cu's header: A_xx G^2 B^2 B^2, ..., 2 A_xy (GB)(GB) B^2, ...,
+// b_x (GB) B^2 B^2, ...). One warp per element as in q6tc_perl_kernel: per term and point
+// plane l, the y and x contractions of A_t(l) ([i][j] fragment) with the squared / mixed
+// tables are two DMMA pairs and a transpose, the z contraction a DFMA accumulation into
+// the 7 node-plane fragments. The element diagonals go through the same discontinuous
+// L-vector and assembly as the operator (fixed order, no atomics); Dirichlet rows get 1.
+template <int NL>
+__global__ void __launch_bounds__(32 * q6::WARPS, 3)
+q6tc_diag_kernel(const OpParams P, const Tables T, double* __restrict__ ev) {
+  using namespace q6;
+  constexpr bool TMA = (NL * 343 * sizeof(double)) % 16 == 0;
+  constexpr uint32_t LIN_BYTES = NL * 343 * sizeof(double);
+  extern __shared__ __align__(16) double q6sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  const int64_t E = (int64_t)P.nx * P.ny * P.nz;
+  const bool rowv = r < 7;
+  const bool colv[2] = {2 * q < 7, 2 * q + 1 < 7};
+  const Frag zero = {{0.0, 0.0}};
+  // W operands: W[c = point 2q + s][n = node r] of the kind 0: B^2, 1: G^2, 2: G B
+  auto tk = [&](int kind, int s) {
+    const int c = 2 * q + s, n = r;
+    if (c >= 7 || n >= 7) return 0.0;
+    const double b = T.B[c][n], g = T.G[c][n];
+    return kind == 0 ? b * b : kind == 1 ? g * g : g * b;
+  };
+  const double W0[2] = {tk(0, 0), tk(0, 1)}, W1[2] = {tk(1, 0), tk(1, 1)}, W2[2] = {tk(2, 0), tk(2, 1)};
+  // per term: x table, y table, z table, weight (diag.cu's TX / TY / TZ / WT)
+  constexpr int TX[9] = {1, 0, 0, 2, 2, 0, 2, 0, 0};
+  constexpr int TY[9] = {0, 1, 0, 2, 0, 2, 0, 2, 0};
+  constexpr int TZ[9] = {0, 0, 1, 0, 2, 2, 0, 0, 2};
+  // z tables in shared memory (broadcast reads; kept out of registers): zt[kind][l][c]
+  double* const zt = q6sm + (TMA ? (size_t)WARPS * (NL * 343) + WARPS : 0);
+  for (int k = threadIdx.x; k < 3 * 49; k += blockDim.x) {
+    const int kind = k / 49, l = (k % 49) / 7, c = k % 7;
+    const double b = T.B[l][c], g = T.G[l][c];
+    zt[k] = kind == 0 ? b * b : kind == 1 ? g * g : g * b;
+  }
+  __syncthreads();
+  double* const lbuf = q6sm + (size_t)wid * (NL * 343);
+  uint64_t* const lbar = reinterpret_cast<uint64_t*>(q6sm + (size_t)WARPS * (NL * 343)) + wid;
+  uint32_t lphase = 0;
+  auto issue = [&](int64_t en) {
+    if constexpr (TMA) {
+      if (lane == 0 && en < E) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(lbar, LIN_BYTES);
+        mbar_arrive(lbar);
+        bulk_g2s(lbuf, P.lin + en * (NL * 343), LIN_BYTES, lbar);
+      }
+    }
+  };
+  if constexpr (TMA) {
+    if (lane == 0) {
+      mbar_init(lbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    issue((int64_t)blockIdx.x * WARPS + wid);
+  }
+  for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
+    const int ex = (int)(e % P.nx), ey = (int)((e / P.nx) % P.ny), ez = (int)(e / ((int64_t)P.nx * P.ny));
+    const double* linp = P.lin + e * (NL * 343);
+    if constexpr (TMA) {
+      mbar_wait(lbar, lphase);
+      lphase ^= 1u;
+    }
+    Frag Dg[7];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) Dg[c] = zero;
+#pragma unroll 1
+    for (int t = 0; t < NL; ++t) {
+      const int ky = TY[t], kx = TX[t];
+      const double wy[2] = {ky == 0 ? W0[0] : ky == 1 ? W1[0] : W2[0], ky == 0 ? W0[1] : ky == 1 ? W1[1] : W2[1]};
+      const double wx[2] = {kx == 0 ? W0[0] : kx == 1 ? W1[0] : W2[0], kx == 0 ? W0[1] : kx == 1 ? W1[1] : W2[1]};
+      const double wt = t >= 3 && t < 6 ? 2.0 : 1.0;   // off-diagonal A terms count twice
+      const double* ztt = zt + 49 * TZ[t];
+#pragma unroll
+      for (int l = 0; l < 7; ++l) {
+        Frag A;
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+          const int o = (l * NL + t) * 49 + (2 * q + s2) * 7 + r;
+          A.v[s2] = !(rowv && colv[s2]) ? 0.0 : TMA ? lbuf[o] : __ldcs(linp + o);
+        }
+        const Frag yb = contract_cols(A, wy, zero);                          // [i][b]
+        Frag ba = contract_cols(transpose(yb, lane), wx, zero);              // [b][a]
+        ba.v[0] *= wt;
+        ba.v[1] *= wt;
+#pragma unroll
+        for (int c = 0; c < 7; ++c) {
+          const double tz = ztt[l * 7 + c];
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2) Dg[c].v[s2] = fma(tz, ba.v[s2], Dg[c].v[s2]);
+        }
+      }
+    }
+    if constexpr (TMA) {
+      __syncwarp();
+      issue(e + (int64_t)gridDim.x * WARPS);
+    }
+    const int64_t LXd = 7 * (int64_t)P.nx, LYd = 7 * (int64_t)P.ny;
+    double* out = ev + ((int64_t)(7 * ez) * LYd + 7 * ey) * LXd + 7 * ex;
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      if (rowv) {
+        double* o = out + ((int64_t)c * LYd + r) * LXd;
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2)
+          if (colv[s2]) o[2 * q + s2] = Dg[c].v[s2];
+      }
+    }
+  }
+}
+
+template <int NL>
+static cudaError_t q6tc_diag_t(const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st) {
+  constexpr bool TMA = (NL * 343 * sizeof(double)) % 16 == 0;
+  constexpr size_t smem = (TMA ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS : 0) + sizeof(double) * 3 * 49;
+  const void* kfn = (const void*)q6tc_diag_kernel<NL>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int slots = 0;
+  if ((e = persistent_slots(kfn, 32 * q6::WARPS, smem, &slots)) != cudaSuccess) return e;
+  const int64_t E = (int64_t)P.nx * P.ny * P.nz;
+  const int64_t want = (E + q6::WARPS - 1) / q6::WARPS;
+  q6tc_diag_kernel<NL><<<(unsigned)(want < slots ? want : slots), 32 * q6::WARPS, smem, st>>>(P, T, ev);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int rows = P.My * P.Mz;
+  const size_t asm_smem = sizeof(double) * 7 * (size_t)P.nx * (kAsmThreads / 32);
+  if (asm_smem > 48 * 1024) return cudaErrorInvalidValue;
+  const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
+  evec_assemble_kernel<<<(unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks), kAsmThreads, asm_smem, st>>>(
+      P, ev, diag, nullptr, nullptr, 1.0);   // Dirichlet rows: 1 (the identity there)
+  return cudaGetLastError();
+}
+
+cudaError_t q6tc_diag(int model, const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st) {
+  return lin_values(model) == 9 ? q6tc_diag_t<9>(P, T, ev, diag, st) : q6tc_diag_t<6>(P, T, ev, diag, st);
 }
 
 }  // namespace feod

@@ -20,8 +20,12 @@ TOL = 1e-11
 # (recipe, reduced n): n chosen so the mesh spans several bricks with a ragged last brick;
 # the last four cases also span two brick slabs in z (BZ = 16, Q6: 8), so every fix-up set
 # (x-, y- and z-faces, edges, corners) is exercised on full vectors
+# Q6 on affine meshes with the kappa(u) models (9 stored values per point, rho for HEAT):
+# the tensor-core path's general branches (C4 itself is the p-Laplacian)
+Q6_NL = dataclasses.replace(W.C3, k=6, q=7, perturbed=False)
+Q6_HEAT = dataclasses.replace(W.C5, k=6, q=7)
 CASES = [(W.C1, 4), (W.C1, 7), (W.C2, 11), (W.C3, 6), (W.C3, 5), (W.C4, 3), (W.C5, 6), (W.C5, 9),
-         (W.C3, 18), (W.C5, 17), (W.C2, 19), (W.C4, 9)]
+         (W.C3, 18), (W.C5, 17), (W.C2, 19), (W.C4, 9), (Q6_NL, 3), (Q6_HEAT, 2)]
 
 
 def _case(w, n):
@@ -96,7 +100,7 @@ def test_linearize_and_jvp_lin_parity(w, n):
     assert rel_l2(Jv, O.jvp(pr, d["u"], d["v"])) <= TOL
 
 
-DIAG_CASES = [(W.C1, 4), (W.C2, 11), (W.C3, 5), (W.C4, 3), (W.C5, 6), (W.C5, 9)]
+DIAG_CASES = [(W.C1, 4), (W.C2, 11), (W.C3, 5), (W.C4, 3), (W.C5, 6), (W.C5, 9), (Q6_NL, 3), (Q6_HEAT, 2)]
 
 
 @pytest.mark.parametrize("w,n", DIAG_CASES, ids=[f"{w.name}n{n}" for w, n in DIAG_CASES])

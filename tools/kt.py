@@ -36,9 +36,10 @@ def main():
         "res_design": lambda: op.res_design_grad(u, lam, out=(out, g)),
         "linearize": lambda: op.linearize(u, out=out),
         "jvp_lin": lambda: op.jvp_lin(v, out=out),
+        "jacobi_diag": lambda: op.jacobi_diag(out=out),
     }
     for c in calls:
-        if c == "jvp_lin":
+        if c in ("jvp_lin", "jacobi_diag"):
             op.linearize(u, out=out2)
         f = fns[c]
         for _ in range(5):
