@@ -45,7 +45,7 @@ struct feod_op {
   bool lin_valid = false;
   int newton_lin = 0;          // Newton-CG: 0 matrix-free JVP, 1 stored linearisation, 2 + Jacobi
   double* jdiag = nullptr;     // Jacobi diagonal (Newton mode 2), N
-  double* evec = nullptr;      // Q6 tensor-core path: element vector, E x 343 (q6tc.cu)
+  double* evec = nullptr;      // discontinuous L-vector, nd^3 x E (q6tc.cu operator and diagonal, diag.cu Q3..Q5)
   bool q6tc = true;            // FEOD_Q6_TC=0 disables the Q6 tensor-core path (experiments)
   bool q6tc_res = true;        // FEOD_Q6_TC_RES=0: the residual on plane_kernel (experiments)
   // Newton-CG: when set, the next operator call also forms the partials of dot_x . out
@@ -158,6 +158,12 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
     for (int m = 0; m < qorder; ++m) h->T.Dh[i][m] = h->T.D[i][m] * wts[i] / wts[m];
   for (int i = 0; i < qorder; ++i)
     for (int a = 0; a < h->nd; ++a) h->T.Bw[i][a] = wts[i] * h->T.B[i][a];
+  for (int i = 0; i < qorder; ++i)
+    for (int a = 0; a < h->nd; ++a) {
+      h->T.B2[i][a] = h->T.B[i][a] * h->T.B[i][a];
+      h->T.G2[i][a] = h->T.G[i][a] * h->T.G[i][a];
+      h->T.GB[i][a] = h->T.G[i][a] * h->T.B[i][a];
+    }
 
   OpParams& P = h->P;
   std::memset(&P, 0, sizeof(P));
@@ -329,7 +335,7 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   if (h->nd == 7 && h->geom == nullptr && h->q6tc && q6tc_supports(mode) && (mode != MODE_RES || h->q6tc_res)) {
     // Q6 on affine meshes (residual, JVP, J^T w, linearisation, stored-linearisation JVP):
     // the FP64 tensor-core kernel + the assembly of its discontinuous L-vector (q6tc.cu)
-    if (!h->evec && cudaMalloc(&h->evec, sizeof(double) * 343 * (size_t)h->E) != cudaSuccess) {
+    if (!h->evec && cudaMalloc(&h->evec, sizeof(double) * 343 * (size_t)h->E) != cudaSuccess) {   // nd = 7
       h->evec = nullptr;
       return fail(FEOD_ENOMEM, std::string(name) + ": element vector");
     }
@@ -485,15 +491,16 @@ extern "C" int feod_set_newton_linearization(feod_handle h, int stored) {
 extern "C" int feod_jacobi_diag(feod_handle h, double* diag) {
   if (!h || !diag) return fail(FEOD_EINVAL, "feod_jacobi_diag: null argument");
   if (!h->lin_valid) return fail(FEOD_EINVAL, "feod_jacobi_diag: no linearisation stored (call feod_linearize)");
+  const size_t evn = (size_t)h->nd * h->nd * h->nd * (size_t)h->E;   // discontinuous L-vector
+  if (h->nd >= 4 && !h->evec && cudaMalloc(&h->evec, sizeof(double) * evn) != cudaSuccess) {
+    h->evec = nullptr;
+    return fail(FEOD_ENOMEM, "feod_jacobi_diag: element vector");
+  }
   if (h->nd == 7 && h->geom == nullptr && h->q6tc) {   // Q6 affine: the tensor-core diagonal (q6tc.cu)
-    if (!h->evec && cudaMalloc(&h->evec, sizeof(double) * 343 * (size_t)h->E) != cudaSuccess) {
-      h->evec = nullptr;
-      return fail(FEOD_ENOMEM, "feod_jacobi_diag: element vector");
-    }
     CK(q6tc_diag(h->coeffs.model, h->P, h->T, h->evec, diag, h->st), "feod_jacobi_diag");
     return FEOD_OK;
   }
-  CK(jacobi_diag_nd(h->nd, h->coeffs.model, h->P, h->T, diag, h->st), "feod_jacobi_diag");
+  CK(jacobi_diag_nd(h->nd, h->coeffs.model, h->P, h->T, h->evec, diag, h->st), "feod_jacobi_diag");
   return FEOD_OK;
 }
 

@@ -41,6 +41,10 @@ struct Tables {
   //   Dh[i][m] = D[i][m] w_i / w_m  (R = w_q Rt at the points),  Bw[i][a] = w_i B[i][a]
   double Dh[kMaxNQ][kMaxNQ];
   double Bw[kMaxNQ][kMaxNQ];
+  // products for the Jacobi diagonal (diag.cu): B2 = B^2, G2 = G^2, GB = G B (entrywise)
+  double B2[kMaxNQ][kMaxNQ];
+  double G2[kMaxNQ][kMaxNQ];
+  double GB[kMaxNQ][kMaxNQ];
 };
 
 // Device-resident scheduler state of one handle.

@@ -15,6 +15,7 @@
 // 1 (J's Dirichlet rows are zero; the preconditioner is the identity there).
 #include "common.cuh"
 #include "kernels.h"
+#include "evec.cuh"
 
 namespace feod {
 
@@ -254,10 +255,117 @@ static cudaError_t diag_nd_t(const OpParams& P, const Tables& T, double* diag, c
   return cudaGetLastError();
 }
 
-cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* diag, cudaStream_t st) {
+
+// Q3, Q4 (plane-kernel orders): one thread per (element, node plane c). Its element's
+// stored linearisation is read straight from HBM (the ND threads of an element are
+// adjacent lanes: one broadcast load), 16-byte loads along i where ND is even:
+//   Z[j][i] = sum_l w_t TZ_t[l][c] A_t(i, j, l)          (z first, TZ from shared memory)
+//   dg[b][a] += sum_i TX_t[i][a] sum_j TY_t[j][b] Z[j][i]   (the products in Tables)
+// The element diagonals go to the discontinuous L-vector and through evec.cuh's
+// deterministic assembly (Dirichlet rows 1) -- one launch per call pair instead of the
+// colour sweep's eight.
+template <int ND, int NL>
+__global__ void __launch_bounds__(128) diag_pt_kernel(const OpParams P, const Tables T, double* __restrict__ ev) {
+  constexpr int NQ = ND, NQ2 = NQ * NQ, NQ3 = NQ2 * NQ;
+  constexpr int TX[9] = {1, 0, 0, 2, 2, 0, 2, 0, 0};
+  constexpr int TY[9] = {0, 1, 0, 2, 0, 2, 0, 2, 0};
+  constexpr int TZ[9] = {0, 0, 1, 0, 2, 2, 0, 0, 2};
+  constexpr double WT[9] = {1, 1, 1, 2, 2, 2, 1, 1, 1};
+  __shared__ double zt[3][NQ][ND];
+  for (int k = threadIdx.x; k < 3 * NQ * ND; k += blockDim.x) {
+    const int kind = k / (NQ * ND), l = (k / ND) % NQ, c = k % ND;
+    zt[kind][l][c] = kind == 0 ? T.B2[l][c] : kind == 1 ? T.G2[l][c] : T.GB[l][c];
+  }
+  __syncthreads();
+  auto tab = [&](int kind, int i, int a) { return kind == 0 ? T.B2[i][a] : kind == 1 ? T.G2[i][a] : T.GB[i][a]; };
+  const int64_t E = (int64_t)P.nx * P.ny * P.nz;
+  const int64_t LXd = ND * (int64_t)P.nx, LYd = ND * (int64_t)P.ny;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < E * ND; it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = it / ND;
+    const int c = (int)(it - e * ND);
+    const double* lin = P.lin + e * (NL * NQ3);   // ptx = 1 at these orders
+    double dg[ND][ND];
+#pragma unroll
+    for (int b = 0; b < ND; ++b)
+#pragma unroll
+      for (int a = 0; a < ND; ++a) dg[b][a] = 0.0;
+#pragma unroll
+    for (int t = 0; t < NL; ++t) {
+      double Z[NQ][NQ];
+#pragma unroll
+      for (int j = 0; j < NQ; ++j)
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) Z[j][i] = 0.0;
+#pragma unroll
+      for (int l = 0; l < NQ; ++l) {
+        const double tz = WT[t] * zt[TZ[t]][l][c];
+        const double* row = lin + (l * NL + t) * NQ2;
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          if constexpr (NQ % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < NQ; i += 2) {
+              const double2 v = __ldg(reinterpret_cast<const double2*>(row + j * NQ + i));
+              Z[j][i] = fma(tz, v.x, Z[j][i]);
+              Z[j][i + 1] = fma(tz, v.y, Z[j][i + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < NQ; ++i) Z[j][i] = fma(tz, __ldg(row + j * NQ + i), Z[j][i]);
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < ND; ++b) {
+        double y[NQ];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < NQ; ++j) s = fma(tab(TY[t], j, b), Z[j][i], s);
+          y[i] = s;
+        }
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+          double s = dg[b][a];
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) s = fma(tab(TX[t], i, a), y[i], s);
+          dg[b][a] = s;
+        }
+      }
+    }
+    const int ex = (int)(e % P.nx), ey = (int)((e / P.nx) % P.ny), ez = (int)(e / ((int64_t)P.nx * P.ny));
+    double* out = ev + ((int64_t)(ND * ez + c) * LYd + ND * ey) * LXd + ND * ex;
+#pragma unroll
+    for (int b = 0; b < ND; ++b)
+#pragma unroll
+      for (int a = 0; a < ND; ++a) out[(int64_t)b * LXd + a] = dg[b][a];
+  }
+}
+
+template <int ND, int NL>
+static cudaError_t diag_pt_t(const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st) {
+  int slots = 0;
+  cudaError_t e = persistent_slots((const void*)diag_pt_kernel<ND, NL>, 128, 0, &slots);
+  if (e != cudaSuccess) return e;
+  const int64_t items = (int64_t)P.nx * P.ny * P.nz * ND;
+  const int64_t b = (items + 127) / 128;
+  diag_pt_kernel<ND, NL><<<(unsigned)(b < slots ? b : slots), 128, 0, st>>>(P, T, ev);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return evec_assemble<ND - 1>(P, ev, diag, nullptr, nullptr, 1.0, st);   // Dirichlet rows: 1
+}
+
+cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* ev, double* diag,
+                           cudaStream_t st) {
+  const bool nine = lin_values(model) == 9;
+  if (ev && nd >= 4 && nd <= 5 && P.ptx == 1 && (size_t)nd * P.nx * sizeof(double) * (kAsmThreads / 32) <= 48 * 1024) {
+    switch (nd) {
+      case 4: return nine ? diag_pt_t<4, 9>(P, T, ev, diag, st) : diag_pt_t<4, 6>(P, T, ev, diag, st);
+      case 5: return nine ? diag_pt_t<5, 9>(P, T, ev, diag, st) : diag_pt_t<5, 6>(P, T, ev, diag, st);
+    }   // (Q5: 36 + 36 accumulators per thread spill; the colour sweep stays)
+  }
   const cudaError_t e = cudaMemsetAsync(diag, 0, sizeof(double) * (size_t)P.Mx * P.My * P.Mz, st);
   if (e != cudaSuccess) return e;
-  const bool nine = lin_values(model) == 9;
   switch (nd) {
     case 2:
     case 3: {

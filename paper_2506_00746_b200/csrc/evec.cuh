@@ -1,0 +1,120 @@
+// G^T + P^T from a discontinuous L-vector (the per-element results of the warp-per-element
+// kernels: q6tc.cu's operator and diagonal at Q6, diag.cu's diagonal at Q3..Q5).
+//
+// Layout: element e's node (a, b, c) of an order-K element (ND = K + 1 nodes per axis) at
+// X' = ND ex + a, Y' = ND ey + b, Z' = ND ez + c of an (ND nx) x (ND ny) x (ND nz) array,
+// x fastest: neighbouring elements' node rows are adjacent, so the assembly reads it row
+// by row, coalesced. DOF X of an axis is node a = X - K e of element e (X' = X + e); an
+// element-boundary DOF (X = K e, 0 < e < n) has the two candidates X' = ND e - 1 and ND e
+// (ascending element order), any other DOF the one X' = ND min(X / K, n - 1) + a.
+//
+// A warp per DOF row (Y, Z) with a shared-memory row buffer of its own: stage 1 sums each
+// X' of the row over the row's <= 4 source rows (the row-uniform y / z candidates, z then
+// y ascending; lanes over X', coalesced, kAsmUnroll X' in flight per lane), stage 2 gives
+// each DOF X its one or two X' sums (left element first) and applies P^T (Dirichlet rows
+// get dirval). A fixed summation order everywhere: deterministic, no atomics.
+// With dotx != nullptr (Newton-CG) the kernel also forms the partial sums of dotx . out per
+// CTA (rows in the warp's order, lanes by a butterfly, warps in order) into dpart[blockIdx.x]
+// over a fixed grid of kRedBlocks CTAs: the CG's p.Ap needs no pass of its own and stays
+// bitwise reproducible (reduce_partials in blas1.cu finishes it).
+#pragma once
+#include "common.cuh"
+#include "kernels.h"
+
+namespace feod {
+
+template <int K>
+FEOD_DEV int evec_cands(int G, int ne, int* c) {
+  constexpr int ND = K + 1;
+  if (G % K == 0 && G > 0 && G < K * ne) {
+    c[0] = ND * (G / K) - 1;
+    c[1] = ND * (G / K);
+    return 2;
+  }
+  const int e = min(G / K, ne - 1);
+  c[0] = ND * e + (G - K * e);
+  return 1;
+}
+
+constexpr int kAsmThreads = 256;
+constexpr int kAsmUnroll = 8;
+
+template <int K>
+__global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
+                                                                     double* __restrict__ out,
+                                                                     const double* __restrict__ dotx,
+                                                                     double* __restrict__ dpart, double dirval) {
+  constexpr int ND = K + 1;
+  extern __shared__ __align__(16) double asm_sm[];
+  double acc = 0.0;
+  const int LX = ND * P.nx;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* const t = asm_sm + (size_t)wid * LX;
+  const int64_t LYd = ND * (int64_t)P.ny;
+  const int rows = P.My * P.Mz;
+  const int warps = gridDim.x * (kAsmThreads / 32);
+  for (int YZ = blockIdx.x * (kAsmThreads / 32) + wid; YZ < rows; YZ += warps) {
+    const int Y = YZ % P.My, Z = YZ / P.My;
+    int cy[2], cz[2];
+    const int nyc = evec_cands<K>(Y, P.ny, cy), nzc = evec_cands<K>(Z, P.nz, cz);
+    const double* src[4] = {ev, ev, ev, ev};
+    int ns = 0;
+    for (int kz = 0; kz < nzc; ++kz)
+      for (int ky = 0; ky < nyc; ++ky) src[ns++] = ev + ((int64_t)cz[kz] * LYd + cy[ky]) * LX;
+    for (int X0 = 0; X0 < LX; X0 += 32 * kAsmUnroll) {
+      double v[kAsmUnroll][4];
+#pragma unroll
+      for (int m = 0; m < kAsmUnroll; ++m) {
+        const int Xp = X0 + 32 * m + lane;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[m][k] = (k < ns && Xp < LX) ? __ldcs(src[k] + Xp) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < kAsmUnroll; ++m) {
+        const int Xp = X0 + 32 * m + lane;
+        if (Xp < LX) t[Xp] = ((v[m][0] + v[m][1]) + v[m][2]) + v[m][3];   // absent sources add +0.0 (exact)
+      }
+    }
+    __syncwarp();
+    const bool dyz = ((P.faces & 4u) && Y == 0) || ((P.faces & 8u) && Y == P.My - 1) ||
+                     ((P.faces & 16u) && Z == 0) || ((P.faces & 32u) && Z == P.Mz - 1);
+    double* orow = out + (int64_t)P.Mx * YZ;
+    for (int X = lane; X < P.Mx; X += 32) {
+      const int e = X / K, a = X - K * e;
+      double s;
+      if (a == 0 && e > 0 && e < P.nx) s = t[ND * e - 1] + t[ND * e];   // left element first
+      else s = t[X + min(e, P.nx - 1)];   // X = K nx: the last element's node K, X' = ND nx - 1
+      const bool dir = dyz || ((P.faces & 1u) && X == 0) || ((P.faces & 2u) && X == P.Mx - 1);
+      const double o = dir ? dirval : s;
+      orow[X] = o;
+      if (dotx) acc = fma(__ldcs(dotx + (int64_t)P.Mx * YZ + X), o, acc);
+    }
+    __syncwarp();
+  }
+  if (dotx) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __syncthreads();   // the row buffers are free: reuse for the warp sums
+    if (lane == 0) asm_sm[wid] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < kAsmThreads / 32; ++w) sum += asm_sm[w];
+      dpart[blockIdx.x] = sum;
+    }
+  }
+}
+
+template <int K>
+inline cudaError_t evec_assemble(const OpParams& P, const double* ev, double* out, const double* dotx, double* dpart,
+                                 double dirval, cudaStream_t st) {
+  const int rows = P.My * P.Mz;
+  const size_t smem = sizeof(double) * (K + 1) * (size_t)P.nx * (kAsmThreads / 32);
+  if (smem > 48 * 1024) return cudaErrorInvalidValue;   // (K + 1) nx <= 768
+  const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
+  const unsigned grid = dotx ? (unsigned)kRedBlocks : (unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks);
+  evec_assemble_kernel<K><<<grid, kAsmThreads, smem, st>>>(P, ev, out, dotx, dpart, dirval);
+  return cudaGetLastError();
+}
+
+}  // namespace feod

@@ -88,7 +88,9 @@ cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, co
 cudaError_t element_matrices_elm_nd(int nd, int model, bool affine, const OpParams& P, const Tables& T,
                                     const double* u, int e0, int ne, double* Ke, cudaStream_t st);
 // Jacobi diagonal of the stored linearisation (diag.cu, K8)
-cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* diag, cudaStream_t st);
+// ev: scratch for the discontinuous L-vector (nd^3 x E doubles) of the Q3..Q5 path, or null
+cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* ev, double* diag,
+                           cudaStream_t st);
 cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st);
 // BiCGStab for the adjoint solve (krylov.cu)
 cudaError_t mask_dirichlet(double* x, const OpParams& P, cudaStream_t st);

@@ -27,6 +27,7 @@
 #include "kernels.h"
 #include "physics.cuh"
 #include "pointwise.cuh"
+#include "evec.cuh"
 
 namespace feod {
 
@@ -532,99 +533,6 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
   }
 }
 
-// G^T + P^T from the discontinuous L-vector: DOF X of an axis is node a = X - 6 e of
-// element e (X' = 7e + a = X + e); an element-boundary DOF (X = 6 e, 0 < e < n) has the
-// two candidates X' = 7e - 1 and 7e (ascending element order). A CTA per DOF row (Y, Z):
-// stage 1 sums, for every X' of the row, its <= 4 source rows (the row-uniform y / z
-// candidates, z then y ascending) into shared memory with coalesced loads; stage 2 gives
-// each DOF its one or two X' sums (left element first) and applies P^T. Deterministic,
-// no atomics.
-FEOD_DEV int q6_cands(int G, int ne, int* c) {
-  if (G % 6 == 0 && G > 0 && G < 6 * ne) {
-    c[0] = 7 * (G / 6) - 1;
-    c[1] = 7 * (G / 6);
-    return 2;
-  }
-  const int e = min(G / 6, ne - 1);
-  c[0] = 7 * e + (G - 6 * e);
-  return 1;
-}
-
-constexpr int kAsmThreads = 256;
-constexpr int kAsmUnroll = 8;   // X' loads per lane issued together
-
-// A warp per DOF row (Y, Z) with a shared-memory row buffer of its own: stage 1 sums
-// each X' of the row over the row's <= 4 source rows (lanes over X', coalesced, the
-// loads of kAsmUnroll X' in flight together), stage 2 gives each DOF X its one or two
-// X' sums (left element first) and applies P^T.
-// With dotx != nullptr (Newton-CG, feod_newton_cg) the kernel also forms the partial sums
-// of dotx . out per CTA (rows in the warp's order, warps in order) into dpart[blockIdx.x]:
-// a fixed grid of kRedBlocks CTAs, so the CG's p.Ap needs no pass of its own and stays
-// bitwise reproducible (reduce_partials in blas1.cu finishes it).
-__global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
-                                                                     double* __restrict__ out,
-                                                                     const double* __restrict__ dotx,
-                                                                     double* __restrict__ dpart, double dirval) {
-  extern __shared__ __align__(16) double asm_sm[];
-  double acc = 0.0;
-  const int LX = 7 * P.nx;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* const t = asm_sm + (size_t)wid * LX;
-  const int64_t LYd = 7 * (int64_t)P.ny;
-  const int rows = P.My * P.Mz;
-  const int warps = gridDim.x * (kAsmThreads / 32);
-  for (int YZ = blockIdx.x * (kAsmThreads / 32) + wid; YZ < rows; YZ += warps) {
-    const int Y = YZ % P.My, Z = YZ / P.My;
-    int cy[2], cz[2];
-    const int nyc = q6_cands(Y, P.ny, cy), nzc = q6_cands(Z, P.nz, cz);
-    const double* src[4] = {ev, ev, ev, ev};
-    int ns = 0;
-    for (int kz = 0; kz < nzc; ++kz)
-      for (int ky = 0; ky < nyc; ++ky) src[ns++] = ev + ((int64_t)cz[kz] * LYd + cy[ky]) * LX;
-    for (int X0 = 0; X0 < LX; X0 += 32 * kAsmUnroll) {
-      double v[kAsmUnroll][4];
-#pragma unroll
-      for (int m = 0; m < kAsmUnroll; ++m) {
-        const int Xp = X0 + 32 * m + lane;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[m][k] = (k < ns && Xp < LX) ? __ldcs(src[k] + Xp) : 0.0;
-      }
-#pragma unroll
-      for (int m = 0; m < kAsmUnroll; ++m) {
-        const int Xp = X0 + 32 * m + lane;
-        if (Xp < LX) t[Xp] = ((v[m][0] + v[m][1]) + v[m][2]) + v[m][3];   // absent sources add +0.0
-      }
-    }
-    __syncwarp();
-    const bool dyz = ((P.faces & 4u) && Y == 0) || ((P.faces & 8u) && Y == P.My - 1) ||
-                     ((P.faces & 16u) && Z == 0) || ((P.faces & 32u) && Z == P.Mz - 1);
-    double* orow = out + (int64_t)P.Mx * YZ;
-    for (int X = lane; X < P.Mx; X += 32) {
-      const int e = X / 6, a = X - 6 * e;
-      double s;
-      if (a == 0 && e > 0 && e < P.nx) s = t[7 * e - 1] + t[7 * e];   // left element first
-      else s = t[X + min(e, P.nx - 1)];   // X = 6 nx: the last element's node 6, X' = 7 nx - 1
-      const bool dir = dyz || ((P.faces & 1u) && X == 0) || ((P.faces & 2u) && X == P.Mx - 1);
-      const double o = dir ? dirval : s;
-      orow[X] = o;
-      if (dotx) acc = fma(__ldcs(dotx + (int64_t)P.Mx * YZ + X), o, acc);
-    }
-    __syncwarp();
-  }
-  if (dotx) {   // fixed-order CTA sum: lanes by a butterfly, then the warps in order
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    __syncthreads();   // the row buffers are free: reuse for the warp sums
-    if (lane == 0) asm_sm[wid] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double sum = 0.0;
-      for (int w = 0; w < kAsmThreads / 32; ++w) sum += asm_sm[w];
-      dpart[blockIdx.x] = sum;
-    }
-  }
-}
-
 template <int MODE, int MODEL>
 static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double* in0, const double* in1, double* ev,
                                double* out, const double* dotx, double* dpart, cudaStream_t st) {
@@ -652,15 +560,9 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
   q6tc_kernel<MODE, MODEL><<<grid, 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev);
 #endif
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int rows = P.My * P.Mz;
-  const size_t asm_smem = sizeof(double) * 7 * (size_t)P.nx * (kAsmThreads / 32);
-  if (asm_smem > 48 * 1024) return cudaErrorInvalidValue;   // nx <= 109
   OpParams Pa = P;
   if (MODE == MODE_VJP && P.vjp_keep_rows) Pa.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
-  const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
-  const unsigned agrid = dotx ? (unsigned)kRedBlocks : (unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks);
-  evec_assemble_kernel<<<agrid, kAsmThreads, asm_smem, st>>>(Pa, ev, out, dotx, dpart, 0.0);
-  return cudaGetLastError();
+  return evec_assemble<q6::K>(Pa, ev, out, dotx, dpart, 0.0, st);
 }
 
 // C4's path: Q6 on affine meshes, the modes above (other modes / perturbed meshes use plane_kernel)
@@ -824,13 +726,7 @@ static cudaError_t q6tc_diag_t(const OpParams& P, const Tables& T, double* ev, d
   const int64_t want = (E + q6::WARPS - 1) / q6::WARPS;
   q6tc_diag_kernel<NL><<<(unsigned)(want < slots ? want : slots), 32 * q6::WARPS, smem, st>>>(P, T, ev);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int rows = P.My * P.Mz;
-  const size_t asm_smem = sizeof(double) * 7 * (size_t)P.nx * (kAsmThreads / 32);
-  if (asm_smem > 48 * 1024) return cudaErrorInvalidValue;
-  const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
-  evec_assemble_kernel<<<(unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks), kAsmThreads, asm_smem, st>>>(
-      P, ev, diag, nullptr, nullptr, 1.0);   // Dirichlet rows: 1 (the identity there)
-  return cudaGetLastError();
+  return evec_assemble<q6::K>(P, ev, diag, nullptr, nullptr, 1.0, st);   // Dirichlet rows: 1 (the identity there)
 }
 
 cudaError_t q6tc_diag(int model, const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st) {
