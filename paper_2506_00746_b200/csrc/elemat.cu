@@ -39,7 +39,10 @@ struct EmShape {
   static constexpr int NP = (NN + 7) / 8 * 8;          // padded node count (DMMA m, n)
   static constexpr int KD = (3 * Q + 3) / 4 * 4;       // padded inner dimension (DMMA k)
   static constexpr int MT = em_table<ND>() ? NP * KD : 0;   // M^T [i][k]
-  static constexpr int NM = KD * NP;                   // N [k][j]
+  // N's row stride: = 4 (mod 16) doubles, so the B fragment's 4 k-rows x 4 columns of a
+  // half-warp hit 16 different bank pairs (a stride of NP = 64 put all 4 rows on one bank)
+  static constexpr int NPS = NP + ((4 - NP % 16) + 16) % 16;
+  static constexpr int NM = KD * NPS;                  // N [k][j]
   static constexpr size_t SMEM = sizeof(double) * (MT + NM + 9 * Q + 4 * Q + NN + 2 * NQ * ND + 3 * NQ);
 };
 
@@ -48,11 +51,11 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
                                                                const double* __restrict__ u, int e0, int ne,
                                                                double* __restrict__ Ke) {
   using S = EmShape<ND>;
-  constexpr int NQ = S::NQ, Q = S::Q, NN = S::NN, NP = S::NP, KD = S::KD;
+  constexpr int NQ = S::NQ, Q = S::Q, NN = S::NN, NP = S::NP, KD = S::KD, NPS = S::NPS;
   constexpr int K = ND - 1;
   extern __shared__ double sm[];
   double* MTs = sm;                      // [NP][KD]
-  double* Ns = MTs + S::MT;              // [KD][NP]
+  double* Ns = MTs + S::MT;              // [KD][NPS]
   double* PW = Ns + S::NM;               // [9][Q]: A (xx yy zz xy xz yz), b
   double* UQ = PW + 9 * Q;               // [4][Q]: u, gh_x, gh_y, gh_z at the points
   double* UE = UQ + 4 * Q;               // [NN] element DOFs
@@ -96,18 +99,45 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
       UE[t] = u[(int64_t)(K * ex + ia) + (int64_t)P.Mx * ((K * ey + ib) + (int64_t)P.My * (K * ez + ic))];
     }
     __syncthreads();
-    // B: value and reference gradient of u at the points
-    for (int t = tid; t < 4 * Q; t += kEmThreads) {
-      const int d = t / Q, q = t % Q;
-      double s = 0.0;
-      if (d == 0) {
-        for (int i = 0; i < NN; ++i) s = fma(phi(0, q, i), UE[i], s);
-      } else {
-        for (int i = 0; i < NN; ++i) s = fma(mt(i, (d - 1) * Q + q), UE[i], s);
+    // B: value and reference gradient of u at the points, sum-factorised x, y, z in shared
+    // memory (PW is free scratch until the linearisation below): V = B_x u, Vx = G_x u;
+    // W = B_y V, Wy = G_y V, Wx = B_y Vx; U = B_z W, Uz = G_z W, Uy = B_z Wy, Ux = B_z Wx
+    {
+      constexpr int S1 = NQ * ND * ND, S2 = NQ * NQ * ND;
+      double* V = PW;             // [2][c][b][i]
+      double* Wc = PW + 2 * S1;   // [3][c][j][i]
+      for (int t = tid; t < 2 * S1; t += kEmThreads) {
+        const int ch = t / S1, r = t % S1, i = r % NQ, cb = r / NQ;
+        const double* tb = (ch == 0 ? Bt : Gt) + i * ND;
+        const double* ue = UE + cb * ND;
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < ND; ++a) s = fma(tb[a], ue[a], s);
+        V[t] = s;
       }
-      UQ[t] = s;
+      __syncthreads();
+      for (int t = tid; t < 3 * S2; t += kEmThreads) {
+        const int ch = t / S2, r = t % S2, i = r % NQ, j = (r / NQ) % NQ, c = r / (NQ * NQ);
+        const double* tb = (ch == 1 ? Gt : Bt) + j * ND;
+        const double* vs = V + (ch == 2 ? S1 : 0) + c * ND * NQ + i;
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < ND; ++b) s = fma(tb[b], vs[b * NQ], s);
+        Wc[t] = s;
+      }
+      __syncthreads();
+      for (int t = tid; t < 4 * Q; t += kEmThreads) {
+        const int d = t / Q, q = t % Q, ij = q % (NQ * NQ), l = q / (NQ * NQ);
+        // d = 0: U from W (B), 1: Ux from Wx (B), 2: Uy from Wy (B), 3: Uz from W (G)
+        const double* tb = (d == 3 ? Gt : Bt) + l * ND;
+        const double* ws = Wc + (d == 1 ? 2 * S2 : d == 2 ? S2 : 0) + ij;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < ND; ++c) s = fma(tb[c], ws[c * NQ * NQ], s);
+        UQ[t] = s;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     const double rho = (MODEL == HEAT) ? P.rho[e] : 1.0;
     auto metric = [&](int q, Metric& M, double& W) {
       const int qx = q % NQ, qy = (q / NQ) % NQ, qz = q / (NQ * NQ);
@@ -160,11 +190,11 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
           n1 = axy * g0 + ayy * g1 + ayz * g2 + PW[7 * Q + q] * p0;
           n2 = axz * g0 + ayz * g1 + azz * g2 + PW[8 * Q + q] * p0;
         }
-        Ns[(0 * Q + q) * NP + j] = n0;
-        Ns[(1 * Q + q) * NP + j] = n1;
-        Ns[(2 * Q + q) * NP + j] = n2;
+        Ns[(0 * Q + q) * NPS + j] = n0;
+        Ns[(1 * Q + q) * NPS + j] = n1;
+        Ns[(2 * Q + q) * NPS + j] = n2;
       }
-      for (int t = tid; t < (KD - 3 * Q) * NP; t += kEmThreads) Ns[3 * Q * NP + t] = 0.0;
+      for (int t = tid; t < (KD - 3 * Q) * NPS; t += kEmThreads) Ns[3 * Q * NPS + t] = 0.0;
     } else {
       // ELM: column j of N from a dual evaluation of D seeded with (phi_j, grad phi_j)
       for (int t = tid; t < Q * NP; t += kEmThreads) {
@@ -180,11 +210,11 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
           flux_hat<MODEL>(ud, gh, M, W, rho, P, Fh);
           c0 = Fh[0].d; c1 = Fh[1].d; c2 = Fh[2].d;
         }
-        Ns[(0 * Q + q) * NP + j] = c0;
-        Ns[(1 * Q + q) * NP + j] = c1;
-        Ns[(2 * Q + q) * NP + j] = c2;
+        Ns[(0 * Q + q) * NPS + j] = c0;
+        Ns[(1 * Q + q) * NPS + j] = c1;
+        Ns[(2 * Q + q) * NPS + j] = c2;
       }
-      for (int t = tid; t < (KD - 3 * Q) * NP; t += kEmThreads) Ns[3 * Q * NP + t] = 0.0;
+      for (int t = tid; t < (KD - 3 * Q) * NPS; t += kEmThreads) Ns[3 * Q * NPS + t] = 0.0;
     }
     __syncthreads();
     // K = M^T N on the tensor cores: a warp owns one 8-row strip and all TR column
@@ -197,12 +227,12 @@ __global__ void __launch_bounds__(kEmThreads, 1) elemat_kernel(const OpParams P,
 #pragma unroll
       for (int c = 0; c < TR; ++c) acc[c][0] = acc[c][1] = 0.0;
       const int ai = r8 + (lane >> 2);
-      const double* bp = Ns + (lane & 3) * NP + (lane >> 2);
+      const double* bp = Ns + (lane & 3) * NPS + (lane >> 2);
 #pragma unroll 2
       for (int k0 = 0; k0 < KD; k0 += 4) {
         const double a = mt(ai, k0 + (lane & 3));
 #pragma unroll
-        for (int c = 0; c < TR; ++c) dmma884(acc[c][0], acc[c][1], a, bp[k0 * NP + 8 * c]);
+        for (int c = 0; c < TR; ++c) dmma884(acc[c][0], acc[c][1], a, bp[k0 * NPS + 8 * c]);
       }
       const int i = r8 + (lane >> 2);
 #pragma unroll
