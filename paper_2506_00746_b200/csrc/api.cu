@@ -48,6 +48,7 @@ struct feod_op {
   double* evec = nullptr;      // discontinuous L-vector, nd^3 x E (q6tc.cu operator and diagonal, diag.cu Q3..Q5)
   bool q6tc = true;            // FEOD_Q6_TC=0 disables the Q6 tensor-core path (experiments)
   bool q6tc_res = true;        // FEOD_Q6_TC_RES=0: the residual on plane_kernel (experiments)
+  bool q6tc_lin = false;       // FEOD_Q6_TC_LIN=1: feod_linearize on it too (experiments)
   // Newton-CG: when set, the next operator call also forms the partials of dot_x . out
   // into dot_part (q6tc assembly) and sets dot_fused; cleared by the call
   const double* dot_x = nullptr;
@@ -192,6 +193,7 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   P.nbz = (mesh->nz + P.tbz - 1) / P.tbz;
   if (const char* env = std::getenv("FEOD_Q6_TC")) h->q6tc = std::atoi(env) != 0;   // experiments
   if (const char* env = std::getenv("FEOD_Q6_TC_RES")) h->q6tc_res = std::atoi(env) != 0;
+  if (const char* env = std::getenv("FEOD_Q6_TC_LIN")) h->q6tc_lin = std::atoi(env) != 0;
   P.ptx = h->bi.ptx;
   P.pnbx = (mesh->nx + P.ptx - 1) / P.ptx;
   P.shell_stride = shell_size(order * P.tbx + 1, order * P.tby + 1, order * P.tbz + 1);
@@ -332,7 +334,8 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
   int grid = 0;
   // MODE_PAJVP reads the stored linearisation only, whatever the geometry
   const bool aff = mode == MODE_PAJVP ? true : h->geom == nullptr;
-  if (h->nd == 7 && h->geom == nullptr && h->q6tc && q6tc_supports(mode) && (mode != MODE_RES || h->q6tc_res)) {
+  if (h->nd == 7 && h->geom == nullptr && h->q6tc && (q6tc_supports(mode) || (mode == MODE_LIN && h->q6tc_lin)) &&
+      (mode != MODE_RES || h->q6tc_res)) {
     // Q6 on affine meshes (residual, JVP, J^T w, linearisation, stored-linearisation JVP):
     // the FP64 tensor-core kernel + the assembly of its discontinuous L-vector (q6tc.cu)
     if (!h->evec && cudaMalloc(&h->evec, sizeof(double) * 343 * (size_t)h->E) != cudaSuccess) {   // nd = 7
@@ -642,8 +645,8 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
       h->dot_part = nullptr;
       if (rc) { h->st = keep; return rc; }
       cudaError_t e = fused ? cudaSuccess : dot_partial(p, Ap, N, part, st);
-      if (e == cudaSuccess) e = cg_update(rr_old, part, sc + 1, p, Ap, d, r, N, part2, bad, st, pre);
-      if (e == cudaSuccess) e = cg_dir(part2, rr_new, rr_old, r, p, N, st, pre);
+      if (e == cudaSuccess) e = cg_update(rr_old, part, sc + 1, Ap, r, N, part2, bad, st, pre);
+      if (e == cudaSuccess) e = cg_dir(part2, rr_new, rr_old, sc + 1, r, p, d, N, st, pre);
       if (e != cudaSuccess) { h->st = keep; return cuda_fail(e, "feod_newton_cg: CG"); }
     }
     h->st = keep;

@@ -85,13 +85,14 @@ FEOD_DEV double reduce_partials(const double* __restrict__ partials, double* sh)
 }
 
 // alpha = rr / pAp (pAp reduced here from dot_partial's partials; CTA 0 keeps it in
-// *pAp);  d += alpha p;  r -= alpha Ap;  partials of r.r (same fixed grid as dot_partial)
-// (with diag: the partials are of r . M^{-1} r, the preconditioned CG's rz)
+// *pAp);  r -= alpha Ap;  partials of r.r (same fixed grid as dot_partial)
+// (with diag: the partials are of r . M^{-1} r, the preconditioned CG's rz). The update
+// d += alpha p is deferred to cg_dir, which reads p anyway (one vector pass less, the same
+// alpha and p: bitwise the same d).
 __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __restrict__ rr,
                                                                 const double* __restrict__ pAp_partials,
                                                                 double* __restrict__ pAp,
-                                                                const double* __restrict__ p,
-                                                                const double* __restrict__ Ap, double* __restrict__ d,
+                                                                const double* __restrict__ Ap,
                                                                 double* __restrict__ r, int64_t n,
                                                                 double* __restrict__ partials, int* __restrict__ bad,
                                                                 const double* __restrict__ diag) {
@@ -105,16 +106,15 @@ __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __
   double acc[kUnroll] = {};
   int64_t i = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
   for (; i + (kUnroll - 1) * kRedStride < n; i += kUnroll * kRedStride) {
-    double pv[kUnroll], av[kUnroll], dv[kUnroll], rv[kUnroll];
+    double av[kUnroll], rv[kUnroll];
 #pragma unroll
     for (int t = 0; t < kUnroll; ++t) {
       const int64_t j = i + t * kRedStride;
-      pv[t] = __ldcs(p + j); av[t] = __ldcs(Ap + j); dv[t] = d[j]; rv[t] = r[j];
+      av[t] = __ldcs(Ap + j); rv[t] = r[j];
     }
 #pragma unroll
     for (int t = 0; t < kUnroll; ++t) {
       const int64_t j = i + t * kRedStride;
-      d[j] = fma(alpha, pv[t], dv[t]);
       const double ri = fma(-alpha, av[t], rv[t]);
       r[j] = ri;
       acc[t] = fma(ri, diag ? ri / diag[j] : ri, acc[t]);
@@ -123,7 +123,6 @@ __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __
 #pragma unroll
   for (int t = 0; t < kUnroll - 1; ++t)
     if (i < n) {
-      d[i] = fma(alpha, p[i], d[i]);
       const double ri = fma(-alpha, Ap[i], r[i]);
       r[i] = ri;
       acc[t] = fma(ri, diag ? ri / diag[i] : ri, acc[t]);
@@ -133,31 +132,43 @@ __global__ void __launch_bounds__(kRedThreads) cg_update_kernel(const double* __
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+// d += (rz_old / pAp) p  (the update deferred from cg_update: the same alpha bits), then
 // p = z + (rz_new / rz_old) p,  z = M^{-1} r (z = r without preconditioner); rz_new is
 // reduced here from cg_update's partials (CTA 0 stores it for the next iteration, the
 // other slot of the ping-pong than the rz_old read here)
 __global__ void __launch_bounds__(kRedThreads) cg_dir_kernel(const double* __restrict__ rr_partials,
                                                              double* __restrict__ rr_new,
                                                              const double* __restrict__ rr_old,
+                                                             const double* __restrict__ pAp,
                                                              const double* __restrict__ r, double* __restrict__ p,
-                                                             int64_t n, const double* __restrict__ diag) {
+                                                             double* __restrict__ d, int64_t n,
+                                                             const double* __restrict__ diag) {
   __shared__ double sh[kRedThreads];
   const double rn = reduce_partials(rr_partials, sh);
   if (blockIdx.x == 0 && threadIdx.x == 0) *rr_new = rn;
   const double beta = rn / *rr_old;
+  const double alpha = *rr_old / *pAp;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
-    double pv[kUnroll], rv[kUnroll];
+    double pv[kUnroll], rv[kUnroll], dv[kUnroll];
 #pragma unroll
     for (int t = 0; t < kUnroll; ++t) {
       pv[t] = p[i + t * stride];
+      dv[t] = d[i + t * stride];
       rv[t] = diag ? __ldcs(r + i + t * stride) / diag[i + t * stride] : __ldcs(r + i + t * stride);
     }
 #pragma unroll
-    for (int t = 0; t < kUnroll; ++t) p[i + t * stride] = fma(beta, pv[t], rv[t]);
+    for (int t = 0; t < kUnroll; ++t) {
+      d[i + t * stride] = fma(alpha, pv[t], dv[t]);
+      p[i + t * stride] = fma(beta, pv[t], rv[t]);
+    }
   }
-  for (; i < n; i += stride) p[i] = fma(beta, p[i], diag ? r[i] / diag[i] : r[i]);
+  for (; i < n; i += stride) {
+    const double pv = p[i];
+    d[i] = fma(alpha, pv, d[i]);
+    p[i] = fma(beta, pv, diag ? r[i] / diag[i] : r[i]);
+  }
 }
 
 // u += d
@@ -175,15 +186,14 @@ cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n,
   cg_init_kernel<<<grid_for(n), 256, 0, st>>>(F, r, p, d, diag, n);
   return cudaGetLastError();
 }
-cudaError_t cg_update(const double* rr, const double* pAp_partials, double* pAp, const double* p, const double* Ap,
-                      double* d, double* r, int64_t n, double* partials, int* bad, cudaStream_t st,
-                      const double* diag) {
-  cg_update_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(rr, pAp_partials, pAp, p, Ap, d, r, n, partials, bad, diag);
+cudaError_t cg_update(const double* rr, const double* pAp_partials, double* pAp, const double* Ap, double* r, int64_t n,
+                      double* partials, int* bad, cudaStream_t st, const double* diag) {
+  cg_update_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(rr, pAp_partials, pAp, Ap, r, n, partials, bad, diag);
   return cudaGetLastError();
 }
-cudaError_t cg_dir(const double* rr_partials, double* rr_new, const double* rr_old, const double* r, double* p,
-                   int64_t n, cudaStream_t st, const double* diag) {
-  cg_dir_kernel<<<grid_for(n), kRedThreads, 0, st>>>(rr_partials, rr_new, rr_old, r, p, n, diag);
+cudaError_t cg_dir(const double* rr_partials, double* rr_new, const double* rr_old, const double* pAp, const double* r,
+                   double* p, double* d, int64_t n, cudaStream_t st, const double* diag) {
+  cg_dir_kernel<<<grid_for(n), kRedThreads, 0, st>>>(rr_partials, rr_new, rr_old, pAp, r, p, d, n, diag);
   return cudaGetLastError();
 }
 cudaError_t axpy1(double* u, const double* d, int64_t n, cudaStream_t st) {

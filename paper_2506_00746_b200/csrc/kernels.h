@@ -69,11 +69,10 @@ cudaError_t reduce_final(const double* partials, double* out, cudaStream_t st);
 namespace feod {
 cudaError_t cg_init(const double* F, double* r, double* p, double* d, int64_t n, cudaStream_t st,
                     const double* diag = nullptr);
-cudaError_t cg_update(const double* rr, const double* pAp_partials, double* pAp, const double* p, const double* Ap,
-                      double* d, double* r, int64_t n, double* partials, int* bad, cudaStream_t st,
-                      const double* diag = nullptr);
-cudaError_t cg_dir(const double* rr_partials, double* rr_new, const double* rr_old, const double* r, double* p,
-                   int64_t n, cudaStream_t st, const double* diag = nullptr);
+cudaError_t cg_update(const double* rr, const double* pAp_partials, double* pAp, const double* Ap, double* r, int64_t n,
+                      double* partials, int* bad, cudaStream_t st, const double* diag = nullptr);
+cudaError_t cg_dir(const double* rr_partials, double* rr_new, const double* rr_old, const double* pAp, const double* r,
+                   double* p, double* d, int64_t n, cudaStream_t st, const double* diag = nullptr);
 // element tangent matrices on the FP64 tensor cores (elemat.cu, K9): nd = 2..4
 cudaError_t element_matrices_nd(int nd, int model, bool affine, bool elm, const OpParams& P, const Tables& T,
                                 const double* u, int e0, int ne, double* Ke, cudaStream_t st);

@@ -589,6 +589,7 @@ cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, co
     case MODE_RES: return q6tc_mode<MODE_RES>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
     case MODE_JVP: return q6tc_mode<MODE_JVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
     case MODE_VJP: return q6tc_mode<MODE_VJP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
+    case MODE_LIN: return q6tc_mode<MODE_LIN>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
     case MODE_PAJVP: return q6tc_mode<MODE_PAJVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
   }
   return cudaErrorInvalidValue;
