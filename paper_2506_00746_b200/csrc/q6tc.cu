@@ -63,8 +63,26 @@ FEOD_DEV Frag transpose(const Frag& m, int lane) {
   }
   return o;
 }
+// The same through a per-warp shared-memory scratch (two 8 x 18 buffers used in turn: one
+// __syncwarp per transpose; the pitch 18 = 2 mod 16 doubles keeps each half-warp's column
+// reads on 16 different bank pairs): one 16-byte store + two 8-byte loads instead of
+// eight 32-bit shuffles and four selects
+FEOD_DEV Frag transpose_sm(const Frag& m, int lane, double* scr, int& tb) {
+  const int r = lane >> 2, q = lane & 3;
+  double* b = scr + tb * (8 * 18);
+  tb ^= 1;
+  *reinterpret_cast<double2*>(b + r * 18 + 2 * q) = make_double2(m.v[0], m.v[1]);
+  __syncwarp();
+  Frag o;
+  o.v[0] = b[(2 * q) * 18 + r];
+  o.v[1] = b[(2 * q + 1) * 18 + r];
+  return o;
+}
 }  // namespace q6
 
+#ifndef FEOD_Q6_SMT   // shared-memory transposes in q6tc_perl_kernel (not PAJVP: its shared memory
+#define FEOD_Q6_SMT 1 // holds the stored linearisation)
+#endif
 #ifndef FEOD_Q6_MINB_JVP
 #define FEOD_Q6_MINB_JVP 3
 #endif
@@ -350,6 +368,14 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
   const bool rowv = r < 7;
   const bool colv[2] = {2 * q < 7, 2 * q + 1 < 7};
   const Frag zero = {{0.0, 0.0}};
+  constexpr bool SMT = FEOD_Q6_SMT && MODE != MODE_PAJVP;
+  constexpr size_t FSTAGE_DOUBLES = (FEOD_Q6_FSTAGE && MODE != MODE_PAJVP) ? (size_t)WARPS * NIN * 344 : 0;
+  double* const tscr = q6sm + FSTAGE_DOUBLES + (size_t)wid * (2 * 8 * 18);
+  int tbuf = 0;
+  auto tr = [&](const Frag& m) -> Frag {
+    if constexpr (SMT) return transpose_sm(m, lane, tscr, tbuf);
+    else return transpose(m, lane);
+  };
 
   // x and y of one field: node plane c (rows y, columns x) -> Ep[c] = [i][j]; the nodes come
   // from the warp's shared-memory copy of the element (fb, staged one element ahead) or,
@@ -367,7 +393,7 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
       }
     }
 #pragma unroll
-    for (int c = 0; c < 7; ++c) Ep[c] = contract_cols(transpose(contract_cols(X[c], WB, zero), lane), WB, zero);
+    for (int c = 0; c < 7; ++c) Ep[c] = contract_cols(tr(contract_cols(X[c], WB, zero)), WB, zero);
   };
 
   constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
@@ -467,7 +493,7 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
           Uzl[f].v[t] = b;
         }
         Uyl[f] = contract_cols(Ul[f], WD, zero);                                   // d/dy: [i][j']
-        Uxl[f] = transpose(contract_cols(transpose(Ul[f], lane), WD, zero), lane);   // d/dx: [i'][j]
+        Uxl[f] = tr(contract_cols(tr(Ul[f]), WD, zero));   // d/dx: [i'][j]
       }
       Frag Fx, Fy, Fz, V;
 #pragma unroll
@@ -504,7 +530,7 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
         V.v[t] = value_channel(MODE, 0) ? F0[3] : 0.0;
       }
       // B^T at plane l: R_l = V + Dx^T Fx + Dy^T Fy, then z into the node-plane accumulators
-      Frag R = transpose(contract_cols(transpose(Fx, lane), WDt, zero), lane);
+      Frag R = tr(contract_cols(tr(Fx), WDt, zero));
       R.v[0] += V.v[0];
       R.v[1] += V.v[1];
       R = contract_cols(Fy, WDt, R);
@@ -522,7 +548,7 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
 #pragma unroll
     for (int c = 0; c < 7; ++c) {
       const Frag ty = contract_cols(S[c], WBt, zero);                      // [i][b]
-      const Frag nd = contract_cols(transpose(ty, lane), WBt, zero);       // [b][a]
+      const Frag nd = contract_cols(tr(ty), WBt, zero);       // [b][a]
       if (rowv) {
         double* o = out + ((int64_t)c * LYd + r) * LXd;
 #pragma unroll
@@ -540,7 +566,8 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
   constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
 #if FEOD_Q6_PERL
   constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS
-                                  : FEOD_Q6_FSTAGE ? sizeof(double) * q6_nin<MODE>() * 344 * q6::WARPS : 0;
+                                  : sizeof(double) * q6::WARPS *
+                                        ((FEOD_Q6_FSTAGE ? q6_nin<MODE>() * 344 : 0) + (FEOD_Q6_SMT ? 2 * 8 * 18 : 0));
   const void* kfn = (const void*)q6tc_perl_kernel<MODE, MODEL>;
 #else
   constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS
