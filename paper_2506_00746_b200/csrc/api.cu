@@ -164,6 +164,7 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
       h->T.B2[i][a] = h->T.B[i][a] * h->T.B[i][a];
       h->T.G2[i][a] = h->T.G[i][a] * h->T.G[i][a];
       h->T.GB[i][a] = h->T.G[i][a] * h->T.B[i][a];
+      h->T.Gw[i][a] = wts[i] * h->T.G[i][a];
     }
 
   OpParams& P = h->P;

@@ -45,6 +45,7 @@ struct Tables {
   double B2[kMaxNQ][kMaxNQ];
   double G2[kMaxNQ][kMaxNQ];
   double GB[kMaxNQ][kMaxNQ];
+  double Gw[kMaxNQ][kMaxNQ];   // w_i G[i][a] (weight-folded z-transpose of the Q6 tensor-core kernel)
 };
 
 // Device-resident scheduler state of one handle.

@@ -363,8 +363,19 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
     if (c >= 7 || n >= 7) return 0.0;
     return kind == 0 ? T.B[n][c] : kind == 1 ? T.D[n][c] : kind == 2 ? T.B[c][n] : T.D[c][n];
   };
+  // FOLD: the quadrature weight w_i w_j w_l moves out of the points into the transposed
+  // tables (F = w_q F~ with M = diag(c), W = vol at the points; R = w_i w_j w_l R~ with
+  // Dh[i][m] = D[i][m] w_i / w_m, then w_l into the z-transpose (Bw, Gw) and w_j, w_i into
+  // the y / x transposes (Bw)). Not for PAJVP, whose stored values carry the weight.
+  constexpr bool FOLD = MODE != MODE_PAJVP && MODE != MODE_LIN;
+  auto tabf = [&](int kind, int s) {   // 2: Bw[c][n] 3: Dh[c][n]
+    const int c = 2 * q + s, n = r;
+    if (c >= 7 || n >= 7) return 0.0;
+    return kind == 2 ? T.Bw[c][n] : T.Dh[c][n];
+  };
   const double WB[2] = {tab(0, 0), tab(0, 1)}, WD[2] = {tab(1, 0), tab(1, 1)};
-  const double WBt[2] = {tab(2, 0), tab(2, 1)}, WDt[2] = {tab(3, 0), tab(3, 1)};
+  const double WBt[2] = {FOLD ? tabf(2, 0) : tab(2, 0), FOLD ? tabf(2, 1) : tab(2, 1)};
+  const double WDt[2] = {FOLD ? tabf(3, 0) : tab(3, 0), FOLD ? tabf(3, 1) : tab(3, 1)};
   const bool rowv = r < 7;
   const bool colv[2] = {2 * q < 7, 2 * q + 1 < 7};
   const Frag zero = {{0.0, 0.0}};
@@ -501,7 +512,7 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
         const int j = 2 * q + t;
         double F0[4] = {0.0, 0.0, 0.0, 0.0}, F1[4];
         if (rowv && colv[t]) {
-          const double wq = T.w[r] * T.w[j] * T.w[l];
+          const double wq = FOLD ? 1.0 : T.w[r] * T.w[j] * T.w[l];
           const Metric M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
           const double W = wq * P.vol;
           double u0[NIN], gx[NIN], gy[NIN], gz[NIN];
@@ -537,7 +548,9 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
 #pragma unroll
       for (int c = 0; c < 7; ++c)
 #pragma unroll
-        for (int t = 0; t < 2; ++t) S[c].v[t] = fma(T.B[l][c], R.v[t], fma(T.G[l][c], Fz.v[t], S[c].v[t]));
+        for (int t = 0; t < 2; ++t)
+          S[c].v[t] = FOLD ? fma(T.Bw[l][c], R.v[t], fma(T.Gw[l][c], Fz.v[t], S[c].v[t]))
+                           : fma(T.B[l][c], R.v[t], fma(T.G[l][c], Fz.v[t], S[c].v[t]));
     }
     if constexpr (TMA_LIN) {   // buffer reads done: stage the next element's values
       __syncwarp();
