@@ -80,8 +80,11 @@ FEOD_DEV Frag transpose_sm(const Frag& m, int lane, double* scr, int& tb) {
 }
 }  // namespace q6
 
-#ifndef FEOD_Q6_SMT   // shared-memory transposes in q6tc_perl_kernel (not PAJVP: its shared memory
-#define FEOD_Q6_SMT 1 // holds the stored linearisation)
+#ifndef FEOD_Q6_SMT   // shared-memory transposes in q6tc_perl_kernel
+#define FEOD_Q6_SMT 1
+#endif
+#ifndef FEOD_Q6_SMT_PA   // ... also in PAJVP (whose shared memory also holds the stored linearisation)
+#define FEOD_Q6_SMT_PA 0
 #endif
 #ifndef FEOD_Q6_MINB_JVP
 #define FEOD_Q6_MINB_JVP 3
@@ -379,9 +382,12 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
   const bool rowv = r < 7;
   const bool colv[2] = {2 * q < 7, 2 * q + 1 < 7};
   const Frag zero = {{0.0, 0.0}};
-  constexpr bool SMT = FEOD_Q6_SMT && MODE != MODE_PAJVP;
-  constexpr size_t FSTAGE_DOUBLES = (FEOD_Q6_FSTAGE && MODE != MODE_PAJVP) ? (size_t)WARPS * NIN * 344 : 0;
-  double* const tscr = q6sm + FSTAGE_DOUBLES + (size_t)wid * (2 * 8 * 18);
+  constexpr bool SMT = FEOD_Q6_SMT && (MODE != MODE_PAJVP || FEOD_Q6_SMT_PA);
+  // shared memory: [stored linearisation per warp + mbarriers (PAJVP) | staged fields] [transpose scratch]
+  constexpr size_t LEAD_DOUBLES = (MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0)
+                                      ? (size_t)WARPS * NL * 343 + WARPS
+                                  : FEOD_Q6_FSTAGE ? (size_t)WARPS * NIN * 344 : 0;
+  double* const tscr = q6sm + LEAD_DOUBLES + (size_t)wid * (2 * 8 * 18);
   int tbuf = 0;
   auto tr = [&](const Frag& m) -> Frag {
     if constexpr (SMT) return transpose_sm(m, lane, tscr, tbuf);
@@ -578,7 +584,8 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
   constexpr int NL = lin_values(MODEL);
   constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
 #if FEOD_Q6_PERL
-  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS
+  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS +
+                                        (FEOD_Q6_SMT && FEOD_Q6_SMT_PA ? sizeof(double) * q6::WARPS * 2 * 8 * 18 : 0)
                                   : sizeof(double) * q6::WARPS *
                                         ((FEOD_Q6_FSTAGE ? q6_nin<MODE>() * 344 : 0) + (FEOD_Q6_SMT ? 2 * 8 * 18 : 0));
   const void* kfn = (const void*)q6tc_perl_kernel<MODE, MODEL>;

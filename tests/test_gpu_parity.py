@@ -100,7 +100,11 @@ def test_linearize_and_jvp_lin_parity(w, n):
     assert rel_l2(Jv, O.jvp(pr, d["u"], d["v"])) <= TOL
 
 
-DIAG_CASES = [(W.C1, 4), (W.C2, 11), (W.C3, 5), (W.C4, 3), (W.C5, 6), (W.C5, 9), (Q6_NL, 3), (Q6_HEAT, 2)]
+# Q4 (thread-per-plane path, odd point count) and Q5 (the colour sweep), perturbed
+Q4_NL = dataclasses.replace(W.C3, k=4, q=5)
+Q5_PL = dataclasses.replace(W.C2, k=5, q=6)
+DIAG_CASES = [(W.C1, 4), (W.C2, 11), (W.C3, 5), (W.C4, 3), (W.C5, 6), (W.C5, 9), (Q6_NL, 3), (Q6_HEAT, 2),
+              (Q4_NL, 3), (Q5_PL, 2)]
 
 
 @pytest.mark.parametrize("w,n", DIAG_CASES, ids=[f"{w.name}n{n}" for w, n in DIAG_CASES])
