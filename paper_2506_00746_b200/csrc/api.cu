@@ -496,7 +496,7 @@ extern "C" int feod_jacobi_diag(feod_handle h, double* diag) {
   if (!h || !diag) return fail(FEOD_EINVAL, "feod_jacobi_diag: null argument");
   if (!h->lin_valid) return fail(FEOD_EINVAL, "feod_jacobi_diag: no linearisation stored (call feod_linearize)");
   const size_t evn = (size_t)h->nd * h->nd * h->nd * (size_t)h->E;   // discontinuous L-vector
-  if (h->nd >= 4 && !h->evec && cudaMalloc(&h->evec, sizeof(double) * evn) != cudaSuccess) {
+  if (!h->evec && cudaMalloc(&h->evec, sizeof(double) * evn) != cudaSuccess) {
     h->evec = nullptr;
     return fail(FEOD_ENOMEM, "feod_jacobi_diag: element vector");
   }

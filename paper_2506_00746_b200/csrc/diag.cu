@@ -129,24 +129,30 @@ __global__ void __launch_bounds__(kDiagThreads) diag_color_kernel(const OpParams
 // low order: C5 2.3 ms).
 template <int ND, int NT>
 __global__ void __launch_bounds__(128) diag_elem_kernel(const OpParams P, const Tables T, int color,
-                                                        double* __restrict__ diag) {
+                                                        double* __restrict__ diag, double* __restrict__ ev) {
   constexpr int NQ = ND, NQ2 = NQ * NQ, NQ3 = NQ2 * NQ, NL = NT;
   constexpr int TX[9] = {1, 0, 0, 2, 2, 0, 2, 0, 0};
   constexpr int TY[9] = {0, 1, 0, 2, 0, 2, 0, 2, 0};
   constexpr int TZ[9] = {0, 0, 1, 0, 2, 2, 0, 0, 2};
   constexpr double WT[9] = {1, 1, 1, 2, 2, 2, 1, 1, 1};
-  const int hx = (P.nx + 1 - (color & 1)) / 2, hy = (P.ny + 1 - ((color >> 1) & 1)) / 2;
-  const int hz = (P.nz + 1 - ((color >> 2) & 1)) / 2;
+  // ev != nullptr: every element in natural order (consecutive threads = consecutive x
+  // elements: the interleaved per-point stream is read coalesced), the element diagonal
+  // written to the discontinuous L-vector for evec.cuh's assembly; else colour `color`
+  // (stride-2 elements) with read-modify-write into diag
+  const bool all = ev != nullptr;
+  const int hx = all ? P.nx : (P.nx + 1 - (color & 1)) / 2, hy = all ? P.ny : (P.ny + 1 - ((color >> 1) & 1)) / 2;
+  const int hz = all ? P.nz : (P.nz + 1 - ((color >> 2) & 1)) / 2;
   const int64_t ne = (int64_t)hx * hy * hz;
+  const int sx = all ? 1 : 2, ox = all ? 0 : (color & 1), oy = all ? 0 : ((color >> 1) & 1), oz = all ? 0 : ((color >> 2) & 1);
   // 1D factor tables: 0 = B^2, 1 = G^2, 2 = G B
   auto tab = [&](int k, int i, int a) {
     const double b = T.B[i][a], g = T.G[i][a];
     return k == 0 ? b * b : k == 1 ? g * g : g * b;
   };
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
-    const int ex = 2 * (int)(e % hx) + (color & 1);
-    const int ey = 2 * (int)((e / hx) % hy) + ((color >> 1) & 1);
-    const int ez = 2 * (int)(e / ((int64_t)hx * hy)) + ((color >> 2) & 1);
+    const int ex = sx * (int)(e % hx) + ox;
+    const int ey = sx * (int)((e / hx) % hy) + oy;
+    const int ez = sx * (int)(e / ((int64_t)hx * hy)) + oz;
     const int64_t px = P.ptx;
     const double* lin = P.lin + pt_base(P, ex, ey, ez, NL * NQ3);
     double dg[ND * ND * ND];
@@ -192,27 +198,46 @@ __global__ void __launch_bounds__(128) diag_elem_kernel(const OpParams P, const 
           }
     }
     const int K = ND - 1;
+    if (all) {
+      const int64_t LXd = ND * (int64_t)P.nx, LYd = ND * (int64_t)P.ny;
+      double* out = ev + ((int64_t)(ND * ez) * LYd + ND * ey) * LXd + ND * ex;
 #pragma unroll
-    for (int c = 0; c < ND; ++c)
+      for (int c = 0; c < ND; ++c)
 #pragma unroll
-      for (int b = 0; b < ND; ++b)
+        for (int b = 0; b < ND; ++b)
 #pragma unroll
-        for (int a = 0; a < ND; ++a) {
-          const int64_t g = (int64_t)(K * ex + a) + (int64_t)P.Mx * ((K * ey + b) + (int64_t)P.My * (K * ez + c));
-          diag[g] += dg[a + ND * (b + ND * c)];
-        }
+          for (int a = 0; a < ND; ++a) out[((int64_t)c * LYd + b) * LXd + a] = dg[a + ND * (b + ND * c)];
+    } else {
+#pragma unroll
+      for (int c = 0; c < ND; ++c)
+#pragma unroll
+        for (int b = 0; b < ND; ++b)
+#pragma unroll
+          for (int a = 0; a < ND; ++a) {
+            const int64_t g = (int64_t)(K * ex + a) + (int64_t)P.Mx * ((K * ey + b) + (int64_t)P.My * (K * ez + c));
+            diag[g] += dg[a + ND * (b + ND * c)];
+          }
+    }
   }
 }
 
 template <int ND, int NT>
-static cudaError_t diag_elem_t(const OpParams& P, const Tables& T, double* diag, cudaStream_t st) {
+static cudaError_t diag_elem_t(const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st) {
+  if (ev) {   // one launch over all elements + the deterministic assembly (Dirichlet rows 1)
+    const int64_t ne = (int64_t)P.nx * P.ny * P.nz;
+    const int64_t b = (ne + 127) / 128;
+    diag_elem_kernel<ND, NT><<<(unsigned)(b < 148 * 32 ? b : 148 * 32), 128, 0, st>>>(P, T, 0, diag, ev);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return evec_assemble<ND - 1>(P, ev, diag, nullptr, nullptr, 1.0, st);
+  }
   for (int color = 0; color < 8; ++color) {
     const int hx = (P.nx + 1 - (color & 1)) / 2, hy = (P.ny + 1 - ((color >> 1) & 1)) / 2,
               hz = (P.nz + 1 - ((color >> 2) & 1)) / 2;
     const int64_t ne = (int64_t)hx * hy * hz;
     if (ne == 0) continue;
     const int64_t b = (ne + 127) / 128;
-    diag_elem_kernel<ND, NT><<<(unsigned)(b < 148 * 32 ? b : 148 * 32), 128, 0, st>>>(P, T, color, diag);
+    diag_elem_kernel<ND, NT><<<(unsigned)(b < 148 * 32 ? b : 148 * 32), 128, 0, st>>>(P, T, color, diag, nullptr);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -358,6 +383,11 @@ static cudaError_t diag_pt_t(const OpParams& P, const Tables& T, double* ev, dou
 cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* ev, double* diag,
                            cudaStream_t st) {
   const bool nine = lin_values(model) == 9;
+  // Q1, Q2: every element in one launch into the discontinuous L-vector + assembly (the
+  // Dirichlet rows set there); C5 2293 (8 colours, r01) -> 714 (colours, thread per element)
+  if (ev && nd <= 3 && (size_t)nd * P.nx * sizeof(double) * (kAsmThreads / 32) <= 48 * 1024)
+    return nd == 2 ? (nine ? diag_elem_t<2, 9>(P, T, ev, diag, st) : diag_elem_t<2, 6>(P, T, ev, diag, st))
+                   : (nine ? diag_elem_t<3, 9>(P, T, ev, diag, st) : diag_elem_t<3, 6>(P, T, ev, diag, st));
   if (ev && nd >= 4 && nd <= 5 && P.ptx == 1 && (size_t)nd * P.nx * sizeof(double) * (kAsmThreads / 32) <= 48 * 1024) {
     switch (nd) {
       case 4: return nine ? diag_pt_t<4, 9>(P, T, ev, diag, st) : diag_pt_t<4, 6>(P, T, ev, diag, st);
@@ -369,8 +399,8 @@ cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T
   switch (nd) {
     case 2:
     case 3: {
-      cudaError_t e2 = nd == 2 ? (nine ? diag_elem_t<2, 9>(P, T, diag, st) : diag_elem_t<2, 6>(P, T, diag, st))
-                               : (nine ? diag_elem_t<3, 9>(P, T, diag, st) : diag_elem_t<3, 6>(P, T, diag, st));
+      cudaError_t e2 = nd == 2 ? (nine ? diag_elem_t<2, 9>(P, T, nullptr, diag, st) : diag_elem_t<2, 6>(P, T, nullptr, diag, st))
+                               : (nine ? diag_elem_t<3, 9>(P, T, nullptr, diag, st) : diag_elem_t<3, 6>(P, T, nullptr, diag, st));
       if (e2 != cudaSuccess) return e2;
       const int64_t n = (int64_t)P.Mx * P.My * P.Mz;
       const int64_t b = (n + 255) / 256;
