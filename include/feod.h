@@ -105,7 +105,8 @@ typedef struct feod_op* feod_handle;
  * copies the vertices and computes the per-point metric
  * M_q = w_q detJ_q J_q^{-1} J_q^{-T} (6 doubles per point)
  * on `cuda_stream` (a cudaStream_t, NULL = legacy default stream). Rejects
- * meshes with detJ <= 0 at any point (FEOD_EINVAL). Synchronises the stream. */
+ * meshes with detJ <= 0 at any point and meshes of 2^31 or more elements
+ * (FEOD_EINVAL). Synchronises the stream. */
 FEOD_API int feod_create(const feod_mesh* mesh, int order, int qorder, const feod_coeffs* coeffs,
                 void* cuda_stream, feod_handle* out);
 FEOD_API int feod_destroy(feod_handle h);

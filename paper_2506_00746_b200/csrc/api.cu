@@ -131,6 +131,8 @@ extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const f
   const int64_t Mx = (int64_t)order * mesh->nx + 1, My = (int64_t)order * mesh->ny + 1,
                 Mz = (int64_t)order * mesh->nz + 1;
   if (Mx > (1 << 30) || My > (1 << 30) || Mz > (1 << 30)) return fail(FEOD_EINVAL, "feod_create: mesh too large");
+  if ((int64_t)mesh->nx * mesh->ny * mesh->nz >= (int64_t(1) << 31))
+    return fail(FEOD_EINVAL, "feod_create: more than 2^31 - 1 elements");
 
   feod_op* h = new (std::nothrow) feod_op();
   if (!h) return fail(FEOD_ENOMEM, "feod_create: host allocation");

@@ -79,10 +79,18 @@ FEOD_HD double pow_case(double a, double e, int pc) {
   return ::pow(a, e);
 }
 // sqrt of a dual through one reciprocal square root (device): s = a r, s' = a' r / 2 with
-// r = 1/sqrt(a) -- no division on the derivative; a == 0 gives (0, 0) (reading A20)
+// r = 1/sqrt(a) -- no division, no libdevice special-case paths; a == 0 gives (0, 0)
+// (reading A20)
 template <class T> FEOD_HD dual<T> sqrt_rs(dual<T> a) {
 #ifdef __CUDA_ARCH__
-  const T r = ::rsqrt(a.v);
+  // r from the hardware approximation (MUFU.RSQ64H, ~20 correct bits) and two Newton steps
+  // r <- r (3/2 - a r^2 / 2) (~40, then full double precision); a <= 0 (only a == 0 occurs,
+  // reading A20) takes the branch-free zero below
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"((double)a.v));
+  const double h = -0.5 * a.v;
+  r = r * fma(h * r, r, 1.5);
+  r = r * fma(h * r, r, 1.5);
   const bool pos = a.v > T(0);
   return {pos ? a.v * r : T(0), pos ? (T(0.5) * a.d) * r : T(0)};
 #else

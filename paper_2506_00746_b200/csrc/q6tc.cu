@@ -78,6 +78,14 @@ FEOD_DEV Frag transpose_sm(const Frag& m, int lane, double* scr, int& tb) {
   o.v[1] = b[(2 * q + 1) * 18 + r];
   return o;
 }
+// element coordinates by 32-bit unsigned division (E < 2^31, checked at feod_create; the
+// 64-bit divisions were ~10 % of the kernel's instructions)
+FEOD_DEV void q6_coords(const OpParams& P, int64_t e, int& ex, int& ey, int& ez) {
+  const unsigned u = (unsigned)e, t = u / (unsigned)P.nx;
+  ex = (int)(u - t * (unsigned)P.nx);
+  ey = (int)(t % (unsigned)P.ny);
+  ez = (int)(t / (unsigned)P.ny);
+}
 }  // namespace q6
 
 #ifndef FEOD_Q6_SMT   // shared-memory transposes in q6tc_perl_kernel
@@ -196,7 +204,8 @@ q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, co
   }
 
   for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
-    const int ex = (int)(e % P.nx), ey = (int)((e / P.nx) % P.ny), ez = (int)(e / ((int64_t)P.nx * P.ny));
+    int ex, ey, ez;
+    q6_coords(P, e, ex, ey, ez);
     Frag U[7], Ux[7], Uy[7], Uz[7];   // the last field's channels (the fluxes overwrite Ux, Uy, Uz)
     if constexpr (NIN == 2) {
       forward(in0, ex, ey, ez, false, U, Ux, Uy, Uz);
@@ -444,7 +453,8 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
   double* const fbuf = q6sm + (size_t)wid * (NIN * FB);
   auto stage_fields = [&](int64_t en) {
     if (en >= E) return;
-    const int ex = (int)(en % P.nx), ey = (int)((en / P.nx) % P.ny), ez = (int)(en / ((int64_t)P.nx * P.ny));
+    int ex, ey, ez;
+    q6_coords(P, en, ex, ey, ez);
     const int64_t base = (int64_t)(K * ex) + (int64_t)P.Mx * ((K * ey) + (int64_t)P.My * (K * ez));
     if constexpr (FSTAGE) {
       for (int idx = lane; idx < 343; idx += 32) {
@@ -468,7 +478,8 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
   }
 
   for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
-    const int ex = (int)(e % P.nx), ey = (int)((e / P.nx) % P.ny), ez = (int)(e / ((int64_t)P.nx * P.ny));
+    int ex, ey, ez;
+    q6_coords(P, e, ex, ey, ez);
     Frag Ep[NIN][7];
     if constexpr (FSTAGE) {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -707,7 +718,8 @@ q6tc_diag_kernel(const OpParams P, const Tables T, double* __restrict__ ev) {
     issue((int64_t)blockIdx.x * WARPS + wid);
   }
   for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
-    const int ex = (int)(e % P.nx), ey = (int)((e / P.nx) % P.ny), ez = (int)(e / ((int64_t)P.nx * P.ny));
+    int ex, ey, ez;
+    q6_coords(P, e, ex, ey, ez);
     const double* linp = P.lin + e * (NL * 343);
     if constexpr (TMA) {
       mbar_wait(lbar, lphase);

@@ -121,6 +121,28 @@ def test_determinism_c2_repeated_jvp():
     assert torch.equal(op2.jvp(u, v), ref)
 
 
+def test_determinism_c4_tensor_core_path():
+    """The Q6 tensor-core path (warp-per-element kernel + discontinuous L-vector assembly,
+    fixed summation order) is bitwise reproducible: repeated residual, JVP, J^T w,
+    stored-linearisation JVP and Jacobi diagonal at full C4 size, and across handles."""
+    import torch
+    w = W.C4
+    d = W.draw(w)
+    op = operator(w, d)
+    u, v = cuda(d["u"]), cuda(d["v"])
+    op.linearize(u)
+    calls = [lambda o: op.residual(u, out=o), lambda o: op.jvp(u, v, out=o), lambda o: op.vjp(u, v, out=o),
+             lambda o: op.jvp_lin(v, out=o), lambda o: op.jacobi_diag(out=o)]
+    for f in calls:
+        ref = f(torch.empty_like(u)).clone()
+        out = torch.empty_like(u)
+        for _ in range(10):
+            f(out)
+            assert torch.equal(out, ref)
+    op2 = operator(w, d)
+    assert torch.equal(op2.jvp(u, v), op.jvp(u, v))
+
+
 def test_vjp_sampled(full):
     """J^T w (NEXT-1) at full size on sampled rows (oracle from the touching elements)."""
     w, d, pr, op = full
