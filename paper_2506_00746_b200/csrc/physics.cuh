@@ -17,6 +17,21 @@ namespace feod {
 
 struct Metric { double xx, yy, zz, xy, xz, yz; };
 
+// 1 / x for x > 0 (W = w detJ; feod_create rejects detJ <= 0). Device: the hardware
+// approximation (MUFU.RCP64H) and two Newton steps r <- r (2 - x r) -- no IEEE division
+// with its special-case paths; the host (tests) divides.
+FEOD_HD double recip(double x) {
+#ifdef __CUDA_ARCH__
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+#else
+  return 1.0 / x;
+#endif
+}
+
 // DIAG: the metric is diagonal (uniform affine grid: M = w_q diag(cx, cy, cz)), so the
 // off-diagonal products are skipped (they are exact zeros; IEEE arithmetic would not
 // let the compiler drop x * 0.0 on its own).
@@ -42,7 +57,7 @@ FEOD_DEV void flux_hat(const T& u, const T gh[3], const Metric& M, double W, con
     T s = gh[0] * (gh[0] * P.cxv) + gh[1] * (gh[1] * P.cyv) + gh[2] * (gh[2] * P.czv) + P.eps2;
     kappa = pow_case(s, P.half_pm2, P.pcase);
   } else if constexpr (MODEL == PLAPLACE) {
-    T s = (gh[0] * a[0] + gh[1] * a[1] + gh[2] * a[2]) * (1.0 / W) + P.eps2;
+    T s = (gh[0] * a[0] + gh[1] * a[1] + gh[2] * a[2]) * recip(W) + P.eps2;
     kappa = pow_case(s, P.half_pm2, P.pcase);
   } else if constexpr (MODEL == NLDIFF) {
     kappa = u * u + 1.0;
