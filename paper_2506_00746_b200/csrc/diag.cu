@@ -17,6 +17,10 @@
 #include "kernels.h"
 #include "evec.cuh"
 
+#ifndef FEOD_DIAG_Q3_WARP
+#define FEOD_DIAG_Q3_WARP 1   // Q3: the half-warp-per-element diagonal (0: thread per node plane)
+#endif
+
 namespace feod {
 
 constexpr int kDiagThreads = 128;
@@ -380,6 +384,100 @@ static cudaError_t diag_pt_t(const OpParams& P, const Tables& T, double* ev, dou
   return evec_assemble<ND - 1>(P, ev, diag, nullptr, nullptr, 1.0, st);   // Dirichlet rows: 1
 }
 
+
+// Q3 (the C3 order): a half-warp per element, lane = point column (j, i). The element's
+// stored linearisation plane (l, term) is one coalesced 128-byte row per half-warp; each
+// lane contracts its column along z in registers, the terms sharing (x, y) tables are
+// summed (6 groups), then the y and the x contractions are two rotated 4-lane
+// reduce-scatters (3 64-bit shuffles each, the tables rotated per lane as in the plane
+// kernel's B^T): lane (j, i) ends with diag(a = i, b = j, c) for c = 0..3.
+template <int NL>
+__global__ void __launch_bounds__(128, 4) diag_q3_kernel(const OpParams P, const Tables T, double* __restrict__ ev) {
+  constexpr int TZ[9] = {0, 0, 1, 0, 2, 2, 0, 0, 2};
+  constexpr double WT[9] = {1, 1, 1, 2, 2, 2, 1, 1, 1};
+  constexpr int GT[9] = {0, 1, 2, 3, 4, 5, 4, 5, 2};   // term -> group of equal (x, y) tables
+  constexpr int GX[6] = {1, 0, 0, 2, 2, 0};            // group x table kind (0 B^2, 1 G^2, 2 GB)
+  constexpr int GY[6] = {0, 1, 0, 2, 0, 2};            // group y table kind
+  const int lane = threadIdx.x & 31, half = lane >> 4, pl = lane & 15, j = pl >> 2, i = pl & 3;
+  auto tab = [&](int kind, int p, int n) { return kind == 0 ? T.B2[p][n] : kind == 1 ? T.G2[p][n] : T.GB[p][n]; };
+  double ty[3][4], tx[3][4];   // per lane, rotated: ty[kind][k] = TY_kind[j][(j - k) & 3]
+#pragma unroll
+  for (int kd = 0; kd < 3; ++kd)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ty[kd][k] = tab(kd, j, (j - k) & 3);
+      tx[kd][k] = tab(kd, i, (i - k) & 3);
+    }
+  const int hb = half * 16;
+  const int64_t E = (int64_t)P.nx * P.ny * P.nz;
+  const int64_t LXd = 4 * (int64_t)P.nx, LYd = 4 * (int64_t)P.ny;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); 2 * w < E; w += nw) {
+    const int64_t e = 2 * w + half;
+    const bool ev_ok = e < E;
+    const double* lin = P.lin + (ev_ok ? e : 0) * (NL * 64) + pl;
+    double Z[6][4];
+#pragma unroll
+    for (int g = 0; g < 6; ++g)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) Z[g][c] = 0.0;
+#pragma unroll
+    for (int t = 0; t < NL; ++t) {
+      double A[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) A[l] = __ldcs(lin + (l * NL + t) * 16);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double s = Z[GT[t]][c];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) s = fma(WT[t] * tab(TZ[t], l, c), A[l], s);
+        Z[GT[t]][c] = s;
+      }
+    }
+    double dg[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int g = 0; g < 6; ++g)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        // y: lane (j, i) gets Y(i, b = j) = sum_j' TY[j'][j] Z(i, j'): lane (j', i) sends TY[j'][(j' - k)] Z
+        // to lane ((j' - k) & 3, i), i.e. lane (j, i) receives from j' = (j + k) & 3
+        double y = ty[GY[g]][0] * Z[g][c];
+#pragma unroll
+        for (int k = 1; k < 4; ++k)
+          y += __shfl_sync(0xffffffffu, ty[GY[g]][k] * Z[g][c], hb + ((j + k) & 3) * 4 + i);
+        // x: lane (j, i) gets D(a = i, b = j) = sum_i' TX[i'][i] Y(i', j)
+        double x = tx[GX[g]][0] * y;
+#pragma unroll
+        for (int k = 1; k < 4; ++k) x += __shfl_sync(0xffffffffu, tx[GX[g]][k] * y, hb + j * 4 + ((i + k) & 3));
+        dg[c] += x;
+      }
+    if (ev_ok) {
+      int ex, ey, ez;
+      {
+        const unsigned u = (unsigned)e, q = u / (unsigned)P.nx;
+        ex = (int)(u - q * (unsigned)P.nx);
+        ey = (int)(q % (unsigned)P.ny);
+        ez = (int)(q / (unsigned)P.ny);
+      }
+      double* out = ev + ((int64_t)(4 * ez) * LYd + 4 * ey + j) * LXd + 4 * ex + i;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) out[(int64_t)c * LYd * LXd] = dg[c];
+    }
+  }
+}
+
+template <int NL>
+static cudaError_t diag_q3_t(const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st) {
+  int slots = 0;
+  cudaError_t e = persistent_slots((const void*)diag_q3_kernel<NL>, 128, 0, &slots);
+  if (e != cudaSuccess) return e;
+  const int64_t warps = ((int64_t)P.nx * P.ny * P.nz + 1) / 2;
+  const int64_t b = (warps + 3) / 4;
+  diag_q3_kernel<NL><<<(unsigned)(b < slots ? b : slots), 128, 0, st>>>(P, T, ev);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return evec_assemble<3>(P, ev, diag, nullptr, nullptr, 1.0, st);   // Dirichlet rows: 1
+}
+
 cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* ev, double* diag,
                            cudaStream_t st) {
   const bool nine = lin_values(model) == 9;
@@ -390,7 +488,9 @@ cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T
                    : (nine ? diag_elem_t<3, 9>(P, T, ev, diag, st) : diag_elem_t<3, 6>(P, T, ev, diag, st));
   if (ev && nd >= 4 && nd <= 5 && P.ptx == 1 && (size_t)nd * P.nx * sizeof(double) * (kAsmThreads / 32) <= 48 * 1024) {
     switch (nd) {
-      case 4: return nine ? diag_pt_t<4, 9>(P, T, ev, diag, st) : diag_pt_t<4, 6>(P, T, ev, diag, st);
+      case 4:
+        if (FEOD_DIAG_Q3_WARP) return nine ? diag_q3_t<9>(P, T, ev, diag, st) : diag_q3_t<6>(P, T, ev, diag, st);
+        return nine ? diag_pt_t<4, 9>(P, T, ev, diag, st) : diag_pt_t<4, 6>(P, T, ev, diag, st);
       case 5: return nine ? diag_pt_t<5, 9>(P, T, ev, diag, st) : diag_pt_t<5, 6>(P, T, ev, diag, st);
     }   // (Q5: 36 + 36 accumulators per thread spill; the colour sweep stays)
   }
