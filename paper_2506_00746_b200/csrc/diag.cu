@@ -394,21 +394,25 @@ static cudaError_t diag_pt_t(const OpParams& P, const Tables& T, double* ev, dou
 template <int NL>
 __global__ void __launch_bounds__(128, 4) diag_q3_kernel(const OpParams P, const Tables T, double* __restrict__ ev) {
   constexpr int TZ[9] = {0, 0, 1, 0, 2, 2, 0, 0, 2};
-  constexpr double WT[9] = {1, 1, 1, 2, 2, 2, 1, 1, 1};
   constexpr int GT[9] = {0, 1, 2, 3, 4, 5, 4, 5, 2};   // term -> group of equal (x, y) tables
   constexpr int GX[6] = {1, 0, 0, 2, 2, 0};            // group x table kind (0 B^2, 1 G^2, 2 GB)
   constexpr int GY[6] = {0, 1, 0, 2, 0, 2};            // group y table kind
   const int lane = threadIdx.x & 31, half = lane >> 4, pl = lane & 15, j = pl >> 2, i = pl & 3;
   auto tab = [&](int kind, int p, int n) { return kind == 0 ? T.B2[p][n] : kind == 1 ? T.G2[p][n] : T.GB[p][n]; };
-  double ty[3][4], tx[3][4];   // per lane, rotated: ty[kind][k] = TY_kind[j][(j - k) & 3]
+  // receive-side tables: lane (j, i) takes Z(i, j') from lane j' = (j + k) & 3 and weights it
+  // with TY[j'][j] (ty[kind][k]); likewise TX[i'][i] for i' = (i + k) & 3
+  double ty[3][4], tx[3][4];
+  int sy[4], sx[4];
 #pragma unroll
-  for (int kd = 0; kd < 3; ++kd)
+  for (int k = 0; k < 4; ++k) {
+    sy[k] = half * 16 + ((j + k) & 3) * 4 + i;
+    sx[k] = half * 16 + j * 4 + ((i + k) & 3);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      ty[kd][k] = tab(kd, j, (j - k) & 3);
-      tx[kd][k] = tab(kd, i, (i - k) & 3);
+    for (int kd = 0; kd < 3; ++kd) {
+      ty[kd][k] = tab(kd, (j + k) & 3, j);
+      tx[kd][k] = tab(kd, (i + k) & 3, i);
     }
-  const int hb = half * 16;
+  }
   const int64_t E = (int64_t)P.nx * P.ny * P.nz;
   const int64_t LXd = 4 * (int64_t)P.nx, LYd = 4 * (int64_t)P.ny;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -426,11 +430,15 @@ __global__ void __launch_bounds__(128, 4) diag_q3_kernel(const OpParams P, const
       double A[4];
 #pragma unroll
       for (int l = 0; l < 4; ++l) A[l] = __ldcs(lin + (l * NL + t) * 16);
+      if (t >= 3 && t < 6) {   // the off-diagonal A terms count twice
+#pragma unroll
+        for (int l = 0; l < 4; ++l) A[l] += A[l];
+      }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         double s = Z[GT[t]][c];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) s = fma(WT[t] * tab(TZ[t], l, c), A[l], s);
+        for (int l = 0; l < 4; ++l) s = fma(tab(TZ[t], l, c), A[l], s);
         Z[GT[t]][c] = s;
       }
     }
@@ -439,16 +447,13 @@ __global__ void __launch_bounds__(128, 4) diag_q3_kernel(const OpParams P, const
     for (int g = 0; g < 6; ++g)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        // y: lane (j, i) gets Y(i, b = j) = sum_j' TY[j'][j] Z(i, j'): lane (j', i) sends TY[j'][(j' - k)] Z
-        // to lane ((j' - k) & 3, i), i.e. lane (j, i) receives from j' = (j + k) & 3
+        // y: Y(i, b = j) = sum_j' TY[j'][j] Z(i, j'); x: D(a = i, b = j) = sum_i' TX[i'][i] Y(i', j)
         double y = ty[GY[g]][0] * Z[g][c];
 #pragma unroll
-        for (int k = 1; k < 4; ++k)
-          y += __shfl_sync(0xffffffffu, ty[GY[g]][k] * Z[g][c], hb + ((j + k) & 3) * 4 + i);
-        // x: lane (j, i) gets D(a = i, b = j) = sum_i' TX[i'][i] Y(i', j)
+        for (int k = 1; k < 4; ++k) y = fma(ty[GY[g]][k], __shfl_sync(0xffffffffu, Z[g][c], sy[k]), y);
         double x = tx[GX[g]][0] * y;
 #pragma unroll
-        for (int k = 1; k < 4; ++k) x += __shfl_sync(0xffffffffu, tx[GX[g]][k] * y, hb + j * 4 + ((i + k) & 3));
+        for (int k = 1; k < 4; ++k) x = fma(tx[GX[g]][k], __shfl_sync(0xffffffffu, y, sx[k]), x);
         dg[c] += x;
       }
     if (ev_ok) {
