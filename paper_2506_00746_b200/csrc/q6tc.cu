@@ -1,25 +1,20 @@
-// K11 — Q6 operator kernel on the FP64 tensor cores (C4):
-// F(u) and J(u)v (Eq. 1 / Eq. 2) for k = 6, q = 7 on affine meshes.
+// K11 / K12 -- Q6 on affine meshes on the FP64 tensor cores (C4):
+// F(u), J(u)v, J(u)^T w and the stored-linearisation J v (Eq. 1 / Eq. 2, PAPER.md:155,
+// :160) for k = 6, q = 7, and the Jacobi diagonal of the stored linearisation.
 //
-// One WARP per element, no shared memory, no block barriers. Each z-plane c (or point
-// plane l) of a 7x7x7 element array is one 8x8 DMMA fragment (padding row/column 7 = 0):
-// lane L holds entries (r = L/4, c = 2 (L%4) + t), t = 0, 1 ("D layout" of
-// mma.sync.m8n8k4.f64). Then
+// One WARP per element, no block barriers. Each z-plane c (or point plane l) of a 7x7x7
+// element array is one 8x8 DMMA fragment (padding row/column 7 = 0): lane L holds entries
+// (r = L/4, c = 2 (L%4) + t), t = 0, 1 ("D layout" of mma.sync.m8n8k4.f64). Then
 //   - a contraction over the fragment's COLUMN index is two DMMAs with no data movement:
 //     with the k-order permuted to (k-step s, k-lane q) <-> column 2q + s, the A operand of
 //     k-step s is the lane's own register t = s (the 1D table is arranged to match);
 //   - a contraction over the ROW index first transposes the fragment inside the warp
-//     (8 64-bit shuffles per fragment);
+//     (through a per-warp shared-memory scratch, FEOD_Q6_SMT; or 64-bit shuffles);
 //   - the z-contraction (across the 7 fragments) is plain register DFMA.
-// B: x (columns, DMMA), y (transpose + DMMA), z (DFMA) to the points; gradients by
-// collocation (D on the Gauss points): Uy (columns), Ux (transpose, DMMA, transpose back),
-// Uz (DFMA). D: point_op (pointwise.cuh) on the 14 slots a lane holds per plane.
-// B^T: Dz^T (DFMA), Dy^T (DMMA accumulating), Dx^T (transpose, DMMA, transpose back,
-// add), then B^T z (DFMA), y (DMMA), x (transpose + DMMA) to the nodes.
-// DMMA runs at 37.2 TF/s (profiles/r02_peaks_fp64.json); the 7 -> 8 padding leaves 77 %
-// of its FMAs useful. The element's node results go to an element vector (E x 343); the
-// assembly kernel sums each DOF's <= 8 contributions in a fixed order and applies P^T
-// -- deterministic, no atomics.
+// DMMA runs at 37.2 TF/s (profiles/r02_peaks_fp64.json) on the same FP64 pipe as DFMA;
+// the 7 -> 8 padding leaves 67 % of its FMAs useful. The element's node results go to the
+// discontinuous L-vector and evec.cuh's assembly sums each DOF's <= 8 contributions in a
+// fixed order and applies P^T -- deterministic, no atomics. DESIGN.md §6.0b.
 #include <algorithm>
 
 #include "common.cuh"
@@ -94,261 +89,18 @@ FEOD_DEV void q6_coords(const OpParams& P, int64_t e, int& ex, int& ey, int& ez)
 #ifndef FEOD_Q6_SMT_PA   // ... also in PAJVP (whose shared memory also holds the stored linearisation)
 #define FEOD_Q6_SMT_PA 0
 #endif
-#ifndef FEOD_Q6_MINB_JVP
-#define FEOD_Q6_MINB_JVP 3
-#endif
-#ifndef FEOD_Q6_MINB_RES
-#define FEOD_Q6_MINB_RES 3
-#endif
 // modes: RES (F(u)), JVP (J(u) v), VJP (J(u)^T w, w's Dirichlet entries masked, reading
 // A17), LIN (F(u) and the point linearisation written to P.lin), PAJVP (J(u0) v from P.lin)
 template <int MODE> constexpr int q6_nin() { return (MODE == MODE_JVP || MODE == MODE_VJP) ? 2 : 1; }
 
-template <int MODE, int MODEL>
-__global__ void __launch_bounds__(32 * q6::WARPS, q6_nin<MODE>() == 1 ? FEOD_Q6_MINB_RES : FEOD_Q6_MINB_JVP)
-q6tc_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, const double* __restrict__ in1,
-            double* __restrict__ ev) {
-  using namespace q6;
-  constexpr int NIN = q6_nin<MODE>();
-  constexpr int NL = lin_values(MODEL);   // stored linearisation values per point (LIN, PAJVP)
-  // two-field modes: the first field's four point channels are parked in shared memory
-  // (lane-interleaved, conflict-free), so only one field's 56 doubles are live in registers
-  extern __shared__ __align__(16) double q6sm[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* park = q6sm + (size_t)wid * (4 * 7 * 2 * 32);   // [channel][plane][t][lane]
-  auto pk = [&](int ch, int l, int t) -> double& { return park[((ch * 7 + l) * 2 + t) * 32 + lane]; };
-  const int r = lane >> 2, q = lane & 3;                  // fragment row, column pair (2q, 2q+1)
-  const int64_t E = (int64_t)P.nx * P.ny * P.nz;
-  // table operands (k-order permuted: k-step s <-> column 2q + s), zero outside 7x7
-  auto tab = [&](int kind, int s) {   // 0: B[n][c] 1: D[n][c] 2: B[c][n] 3: D[c][n]
-    const int c = 2 * q + s, n = r;
-    if (c >= 7 || n >= 7) return 0.0;
-    return kind == 0 ? T.B[n][c] : kind == 1 ? T.D[n][c] : kind == 2 ? T.B[c][n] : T.D[c][n];
-  };
-  const double WB[2] = {tab(0, 0), tab(0, 1)}, WD[2] = {tab(1, 0), tab(1, 1)};
-  const double WBt[2] = {tab(2, 0), tab(2, 1)}, WDt[2] = {tab(3, 0), tab(3, 1)};
-  const bool rowv = r < 7;
-  const bool colv[2] = {2 * q < 7, 2 * q + 1 < 7};
-  const Frag zero = {{0.0, 0.0}};
-
-  // B and the collocated gradients of one field: nodes z = c in fragment c (rows y,
-  // columns x) -> U, Ux, Uy, Uz at the points, plane l, fragment [i][j]
-  auto forward = [&](const double* __restrict__ src, int ex, int ey, int ez, bool mask, Frag* U, Frag* Ux, Frag* Uy,
-                     Frag* Uz) {
-    Frag X[7];
-#pragma unroll
-    for (int c = 0; c < 7; ++c) {
-      const int64_t row = (int64_t)(K * ex) + (int64_t)P.Mx * ((K * ey + r) + (int64_t)P.My * (K * ez + c));
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        double x = (rowv && colv[t]) ? __ldg(src + row + 2 * q + t) : 0.0;
-        if (mask && is_dirichlet(K * ex + 2 * q + t, K * ey + r, K * ez + c, P.Mx, P.My, P.Mz, P.faces)) x = 0.0;
-        X[c].v[t] = x;
-      }
-    }
-    Frag Ep[7];   // after x and y: [i][j] per node plane c
-#pragma unroll
-    for (int c = 0; c < 7; ++c) {
-      const Frag t1 = contract_cols(X[c], WB, zero);          // [y][i]
-      Ep[c] = contract_cols(transpose(t1, lane), WB, zero);   // [i][j]
-    }
-#pragma unroll
-    for (int l = 0; l < 7; ++l)   // z: points plane l, [i][j]
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        double s = T.B[l][0] * Ep[0].v[t];
-#pragma unroll
-        for (int c = 1; c < 7; ++c) s = fma(T.B[l][c], Ep[c].v[t], s);
-        U[l].v[t] = s;
-      }
-#pragma unroll
-    for (int l = 0; l < 7; ++l) {
-      Uy[l] = contract_cols(U[l], WD, zero);                                  // d/dy: [i][j']
-      Ux[l] = transpose(contract_cols(transpose(U[l], lane), WD, zero), lane);   // d/dx: [i'][j]
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        double s = T.D[l][0] * U[0].v[t];
-#pragma unroll
-        for (int m = 1; m < 7; ++m) s = fma(T.D[l][m], U[m].v[t], s);
-        Uz[l].v[t] = s;
-      }
-    }
-  };
-
-  // PAJVP with 16-byte sized element records (p-Laplacian, 6 values per point): each warp
-  // stages its element's stored linearisation in shared memory by one TMA bulk copy,
-  // issued right after the previous element's pointwise phase (it lands during that
-  // element's B^T and this element's B)
-  constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
-  constexpr uint32_t LIN_BYTES = NL * 343 * sizeof(double);
-  double* const lbuf = q6sm + (size_t)wid * (NL * 343);
-  uint64_t* const lbar = reinterpret_cast<uint64_t*>(q6sm + (size_t)WARPS * (NL * 343)) + wid;
-  uint32_t lphase = 0;
-  auto issue_lin = [&](int64_t en) {
-    if constexpr (TMA_LIN) {
-      if (lane == 0 && en < E) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(lbar, LIN_BYTES);
-        mbar_arrive(lbar);
-        bulk_g2s(lbuf, P.lin + en * (NL * 343), LIN_BYTES, lbar);
-      }
-    }
-  };
-  if constexpr (TMA_LIN) {
-    if (lane == 0) {
-      mbar_init(lbar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    issue_lin((int64_t)blockIdx.x * WARPS + wid);
-  }
-
-  for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
-    int ex, ey, ez;
-    q6_coords(P, e, ex, ey, ez);
-    Frag U[7], Ux[7], Uy[7], Uz[7];   // the last field's channels (the fluxes overwrite Ux, Uy, Uz)
-    if constexpr (NIN == 2) {
-      forward(in0, ex, ey, ez, false, U, Ux, Uy, Uz);
-#pragma unroll
-      for (int l = 0; l < 7; ++l)
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          pk(0, l, t) = U[l].v[t];
-          pk(1, l, t) = Ux[l].v[t];
-          pk(2, l, t) = Uy[l].v[t];
-          pk(3, l, t) = Uz[l].v[t];
-        }
-      __syncwarp();
-      forward(in1, ex, ey, ez, MODE == MODE_VJP, U, Ux, Uy, Uz);
-    } else {
-      forward(in0, ex, ey, ez, false, U, Ux, Uy, Uz);
-    }
-    // ---- D at the points (slot (i = r, j = 2q + t) of plane l); fluxes over Ux / Uy / Uz
-    const double rho_e = (MODEL == HEAT && MODE != MODE_PAJVP) ? __ldg(P.rho + e) : 1.0;
-    // the element's stored linearisation, [l][NL][j][i] (the plane kernel's layout, ptx = 1)
-    double* const linp = (MODE == MODE_LIN || MODE == MODE_PAJVP) ? P.lin + e * (NL * 343) : nullptr;
-    if constexpr (MODE == MODE_PAJVP && !TMA_LIN) {   // next element's values into L2 while this one computes
-      const int64_t en = e + (int64_t)gridDim.x * WARPS;
-      if (lane == 0 && en < E) prefetch_l2_bulk(P.lin + en * (NL * 343), NL * 343 * sizeof(double));
-    }
-    if constexpr (TMA_LIN) {
-      mbar_wait(lbar, lphase);
-      lphase ^= 1u;
-    }
-    constexpr int NSV = MODE == MODE_PAJVP ? NL : 1;
-    double svn[2][NSV];   // PAJVP: plane l's stored values, requested one plane ahead
-    auto load_sv = [&](int l, double (*dst)[NSV]) {
-      if constexpr (MODE == MODE_PAJVP) {
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int c = 0; c < NL; ++c)
-            dst[t][c] = !(rowv && colv[t]) ? 0.0
-                        : TMA_LIN ? lbuf[(l * NL + c) * 49 + (2 * q + t) * 7 + r]
-                                  : ld_stream(linp + (l * NL + c) * 49 + (2 * q + t) * 7 + r);
-      }
-    };
-    load_sv(0, svn);
-    Frag V[7];   // value channel (residual: the load term)
-#pragma unroll
-    for (int l = 0; l < 7; ++l) {
-      double sv[2][NSV];
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int c = 0; c < NSV; ++c) sv[t][c] = svn[t][c];
-      if (l + 1 < 7) load_sv(l + 1, svn);
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int j = 2 * q + t;
-        double F0[4] = {0.0, 0.0, 0.0, 0.0}, F1[4];
-        if (rowv && colv[t]) {
-          const double wq = T.w[r] * T.w[j] * T.w[l];
-          const Metric M = {wq * P.cx, wq * P.cy, wq * P.cz, 0.0, 0.0, 0.0};
-          const double W = wq * P.vol;
-          double Ul[NIN], Uxl[NIN], Uyl[NIN], Uzl[NIN];
-          if constexpr (NIN == 2) {
-            Ul[0] = pk(0, l, t); Uxl[0] = pk(1, l, t); Uyl[0] = pk(2, l, t); Uzl[0] = pk(3, l, t);
-          }
-          Ul[NIN - 1] = U[l].v[t];
-          Uxl[NIN - 1] = Ux[l].v[t];
-          Uyl[NIN - 1] = Uy[l].v[t];
-          Uzl[NIN - 1] = Uz[l].v[t];
-          double gpart = 0.0, lv[NL];
-          point_op<MODE, MODEL, true>(Ul, Uxl, Uyl, Uzl, M, W, rho_e, P, sv[t], F0, F1, gpart, lv);
-          if constexpr (MODE == MODE_LIN) {
-#pragma unroll
-            for (int c = 0; c < NL; ++c) linp[(l * NL + c) * 49 + j * 7 + r] = lv[c];
-          }
-        }
-        Ux[l].v[t] = F0[0];
-        Uy[l].v[t] = F0[1];
-        Uz[l].v[t] = F0[2];
-        V[l].v[t] = value_channel(MODE, 0) ? F0[3] : 0.0;
-      }
-    }
-    if constexpr (NIN == 2) __syncwarp();   // park reads done before the next element's writes
-    if constexpr (TMA_LIN) {                // buffer reads done: stage the next element's values
-      __syncwarp();
-      issue_lin(e + (int64_t)gridDim.x * WARPS);
-    }
-    // ---- B^T: R = Dx^T Fx + Dy^T Fy + Dz^T Fz + V at the points, then z, y, x to the nodes
-    Frag R[7];
-#pragma unroll
-    for (int m = 0; m < 7; ++m)
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        double s = V[m].v[t];
-#pragma unroll
-        for (int l = 0; l < 7; ++l) s = fma(T.D[l][m], Uz[l].v[t], s);
-        R[m].v[t] = s;
-      }
-#pragma unroll
-    for (int l = 0; l < 7; ++l) {
-      const Frag rx = transpose(contract_cols(transpose(Ux[l], lane), WDt, zero), lane);   // Dx^T Fx
-      Frag acc = R[l];
-      acc.v[0] += rx.v[0];
-      acc.v[1] += rx.v[1];
-      R[l] = contract_cols(Uy[l], WDt, acc);   // + Dy^T Fy
-    }
-    // element node (a, b, c) -> the discontinuous L-vector (7 nx) x (7 ny) x (7 nz), x fastest:
-    // an element's 7-node x-rows are contiguous and neighbours' rows adjacent, so the
-    // assembly reads it row by row, coalesced
-    const int64_t LXd = 7 * (int64_t)P.nx, LYd = 7 * (int64_t)P.ny;
-    double* out = ev + ((int64_t)(7 * ez) * LYd + 7 * ey) * LXd + 7 * ex;
-#pragma unroll
-    for (int c = 0; c < 7; ++c) {
-      Frag S;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        double s = T.B[0][c] * R[0].v[t];
-#pragma unroll
-        for (int l = 1; l < 7; ++l) s = fma(T.B[l][c], R[l].v[t], s);
-        S.v[t] = s;
-      }
-      const Frag ty = contract_cols(S, WBt, zero);                      // [i][b]
-      const Frag nd = contract_cols(transpose(ty, lane), WBt, zero);    // [b][a]
-      if (rowv) {
-        double* o = out + ((int64_t)c * LYd + r) * LXd;
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-          if (colv[t]) o[2 * q + t] = nd.v[t];
-      }
-    }
-  }
-}
-
-// Per-point-plane variant (FEOD_Q6_PERL, default): after x and y, each field keeps only
-// its 7 node-plane fragments Ep[c] ([i][j]); point plane l is then formed, differentiated,
-// passed through D and transposed back in one step -- U_l = sum_c B[l][c] Ep[c] and
-// Uz_l = sum_c G[l][c] Ep[c] (DFMA), Uy_l / Ux_l by DMMA; after D,
-// R_l = V_l + Dy^T Fy_l + Dx^T Fx_l (DMMA) and the z-transpose accumulates
-// S[c] += B[l][c] R_l + G[l][c] Fz_l (DFMA). The same contractions as above (G = D B
-// exactly, k <= q - 1), with 7 fragments per field and 7 accumulators live instead of
-// 4 x 7 point channels: no shared-memory parking, fewer registers.
-#ifndef FEOD_Q6_PERL
-#define FEOD_Q6_PERL 1
-#endif
+// Per point plane: after x and y, each field keeps only its 7 node-plane fragments Ep[c]
+// ([i][j]); point plane l is then formed, differentiated, passed through D and transposed
+// back in one step -- U_l = sum_c B[l][c] Ep[c] and Uz_l = sum_c G[l][c] Ep[c] (DFMA),
+// Uy_l / Ux_l by DMMA with the collocated derivative D (G = D B exactly, k <= q - 1); after
+// D, R_l = V_l + Dy^T Fy_l + Dx^T Fx_l (DMMA) and the z-transpose accumulates
+// S[c] += B[l][c] R_l + G[l][c] Fz_l (DFMA); finally y and x of each S[c] (DMMA). 7 fragments
+// per field and 7 accumulators live (the first version held all 4 x 7 point channels and
+// parked a field in shared memory: more registers, slower -- DESIGN.md §11).
 #ifndef FEOD_Q6_FSTAGE   // shared-memory staging of the input fields (measured C4: JVP 304 -> 336 us
 #define FEOD_Q6_FSTAGE 0   // with it, residual 225 -> 255; the L2 prefetch alone is kept)
 #endif
@@ -594,17 +346,11 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
                                double* out, const double* dotx, double* dpart, cudaStream_t st) {
   constexpr int NL = lin_values(MODEL);
   constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
-#if FEOD_Q6_PERL
   constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS +
                                         (FEOD_Q6_SMT && FEOD_Q6_SMT_PA ? sizeof(double) * q6::WARPS * 2 * 8 * 18 : 0)
                                   : sizeof(double) * q6::WARPS *
                                         ((FEOD_Q6_FSTAGE ? q6_nin<MODE>() * 344 : 0) + (FEOD_Q6_SMT ? 2 * 8 * 18 : 0));
   const void* kfn = (const void*)q6tc_perl_kernel<MODE, MODEL>;
-#else
-  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS
-                          : q6_nin<MODE>() == 1 ? 0 : sizeof(double) * q6::WARPS * 4 * 7 * 2 * 32;
-  const void* kfn = (const void*)q6tc_kernel<MODE, MODEL>;
-#endif
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int slots = 0;
@@ -612,11 +358,7 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
   const int64_t E = (int64_t)P.nx * P.ny * P.nz;
   const int64_t want = (E + q6::WARPS - 1) / q6::WARPS;
   const unsigned grid = (unsigned)(want < slots ? want : slots);
-#if FEOD_Q6_PERL
   q6tc_perl_kernel<MODE, MODEL><<<grid, 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev);
-#else
-  q6tc_kernel<MODE, MODEL><<<grid, 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev);
-#endif
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   OpParams Pa = P;
   if (MODE == MODE_VJP && P.vjp_keep_rows) Pa.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
