@@ -488,10 +488,10 @@ cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T
   const bool nine = lin_values(model) == 9;
   // Q1, Q2: every element in one launch into the discontinuous L-vector + assembly (the
   // Dirichlet rows set there); C5 2293 (8 colours, r01) -> 714 (colours, thread per element)
-  if (ev && nd <= 3 && (size_t)nd * P.nx * sizeof(double) * (kAsmThreads / 32) <= 48 * 1024)
+  if (ev && nd <= 3 && (size_t)nd * P.nx * sizeof(double) * (kAsmThreads / 32) <= 227 * 1024)
     return nd == 2 ? (nine ? diag_elem_t<2, 9>(P, T, ev, diag, st) : diag_elem_t<2, 6>(P, T, ev, diag, st))
                    : (nine ? diag_elem_t<3, 9>(P, T, ev, diag, st) : diag_elem_t<3, 6>(P, T, ev, diag, st));
-  if (ev && nd >= 4 && nd <= 5 && P.ptx == 1 && (size_t)nd * P.nx * sizeof(double) * (kAsmThreads / 32) <= 48 * 1024) {
+  if (ev && nd >= 4 && nd <= 5 && P.ptx == 1 && (size_t)nd * P.nx * sizeof(double) * (kAsmThreads / 32) <= 227 * 1024) {
     switch (nd) {
       case 4:
         if (FEOD_DIAG_Q3_WARP) return nine ? diag_q3_t<9>(P, T, ev, diag, st) : diag_q3_t<6>(P, T, ev, diag, st);

@@ -110,7 +110,12 @@ inline cudaError_t evec_assemble(const OpParams& P, const double* ev, double* ou
                                  double dirval, cudaStream_t st) {
   const int rows = P.My * P.Mz;
   const size_t smem = sizeof(double) * (K + 1) * (size_t)P.nx * (kAsmThreads / 32);
-  if (smem > 48 * 1024) return cudaErrorInvalidValue;   // (K + 1) nx <= 768
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;   // (K + 1) nx <= 3632 (8 row buffers)
+  if (smem > 48 * 1024) {   // beyond the default: opt in (per call: a handle may live on any device)
+    const cudaError_t e = cudaFuncSetAttribute(evec_assemble_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
   const unsigned grid = dotx ? (unsigned)kRedBlocks : (unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks);
   evec_assemble_kernel<K><<<grid, kAsmThreads, smem, st>>>(P, ev, out, dotx, dpart, dirval);

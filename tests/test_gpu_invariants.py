@@ -198,3 +198,24 @@ def test_two_handles_on_concurrent_streams_are_bitwise_reproducible():
     for k in range(2):
         for r, j, t in outs[k]:
             assert torch.equal(r, ref[k][0]) and torch.equal(j, ref[k][1]) and torch.equal(t, ref[k][2])
+
+
+def test_q6_long_rows_and_odd_boxes():
+    """The Q6 tensor-core path on boxes with nx != ny != nz, odd Dirichlet face subsets and
+    rows longer than the default shared-memory row buffers of the assembly (nx = 120:
+    7 nx x 8 doubles > 48 KB per CTA, the opt-in path): residual, J v, J^T w, the stored
+    linearisation and the Jacobi diagonal against the oracle."""
+    import paper_2506_00746_b200 as fe
+    for (nx, ny, nz), faces, model in (((120, 1, 1), 1 | 2 | 16, 0), ((3, 2, 4), 4 | 32, 1), ((2, 3, 1), 63, 2)):
+        rng = np.random.default_rng(nx + ny)
+        rho = rng.uniform(0.1, 1, nx * ny * nz)
+        pr = O.Problem(nx, ny, nz, 6, 7, model, 3.0, 1e-2, 0.5, faces, None, rho)
+        N = pr.n_dofs
+        u, v = (rng.uniform(-1, 1, N) for _ in range(2))
+        op = fe.Operator(nx, ny, nz, 6, 7, model, 3.0, 1e-2, 0.5, None, faces, cuda(rho))
+        assert rel_l2(host(op.residual(cuda(u))), O.residual(pr, u)) <= 1e-11
+        assert rel_l2(host(op.jvp(cuda(u), cuda(v))), O.jvp(pr, u, v)) <= 1e-11
+        assert rel_l2(host(op.vjp(cuda(u), cuda(v))), O.vjp(pr, u, v)) <= 1e-11
+        op.linearize(cuda(u))
+        assert rel_l2(host(op.jvp_lin(cuda(v))), O.jvp(pr, u, v)) <= 1e-11
+        assert rel_l2(host(op.jacobi_diag()), O.jacobi_diag(pr, u)) <= 1e-11
