@@ -52,6 +52,9 @@
 #ifndef FEOD_PREFETCH
 #define FEOD_PREFETCH 1
 #endif
+#ifndef FEOD_Q3_RES_NCH3
+#define FEOD_Q3_RES_NCH3 1   // the Q3 residual with 3 exchange channels (measured 1-2 % faster at full clock)
+#endif
 #ifndef FEOD_NCH3_MIN
 #define FEOD_NCH3_MIN 6   // orders (ND) from which the exchange carries 3 channels
 #endif
@@ -185,7 +188,7 @@ struct PShape {
   // exchange channels: 2 ([W | Wy], x-derivative collocated over the lane group,
   // fewer FLOPs) up to Q4; 3 ([W | Wx | Wy], no cross-lane traffic) for Q5/Q6
   // (Q3 residual: 3 channels measured 1-2 % faster, the Q3 two-field modes 2 channels)
-  static constexpr int NCH = (ND >= FEOD_NCH3_MIN || (ND == 4 && MODE == MODE_RES)) ? 3 : 2;
+  static constexpr int NCH = (ND >= FEOD_NCH3_MIN || (ND == 4 && MODE == MODE_RES && FEOD_Q3_RES_NCH3)) ? 3 : 2;
   static constexpr XbPad XP = xb_pad(ND, NIN, NCH);
   static constexpr int SI = XP.SI, SJ = XP.SJ, SE = XP.SE, SF = ND * SJ;
   // element buffer (compute -> IO), per layer parity and output: [EL][b][a][c]

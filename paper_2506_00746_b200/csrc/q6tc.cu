@@ -62,15 +62,17 @@ FEOD_DEV Frag transpose(const Frag& m, int lane) {
 // __syncwarp per transpose; the pitch 18 = 2 mod 16 doubles keeps each half-warp's column
 // reads on 16 different bank pairs): one 16-byte store + two 8-byte loads instead of
 // eight 32-bit shuffles and four selects
+template <int NBUF>
 FEOD_DEV Frag transpose_sm(const Frag& m, int lane, double* scr, int& tb) {
   const int r = lane >> 2, q = lane & 3;
   double* b = scr + tb * (8 * 18);
-  tb ^= 1;
+  if (NBUF == 2) tb ^= 1;
   *reinterpret_cast<double2*>(b + r * 18 + 2 * q) = make_double2(m.v[0], m.v[1]);
   __syncwarp();
   Frag o;
   o.v[0] = b[(2 * q) * 18 + r];
   o.v[1] = b[(2 * q + 1) * 18 + r];
+  if (NBUF == 1) __syncwarp();   // one buffer: reads done before its next write
   return o;
 }
 // element coordinates by 32-bit unsigned division (E < 2^31, checked at feod_create; the
@@ -86,8 +88,8 @@ FEOD_DEV void q6_coords(const OpParams& P, int64_t e, int& ex, int& ey, int& ez)
 #ifndef FEOD_Q6_SMT   // shared-memory transposes in q6tc_perl_kernel
 #define FEOD_Q6_SMT 1
 #endif
-#ifndef FEOD_Q6_SMT_PA   // ... also in PAJVP (whose shared memory also holds the stored linearisation)
-#define FEOD_Q6_SMT_PA 0
+#ifndef FEOD_Q6_SMT_PA   // ... also in PAJVP, with ONE scratch buffer per warp (its shared memory also
+#define FEOD_Q6_SMT_PA 0 // holds the stored linearisation; measured C4 jvp_lin 235 -> 240 us: off)
 #endif
 // modes: RES (F(u)), JVP (J(u) v), VJP (J(u)^T w, w's Dirichlet entries masked, reading
 // A17), LIN (F(u) and the point linearisation written to P.lin), PAJVP (J(u0) v from P.lin)
@@ -148,10 +150,11 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
   constexpr size_t LEAD_DOUBLES = (MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0)
                                       ? (size_t)WARPS * NL * 343 + WARPS
                                   : FEOD_Q6_FSTAGE ? (size_t)WARPS * NIN * 344 : 0;
-  double* const tscr = q6sm + LEAD_DOUBLES + (size_t)wid * (2 * 8 * 18);
+  constexpr int TBUF = MODE == MODE_PAJVP ? 1 : 2;   // transpose scratch buffers per warp
+  double* const tscr = q6sm + LEAD_DOUBLES + (size_t)wid * (TBUF * 8 * 18);
   int tbuf = 0;
   auto tr = [&](const Frag& m) -> Frag {
-    if constexpr (SMT) return transpose_sm(m, lane, tscr, tbuf);
+    if constexpr (SMT) return transpose_sm<TBUF>(m, lane, tscr, tbuf);
     else return transpose(m, lane);
   };
 
@@ -347,7 +350,7 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
   constexpr int NL = lin_values(MODEL);
   constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
   constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS +
-                                        (FEOD_Q6_SMT && FEOD_Q6_SMT_PA ? sizeof(double) * q6::WARPS * 2 * 8 * 18 : 0)
+                                        (FEOD_Q6_SMT && FEOD_Q6_SMT_PA ? sizeof(double) * q6::WARPS * 1 * 8 * 18 : 0)
                                   : sizeof(double) * q6::WARPS *
                                         ((FEOD_Q6_FSTAGE ? q6_nin<MODE>() * 344 : 0) + (FEOD_Q6_SMT ? 2 * 8 * 18 : 0));
   const void* kfn = (const void*)q6tc_perl_kernel<MODE, MODEL>;
