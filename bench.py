@@ -534,11 +534,11 @@ def main():
                              "ms_without_graphs": statistics.median(tg),
                              "note": "feod_newton_cg: CG iterations as a replayed CUDA graph (5 launches per iteration, "
                                      "alpha/beta reduced in-kernel), host sync once per Newton step"}
-    if w.k <= 3 and world == 1:
+    if world == 1:
         # NEXT-4 (Table-1 analogue): element tangents K_e = B^T J_D B on the FP64 tensor cores,
         # RES (integration-point AD) and ELM (element-level forward AD), on a bounded element range
         nn, Qp = (w.k + 1) ** 3, w.q ** 3
-        ne = min(op.n_elems, 16384)
+        ne = min(op.n_elems, 16384 if w.k <= 3 else 1024)   # Q6: K_e is 941 KB per element
         Ke = torch.empty((ne, nn, nn), dtype=torch.float64, device=u.device)
         pw = {W.PLAPLACE: 35, W.NLDIFF: 19, W.HEAT: 19}[w.model] * (2 if w.perturbed else 1)   # dual flux flops
         gemm = 2.0 * nn * nn * 3 * Qp

@@ -143,8 +143,11 @@ FEOD_API int feod_vjp(feod_handle h, const double* u, const double* w, double* J
  *   is the tangent of the element residual B^T D(B u_e) along e_j, the dual  *
  *   pushed through the sum-factorised B, D and B^T -- nd^3 dual evaluations  *
  *   of D per point.                                       *
- * No Dirichlet handling (element level). Orders 1..3 (FEOD_EUNSUPPORTED      *
- * above: an element matrix no longer fits one CTA's shared memory).          */
+ * No Dirichlet handling (element level). All orders 1..6: from order 4 on    *
+ * RES runs as a tiled product with on-chip operand generation, and ELM keeps *
+ * its per-seed tangent arrays in a handle-owned device scratch (allocated on *
+ * first use, up to 296 CTAs' worth: Q6 ~1.1 GB; FEOD_ENOMEM if it cannot be  *
+ * allocated). Q6 K_e is 941 KB per element: the caller sizes ne to Ke.      */
 FEOD_API int feod_element_matrices(feod_handle h, const double* u, int64_t e0, int64_t ne, int elm, double* Ke);
 /* Adjoint solve (the adjoint analysis of PAPER.md:199): *
  * lambda (device, length N) <- `iters` BiCGStab iterations from lambda = 0 on  *

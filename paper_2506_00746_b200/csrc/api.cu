@@ -46,6 +46,8 @@ struct feod_op {
   int newton_lin = 0;          // Newton-CG: 0 matrix-free JVP, 1 stored linearisation, 2 + Jacobi
   double* jdiag = nullptr;     // Jacobi diagonal (Newton mode 2), N
   double* evec = nullptr;      // discontinuous L-vector, nd^3 x E (q6tc.cu operator and diagonal, diag.cu Q3..Q5)
+  double* em_scr = nullptr;    // ELM element tangents at Q4..Q6: per-CTA tangent arrays (elm.cu)
+  size_t em_scr_n = 0;         // its length in doubles
   bool q6tc = true;            // FEOD_Q6_TC=0 disables the Q6 tensor-core path (experiments)
   bool q6tc_res = true;        // FEOD_Q6_TC_RES=0: the residual on plane_kernel (experiments)
   bool q6tc_lin = false;       // FEOD_Q6_TC_LIN=1: feod_linearize on it too (experiments)
@@ -108,6 +110,7 @@ static void free_all(feod_op* h) {
   cudaFree(h->kwork);
   cudaFree(h->jdiag);
   cudaFree(h->evec);
+  cudaFree(h->em_scr);
 }
 
 extern "C" int feod_create(const feod_mesh* mesh, int order, int qorder, const feod_coeffs* coeffs,
@@ -514,16 +517,29 @@ extern "C" int feod_element_matrices(feod_handle h, const double* u, int64_t e0,
   if (!h || !u || !Ke) return fail(FEOD_EINVAL, "feod_element_matrices: null argument");
   if (e0 < 0 || ne < 0 || e0 + ne > h->E || (elm != 0 && elm != 1))
     return fail(FEOD_EINVAL, "feod_element_matrices: element range or mode out of bounds");
-  if (h->nd > 4) return fail(FEOD_EUNSUPPORTED, "feod_element_matrices: built for orders 1..3");
   if (h->coeffs.model == FEOD_HEAT_DESIGN && !h->P.rho) return fail(FEOD_EINVAL, "feod_element_matrices: rho unset");
   if (ne == 0) return FEOD_OK;
-  if (elm)   // element-level forward AD through B, D, B^T (Table 1's ELM), elm.cu
-    CK(element_matrices_elm_nd(h->nd, h->coeffs.model, h->geom == nullptr, h->P, h->T, u, (int)e0, (int)ne, Ke, h->st),
+  const bool affine = h->geom == nullptr;
+  if (elm) {   // element-level forward AD through B, D, B^T (Table 1's ELM), elm.cu
+    const size_t per = elm_scratch_per_cta(h->nd);
+    if (per && !h->em_scr) {   // Q4..Q6: the seeds' tangent arrays for up to 2 CTAs per SM
+      const size_t n = per * (size_t)(h->E < 2 * 148 ? h->E : 2 * 148);
+      if (cudaMalloc(&h->em_scr, sizeof(double) * n) != cudaSuccess) {
+        h->em_scr = nullptr;
+        return fail(FEOD_ENOMEM, "feod_element_matrices: ELM scratch");
+      }
+      h->em_scr_n = n;
+    }
+    CK(element_matrices_elm_nd(h->nd, h->coeffs.model, affine, h->P, h->T, u, (int)e0, (int)ne, Ke, h->em_scr,
+                               h->em_scr_n, h->st),
        "feod_element_matrices");
-  else       // integration-point AD + K_e = M^T N on the FP64 tensor cores (Table 1's RES), elemat.cu
-    CK(element_matrices_nd(h->nd, h->coeffs.model, h->geom == nullptr, false, h->P, h->T, u, (int)e0, (int)ne, Ke,
-                           h->st),
+  } else if (h->nd <= 4) {   // integration-point AD + K_e = M^T N on the FP64 tensor cores (Table 1's RES), elemat.cu
+    CK(element_matrices_nd(h->nd, h->coeffs.model, affine, false, h->P, h->T, u, (int)e0, (int)ne, Ke, h->st),
        "feod_element_matrices");
+  } else {     // Q4..Q6: the same product tiled, operands generated on chip (elemat_hi.cu)
+    CK(element_matrices_hi_nd(h->nd, h->coeffs.model, affine, h->P, h->T, u, (int)e0, (int)ne, Ke, h->st),
+       "feod_element_matrices");
+  }
   return FEOD_OK;
 }
 

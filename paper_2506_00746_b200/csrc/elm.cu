@@ -10,7 +10,9 @@
 // against RES's 4), which is the growth Table 1 reports.
 //
 // One CTA per element (persistent over the range), one thread per seed j; the seed's
-// tangent arrays live in shared memory, thread-interleaved ([slot][thread]: conflict-free).
+// tangent arrays are thread-interleaved ([slot][thread]: conflict-free / coalesced) in
+// shared memory up to Q3, and from Q4 on (Q4: 512 KB per CTA, Q6: 3.9 MB) in a global
+// scratch slice per CTA (L2 / HBM traffic: ELM is the slow column of Table 1).
 // The value part of the dual (u_e, B u_e at the points) is the same for every seed and
 // is computed once per element.
 #include "common.cuh"
@@ -25,19 +27,21 @@ struct ElmShape {
   static constexpr int NQ = ND, Q = ND * ND * ND, NN = ND * ND * ND;
   static constexpr int NT = (NN + 31) / 32 * 32;        // one thread per seed column
   static constexpr int SLOTS = 4 * Q;                    // per-thread tangent arrays (values + 3 gradients)
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)SLOTS * NT + 4 * Q + NN);
+  static constexpr bool GLOBAL = ND >= 5;                // tangent arrays in the global scratch
+  static constexpr size_t SCRATCH = GLOBAL ? (size_t)SLOTS * NT : 0;   // doubles per CTA
+  static constexpr size_t SMEM = sizeof(double) * ((GLOBAL ? 0 : (size_t)SLOTS * NT) + 4 * Q + NN);
 };
 
 template <int ND, int MODEL, bool AFFINE>
 __global__ void __launch_bounds__(ElmShape<ND>::NT) elm_kernel(const OpParams P, const Tables T,
                                                                const double* __restrict__ u, int e0, int ne,
-                                                               double* __restrict__ Ke) {
+                                                               double* __restrict__ Ke, double* __restrict__ scr) {
   using S = ElmShape<ND>;
   constexpr int NQ = S::NQ, Q = S::Q, NN = S::NN, NT = S::NT, K = ND - 1;
   constexpr int NQ2 = NQ * NQ;
   extern __shared__ double sm[];
-  double* W = sm;                         // [SLOTS][NT] this thread's tangent arrays
-  double* UQ = W + (size_t)S::SLOTS * NT; // [4][Q] value part: u, gh_x, gh_y, gh_z at the points
+  double* W = S::GLOBAL ? scr + blockIdx.x * S::SCRATCH : sm;   // [SLOTS][NT] this thread's tangent arrays
+  double* UQ = S::GLOBAL ? sm : W + (size_t)S::SLOTS * NT;        // [4][Q] value part: u, gh_x, gh_y, gh_z
   double* UE = UQ + 4 * Q;                // [NN] element DOFs
   const int tid = threadIdx.x;
   const bool seed = tid < NN;             // thread tid differentiates along e_tid
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(ElmShape<ND>::NT) elm_kernel(const OpParams P,
 
 template <int ND, int MODEL, bool AFFINE>
 static cudaError_t elm_launch(const OpParams& P, const Tables& T, const double* u, int e0, int ne, double* Ke,
-                              cudaStream_t st) {
+                              double* scr, size_t scr_doubles, cudaStream_t st) {
   using S = ElmShape<ND>;
   cudaError_t e = cudaFuncSetAttribute(elm_kernel<ND, MODEL, AFFINE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)S::SMEM);
@@ -185,32 +189,50 @@ static cudaError_t elm_launch(const OpParams& P, const Tables& T, const double* 
   int slots = 0;
   if ((e = persistent_slots((const void*)elm_kernel<ND, MODEL, AFFINE>, S::NT, S::SMEM, &slots)) != cudaSuccess)
     return e;
+  if (S::GLOBAL) {   // the grid is bounded by the scratch the caller provides
+    if (!scr) return cudaErrorInvalidValue;
+    const size_t cap = scr_doubles / S::SCRATCH;
+    if ((size_t)slots > cap) slots = (int)cap;
+  }
   const int g = ne < slots ? ne : slots;
-  if (g <= 0) return cudaSuccess;
-  elm_kernel<ND, MODEL, AFFINE><<<g, S::NT, S::SMEM, st>>>(P, T, u, e0, ne, Ke);
+  if (g <= 0) return ne > 0 ? cudaErrorInvalidValue : cudaSuccess;
+  elm_kernel<ND, MODEL, AFFINE><<<g, S::NT, S::SMEM, st>>>(P, T, u, e0, ne, Ke, scr);
   return cudaGetLastError();
 }
 
 template <int ND>
 static cudaError_t elm_nd_t(int model, bool affine, const OpParams& P, const Tables& T, const double* u, int e0,
-                            int ne, double* Ke, cudaStream_t st) {
+                            int ne, double* Ke, double* scr, size_t scr_doubles, cudaStream_t st) {
   switch (model) {
-    case PLAPLACE: return affine ? elm_launch<ND, PLAPLACE, true>(P, T, u, e0, ne, Ke, st)
-                                 : elm_launch<ND, PLAPLACE, false>(P, T, u, e0, ne, Ke, st);
-    case NLDIFF: return affine ? elm_launch<ND, NLDIFF, true>(P, T, u, e0, ne, Ke, st)
-                               : elm_launch<ND, NLDIFF, false>(P, T, u, e0, ne, Ke, st);
-    case HEAT: return affine ? elm_launch<ND, HEAT, true>(P, T, u, e0, ne, Ke, st)
-                             : elm_launch<ND, HEAT, false>(P, T, u, e0, ne, Ke, st);
+    case PLAPLACE: return affine ? elm_launch<ND, PLAPLACE, true>(P, T, u, e0, ne, Ke, scr, scr_doubles, st)
+                                 : elm_launch<ND, PLAPLACE, false>(P, T, u, e0, ne, Ke, scr, scr_doubles, st);
+    case NLDIFF: return affine ? elm_launch<ND, NLDIFF, true>(P, T, u, e0, ne, Ke, scr, scr_doubles, st)
+                               : elm_launch<ND, NLDIFF, false>(P, T, u, e0, ne, Ke, scr, scr_doubles, st);
+    case HEAT: return affine ? elm_launch<ND, HEAT, true>(P, T, u, e0, ne, Ke, scr, scr_doubles, st)
+                             : elm_launch<ND, HEAT, false>(P, T, u, e0, ne, Ke, scr, scr_doubles, st);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t element_matrices_elm_nd(int nd, int model, bool affine, const OpParams& P, const Tables& T,
-                                    const double* u, int e0, int ne, double* Ke, cudaStream_t st) {
+size_t elm_scratch_per_cta(int nd) {
   switch (nd) {
-    case 2: return elm_nd_t<2>(model, affine, P, T, u, e0, ne, Ke, st);
-    case 3: return elm_nd_t<3>(model, affine, P, T, u, e0, ne, Ke, st);
-    case 4: return elm_nd_t<4>(model, affine, P, T, u, e0, ne, Ke, st);
+    case 5: return ElmShape<5>::SCRATCH;
+    case 6: return ElmShape<6>::SCRATCH;
+    case 7: return ElmShape<7>::SCRATCH;
+  }
+  return 0;
+}
+
+cudaError_t element_matrices_elm_nd(int nd, int model, bool affine, const OpParams& P, const Tables& T,
+                                    const double* u, int e0, int ne, double* Ke, double* scr, size_t scr_doubles,
+                                    cudaStream_t st) {
+  switch (nd) {
+    case 2: return elm_nd_t<2>(model, affine, P, T, u, e0, ne, Ke, scr, scr_doubles, st);
+    case 3: return elm_nd_t<3>(model, affine, P, T, u, e0, ne, Ke, scr, scr_doubles, st);
+    case 4: return elm_nd_t<4>(model, affine, P, T, u, e0, ne, Ke, scr, scr_doubles, st);
+    case 5: return elm_nd_t<5>(model, affine, P, T, u, e0, ne, Ke, scr, scr_doubles, st);
+    case 6: return elm_nd_t<6>(model, affine, P, T, u, e0, ne, Ke, scr, scr_doubles, st);
+    case 7: return elm_nd_t<7>(model, affine, P, T, u, e0, ne, Ke, scr, scr_doubles, st);
   }
   return cudaErrorNotSupported;
 }

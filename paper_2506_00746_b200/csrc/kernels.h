@@ -83,9 +83,16 @@ cudaError_t q6tc_diag(int model, const OpParams& P, const Tables& T, double* ev,
 bool q6tc_supports(int mode);
 cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
                      double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st);
-// element tangents by element-level forward AD through B, D and B^T (elm.cu, K10; Table 1's ELM)
+// element tangents by element-level forward AD through B, D and B^T (elm.cu, K10; Table 1's ELM);
+// nd >= 5 keeps the per-seed tangent arrays in scr (elm_scratch_per_cta(nd) doubles per CTA; the
+// grid is bounded by scr_doubles)
+size_t elm_scratch_per_cta(int nd);
 cudaError_t element_matrices_elm_nd(int nd, int model, bool affine, const OpParams& P, const Tables& T,
-                                    const double* u, int e0, int ne, double* Ke, cudaStream_t st);
+                                    const double* u, int e0, int ne, double* Ke, double* scr, size_t scr_doubles,
+                                    cudaStream_t st);
+// element tangents at nd = 5..7 (Q4..Q6): tiled M^T N with on-chip operand generation (elemat_hi.cu, K9b)
+cudaError_t element_matrices_hi_nd(int nd, int model, bool affine, const OpParams& P, const Tables& T,
+                                   const double* u, int e0, int ne, double* Ke, cudaStream_t st);
 // Jacobi diagonal of the stored linearisation (diag.cu, K8)
 // ev: scratch for the discontinuous L-vector (nd^3 x E doubles) of the Q3..Q5 path, or null
 cudaError_t jacobi_diag_nd(int nd, int model, const OpParams& P, const Tables& T, double* ev, double* diag,
