@@ -197,6 +197,19 @@ FEOD_API int feod_res_design_grad(feod_handle h, const double* u, const double* 
  * Host memory should be pinned. */
 FEOD_API int feod_apply_host(feod_handle h, int op, const double* in0, const double* in1, double* out);
 
+/* A stream of nbatch independent problems on HOST buffers, op as in         *
+ * feod_apply_host: step b reads in0[b] (and in1[b] for op != 0) and writes  *
+ * out[b] (N doubles; E for op 2; 2N = [r | Jv] for op 4). Arrays of nbatch  *
+ * host pointers; buffers should be pinned; out[b] must not alias any input. *
+ * Two library-owned device staging sets (8 max(N, E) doubles, allocated on  *
+ * first use): step b+1's uploads overlap step b's operator and downloads    *
+ * (the host link is full duplex), so a step costs max(H2D, D2H, operator)   *
+ * in steady state. Synchronises before returning; on error the steps        *
+ * already queued may have completed. Results are bitwise those of nbatch    *
+ * feod_apply_host calls (the same kernels on the same stream).              */
+FEOD_API int feod_apply_host_batch(feod_handle h, int op, int64_t nbatch, const double* const* in0,
+                                   const double* const* in1, double* const* out);
+
 /* Jacobian-free Newton with unpreconditioned CG (reading A15, BASELINE
  * configs[3]): u (device, length N) is updated in place; for each of
  * newton_steps steps: F = F(u), CG on J(u) d = -F from d = 0 for exactly

@@ -30,7 +30,7 @@ FEOD_OK, FEOD_EINVAL, FEOD_EUNSUPPORTED, FEOD_ENOMEM, FEOD_ECUDA = 0, -1, -2, -3
 EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "feod_num_dofs", "feod_num_elems",
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
            "feod_set_newton_linearization", "feod_brick_shape", "feod_jacobi_diag", "feod_adjoint_solve", "feod_element_matrices",
-           "feod_design_grad", "feod_res_design_grad", "feod_apply_host", "feod_newton_cg",
+           "feod_design_grad", "feod_res_design_grad", "feod_apply_host", "feod_apply_host_batch", "feod_newton_cg",
            "feod_set_cg_graphs", "feod_cg_graph_launches",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
@@ -87,6 +87,7 @@ def load_library(path: str = LIB_PATH):
     lib.feod_element_matrices.argtypes = [vp, dp, i64, i64, ctypes.c_int, dp]
     lib.feod_adjoint_solve.argtypes = [vp, dp, dp, dp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_apply_host.argtypes = [vp, ctypes.c_int, dp, dp, dp]
+    lib.feod_apply_host_batch.argtypes = [vp, ctypes.c_int, i64, vp, vp, vp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_set_cg_graphs.argtypes = [vp, ctypes.c_int]
     lib.feod_cg_graph_launches.argtypes = [vp]
@@ -307,6 +308,36 @@ class Operator:
         _check(self.lib.feod_apply_host(self.h, int(op), a.data_ptr(), 0 if b is None else b.data_ptr(),
                                         res.data_ptr()))
         return res
+
+    def apply_host_batch(self, op, ins0, ins1=None, outs=None):
+        """A stream of host-buffer problems (feod_apply_host_batch): step b maps ins0[b]
+        (and ins1[b]) to outs[b]; uploads of step b+1 overlap step b's operator and
+        downloads. Returns the list of output tensors."""
+        t = self._torch
+        nb = len(ins0)
+        n_out = self.n_elems if op == 2 else (2 * self.n_dofs if op == 4 else self.n_dofs)
+        if op != 0 and (ins1 is None or len(ins1) != nb):
+            raise FeodError(FEOD_EINVAL, "ins1: one host vector per step expected")
+        for lst, name in ((ins0, "ins0"), (ins1 if op != 0 else (), "ins1")):
+            for x in lst:
+                if (not isinstance(x, t.Tensor) or x.device.type != "cpu" or x.dtype != t.float64
+                        or x.numel() != self.n_dofs or not x.is_contiguous()):
+                    raise FeodError(FEOD_EINVAL, f"{name}: contiguous host float64 tensors of length N expected")
+        if outs is None:
+            outs = [t.empty(n_out, dtype=t.float64, pin_memory=True) for _ in range(nb)]
+        if len(outs) != nb:
+            raise FeodError(FEOD_EINVAL, "outs: one host buffer per step expected")
+        for o in outs:
+            if (not isinstance(o, t.Tensor) or o.device.type != "cpu" or o.dtype != t.float64
+                    or o.numel() != n_out or not o.is_contiguous()):
+                raise FeodError(FEOD_EINVAL, f"outs: contiguous host float64 tensors of {n_out} entries expected")
+        P = ctypes.c_void_p * max(nb, 1)
+        a = P(*[x.data_ptr() for x in ins0])
+        b = P(*[x.data_ptr() for x in ins1]) if op != 0 else None
+        o = P(*[x.data_ptr() for x in outs])
+        self._sync_stream()
+        _check(self.lib.feod_apply_host_batch(self.h, int(op), nb, a, b, o))
+        return outs
 
     def newton_cg(self, u0, newton_steps=5, cg_iters=20):
         u = self._dev(u0, self.n_dofs, "u0").clone()

@@ -28,6 +28,9 @@ struct feod_op {
   double* geom = nullptr;
   double* shell = nullptr;     // 2 x nbricks x shell
   double* stage = nullptr;     // host-API staging: 4 x max(N, E)
+  double* stage2 = nullptr;    // feod_apply_host_batch: the second staging set (double buffering)
+  cudaEvent_t bev[6] = {};     // feod_apply_host_batch per set: inputs up, r ready, outputs ready (x2)
+  cudaEvent_t bdown[2] = {};   // feod_apply_host_batch per set: outputs downloaded (set free)
   cudaStream_t cst = nullptr;  // host-API upload stream (op 4 overlaps copies with the operator)
   cudaStream_t dst = nullptr;  // host-API download stream (runs against the uploads: full duplex)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -91,7 +94,12 @@ static void free_all(feod_op* h) {
   cudaFree(h->geom);
   cudaFree(h->shell);
   cudaFree(h->stage);
+  cudaFree(h->stage2);
   for (cudaEvent_t& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t& e : h->bev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t& e : h->bdown)
     if (e) cudaEventDestroy(e);
   if (h->cst) cudaStreamDestroy(h->cst);
   if (h->dst) cudaStreamDestroy(h->dst);
@@ -615,6 +623,71 @@ extern "C" int feod_apply_host(feod_handle h, int op, const double* in0, const d
   const int64_t nout = op == 2 ? h->E : h->N;
   CK(cudaMemcpyAsync(out, d2, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->st), "feod_apply_host: D2H");
   CK(cudaStreamSynchronize(h->st), "feod_apply_host: sync");
+  return FEOD_OK;
+}
+
+// A stream of independent host-buffer problems (one (in0[b], in1[b]) -> out[b] per step):
+// two device staging sets, uploads on cst, the operator on the handle's stream, downloads
+// on dst. Step b + 1's uploads run while step b computes and downloads (the host link is
+// full duplex), so in steady state a step costs max(H2D, D2H, operator) instead of their sum.
+extern "C" int feod_apply_host_batch(feod_handle h, int op, int64_t nbatch, const double* const* in0,
+                                     const double* const* in1, double* const* out) {
+  if (!h || nbatch < 0 || (nbatch > 0 && (!in0 || !out || (op != 0 && !in1))))
+    return fail(FEOD_EINVAL, "feod_apply_host_batch: null argument");
+  if (op < 0 || op > 4) return fail(FEOD_EINVAL, "feod_apply_host_batch: op must be 0 .. 4");
+  for (int64_t b = 0; b < nbatch; ++b)
+    if (!in0[b] || !out[b] || (op != 0 && !in1[b])) return fail(FEOD_EINVAL, "feod_apply_host_batch: null buffer");
+  if (nbatch == 0) return FEOD_OK;
+  const int64_t len = h->N > h->E ? h->N : h->E;
+  for (double** sp : {&h->stage, &h->stage2})
+    if (!*sp && cudaMalloc(sp, sizeof(double) * 4 * (size_t)len) != cudaSuccess) {
+      *sp = nullptr;
+      return fail(FEOD_ENOMEM, "feod_apply_host_batch: staging buffers");
+    }
+  if (!h->cst) {
+    CK(cudaStreamCreateWithFlags(&h->cst, cudaStreamNonBlocking), "feod_apply_host_batch: stream");
+    CK(cudaStreamCreateWithFlags(&h->dst, cudaStreamNonBlocking), "feod_apply_host_batch: stream");
+    for (cudaEvent_t& e : h->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "feod_apply_host_batch");
+  }
+  if (!h->bev[0]) {
+    for (cudaEvent_t& e : h->bev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "feod_apply_host_batch");
+    for (cudaEvent_t& e : h->bdown) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "feod_apply_host_batch");
+  }
+  const size_t nb_in = sizeof(double) * (size_t)h->N;
+  const size_t nb_out = sizeof(double) * (size_t)(op == 2 ? h->E : h->N);
+  CK(cudaEventRecord(h->ev[3], h->st), "feod_apply_host_batch");   // earlier work on the handle's stream
+  CK(cudaStreamWaitEvent(h->cst, h->ev[3], 0), "feod_apply_host_batch");
+  for (int64_t b = 0; b < nbatch; ++b) {
+    const int s = (int)(b & 1);
+    double* d0 = s ? h->stage2 : h->stage;
+    double *d1 = d0 + len, *d2 = d0 + 2 * len, *d3 = d0 + 3 * len;
+    cudaEvent_t up = h->bev[3 * s], rdy_r = h->bev[3 * s + 1], rdy = h->bev[3 * s + 2], down = h->bdown[s];
+    if (b >= 2) CK(cudaStreamWaitEvent(h->cst, down, 0), "feod_apply_host_batch");   // set s free
+    CK(cudaMemcpyAsync(d0, in0[b], nb_in, cudaMemcpyHostToDevice, h->cst), "feod_apply_host_batch: H2D");
+    if (op != 0) CK(cudaMemcpyAsync(d1, in1[b], nb_in, cudaMemcpyHostToDevice, h->cst), "feod_apply_host_batch: H2D");
+    CK(cudaEventRecord(up, h->cst), "feod_apply_host_batch");
+    CK(cudaStreamWaitEvent(h->st, up, 0), "feod_apply_host_batch");
+    int rc = op == 0 || op == 4 ? feod_residual(h, d0, d2)
+             : op == 1          ? feod_jvp(h, d0, d1, d2)
+             : op == 2          ? feod_design_grad(h, d0, d1, d2)
+                                : feod_vjp(h, d0, d1, d2);
+    if (rc != FEOD_OK) return rc;
+    CK(cudaEventRecord(rdy_r, h->st), "feod_apply_host_batch");
+    if (op == 4) {
+      if ((rc = feod_jvp(h, d0, d1, d3)) != FEOD_OK) return rc;
+      CK(cudaEventRecord(rdy, h->st), "feod_apply_host_batch");
+    }
+    CK(cudaStreamWaitEvent(h->dst, rdy_r, 0), "feod_apply_host_batch");   // r downloads while the JVP runs
+    CK(cudaMemcpyAsync(out[b], d2, nb_out, cudaMemcpyDeviceToHost, h->dst), "feod_apply_host_batch: D2H");
+    if (op == 4) {
+      CK(cudaStreamWaitEvent(h->dst, rdy, 0), "feod_apply_host_batch");
+      CK(cudaMemcpyAsync(out[b] + h->N, d3, nb_out, cudaMemcpyDeviceToHost, h->dst), "feod_apply_host_batch: D2H");
+    }
+    CK(cudaEventRecord(down, h->dst), "feod_apply_host_batch");
+  }
+  CK(cudaStreamSynchronize(h->st), "feod_apply_host_batch: sync");
+  CK(cudaStreamSynchronize(h->cst), "feod_apply_host_batch: sync");
+  CK(cudaStreamSynchronize(h->dst), "feod_apply_host_batch: sync");
   return FEOD_OK;
 }
 

@@ -104,6 +104,32 @@ def test_host_buffer_path_matches_device():
     assert torch.equal(rj[n:], op.jvp(uh.cuda(), vh.cuda()).cpu())
 
 
+@pytest.mark.parametrize("w", [W.C3.resized(6), W.C5.resized(5)], ids=["C3n6", "C5n5"])
+def test_host_batch_matches_single_calls(w):
+    """feod_apply_host_batch (double-buffered staging, uploads of step b+1 under step b):
+    every step bitwise equal to its own feod_apply_host call, for 5 different input pairs
+    (odd count: the last step uses set 0 again), for every op; and op 4 against the oracle."""
+    import torch
+    from gpu_util import operator, problem
+    d = W.draw(w)
+    op = operator(w, d)
+    rng = np.random.default_rng(11)
+    us = [torch.as_tensor(d["u"] + 0.1 * rng.standard_normal(w.n_dofs)).pin_memory() for _ in range(5)]
+    vs = [torch.as_tensor(rng.standard_normal(w.n_dofs)).pin_memory() for _ in range(5)]
+    ops = (0, 1, 3, 4) + ((2,) if w.model == W.HEAT else ())
+    for o in ops:
+        outs = op.apply_host_batch(o, us, None if o == 0 else vs)
+        for b in range(5):
+            assert torch.equal(outs[b], op.apply_host(o, us[b], None if o == 0 else vs[b])), (o, b)
+    outs = op.apply_host_batch(4, us, vs)
+    pr, n = problem(w, d), op.n_dofs
+    for b in (0, 4):
+        ub, vb = us[b].numpy(), vs[b].numpy()
+        assert rel_l2(outs[b][:n].numpy(), O.residual(pr, ub)) <= 1e-11
+        assert rel_l2(outs[b][n:].numpy(), O.jvp(pr, ub, vb)) <= 1e-11
+    assert op.apply_host_batch(4, [], []) == []
+
+
 def test_error_paths():
     import torch
     import paper_2506_00746_b200 as fe
