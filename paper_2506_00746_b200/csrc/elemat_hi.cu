@@ -21,6 +21,17 @@
 namespace feod {
 
 constexpr int kEhThreads = 256;
+// experiment knobs: points per k-chunk, output-tile width (64: 32x32 warp tiles, 128: 32x64),
+// CTAs per SM the register budget is sized for
+#ifndef FEOD_EH_KC
+#define FEOD_EH_KC 8
+#endif
+#ifndef FEOD_EH_CB
+#define FEOD_EH_CB 64
+#endif
+#ifndef FEOD_EH_MINB
+#define FEOD_EH_MINB 1
+#endif
 
 FEOD_DEV void dmma884_hi(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -31,9 +42,11 @@ FEOD_DEV void dmma884_hi(double& d0, double& d1, double a, double b) {
 template <int ND>
 struct EhShape {
   static constexpr int NQ = ND, Q = ND * ND * ND, NN = ND * ND * ND;
-  static constexpr int KC = 8, KR = 3 * KC;              // points per k-chunk, k-rows per chunk (4 | KR)
+  static constexpr int KC = FEOD_EH_KC, KR = 3 * KC;     // points per k-chunk, k-rows per chunk (4 | KR)
+  static_assert(KR % 4 == 0, "k-chunk of whole DMMA k-steps");
   static constexpr int NCH = (Q + KC - 1) / KC;
-  static constexpr int RB = 128, CB = 64;                // output tile
+  static constexpr int RB = 128, CB = FEOD_EH_CB;        // output tile
+  static constexpr int WCT = CB / 16;                    // 8-column tiles per warp (warps as 4 x 2)
   static constexpr int RT = (NN + RB - 1) / RB, CT = (NN + CB - 1) / CB;
   static constexpr int MS = RB + 4, NS = CB + 4;         // row strides = 4 (mod 16) doubles: conflict-free fragments
   static constexpr int STAGE = KR * (MS + NS);
@@ -42,12 +55,12 @@ struct EhShape {
 };
 
 template <int ND, int MODEL, bool AFFINE>
-__global__ void __launch_bounds__(kEhThreads, 1) elemat_hi_kernel(const OpParams P, const Tables T,
+__global__ void __launch_bounds__(kEhThreads, FEOD_EH_MINB) elemat_hi_kernel(const OpParams P, const Tables T,
                                                                   const double* __restrict__ u, int e0, int ne,
                                                                   double* __restrict__ Ke) {
   using S = EhShape<ND>;
   constexpr int NQ = S::NQ, Q = S::Q, NN = S::NN, KC = S::KC, KR = S::KR, MS = S::MS, NS = S::NS;
-  constexpr int RB = S::RB, CB = S::CB;
+  constexpr int RB = S::RB, CB = S::CB, WCT = S::WCT;
   constexpr int K = ND - 1;
   extern __shared__ double sm[];
   double* STG = sm;                       // [2][KR][MS] M^T chunk, then [2][KR][NS] N chunk
@@ -59,7 +72,7 @@ __global__ void __launch_bounds__(kEhThreads, 1) elemat_hi_kernel(const OpParams
   double* Wt = Gt + NQ * ND;              // [NQ]
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int wr = warp & 3, wc = warp >> 2;   // the warp's 32 x 32 sub-tile of the 128 x 64 output tile
+  const int wr = warp & 3, wc = warp >> 2;   // the warp's 32 x (8 WCT) sub-tile of the RB x CB output tile
 
   for (int t = tid; t < NQ * ND; t += kEhThreads) {
     Bt[t] = T.B[t / ND][t % ND];
@@ -197,31 +210,31 @@ __global__ void __launch_bounds__(kEhThreads, 1) elemat_hi_kernel(const OpParams
     double* Ko = Ke + (int64_t)(e - e0) * NN * NN;
     for (int tile = 0; tile < S::RT * S::CT; ++tile) {
       const int r0 = (tile / S::CT) * RB, c0 = (tile % S::CT) * CB;
-      const int wr0 = r0 + 32 * wr, wc0 = c0 + 32 * wc;   // the warp's sub-tile origin
+      const int wr0 = r0 + 32 * wr, wc0 = c0 + 8 * WCT * wc;   // the warp's sub-tile origin
       const bool live = wr0 < NN && wc0 < NN;
-      double acc[4][4][2];
+      double acc[4][WCT][2];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+        for (int c = 0; c < WCT; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
       stage(0, r0, c0, 0);
       __syncthreads();
       for (int ch = 0; ch < S::NCH; ++ch) {
         if (ch + 1 < S::NCH) stage(ch + 1, r0, c0, (ch + 1) & 1);   // overlaps this chunk's product
         if (live) {
           const double* Ms = STG + (ch & 1) * KR * MS + (lane & 3) * MS + 32 * wr + (lane >> 2);
-          const double* Ns = STG + 2 * KR * MS + (ch & 1) * KR * NS + (lane & 3) * NS + 32 * wc + (lane >> 2);
+          const double* Ns = STG + 2 * KR * MS + (ch & 1) * KR * NS + (lane & 3) * NS + 8 * WCT * wc + (lane >> 2);
 #pragma unroll
           for (int k0 = 0; k0 < KR; k0 += 4) {
-            double fa[4], fb[4];
+            double fa[4], fb[WCT];
 #pragma unroll
             for (int a = 0; a < 4; ++a) fa[a] = Ms[k0 * MS + 8 * a];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) fb[c] = Ns[k0 * NS + 8 * c];
+            for (int c = 0; c < WCT; ++c) fb[c] = Ns[k0 * NS + 8 * c];
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
-              for (int c = 0; c < 4; ++c) dmma884_hi(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+              for (int c = 0; c < WCT; ++c) dmma884_hi(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
           }
         }
         __syncthreads();   // buffer ch & 1 is restaged at ch + 2
@@ -231,7 +244,7 @@ __global__ void __launch_bounds__(kEhThreads, 1) elemat_hi_kernel(const OpParams
         for (int a = 0; a < 4; ++a) {
           const int i = wr0 + 8 * a + (lane >> 2);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < WCT; ++c) {
             const int j = wc0 + 8 * c + 2 * (lane & 3);
             if (i < NN && j < NN) Ko[(int64_t)i * NN + j] = acc[a][c][0];
             if (i < NN && j + 1 < NN) Ko[(int64_t)i * NN + j + 1] = acc[a][c][1];
