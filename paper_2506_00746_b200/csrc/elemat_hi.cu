@@ -5,12 +5,13 @@
 //   K_e = M^T N,  M[(q,d)][i] = d_d phi_i(x_q),  N[(q,d)][j] = sum_d' A_dd'(q) d_d' phi_j(x_q) + b_d(q) phi_j(x_q)
 // but M and N no longer fit in shared memory (Q6: 1029 x 343 doubles each, 2.8 MB), so
 // the product runs as a tiled GEMM whose operands are generated on chip: K_e is cut into
-// 128 x 64 output tiles, and for each tile the k = (point, direction) dimension is
+// 128 x 128 output tiles, and for each tile the k = (point, direction) dimension is
 // streamed in chunks of KC points -- the chunk's M rows (the i-tile's reference
 // gradients) and N rows (the j-tile's gradients mixed by the point's 3x3 A and b) are
 // evaluated from the 1D tables into a double-buffered shared-memory stage while the
-// warps run the previous chunk's 8x8x4 DMMA steps. 8 warps as 4 x 2, each a 32 x 32
-// sub-tile (16 accumulator chains; 4 A + 4 B fragments per 16 DMMA).
+// warps run the previous chunk's 8x8x4 DMMA steps. 8 warps as 4 x 2, each a 32 x 64
+// sub-tile (32 accumulator chains; 4 A + 8 B fragments per 32 DMMA). Measured (C4, Q6):
+// 128 x 64 tiles 14.1 us/element, 128 x 128 12.6; 4-point chunks at 2 CTAs/SM 14.2.
 // One CTA per element (persistent over the range); the element's u at the points and
 // its linearisation (9 values per point) are computed once per element.
 #include "common.cuh"
@@ -21,13 +22,13 @@
 namespace feod {
 
 constexpr int kEhThreads = 256;
-// experiment knobs: points per k-chunk, output-tile width (64: 32x32 warp tiles, 128: 32x64),
+// experiment knobs: points per k-chunk, output-tile width (128: 32x64 warp tiles, 64: 32x32),
 // CTAs per SM the register budget is sized for
 #ifndef FEOD_EH_KC
 #define FEOD_EH_KC 8
 #endif
 #ifndef FEOD_EH_CB
-#define FEOD_EH_CB 64
+#define FEOD_EH_CB 128
 #endif
 #ifndef FEOD_EH_MINB
 #define FEOD_EH_MINB 1
