@@ -51,7 +51,9 @@ struct EhShape {
   static constexpr int RT = (NN + RB - 1) / RB, CT = (NN + CB - 1) / CB;
   static constexpr int MS = RB + 4, NS = CB + 4;         // row strides = 4 (mod 16) doubles: conflict-free fragments
   static constexpr int STAGE = KR * (MS + NS);
-  static constexpr size_t SMEM = sizeof(double) * (2 * STAGE + 9 * Q + 4 * Q + NN + 2 * NQ * ND + NQ);
+  static constexpr int QP = NCH * KC;                    // points padded to whole chunks
+  static constexpr size_t SMEM = sizeof(double) * (2 * STAGE + 9 * Q + 4 * Q + NN + 2 * NQ * ND + NQ) + sizeof(int) * QP;
+  static_assert(kEhThreads % RB == 0 && kEhThreads % CB == 0, "a thread's tile column is loop-invariant");
   static_assert(2 * NQ * ND * ND + 3 * NQ * NQ * ND <= 9 * Q, "interpolation scratch fits in PW");
 };
 
@@ -71,6 +73,7 @@ __global__ void __launch_bounds__(kEhThreads, FEOD_EH_MINB) elemat_hi_kernel(con
   double* Bt = UE + NN;                   // [NQ][ND]
   double* Gt = Bt + NQ * ND;              // [NQ][ND]
   double* Wt = Gt + NQ * ND;              // [NQ]
+  int* PQ = reinterpret_cast<int*>(Wt + NQ);   // [QP] point q's table row offsets (x | y << 8 | z << 16), -1 past Q
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int wr = warp & 3, wc = warp >> 2;   // the warp's 32 x (8 WCT) sub-tile of the RB x CB output tile
@@ -80,6 +83,8 @@ __global__ void __launch_bounds__(kEhThreads, FEOD_EH_MINB) elemat_hi_kernel(con
     Gt[t] = T.G[t / ND][t % ND];
   }
   for (int t = tid; t < NQ; t += kEhThreads) Wt[t] = T.w[t];
+  for (int q = tid; q < S::QP; q += kEhThreads)
+    PQ[q] = q < Q ? (q % NQ) * ND | ((q / NQ) % NQ) * ND << 8 | (q / (NQ * NQ)) * ND << 16 : -1;
   __syncthreads();
 
   for (int e = e0 + blockIdx.x; e < e0 + ne; e += gridDim.x) {
@@ -166,36 +171,41 @@ __global__ void __launch_bounds__(kEhThreads, FEOD_EH_MINB) elemat_hi_kernel(con
       __syncthreads();
     }
 
-    // shape functions of node n at point q from the 1D tables: value and reference gradient
-    auto shape = [&](int q, int n, double& v, double& gx, double& gy, double& gz) {
-      const int qx = q % NQ, qy = (q / NQ) % NQ, qz = q / (NQ * NQ);
-      const int ia = n % ND, ib = (n / ND) % ND, ic = n / (ND * ND);
-      const double bx = Bt[qx * ND + ia], by = Bt[qy * ND + ib], bz = Bt[qz * ND + ic];
-      const double dx = Gt[qx * ND + ia], dy = Gt[qy * ND + ib], dz = Gt[qz * ND + ic];
+    // shape functions of node (ia, ib, ic) at the point with table offsets pk (PQ) from the
+    // 1D tables: value and reference gradient
+    auto shape = [&](int pk, int ia, int ib, int ic, double& v, double& gx, double& gy, double& gz) {
+      const int ox = (pk & 255) + ia, oy = ((pk >> 8) & 255) + ib, oz = (pk >> 16) + ic;
+      const double bx = Bt[ox], by = Bt[oy], bz = Bt[oz];
+      const double dx = Gt[ox], dy = Gt[oy], dz = Gt[oz];
       const double byz = by * bz;
       v = bx * byz;
       gx = dx * byz;
       gy = bx * dy * bz;
       gz = bx * by * dz;
     };
-    // stage chunk ch of output tile (r0, c0) into buffer b: k-row 3 qq + d of point q = KC ch + qq
-    auto stage = [&](int ch, int r0, int c0, int b) {
+    // stage chunk ch into buffer b: k-row 3 qq + d of point q = KC ch + qq. A thread's tile
+    // column (il = tid % RB of the M rows, tid % CB of the N rows) is fixed, so its node
+    // indices (mi, mj: a | b << 8 | c << 16, -1 outside the element) are computed per tile
+    auto stage = [&](int ch, int mi, int mj, int b) {
       double* Ms = STG + b * KR * MS;
       double* Ns = STG + 2 * KR * MS + b * KR * NS;
-      for (int t = tid; t < KC * RB; t += kEhThreads) {   // M^T rows: reference gradients of the i-tile
-        const int qq = t / RB, il = t % RB, q = KC * ch + qq, i = r0 + il;
+      const int il = tid % RB, jl = tid % CB;
+#pragma unroll
+      for (int m = 0; m < KC * RB / kEhThreads; ++m) {   // M^T rows: reference gradients of the i-tile
+        const int qq = tid / RB + m * (kEhThreads / RB), pk = PQ[KC * ch + qq];
         double v = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
-        if (q < Q && i < NN) shape(q, i, v, gx, gy, gz);
+        if (pk >= 0 && mi >= 0) shape(pk, mi & 255, (mi >> 8) & 255, mi >> 16, v, gx, gy, gz);
         Ms[(3 * qq + 0) * MS + il] = gx;
         Ms[(3 * qq + 1) * MS + il] = gy;
         Ms[(3 * qq + 2) * MS + il] = gz;
       }
-      for (int t = tid; t < KC * CB; t += kEhThreads) {   // N rows: A grad phi_j + b phi_j
-        const int qq = t / CB, jl = t % CB, q = KC * ch + qq, j = c0 + jl;
+#pragma unroll
+      for (int m = 0; m < KC * CB / kEhThreads; ++m) {   // N rows: A grad phi_j + b phi_j
+        const int qq = tid / CB + m * (kEhThreads / CB), q = KC * ch + qq, pk = PQ[q];
         double n0 = 0.0, n1 = 0.0, n2 = 0.0;
-        if (q < Q && j < NN) {
+        if (pk >= 0 && mj >= 0) {
           double v, gx, gy, gz;
-          shape(q, j, v, gx, gy, gz);
+          shape(pk, mj & 255, (mj >> 8) & 255, mj >> 16, v, gx, gy, gz);
           const double axx = PW[q], ayy = PW[Q + q], azz = PW[2 * Q + q], axy = PW[3 * Q + q],
                        axz = PW[4 * Q + q], ayz = PW[5 * Q + q];
           n0 = axx * gx + axy * gy + axz * gz + PW[6 * Q + q] * v;
@@ -207,10 +217,12 @@ __global__ void __launch_bounds__(kEhThreads, FEOD_EH_MINB) elemat_hi_kernel(con
         Ns[(3 * qq + 2) * NS + jl] = n2;
       }
     };
+    auto node = [](int n) { return n < NN ? n % ND | (n / ND) % ND << 8 | n / (ND * ND) << 16 : -1; };
 
     double* Ko = Ke + (int64_t)(e - e0) * NN * NN;
     for (int tile = 0; tile < S::RT * S::CT; ++tile) {
       const int r0 = (tile / S::CT) * RB, c0 = (tile % S::CT) * CB;
+      const int mi = node(r0 + tid % RB), mj = node(c0 + tid % CB);
       const int wr0 = r0 + 32 * wr, wc0 = c0 + 8 * WCT * wc;   // the warp's sub-tile origin
       const bool live = wr0 < NN && wc0 < NN;
       double acc[4][WCT][2];
@@ -218,10 +230,10 @@ __global__ void __launch_bounds__(kEhThreads, FEOD_EH_MINB) elemat_hi_kernel(con
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < WCT; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-      stage(0, r0, c0, 0);
+      stage(0, mi, mj, 0);
       __syncthreads();
       for (int ch = 0; ch < S::NCH; ++ch) {
-        if (ch + 1 < S::NCH) stage(ch + 1, r0, c0, (ch + 1) & 1);   // overlaps this chunk's product
+        if (ch + 1 < S::NCH) stage(ch + 1, mi, mj, (ch + 1) & 1);   // overlaps this chunk's product
         if (live) {
           const double* Ms = STG + (ch & 1) * KR * MS + (lane & 3) * MS + 32 * wr + (lane >> 2);
           const double* Ns = STG + 2 * KR * MS + (ch & 1) * KR * NS + (lane & 3) * NS + 8 * WCT * wc + (lane >> 2);

@@ -28,7 +28,8 @@ def main():
     out2 = torch.empty_like(u)
     g = torch.empty(w.n_elems, dtype=torch.float64, device="cuda")
     nn = (w.k + 1) ** 3
-    Ke = torch.empty((min(16384, w.n_elems), nn, nn), dtype=torch.float64, device="cuda") if w.k <= 3 else None
+    nem = min(16384 if w.k <= 3 else 512, w.n_elems)   # Q4..Q6: K_e up to 941 KB per element
+    Ke = torch.empty((nem, nn, nn), dtype=torch.float64, device="cuda")
     fns = {
         "residual": lambda: op.residual(u, out=out),
         "jvp": lambda: op.jvp(u, v, out=out),
@@ -39,8 +40,8 @@ def main():
         "linearize": lambda: op.linearize(u, out=out),
         "jvp_lin": lambda: op.jvp_lin(v, out=out),
         "jacobi_diag": lambda: op.jacobi_diag(out=out),
-        "elemat": lambda: op.element_matrices(u, 0, min(16384, w.n_elems), out=Ke),
-        "elm": lambda: op.element_matrices(u, 0, min(16384, w.n_elems), elm=True, out=Ke),
+        "elemat": lambda: op.element_matrices(u, 0, nem, out=Ke),
+        "elm": lambda: op.element_matrices(u, 0, nem, elm=True, out=Ke),
     }
     for c in calls:
         if c in ("jvp_lin", "jacobi_diag"):
