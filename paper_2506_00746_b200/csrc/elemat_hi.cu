@@ -9,9 +9,12 @@
 // streamed in chunks of KC points -- the chunk's M rows (the i-tile's reference
 // gradients) and N rows (the j-tile's gradients mixed by the point's 3x3 A and b) are
 // evaluated from the 1D tables into a double-buffered shared-memory stage while the
-// warps run the previous chunk's 8x8x4 DMMA steps. 8 warps as 4 x 2, each a 32 x 64
-// sub-tile (32 accumulator chains; 4 A + 8 B fragments per 32 DMMA). Measured (C4, Q6):
-// 128 x 64 tiles 14.1 us/element, 128 x 128 12.6; 4-point chunks at 2 CTAs/SM 14.2.
+// warps run the previous chunk's 8x8x4 DMMA steps. 16 warps as 4 x 4, each a 32 x 32
+// sub-tile (16 accumulator chains; 4 A + 4 B fragments per 16 DMMA): ptxas issues a warp's
+// DMMAs ~16 cycles apart, so the FP64 pipe needs several warps per scheduler in their DMMA
+// phase while others stage. Measured (C4, Q6, us/element): 8 warps with 128 x 64 tiles
+// 14.1, 128 x 128 12.6, + hoisted index math 11.2, 16 warps 10.2; 4-point chunks at two
+// CTAs per SM 14.2.
 // One CTA per element (persistent over the range); the element's u at the points and
 // its linearisation (9 values per point) are computed once per element.
 #include "common.cuh"
@@ -21,7 +24,10 @@
 
 namespace feod {
 
-constexpr int kEhThreads = 256;
+#ifndef FEOD_EH_WARPS
+#define FEOD_EH_WARPS 16
+#endif
+constexpr int kEhThreads = 32 * FEOD_EH_WARPS;   // warps as 4 x (WARPS / 4) over the output tile
 // experiment knobs: points per k-chunk, output-tile width (128: 32x64 warp tiles, 64: 32x32),
 // CTAs per SM the register budget is sized for
 #ifndef FEOD_EH_KC
@@ -47,7 +53,7 @@ struct EhShape {
   static_assert(KR % 4 == 0, "k-chunk of whole DMMA k-steps");
   static constexpr int NCH = (Q + KC - 1) / KC;
   static constexpr int RB = 128, CB = FEOD_EH_CB;        // output tile
-  static constexpr int WCT = CB / 16;                    // 8-column tiles per warp (warps as 4 x 2)
+  static constexpr int WCT = CB / (2 * FEOD_EH_WARPS);  // 8-column tiles per warp (warps as 4 x WARPS/4)
   static constexpr int RT = (NN + RB - 1) / RB, CT = (NN + CB - 1) / CB;
   static constexpr int MS = RB + 4, NS = CB + 4;         // row strides = 4 (mod 16) doubles: conflict-free fragments
   static constexpr int STAGE = KR * (MS + NS);
