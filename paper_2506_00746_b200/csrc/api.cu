@@ -630,6 +630,9 @@ extern "C" int feod_apply_host(feod_handle h, int op, const double* in0, const d
 // two device staging sets, uploads on cst, the operator on the handle's stream, downloads
 // on dst. Step b + 1's uploads run while step b computes and downloads (the host link is
 // full duplex), so in steady state a step costs max(H2D, D2H, operator) instead of their sum.
+// A set's input half is reused as soon as step b-2's operator has read it and its output
+// half once step b-2's results are down: with one release point per set the period would be
+// (H2D + operator + D2H) / 2 instead.
 extern "C" int feod_apply_host_batch(feod_handle h, int op, int64_t nbatch, const double* const* in0,
                                      const double* const* in1, double* const* out) {
   if (!h || nbatch < 0 || (nbatch > 0 && (!in0 || !out || (op != 0 && !in1))))
@@ -662,21 +665,21 @@ extern "C" int feod_apply_host_batch(feod_handle h, int op, int64_t nbatch, cons
     double* d0 = s ? h->stage2 : h->stage;
     double *d1 = d0 + len, *d2 = d0 + 2 * len, *d3 = d0 + 3 * len;
     cudaEvent_t up = h->bev[3 * s], rdy_r = h->bev[3 * s + 1], rdy = h->bev[3 * s + 2], down = h->bdown[s];
-    if (b >= 2) CK(cudaStreamWaitEvent(h->cst, down, 0), "feod_apply_host_batch");   // set s free
+    // inputs of set s are free once step b-2's operator ran, its outputs once they are downloaded
+    if (b >= 2) CK(cudaStreamWaitEvent(h->cst, rdy, 0), "feod_apply_host_batch");
     CK(cudaMemcpyAsync(d0, in0[b], nb_in, cudaMemcpyHostToDevice, h->cst), "feod_apply_host_batch: H2D");
     if (op != 0) CK(cudaMemcpyAsync(d1, in1[b], nb_in, cudaMemcpyHostToDevice, h->cst), "feod_apply_host_batch: H2D");
     CK(cudaEventRecord(up, h->cst), "feod_apply_host_batch");
     CK(cudaStreamWaitEvent(h->st, up, 0), "feod_apply_host_batch");
+    if (b >= 2) CK(cudaStreamWaitEvent(h->st, down, 0), "feod_apply_host_batch");
     int rc = op == 0 || op == 4 ? feod_residual(h, d0, d2)
              : op == 1          ? feod_jvp(h, d0, d1, d2)
              : op == 2          ? feod_design_grad(h, d0, d1, d2)
                                 : feod_vjp(h, d0, d1, d2);
     if (rc != FEOD_OK) return rc;
     CK(cudaEventRecord(rdy_r, h->st), "feod_apply_host_batch");
-    if (op == 4) {
-      if ((rc = feod_jvp(h, d0, d1, d3)) != FEOD_OK) return rc;
-      CK(cudaEventRecord(rdy, h->st), "feod_apply_host_batch");
-    }
+    if (op == 4 && (rc = feod_jvp(h, d0, d1, d3)) != FEOD_OK) return rc;
+    CK(cudaEventRecord(rdy, h->st), "feod_apply_host_batch");
     CK(cudaStreamWaitEvent(h->dst, rdy_r, 0), "feod_apply_host_batch");   // r downloads while the JVP runs
     CK(cudaMemcpyAsync(out[b], d2, nb_out, cudaMemcpyDeviceToHost, h->dst), "feod_apply_host_batch: D2H");
     if (op == 4) {
