@@ -287,6 +287,9 @@ CASES13 = [
     dict(n=3, k=1, model=PL, perturbed=True, faces=63, p=4.0, eps=1e-3),
     dict(n=2, k=2, model=HT, perturbed=False, faces=1, p=2.0, eps=0.0),
     dict(n=2, k=3, model=NL, perturbed=True, faces=63, p=2.0, eps=0.0),
+    # Q4 / Q5 element tangents (the K9b / ELM orders) pinned the same way
+    dict(n=1, k=4, model=NL, perturbed=True, faces=1, p=2.0, eps=0.0),
+    dict(n=1, k=5, model=PL, perturbed=True, faces=2, p=3.0, eps=1e-2),
 ]
 
 

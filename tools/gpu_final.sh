@@ -3,7 +3,7 @@
 # per-config bench lines, the ncu launch list of the default bench command, and ncu
 # --set full captures of the Q6 tensor-core kernels after the last changes.
 set -u
-O=gpurun_out/r02f
+O=${O:-gpurun_out/r02f}
 mkdir -p $O
 timeout 1500 python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
@@ -22,4 +22,6 @@ mkdir -p gpurun_out/prof
 bash tools/gpu_prof.sh c4final_jvp C4 jvp q6tc_perl
 bash tools/gpu_prof.sh c4final_res C4 residual q6tc_perl
 bash tools/gpu_prof.sh c4final_asm C4 jvp evec_assemble
+bash tools/gpu_prof.sh c4final_emhi C4 elemat elemat_hi 1
 cp gpurun_out/prof/c4final_* $O/ 2>/dev/null
+python tools/link_bw.py > $O/link_bw.json 2>&1
