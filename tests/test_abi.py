@@ -71,6 +71,9 @@ def test_argument_validation_without_gpu(lib):
     assert b"rho" in lib.feod_last_error() or len(lib.feod_last_error()) > 0
     for fn, nargs in (("feod_residual", 3), ("feod_jvp", 4), ("feod_design_grad", 4), ("feod_destroy", 1)):
         assert getattr(lib, fn)(*([None] * nargs)) == fe.FEOD_EINVAL
+    assert lib.feod_element_matrices(None, None, 0, 1, 0, None) == fe.FEOD_EINVAL
+    assert lib.feod_apply_host(None, 4, None, None, None) == fe.FEOD_EINVAL
+    assert lib.feod_apply_host_batch(None, 4, 2, None, None, None) == fe.FEOD_EINVAL
     assert lib.feod_num_dofs(None) == -1
 
 
