@@ -45,6 +45,15 @@ FEOD_DEV Frag contract_cols(const Frag& m, const double w[2], Frag acc) {
   return acc;
 }
 
+// (M W)^T without data movement: the A and B operand layouts of m8n8k4 are each other's
+// transposes, so the same lane registers with the operands swapped give
+// out[m][n] = sum_c W[c][m] M[n][c] -- the column contraction landing transposed
+FEOD_DEV Frag contract_cols_t(const Frag& m, const double w[2], Frag acc) {
+  dmma(acc.v[0], acc.v[1], w[0], m.v[0]);
+  dmma(acc.v[0], acc.v[1], w[1], m.v[1]);
+  return acc;
+}
+
 // M^T in D layout: entry (r', c') = M[c'][r'] lives in lane 4 c' + r'/2, register r' % 2
 FEOD_DEV Frag transpose(const Frag& m, int lane) {
   Frag o;
@@ -147,8 +156,8 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
   const Frag zero = {{0.0, 0.0}};
   constexpr bool SMT = FEOD_Q6_SMT && (MODE != MODE_PAJVP || FEOD_Q6_SMT_PA);
   // shared memory: [stored linearisation per warp + mbarriers (PAJVP) | staged fields] [transpose scratch]
-  constexpr size_t LEAD_DOUBLES = (MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0)
-                                      ? (size_t)WARPS * NL * 343 + WARPS
+  constexpr size_t LEAD_DOUBLES = (MODE == MODE_PAJVP && (NL * 49 * sizeof(double)) % 16 == 0)
+                                      ? (size_t)WARPS * NL * 343 + WARPS * 8
                                   : FEOD_Q6_FSTAGE ? (size_t)WARPS * NIN * 344 : 0;
   constexpr int TBUF = MODE == MODE_PAJVP ? 1 : 2;   // transpose scratch buffers per warp
   double* const tscr = q6sm + LEAD_DOUBLES + (size_t)wid * (TBUF * 8 * 18);
@@ -174,31 +183,37 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
       }
     }
 #pragma unroll
-    for (int c = 0; c < 7; ++c) Ep[c] = contract_cols(tr(contract_cols(X[c], WB, zero)), WB, zero);
+    for (int c = 0; c < 7; ++c) Ep[c] = contract_cols(contract_cols_t(X[c], WB, zero), WB, zero);
   };
 
-  constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
-  constexpr uint32_t LIN_BYTES = NL * 343 * sizeof(double);
+  constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 49 * sizeof(double)) % 16 == 0;
   double* const lbuf = q6sm + (size_t)wid * (NL * 343);
-  uint64_t* const lbar = reinterpret_cast<uint64_t*>(q6sm + (size_t)WARPS * (NL * 343)) + wid;
+  // PAJVP: the element's stored linearisation arrives plane by plane ([l][NL][j][i], 2352 B
+  // per point plane at NL = 6) through a ring of 7 plane slots per warp, one mbarrier each:
+  // as soon as plane l of this element is consumed, the NEXT element's plane l is issued into
+  // the same slot, so every copy has a whole element's time to land (one copy of the whole
+  // element after the last plane left the load exposed: C4 jvp_lin kernel ~195 us against
+  // ~85 us of HBM and ~82 us of FP64 pipe time)
+  constexpr uint32_t PLANE_BYTES = NL * 49 * sizeof(double);
+  uint64_t* const lbar = reinterpret_cast<uint64_t*>(q6sm + (size_t)WARPS * (NL * 343)) + 8 * wid;
   uint32_t lphase = 0;
-  auto issue_lin = [&](int64_t en) {
+  auto issue_plane = [&](int64_t en, int l) {
     if constexpr (TMA_LIN) {
       if (lane == 0 && en < E) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(lbar, LIN_BYTES);
-        mbar_arrive(lbar);
-        bulk_g2s(lbuf, P.lin + en * (NL * 343), LIN_BYTES, lbar);
+        mbar_expect_tx(lbar + l, PLANE_BYTES);
+        mbar_arrive(lbar + l);
+        bulk_g2s(lbuf + l * (NL * 49), P.lin + en * (NL * 343) + l * (NL * 49), PLANE_BYTES, lbar + l);
       }
     }
   };
   if constexpr (TMA_LIN) {
     if (lane == 0) {
-      mbar_init(lbar, 1);
+      for (int l = 0; l < 7; ++l) mbar_init(lbar + l, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    issue_lin((int64_t)blockIdx.x * WARPS + wid);
+    for (int l = 0; l < 7; ++l) issue_plane((int64_t)blockIdx.x * WARPS + wid, l);
   }
   // the next element's input fields: prefetched into L2 right after this element's x-y
   // phase (49 node rows per field); FEOD_Q6_FSTAGE=1 stages them in shared memory by
@@ -251,10 +266,6 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
       const int64_t en = e + (int64_t)gridDim.x * WARPS;
       if (lane == 0 && en < E) prefetch_l2_bulk(P.lin + en * (NL * 343), NL * 343 * sizeof(double));
     }
-    if constexpr (TMA_LIN) {
-      mbar_wait(lbar, lphase);
-      lphase ^= 1u;
-    }
     Frag S[7];
 #pragma unroll
     for (int c = 0; c < 7; ++c) S[c] = zero;
@@ -276,9 +287,10 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
           Uzl[f].v[t] = b;
         }
         Uyl[f] = contract_cols(Ul[f], WD, zero);                                   // d/dy: [i][j']
-        Uxl[f] = tr(contract_cols(tr(Ul[f]), WD, zero));   // d/dx: [i'][j]
+        Uxl[f] = contract_cols_t(tr(Ul[f]), WD, zero);     // d/dx: [i'][j]
       }
       Frag Fx, Fy, Fz, V;
+      if constexpr (TMA_LIN) mbar_wait(lbar + l, lphase);
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int j = 2 * q + t;
@@ -312,10 +324,12 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
         Fz.v[t] = F0[2];
         V.v[t] = value_channel(MODE, 0) ? F0[3] : 0.0;
       }
+      if constexpr (TMA_LIN) {   // plane l's slot is read: refill it with the next element's plane l
+        __syncwarp();
+        issue_plane(e + (int64_t)gridDim.x * WARPS, l);
+      }
       // B^T at plane l: R_l = V + Dx^T Fx + Dy^T Fy, then z into the node-plane accumulators
-      Frag R = tr(contract_cols(tr(Fx), WDt, zero));
-      R.v[0] += V.v[0];
-      R.v[1] += V.v[1];
+      Frag R = contract_cols_t(tr(Fx), WDt, V);
       R = contract_cols(Fy, WDt, R);
 #pragma unroll
       for (int c = 0; c < 7; ++c)
@@ -324,16 +338,13 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
           S[c].v[t] = FOLD ? fma(T.Bw[l][c], R.v[t], fma(T.Gw[l][c], Fz.v[t], S[c].v[t]))
                            : fma(T.B[l][c], R.v[t], fma(T.G[l][c], Fz.v[t], S[c].v[t]));
     }
-    if constexpr (TMA_LIN) {   // buffer reads done: stage the next element's values
-      __syncwarp();
-      issue_lin(e + (int64_t)gridDim.x * WARPS);
-    }
+    if constexpr (TMA_LIN) lphase ^= 1u;
     const int64_t LXd = 7 * (int64_t)P.nx, LYd = 7 * (int64_t)P.ny;
     double* out = ev + ((int64_t)(7 * ez) * LYd + 7 * ey) * LXd + 7 * ex;
 #pragma unroll
     for (int c = 0; c < 7; ++c) {
-      const Frag ty = contract_cols(S[c], WBt, zero);                      // [i][b]
-      const Frag nd = contract_cols(tr(ty), WBt, zero);       // [b][a]
+      const Frag ty = contract_cols_t(S[c], WBt, zero);                    // [b][i]
+      const Frag nd = contract_cols(ty, WBt, zero);                        // [b][a]
       if (rowv) {
         double* o = out + ((int64_t)c * LYd + r) * LXd;
 #pragma unroll
@@ -348,8 +359,8 @@ template <int MODE, int MODEL>
 static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double* in0, const double* in1, double* ev,
                                double* out, const double* dotx, double* dpart, cudaStream_t st) {
   constexpr int NL = lin_values(MODEL);
-  constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 343 * sizeof(double)) % 16 == 0;
-  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS +
+  constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 49 * sizeof(double)) % 16 == 0;
+  constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + 8 * sizeof(uint64_t)) * q6::WARPS +
                                         (FEOD_Q6_SMT && FEOD_Q6_SMT_PA ? sizeof(double) * q6::WARPS * 1 * 8 * 18 : 0)
                                   : sizeof(double) * q6::WARPS *
                                         ((FEOD_Q6_FSTAGE ? q6_nin<MODE>() * 344 : 0) + (FEOD_Q6_SMT ? 2 * 8 * 18 : 0));
@@ -412,8 +423,8 @@ template <int NL>
 __global__ void __launch_bounds__(32 * q6::WARPS, 3)
 q6tc_diag_kernel(const OpParams P, const Tables T, double* __restrict__ ev) {
   using namespace q6;
-  constexpr bool TMA = (NL * 343 * sizeof(double)) % 16 == 0;
-  constexpr uint32_t LIN_BYTES = NL * 343 * sizeof(double);
+  constexpr bool TMA = (NL * 49 * sizeof(double)) % 16 == 0;
+  constexpr uint32_t PLANE_BYTES = NL * 49 * sizeof(double);
   extern __shared__ __align__(16) double q6sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int r = lane >> 2, q = lane & 3;
@@ -434,76 +445,79 @@ q6tc_diag_kernel(const OpParams P, const Tables T, double* __restrict__ ev) {
   constexpr int TY[9] = {0, 1, 0, 2, 0, 2, 0, 2, 0};
   constexpr int TZ[9] = {0, 0, 1, 0, 2, 2, 0, 0, 2};
   // z tables in shared memory (broadcast reads; kept out of registers): zt[kind][l][c]
-  double* const zt = q6sm + (TMA ? (size_t)WARPS * (NL * 343) + WARPS : 0);
+  double* const zt = q6sm + (TMA ? (size_t)WARPS * (NL * 343) + WARPS * 8 : 0);
   for (int k = threadIdx.x; k < 3 * 49; k += blockDim.x) {
     const int kind = k / 49, l = (k % 49) / 7, c = k % 7;
     const double b = T.B[l][c], g = T.G[l][c];
     zt[k] = kind == 0 ? b * b : kind == 1 ? g * g : g * b;
   }
   __syncthreads();
+  // the stored linearisation through the same ring of 7 point-plane slots per warp as
+  // q6tc_perl_kernel<MODE_PAJVP>: plane l of the next element is issued as soon as plane l
+  // of this one is consumed (the loops run plane-outer, term-inner for that)
   double* const lbuf = q6sm + (size_t)wid * (NL * 343);
-  uint64_t* const lbar = reinterpret_cast<uint64_t*>(q6sm + (size_t)WARPS * (NL * 343)) + wid;
+  uint64_t* const lbar = reinterpret_cast<uint64_t*>(q6sm + (size_t)WARPS * (NL * 343)) + 8 * wid;
   uint32_t lphase = 0;
-  auto issue = [&](int64_t en) {
+  auto issue_plane = [&](int64_t en, int l) {
     if constexpr (TMA) {
       if (lane == 0 && en < E) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(lbar, LIN_BYTES);
-        mbar_arrive(lbar);
-        bulk_g2s(lbuf, P.lin + en * (NL * 343), LIN_BYTES, lbar);
+        mbar_expect_tx(lbar + l, PLANE_BYTES);
+        mbar_arrive(lbar + l);
+        bulk_g2s(lbuf + l * (NL * 49), P.lin + en * (NL * 343) + l * (NL * 49), PLANE_BYTES, lbar + l);
       }
     }
   };
   if constexpr (TMA) {
     if (lane == 0) {
-      mbar_init(lbar, 1);
+      for (int l = 0; l < 7; ++l) mbar_init(lbar + l, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    issue((int64_t)blockIdx.x * WARPS + wid);
+    for (int l = 0; l < 7; ++l) issue_plane((int64_t)blockIdx.x * WARPS + wid, l);
   }
   for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
     int ex, ey, ez;
     q6_coords(P, e, ex, ey, ez);
     const double* linp = P.lin + e * (NL * 343);
-    if constexpr (TMA) {
-      mbar_wait(lbar, lphase);
-      lphase ^= 1u;
-    }
     Frag Dg[7];
 #pragma unroll
     for (int c = 0; c < 7; ++c) Dg[c] = zero;
 #pragma unroll 1
-    for (int t = 0; t < NL; ++t) {
-      const int ky = TY[t], kx = TX[t];
-      const double wy[2] = {ky == 0 ? W0[0] : ky == 1 ? W1[0] : W2[0], ky == 0 ? W0[1] : ky == 1 ? W1[1] : W2[1]};
-      const double wx[2] = {kx == 0 ? W0[0] : kx == 1 ? W1[0] : W2[0], kx == 0 ? W0[1] : kx == 1 ? W1[1] : W2[1]};
-      const double wt = t >= 3 && t < 6 ? 2.0 : 1.0;   // off-diagonal A terms count twice
-      const double* ztt = zt + 49 * TZ[t];
+    for (int l = 0; l < 7; ++l) {
+      if constexpr (TMA) mbar_wait(lbar + l, lphase);
+      Frag A[NL];
 #pragma unroll
-      for (int l = 0; l < 7; ++l) {
-        Frag A;
+      for (int t = 0; t < NL; ++t)
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
           const int o = (l * NL + t) * 49 + (2 * q + s2) * 7 + r;
-          A.v[s2] = !(rowv && colv[s2]) ? 0.0 : TMA ? lbuf[o] : __ldcs(linp + o);
+          A[t].v[s2] = !(rowv && colv[s2]) ? 0.0 : TMA ? lbuf[o] : __ldcs(linp + o);
         }
-        const Frag yb = contract_cols(A, wy, zero);                          // [i][b]
-        Frag ba = contract_cols(transpose(yb, lane), wx, zero);              // [b][a]
+      if constexpr (TMA) {   // plane l's slot is in registers: refill it with the next element's plane l
+        __syncwarp();
+        issue_plane(e + (int64_t)gridDim.x * WARPS, l);
+      }
+#pragma unroll
+      for (int t = 0; t < NL; ++t) {
+        const int ky = TY[t], kx = TX[t];
+        const double* wy = ky == 0 ? W0 : ky == 1 ? W1 : W2;
+        const double* wx = kx == 0 ? W0 : kx == 1 ? W1 : W2;
+        const double wt = t >= 3 && t < 6 ? 2.0 : 1.0;   // off-diagonal A terms count twice
+        const double* ztt = zt + 49 * TZ[t] + l * 7;
+        const Frag yb = contract_cols_t(A[t], wy, zero);                     // [b][i]
+        Frag ba = contract_cols(yb, wx, zero);                               // [b][a]
         ba.v[0] *= wt;
         ba.v[1] *= wt;
 #pragma unroll
         for (int c = 0; c < 7; ++c) {
-          const double tz = ztt[l * 7 + c];
+          const double tz = ztt[c];
 #pragma unroll
           for (int s2 = 0; s2 < 2; ++s2) Dg[c].v[s2] = fma(tz, ba.v[s2], Dg[c].v[s2]);
         }
       }
     }
-    if constexpr (TMA) {
-      __syncwarp();
-      issue(e + (int64_t)gridDim.x * WARPS);
-    }
+    if constexpr (TMA) lphase ^= 1u;
     const int64_t LXd = 7 * (int64_t)P.nx, LYd = 7 * (int64_t)P.ny;
     double* out = ev + ((int64_t)(7 * ez) * LYd + 7 * ey) * LXd + 7 * ex;
 #pragma unroll
@@ -520,8 +534,8 @@ q6tc_diag_kernel(const OpParams P, const Tables T, double* __restrict__ ev) {
 
 template <int NL>
 static cudaError_t q6tc_diag_t(const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st) {
-  constexpr bool TMA = (NL * 343 * sizeof(double)) % 16 == 0;
-  constexpr size_t smem = (TMA ? (sizeof(double) * NL * 343 + sizeof(uint64_t)) * q6::WARPS : 0) + sizeof(double) * 3 * 49;
+  constexpr bool TMA = (NL * 49 * sizeof(double)) % 16 == 0;
+  constexpr size_t smem = (TMA ? (sizeof(double) * NL * 343 + 8 * sizeof(uint64_t)) * q6::WARPS : 0) + sizeof(double) * 3 * 49;
   const void* kfn = (const void*)q6tc_diag_kernel<NL>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
