@@ -222,6 +222,14 @@ FEOD_API int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg_i
  * the same arguments every step, the per-call scheduling state lives on the device).
  * enable: 0 or 1. A capture that fails falls back to direct launches. */
 FEOD_API int feod_set_cg_graphs(feod_handle h, int enable);
+/* Newton-CG option: on the Q6 tensor-core path (k = 6,
+ * affine mesh) fuse the CG update into the operator call -- p^T J p is formed element by
+ * element in the operator kernel and r -= alpha J p (with the r.z partials) in the assembly
+ * of its element vector, so J p is never written to or re-read from HBM and the separate
+ * update launch disappears (default on; other paths ignore it). Fixed summation orders:
+ * results are reproducible run to run, and agree with the unfused loop up to rounding
+ * order. enable: 0 or 1; FEOD_EINVAL otherwise. */
+FEOD_API int feod_set_cg_fusion(feod_handle h, int enable);
 /* Number of CG graph replays so far (diagnostic; -1 on a null handle). */
 FEOD_API int64_t feod_cg_graph_launches(feod_handle h);
 /* Newton-CG Jacobian: 0 (default) matrix-free feod_jvp at the current u;   *

@@ -31,7 +31,7 @@ EXPORTS = ("feod_create", "feod_destroy", "feod_set_stream", "feod_set_rho", "fe
            "feod_residual", "feod_jvp", "feod_jvp_res", "feod_vjp", "feod_linearize", "feod_jvp_lin",
            "feod_set_newton_linearization", "feod_brick_shape", "feod_jacobi_diag", "feod_adjoint_solve", "feod_element_matrices",
            "feod_design_grad", "feod_res_design_grad", "feod_apply_host", "feod_apply_host_batch", "feod_newton_cg",
-           "feod_set_cg_graphs", "feod_cg_graph_launches",
+           "feod_set_cg_graphs", "feod_set_cg_fusion", "feod_cg_graph_launches",
            "feod_dot", "feod_profile_next", "feod_last_error", "feod_version")
 
 
@@ -90,6 +90,7 @@ def load_library(path: str = LIB_PATH):
     lib.feod_apply_host_batch.argtypes = [vp, ctypes.c_int, i64, vp, vp, vp]
     lib.feod_newton_cg.argtypes = [vp, dp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     lib.feod_set_cg_graphs.argtypes = [vp, ctypes.c_int]
+    lib.feod_set_cg_fusion.argtypes = [vp, ctypes.c_int]
     lib.feod_cg_graph_launches.argtypes = [vp]
     lib.feod_cg_graph_launches.restype = i64
     lib.feod_dot.argtypes = [vp, dp, dp, i64, dp]
@@ -349,6 +350,10 @@ class Operator:
     def set_cg_graphs(self, enable):
         """Capture the CG iterations of feod_newton_cg as a CUDA graph (default on)."""
         _check(self.lib.feod_set_cg_graphs(self.h, 1 if enable else 0))
+
+    def set_cg_fusion(self, enable):
+        """Fuse the CG update into the Q6 tensor-core operator call of feod_newton_cg (default on)."""
+        _check(self.lib.feod_set_cg_fusion(self.h, 1 if enable else 0))
 
     def cg_graph_launches(self):
         return int(self.lib.feod_cg_graph_launches(self.h))

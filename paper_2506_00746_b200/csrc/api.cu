@@ -59,6 +59,11 @@ struct feod_op {
   const double* dot_x = nullptr;
   double* dot_part = nullptr;
   bool dot_fused = false;
+  // Newton-CG: when set, a Q6 tensor-core operator call also does the CG update behind its
+  // assembly (kernels.h CgFuse) and sets cg_fused; cleared by the call
+  const CgFuse* cg_fuse = nullptr;
+  bool cg_fused = false;
+  bool cg_fusion = true;   // feod_set_cg_fusion
   cudaEvent_t prof_begin = nullptr, prof_end = nullptr;   // one-shot profiling hook
   // Newton-CG: the CG iterations captured as a CUDA graph (on gst), replayed per step
   bool cg_graphs = true, cg_graph_failed = false;
@@ -356,10 +361,14 @@ static int run_op(feod_handle h, int mode, const double* in0, const double* in1,
       h->evec = nullptr;
       return fail(FEOD_ENOMEM, std::string(name) + ": element vector");
     }
-    cudaError_t e = q6tc_run(mode, h->coeffs.model, h->P, h->T, in0, in1, h->evec, out0, h->dot_x, h->dot_part, h->st);
+    const CgFuse* fuse = (mode == MODE_JVP || mode == MODE_PAJVP) ? h->cg_fuse : nullptr;
+    cudaError_t e = q6tc_run(mode, h->coeffs.model, h->P, h->T, in0, in1, h->evec, out0, fuse ? nullptr : h->dot_x,
+                             fuse ? nullptr : h->dot_part, h->st, fuse);
     h->dot_fused = h->dot_x != nullptr;
+    h->cg_fused = fuse != nullptr;
     h->dot_x = nullptr;
     h->dot_part = nullptr;
+    h->cg_fuse = nullptr;
     if (pe) cudaEventRecord(pe, h->st);
     return e == cudaSuccess ? FEOD_OK : cuda_fail(e, name);
   }
@@ -731,16 +740,23 @@ extern "C" int feod_newton_cg(feod_handle h, double* u, int newton_steps, int cg
       double* rr_old = sc + ((it & 1) ? 2 : 0);
       double* rr_new = sc + ((it & 1) ? 0 : 2);
       // p.Ap: fused into the operator's assembly where the path has one (Q6), else a pass
+      // ... and, on the Q6 tensor-core path, the whole update behind the assembly (CgFuse:
+      // Ap is then never written; r, the r.z partials, p.Ap and the breakdown flag are)
+      const CgFuse fz{rr_old, part, sc + 1, r, part2, bad, pre};
       h->dot_x = p;
       h->dot_part = part;
       h->dot_fused = false;
+      h->cg_fuse = h->cg_fusion ? &fz : nullptr;
+      h->cg_fused = false;
       const int rc = h->newton_lin ? feod_jvp_lin(h, p, Ap) : feod_jvp(h, u, p, Ap);
-      const bool fused = h->dot_fused;
+      const bool fused = h->dot_fused, updated = h->cg_fused;
       h->dot_x = nullptr;
       h->dot_part = nullptr;
+      h->cg_fuse = nullptr;
+      h->cg_fused = false;
       if (rc) { h->st = keep; return rc; }
-      cudaError_t e = fused ? cudaSuccess : dot_partial(p, Ap, N, part, st);
-      if (e == cudaSuccess) e = cg_update(rr_old, part, sc + 1, Ap, r, N, part2, bad, st, pre);
+      cudaError_t e = (fused || updated) ? cudaSuccess : dot_partial(p, Ap, N, part, st);
+      if (e == cudaSuccess && !updated) e = cg_update(rr_old, part, sc + 1, Ap, r, N, part2, bad, st, pre);
       if (e == cudaSuccess) e = cg_dir(part2, rr_new, rr_old, sc + 1, r, p, d, N, st, pre);
       if (e != cudaSuccess) { h->st = keep; return cuda_fail(e, "feod_newton_cg: CG"); }
     }
@@ -816,6 +832,13 @@ extern "C" int feod_set_cg_graphs(feod_handle h, int enable) {
   if (!h || enable < 0 || enable > 1) return fail(FEOD_EINVAL, "feod_set_cg_graphs: bad argument");
   h->cg_graphs = enable != 0;
   h->cg_graph_failed = false;
+  return FEOD_OK;
+}
+
+extern "C" int feod_set_cg_fusion(feod_handle h, int enable) {
+  if (!h || enable < 0 || enable > 1) return fail(FEOD_EINVAL, "feod_set_cg_fusion: bad argument");
+  h->cg_fusion = enable != 0;
+  if (h->cg_exec) { cudaGraphExecDestroy(h->cg_exec); h->cg_exec = nullptr; }   // recapture with the other body
   return FEOD_OK;
 }
 

@@ -38,15 +38,39 @@ FEOD_DEV int evec_cands(int G, int ne, int* c) {
 
 constexpr int kAsmThreads = 256;
 constexpr int kAsmUnroll = 8;
+constexpr int kFuseUnroll = 4;
 
-template <int K>
+// FUSE (Newton-CG, kernels.h CgFuse): the row's assembled values update r instead of going
+// to out, and the partials are those of r.z; alpha from the operator kernel's p.Ap partials
+// (the same thread mapping and tree as blas1.cu's reduce_partials, in every CTA)
+template <int K, bool FUSE>
 __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
                                                                      double* __restrict__ out,
                                                                      const double* __restrict__ dotx,
-                                                                     double* __restrict__ dpart, double dirval) {
+                                                                     double* __restrict__ dpart, double dirval,
+                                                                     const CgFuse F) {
   constexpr int ND = K + 1;
   extern __shared__ __align__(16) double asm_sm[];
   double acc = 0.0;
+  double alpha = 0.0;
+  if constexpr (FUSE) {
+    static_assert(kAsmThreads == 256, "the reduction tree below is blas1.cu's (256 threads)");
+    __shared__ double sh[kAsmThreads];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < kRedBlocks; i += kAsmThreads) a += F.pAp_part[i];
+    sh[threadIdx.x] = a;
+    __syncthreads();
+    for (int s = kAsmThreads / 2; s > 0; s >>= 1) {
+      if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+      __syncthreads();
+    }
+    const double den = sh[0];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *F.pAp = den;
+      if (!(den > 0.0)) *F.bad = 1;
+    }
+    alpha = *F.rr / den;
+  }
   const int LX = ND * P.nx;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* const t = asm_sm + (size_t)wid * LX;
@@ -61,6 +85,12 @@ __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpPara
     int ns = 0;
     for (int kz = 0; kz < nzc; ++kz)
       for (int ky = 0; ky < nyc; ++ky) src[ns++] = ev + ((int64_t)cz[kz] * LYd + cy[ky]) * LX;
+    if constexpr (FUSE) {   // the row of r (and of the diagonal) on its way to L2 while stage 1 runs
+      for (int X = 16 * lane; X < P.Mx; X += 16 * 32) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(F.r + (int64_t)P.Mx * YZ + X));
+        if (F.diag) asm volatile("prefetch.global.L2 [%0];" ::"l"(F.diag + (int64_t)P.Mx * YZ + X));
+      }
+    }
     for (int X0 = 0; X0 < LX; X0 += 32 * kAsmUnroll) {
       double v[kAsmUnroll][4];
 #pragma unroll
@@ -79,19 +109,46 @@ __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpPara
     const bool dyz = ((P.faces & 4u) && Y == 0) || ((P.faces & 8u) && Y == P.My - 1) ||
                      ((P.faces & 16u) && Z == 0) || ((P.faces & 32u) && Z == P.Mz - 1);
     double* orow = out + (int64_t)P.Mx * YZ;
-    for (int X = lane; X < P.Mx; X += 32) {
+    auto row_sum = [&](int X) {
       const int e = X / K, a = X - K * e;
       double s;
       if (a == 0 && e > 0 && e < P.nx) s = t[ND * e - 1] + t[ND * e];   // left element first
       else s = t[X + min(e, P.nx - 1)];   // X = K nx: the last element's node K, X' = ND nx - 1
       const bool dir = dyz || ((P.faces & 1u) && X == 0) || ((P.faces & 2u) && X == P.Mx - 1);
-      const double o = dir ? dirval : s;
-      orow[X] = o;
-      if (dotx) acc = fma(__ldcs(dotx + (int64_t)P.Mx * YZ + X), o, acc);
+      return dir ? dirval : s;
+    };
+    if constexpr (FUSE) {
+      // r (and the Jacobi diagonal) kFuseUnroll entries per lane in flight: r is read and
+      // written through one pointer, so a plain per-X loop serialises on every load
+      const int64_t g0 = (int64_t)P.Mx * YZ;
+      for (int X0 = 0; X0 < P.Mx; X0 += 32 * kFuseUnroll) {
+        double rv[kFuseUnroll], dv[kFuseUnroll];
+#pragma unroll
+        for (int m = 0; m < kFuseUnroll; ++m) {
+          const int X = X0 + 32 * m + lane;
+          rv[m] = X < P.Mx ? __ldcs(F.r + g0 + X) : 0.0;
+          dv[m] = (F.diag && X < P.Mx) ? __ldcs(F.diag + g0 + X) : 1.0;
+        }
+#pragma unroll
+        for (int m = 0; m < kFuseUnroll; ++m) {
+          const int X = X0 + 32 * m + lane;
+          if (X < P.Mx) {
+            const double ri = fma(-alpha, row_sum(X), rv[m]);
+            F.r[g0 + X] = ri;
+            acc = fma(ri, F.diag ? ri / dv[m] : ri, acc);
+          }
+        }
+      }
+    } else {
+      for (int X = lane; X < P.Mx; X += 32) {
+        const double o = row_sum(X);
+        orow[X] = o;
+        if (dotx) acc = fma(__ldcs(dotx + (int64_t)P.Mx * YZ + X), o, acc);
+      }
     }
     __syncwarp();
   }
-  if (dotx) {
+  if (FUSE || dotx) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     __syncthreads();   // the row buffers are free: reuse for the warp sums
@@ -100,25 +157,28 @@ __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpPara
     if (threadIdx.x == 0) {
       double sum = 0.0;
       for (int w = 0; w < kAsmThreads / 32; ++w) sum += asm_sm[w];
-      dpart[blockIdx.x] = sum;
+      (FUSE ? F.rz_part : dpart)[blockIdx.x] = sum;
     }
   }
 }
 
 template <int K>
 inline cudaError_t evec_assemble(const OpParams& P, const double* ev, double* out, const double* dotx, double* dpart,
-                                 double dirval, cudaStream_t st) {
+                                 double dirval, cudaStream_t st, const CgFuse* fuse = nullptr) {
   const int rows = P.My * P.Mz;
   const size_t smem = sizeof(double) * (K + 1) * (size_t)P.nx * (kAsmThreads / 32);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;   // (K + 1) nx <= 3632 (8 row buffers)
   if (smem > 48 * 1024) {   // beyond the default: opt in (per call: a handle may live on any device)
-    const cudaError_t e = cudaFuncSetAttribute(evec_assemble_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem);
+    const cudaError_t e = fuse ? cudaFuncSetAttribute(evec_assemble_kernel<K, true>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                               : cudaFuncSetAttribute(evec_assemble_kernel<K, false>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const int ctas = (rows + kAsmThreads / 32 - 1) / (kAsmThreads / 32);
-  const unsigned grid = dotx ? (unsigned)kRedBlocks : (unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks);
-  evec_assemble_kernel<K><<<grid, kAsmThreads, smem, st>>>(P, ev, out, dotx, dpart, dirval);
+  const unsigned grid = (dotx || fuse) ? (unsigned)kRedBlocks : (unsigned)(ctas < kRedBlocks ? ctas : kRedBlocks);
+  if (fuse) evec_assemble_kernel<K, true><<<grid, kAsmThreads, smem, st>>>(P, ev, out, nullptr, nullptr, dirval, *fuse);
+  else evec_assemble_kernel<K, false><<<grid, kAsmThreads, smem, st>>>(P, ev, out, dotx, dpart, dirval, CgFuse{});
   return cudaGetLastError();
 }
 

@@ -81,8 +81,23 @@ cudaError_t element_matrices_nd(int nd, int model, bool affine, bool elm, const 
 // Jacobi diagonal of the stored linearisation at Q6 on affine meshes (q6tc.cu, K12)
 cudaError_t q6tc_diag(int model, const OpParams& P, const Tables& T, double* ev, double* diag, cudaStream_t st);
 bool q6tc_supports(int mode);
+// The CG update fused behind the Q6 operator (Newton-CG, NEXT-3): the operator kernel forms
+// the partials of p.Ap element by element (p's Dirichlet entries are 0 in the CG), and the
+// assembly, instead of writing Ap, applies r -= alpha Ap row by row (alpha = *rr / p.Ap) and
+// forms the partials of r.z -- the Ap vector is never written or re-read, cg_update is not
+// launched. Fixed grids and summation orders throughout.
+struct CgFuse {
+  const double* rr;     // r.z of the current iterate (device scalar)
+  double* pAp_part;     // kRedBlocks partials of p.Ap (written by the operator kernel)
+  double* pAp;          // p.Ap (device scalar, written by the assembly's CTA 0; cg_dir reads it)
+  double* r;            // residual vector, updated in place
+  double* rz_part;      // kRedBlocks partials of r.z (z = r / diag, or r)
+  int* bad;             // set when p.Ap <= 0
+  const double* diag;   // Jacobi diagonal or null
+};
 cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
-                     double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st);
+                     double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st,
+                     const CgFuse* fuse = nullptr);
 // element tangents by element-level forward AD through B, D and B^T (elm.cu, K10; Table 1's ELM);
 // nd >= 5 keeps the per-seed tangent arrays in scr (elm_scratch_per_cta(nd) doubles per CTA; the
 // grid is bounded by scr_doubles)

@@ -121,11 +121,17 @@ template <int MODE> constexpr int q6_nin() { return (MODE == MODE_JVP || MODE ==
 #ifndef FEOD_Q6P_MINB2   // two-field modes and PAJVP (3 CTAs, 168 registers; PAJVP spills at 128)
 #define FEOD_Q6P_MINB2 3
 #endif
-template <int MODE, int MODEL>
+// DOT (CgFuse, JVP / PAJVP): also the partials of v . (J v) per CTA into dpart, formed at the
+// points: v_e . (B^T F) = (B v_e) . F = sum_q w_q (grad v . F~ + v V~), F~ the tangent flux the
+// point already holds -- no extra loads, 4 FMAs per point (v's Dirichlet entries are 0 in the
+// CG, so the row mask P^T changes nothing). A fixed order: per lane over l and the elements,
+// lanes by a butterfly, warps in order.
+template <int MODE, int MODEL, bool DOT = false>
 __global__ void __launch_bounds__(32 * q6::WARPS,
                                   (q6_nin<MODE>() == 2 || MODE == MODE_PAJVP) ? FEOD_Q6P_MINB2 : FEOD_Q6P_MINB1)
 q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in0, const double* __restrict__ in1,
-                 double* __restrict__ ev) {
+                 double* __restrict__ ev, double* __restrict__ dpart) {
+  static_assert(!DOT || MODE == MODE_JVP || MODE == MODE_PAJVP, "v . (J v) needs a tangent mode");
   using namespace q6;
   constexpr int NIN = q6_nin<MODE>();
   constexpr int NL = lin_values(MODEL);
@@ -247,6 +253,7 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
 
+  double dacc = 0.0;
   for (int64_t e = (int64_t)blockIdx.x * WARPS + wid; e < E; e += (int64_t)gridDim.x * WARPS) {
     int ex, ey, ez;
     q6_coords(P, e, ex, ey, ez);
@@ -269,6 +276,7 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
     Frag S[7];
 #pragma unroll
     for (int c = 0; c < 7; ++c) S[c] = zero;
+    double dz[2] = {0.0, 0.0};   // DOT: sum_l w_l (grad v . F~ + v V~) at the lane's two (i, j)
 #pragma unroll
     for (int l = 0; l < 7; ++l) {
       // point plane l of each field: value, collocated x / y derivatives, z derivative
@@ -318,6 +326,12 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
 #pragma unroll
             for (int c = 0; c < NL; ++c) linp[(l * NL + c) * 49 + j * 7 + r] = lv[c];
           }
+          if constexpr (DOT) {
+            constexpr int fv = NIN - 1;   // the direction v: field 1 of the JVP, field 0 of PAJVP
+            double dq = fma(F0[0], gx[fv], fma(F0[1], gy[fv], F0[2] * gz[fv]));
+            if (value_channel(MODE, 0)) dq = fma(F0[3], u0[fv], dq);
+            dz[t] = FOLD ? fma(T.w[l], dq, dz[t]) : dz[t] + dq;   // PAJVP's stored values carry w_q
+          }
         }
         Fx.v[t] = F0[0];
         Fy.v[t] = F0[1];
@@ -352,12 +366,33 @@ q6tc_perl_kernel(const OpParams P, const Tables T, const double* __restrict__ in
           if (colv[t]) o[2 * q + t] = nd.v[t];
       }
     }
+    if constexpr (DOT) {
+      if (rowv) {
+        const double wr = FOLD ? T.w[r] : 1.0;
+        if (colv[0]) dacc = fma(FOLD ? wr * T.w[2 * q] : 1.0, dz[0], dacc);
+        if (colv[1]) dacc = fma(FOLD ? wr * T.w[2 * q + 1] : 1.0, dz[1], dacc);
+      }
+    }
+  }
+  if constexpr (DOT) {   // per-CTA partial in a fixed order (lanes by a butterfly, warps in order); CTA 0 zeroes the tail
+    __shared__ double wsum[WARPS];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, o);
+    if (lane == 0) wsum[wid] = dacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < WARPS; ++w) sum += wsum[w];
+      dpart[blockIdx.x] = sum;
+    }
+    if (blockIdx.x == 0)
+      for (int i = gridDim.x + threadIdx.x; i < kRedBlocks; i += blockDim.x) dpart[i] = 0.0;
   }
 }
 
 template <int MODE, int MODEL>
 static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double* in0, const double* in1, double* ev,
-                               double* out, const double* dotx, double* dpart, cudaStream_t st) {
+                               double* out, const double* dotx, double* dpart, cudaStream_t st, const CgFuse* fuse) {
   constexpr int NL = lin_values(MODEL);
   constexpr bool TMA_LIN = MODE == MODE_PAJVP && (NL * 49 * sizeof(double)) % 16 == 0;
   constexpr size_t smem = TMA_LIN ? (sizeof(double) * NL * 343 + 8 * sizeof(uint64_t)) * q6::WARPS +
@@ -371,22 +406,33 @@ static cudaError_t q6tc_launch(const OpParams& P, const Tables& T, const double*
   if ((e = persistent_slots(kfn, 32 * q6::WARPS, smem, &slots)) != cudaSuccess) return e;
   const int64_t E = (int64_t)P.nx * P.ny * P.nz;
   const int64_t want = (E + q6::WARPS - 1) / q6::WARPS;
-  const unsigned grid = (unsigned)(want < slots ? want : slots);
-  q6tc_perl_kernel<MODE, MODEL><<<grid, 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev);
+  unsigned grid = (unsigned)(want < slots ? want : slots);
+  // CgFuse (JVP / stored-linearisation JVP only): the direction p is the v field
+  const bool fused = fuse && (MODE == MODE_JVP || MODE == MODE_PAJVP);
+  if (fused && grid > (unsigned)kRedBlocks) grid = (unsigned)kRedBlocks;
+  if constexpr (MODE == MODE_JVP || MODE == MODE_PAJVP) {
+    if (fused) {
+      const void* kd = (const void*)q6tc_perl_kernel<MODE, MODEL, true>;
+      if ((e = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+      q6tc_perl_kernel<MODE, MODEL, true><<<grid, 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev, fuse->pAp_part);
+    }
+  }
+  if (!fused) q6tc_perl_kernel<MODE, MODEL><<<grid, 32 * q6::WARPS, smem, st>>>(P, T, in0, in1, ev, nullptr);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   OpParams Pa = P;
   if (MODE == MODE_VJP && P.vjp_keep_rows) Pa.faces = 0;   // J^T w keeps its Dirichlet rows (A17)
-  return evec_assemble<q6::K>(Pa, ev, out, dotx, dpart, 0.0, st);
+  return evec_assemble<q6::K>(Pa, ev, out, dotx, dpart, 0.0, st, fused ? fuse : nullptr);
 }
 
 // C4's path: Q6 on affine meshes, the modes above (other modes / perturbed meshes use plane_kernel)
 template <int MODE>
 static cudaError_t q6tc_mode(int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
-                             double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st) {
+                             double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st,
+                             const CgFuse* fuse) {
   switch (model) {
-    case PLAPLACE: return q6tc_launch<MODE, PLAPLACE>(P, T, in0, in1, ev, out, dotx, dpart, st);
-    case NLDIFF: return q6tc_launch<MODE, NLDIFF>(P, T, in0, in1, ev, out, dotx, dpart, st);
-    case HEAT: return q6tc_launch<MODE, HEAT>(P, T, in0, in1, ev, out, dotx, dpart, st);
+    case PLAPLACE: return q6tc_launch<MODE, PLAPLACE>(P, T, in0, in1, ev, out, dotx, dpart, st, fuse);
+    case NLDIFF: return q6tc_launch<MODE, NLDIFF>(P, T, in0, in1, ev, out, dotx, dpart, st, fuse);
+    case HEAT: return q6tc_launch<MODE, HEAT>(P, T, in0, in1, ev, out, dotx, dpart, st, fuse);
   }
   return cudaErrorInvalidValue;
 }
@@ -398,13 +444,13 @@ bool q6tc_supports(int mode) {
 }
 
 cudaError_t q6tc_run(int mode, int model, const OpParams& P, const Tables& T, const double* in0, const double* in1,
-                     double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st) {
+                     double* ev, double* out, const double* dotx, double* dpart, cudaStream_t st, const CgFuse* fuse) {
   switch (mode) {
-    case MODE_RES: return q6tc_mode<MODE_RES>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
-    case MODE_JVP: return q6tc_mode<MODE_JVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
-    case MODE_VJP: return q6tc_mode<MODE_VJP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
-    case MODE_LIN: return q6tc_mode<MODE_LIN>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
-    case MODE_PAJVP: return q6tc_mode<MODE_PAJVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st);
+    case MODE_RES: return q6tc_mode<MODE_RES>(model, P, T, in0, in1, ev, out, dotx, dpart, st, fuse);
+    case MODE_JVP: return q6tc_mode<MODE_JVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st, fuse);
+    case MODE_VJP: return q6tc_mode<MODE_VJP>(model, P, T, in0, in1, ev, out, dotx, dpart, st, fuse);
+    case MODE_LIN: return q6tc_mode<MODE_LIN>(model, P, T, in0, in1, ev, out, dotx, dpart, st, fuse);
+    case MODE_PAJVP: return q6tc_mode<MODE_PAJVP>(model, P, T, in0, in1, ev, out, dotx, dpart, st, fuse);
   }
   return cudaErrorInvalidValue;
 }

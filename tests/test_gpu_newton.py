@@ -178,3 +178,26 @@ def test_newton_cg_graph_replay_bitwise(stored):
     assert torch.equal(u_graph, u_direct) and n_graph == n_direct
     u_again, _ = op.newton_cg(u0, 3, 20)   # replays the cached graph
     assert op.cg_graph_launches() == 6 and torch.equal(u_again, u_direct)
+
+
+@pytest.mark.parametrize("stored", [0, 1, 2])
+def test_newton_cg_fused_update_matches_unfused(stored):
+    """NEXT-3: feod_set_cg_fusion (the CG update behind the Q6 operator's assembly, p.Ap formed
+    element by element in the operator kernel) against the unfused loop (cg_update on the
+    assembled Ap): the same iterates up to the rounding order of the two dot products. A short
+    run (2 x 6: the roundoff growth of T17 stays small), then the fused run twice (bitwise
+    reproducible)."""
+    import torch
+    w = W.C4.resized(3)
+    d = W.draw(w)
+    op = operator(w, d)
+    op.set_newton_linearization(stored)
+    u0 = cuda(np.zeros(w.n_dofs))
+    op.set_cg_fusion(False)
+    u_a, n_a = op.newton_cg(u0, 2, 6)
+    op.set_cg_fusion(True)
+    u_b, n_b = op.newton_cg(u0, 2, 6)
+    u_c, n_c = op.newton_cg(u0, 2, 6)
+    assert torch.equal(u_b, u_c) and n_b == n_c
+    assert rel_l2(host(u_b), host(u_a)) <= 1e-10
+    assert np.max(np.abs(np.array(n_b) - np.array(n_a)) / np.array(n_a)) <= 1e-10
