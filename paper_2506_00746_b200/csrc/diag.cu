@@ -444,18 +444,26 @@ __global__ void __launch_bounds__(128, 4) diag_q3_kernel(const OpParams P, const
     }
     double dg[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int g = 0; g < 6; ++g)
+    for (int c = 0; c < 4; ++c) {
+      // y per group: Y(i, b = j) = sum_j' TY[j'][j] Z(i, j'), summed over the groups that share
+      // an x table (3 x-contractions instead of 6: the shuffles bound this kernel); then
+      // x: D(a = i, b = j) = sum_i' TX[i'][i] Y(i', j)
+      double Yx[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        // y: Y(i, b = j) = sum_j' TY[j'][j] Z(i, j'); x: D(a = i, b = j) = sum_i' TX[i'][i] Y(i', j)
+      for (int g = 0; g < 6; ++g) {
         double y = ty[GY[g]][0] * Z[g][c];
 #pragma unroll
         for (int k = 1; k < 4; ++k) y = fma(ty[GY[g]][k], __shfl_sync(0xffffffffu, Z[g][c], sy[k]), y);
-        double x = tx[GX[g]][0] * y;
+        Yx[GX[g]] += y;
+      }
 #pragma unroll
-        for (int k = 1; k < 4; ++k) x = fma(tx[GX[g]][k], __shfl_sync(0xffffffffu, y, sx[k]), x);
+      for (int kd = 0; kd < 3; ++kd) {
+        double x = tx[kd][0] * Yx[kd];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) x = fma(tx[kd][k], __shfl_sync(0xffffffffu, Yx[kd], sx[k]), x);
         dg[c] += x;
       }
+    }
     if (ev_ok) {
       int ex, ey, ez;
       {

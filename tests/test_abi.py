@@ -75,6 +75,8 @@ def test_argument_validation_without_gpu(lib):
     assert lib.feod_apply_host(None, 4, None, None, None) == fe.FEOD_EINVAL
     assert lib.feod_apply_host_batch(None, 4, 2, None, None, None) == fe.FEOD_EINVAL
     assert lib.feod_num_dofs(None) == -1
+    assert lib.feod_set_cg_fusion(None, 1) == fe.FEOD_EINVAL
+    assert lib.feod_set_cg_graphs(None, 1) == fe.FEOD_EINVAL
 
 
 def test_operator_refuses_without_cuda():

@@ -23,5 +23,8 @@ bash tools/gpu_prof.sh c4final_jvp C4 jvp q6tc_perl
 bash tools/gpu_prof.sh c4final_res C4 residual q6tc_perl
 bash tools/gpu_prof.sh c4final_asm C4 jvp evec_assemble
 bash tools/gpu_prof.sh c4final_emhi C4 elemat elemat_hi 1
+bash tools/gpu_prof.sh c4final_jvplin C4 jvp_lin q6tc_perl
+bash tools/gpu_prof.sh c4final_diag C4 jacobi_diag q6tc_diag 1
+python tools/newton_time.py 5 > $O/newton_time.txt 2>&1
 cp gpurun_out/prof/c4final_* $O/ 2>/dev/null
 python tools/link_bw.py > $O/link_bw.json 2>&1
