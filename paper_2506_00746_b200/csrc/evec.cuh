@@ -36,6 +36,9 @@ FEOD_DEV int evec_cands(int G, int ne, int* c) {
   return 1;
 }
 
+#ifndef FEOD_ASM_PREFETCH   // L2 prefetch of the warp's next row (measured slower: C4 JVP 248 -> 259 us,
+#define FEOD_ASM_PREFETCH 0   // residual 194 -> 204)
+#endif
 constexpr int kAsmThreads = 256;
 constexpr int kAsmUnroll = 8;
 constexpr int kFuseUnroll = 4;
@@ -85,6 +88,21 @@ __global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpPara
     int ns = 0;
     for (int kz = 0; kz < nzc; ++kz)
       for (int ky = 0; ky < nyc; ++ky) src[ns++] = ev + ((int64_t)cz[kz] * LYd + cy[ky]) * LX;
+#if FEOD_ASM_PREFETCH
+    {   // the warp's NEXT row: its source rows on their way to L2 while this row is summed
+      const int YZn = YZ + warps;
+      if (YZn < rows) {
+        const int Yn = YZn % P.My, Zn = YZn / P.My;
+        int cyn[2], czn[2];
+        const int nyn = evec_cands<K>(Yn, P.ny, cyn), nzn = evec_cands<K>(Zn, P.nz, czn);
+        for (int kz = 0; kz < nzn; ++kz)
+          for (int ky = 0; ky < nyn; ++ky) {
+            const double* sp = ev + ((int64_t)czn[kz] * LYd + cyn[ky]) * LX;
+            for (int X = 16 * lane; X < LX; X += 16 * 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(sp + X));
+          }
+      }
+    }
+#endif
     if constexpr (FUSE) {   // the row of r (and of the diagonal) on its way to L2 while stage 1 runs
       for (int X = 16 * lane; X < P.Mx; X += 16 * 32) {
         asm volatile("prefetch.global.L2 [%0];" ::"l"(F.r + (int64_t)P.Mx * YZ + X));
