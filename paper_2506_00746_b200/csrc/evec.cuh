@@ -39,6 +39,9 @@ FEOD_DEV int evec_cands(int G, int ne, int* c) {
 #ifndef FEOD_ASM_PREFETCH   // L2 prefetch of the warp's next row (measured slower: C4 JVP 248 -> 259 us,
 #define FEOD_ASM_PREFETCH 0   // residual 194 -> 204)
 #endif
+#ifndef FEOD_ASM_MINB   // resident CTAs per SM the assembly is compiled for (registers: 64 at 4)
+#define FEOD_ASM_MINB 4
+#endif
 constexpr int kAsmThreads = 256;
 constexpr int kAsmUnroll = 8;
 constexpr int kFuseUnroll = 4;
@@ -47,7 +50,7 @@ constexpr int kFuseUnroll = 4;
 // to out, and the partials are those of r.z; alpha from the operator kernel's p.Ap partials
 // (the same thread mapping and tree as blas1.cu's reduce_partials, in every CTA)
 template <int K, bool FUSE>
-__global__ void __launch_bounds__(kAsmThreads) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
+__global__ void __launch_bounds__(kAsmThreads, FEOD_ASM_MINB) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
                                                                      double* __restrict__ out,
                                                                      const double* __restrict__ dotx,
                                                                      double* __restrict__ dpart, double dirval,
