@@ -59,12 +59,19 @@ FEOD_DEV void point_op(const double* Ul, const double* Uxl, const double* Uyl, c
     const D gw[3] = {D(Uxl[0], Uxl[1]), D(Uyl[0], Uyl[1]), D(Uzl[0], Uzl[1])};
     D Fg[3];
     flux_hat<MODEL, DIAG>(uw, gw, M, W, rho_e, P, Fg);
-    const D uu(Ul[0], 1.0);
-    const D gu[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
-    D Fu[3];
-    flux_hat<MODEL, DIAG>(uu, gu, M, W, rho_e, P, Fu);
     F0[0] = Fg[0].d; F0[1] = Fg[1].d; F0[2] = Fg[2].d;
-    F0[3] = Uxl[1] * Fu[0].d + Uyl[1] * Fu[1].d + Uzl[1] * Fu[2].d;
+    if constexpr (MODEL == PLAPLACE) {
+      // the p-Laplacian flux does not depend on u: dFh/du = 0 exactly, no second dual
+      // evaluation (IEEE arithmetic would not let the compiler drop its 0.0 * x terms;
+      // it was ~40 % of the point's work: C2 J^T w 258 us against a 181 us JVP)
+      F0[3] = 0.0;
+    } else {
+      const D uu(Ul[0], 1.0);
+      const D gu[3] = {D(Uxl[0]), D(Uyl[0]), D(Uzl[0])};
+      D Fu[3];
+      flux_hat<MODEL, DIAG>(uu, gu, M, W, rho_e, P, Fu);
+      F0[3] = Uxl[1] * Fu[0].d + Uyl[1] * Fu[1].d + Uzl[1] * Fu[2].d;
+    }
   } else if constexpr (MODE == MODE_LIN) {
     // r = F(u) as MODE_RES, and the linearisation of D at the point for MODE_PAJVP
     // ("store only the innermost, pointwise operator component"):
