@@ -39,8 +39,14 @@ FEOD_DEV int evec_cands(int G, int ne, int* c) {
 #ifndef FEOD_ASM_PREFETCH   // L2 prefetch of the warp's next row (measured slower: C4 JVP 248 -> 259 us,
 #define FEOD_ASM_PREFETCH 0   // residual 194 -> 204)
 #endif
-#ifndef FEOD_ASM_MINB   // resident CTAs per SM the assembly is compiled for (registers: 64 at 4)
-#define FEOD_ASM_MINB 4
+// FEOD_ASM_MINB (experiment knob): resident CTAs per SM the assembly is compiled for. Unset
+// (default): no min-blocks hint -- 64 registers, no spills, 4 CTAs per SM. Set to 4 it spills
+// ~170 B after the FUSE refactoring (measured C4 JVP 249 -> 259 us, C3 diagonal 280 -> 307);
+// 5 / 6 are worse still.
+#ifdef FEOD_ASM_MINB
+#define FEOD_ASM_BOUNDS __launch_bounds__(kAsmThreads, FEOD_ASM_MINB)
+#else
+#define FEOD_ASM_BOUNDS __launch_bounds__(kAsmThreads)
 #endif
 constexpr int kAsmThreads = 256;
 constexpr int kAsmUnroll = 8;
@@ -50,7 +56,7 @@ constexpr int kFuseUnroll = 4;
 // to out, and the partials are those of r.z; alpha from the operator kernel's p.Ap partials
 // (the same thread mapping and tree as blas1.cu's reduce_partials, in every CTA)
 template <int K, bool FUSE>
-__global__ void __launch_bounds__(kAsmThreads, FEOD_ASM_MINB) evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
+__global__ void FEOD_ASM_BOUNDS evec_assemble_kernel(const OpParams P, const double* __restrict__ ev,
                                                                      double* __restrict__ out,
                                                                      const double* __restrict__ dotx,
                                                                      double* __restrict__ dpart, double dirval,
