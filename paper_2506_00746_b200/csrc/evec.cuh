@@ -45,6 +45,8 @@ FEOD_DEV int evec_cands(int G, int ne, int* c) {
 // 5 / 6 are worse still.
 #ifdef FEOD_ASM_MINB
 #define FEOD_ASM_BOUNDS __launch_bounds__(kAsmThreads, FEOD_ASM_MINB)
+#elif defined(FEOD_ASM_FUSE_MINB)   // the FUSE variant alone (110 registers without a hint)
+#define FEOD_ASM_BOUNDS __launch_bounds__(kAsmThreads, FUSE ? FEOD_ASM_FUSE_MINB : 1)
 #else
 #define FEOD_ASM_BOUNDS __launch_bounds__(kAsmThreads)
 #endif
